@@ -1,0 +1,155 @@
+/*
+ * fk.h -- C ABI of the B200-native fast-kernel-regression fit path (arXiv 2509.02649).
+ *
+ * libfk.so (paper_2509_02649_b200/libfk.so) exports the five calls of the method's data-parallel
+ * hot path plus a workspace query and a last-error string.  "P:<line>" cites PAPER.md, DESIGN.md
+ * lists the readings R1..R9 taken where the paper is ambiguous.
+ *
+ * Notation (reading R1):
+ *   t(x)     = pi x / (2L)            x in [-L, L]^d  (closed box)
+ *   f(x)     = sum_{||k||_inf <= m} theta_k exp(+i <k, t(x)>)
+ *   mu_q     = sum_j exp(-i <q, t(X_j)>)        ||q||_inf <= 2m   (first row of n*Sigma-hat)
+ *   r_k      = sum_j Y_j exp(-i <k, t(X_j)>)    ||k||_inf <= m    (n*v = Phi^* Y)
+ *   A theta  = r / n,  A = T(mu)/n + lambda M^*M (+ mu_pde D^* C D)
+ *
+ * Conventions shared by every call
+ *   - Layout: a mode vector over {-K..K}^d is stored lexicographically with the LAST coordinate
+ *     fastest, index of k = sum_l (k_l + K) (2K+1)^(d-1-l); complex values are interleaved
+ *     (re, im) doubles (complex128).
+ *   - Outputs are UNNORMALISED sums (reading R5): results of disjoint sample shards add, so a
+ *     multi-GPU fit all-reduces them (sum) and fk_solve divides by the total n.
+ *   - Ownership: every data pointer (points, Y, outputs, workspace, d_status) is caller-owned
+ *     DEVICE memory unless marked "host".  The library never allocates device memory on a call
+ *     after the first one with the same shape (cuFFT plans and the cuSOLVER handle are created
+ *     once and cached); scratch comes from `ws`, sized by fk_workspace_bytes().
+ *   - Ordering: every call is asynchronous and stream-ordered on `stream` (a cudaStream_t; NULL
+ *     = legacy default stream), except fk_solve with rep != NULL, which synchronises `stream`.
+ *   - Errors: argument errors are detected on the host and returned synchronously (no work is
+ *     enqueued); the message is available from fk_last_error() (thread-local).  Data errors found
+ *     by a kernel (a coordinate outside [-L, L], NaN) are OR-ed into *d_status (device int, bit
+ *     FK_E_RANGE) -- the caller zeroes it before and inspects it after synchronising.  Samples
+ *     with such a coordinate are skipped.
+ *   - Accuracy: eps is the requested relative l2 accuracy of each output vector against the
+ *     exact sums (reading R7); valid range [1e-14, 1e-1].  eps >= 1e-7 selects the fp32
+ *     spreading path (cubic B-spline window, fixed-point shared-memory accumulation); smaller eps
+ *     selects the fp64 path (exponential-of-semicircle window, fp64 accumulation).
+ */
+#ifndef FK_H
+#define FK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* fk_stream_t; /* == cudaStream_t */
+
+typedef enum fk_status {
+  FK_OK = 0,
+  FK_E_ARG = 1,         /* invalid argument (n < 0, m < 1, L <= 0, bad dtype/stride, lambda <= 0, ...) */
+  FK_E_RANGE = 2,       /* (d_status bit) a coordinate outside [-L, L] or NaN was skipped */
+  FK_E_EPS = 3,         /* eps outside [1e-14, 1e-1] */
+  FK_E_CUDA = 4,        /* a CUDA / cuFFT / cuSOLVER call failed */
+  FK_E_WORKSPACE = 5,   /* ws_bytes smaller than fk_workspace_bytes() */
+  FK_E_SOLVE = 6,       /* the system is not Hermitian positive definite (Cholesky info > 0) */
+  FK_E_UNSUPPORTED = 7  /* a shape this build does not handle (see fk_last_error) */
+} fk_status;
+
+typedef enum fk_dtype { FK_F32 = 0, FK_F64 = 1 } fk_dtype;
+
+/* n points in d dimensions: coordinate l of sample j is at element ptr[j*stride_n + l*stride_d]
+ * (element strides, not bytes).  Row-major n x d: stride_n = d, stride_d = 1; SoA columns:
+ * stride_n = 1, stride_d = column pitch.  The fast streaming path needs d = 1 and stride_n = 1. */
+typedef struct fk_points {
+  const void* ptr;
+  int32_t dtype; /* fk_dtype */
+  int32_t d;
+  int64_t n;
+  int64_t stride_n;
+  int64_t stride_d;
+} fk_points;
+
+enum { FK_ACCUMULATE = 1 }; /* flags: add into the outputs instead of overwriting them */
+
+/* Moments mu_q = sum_j exp(-i pi <q, X_j> / 2L), ||q||_inf <= 2m (the first row of
+ * n * Sigma-hat, Sigma-hat_{k1,k2} = mu_{k1-k2}/n).  mu_out: (4m+1)^d complex128.  d in {1, 2}.
+ * n = 0 is valid (all moments 0). */
+fk_status fk_moments_type1(fk_points X, double L, int m, double eps, double* mu_out, int flags, void* ws, size_t ws_bytes,
+                           int* d_status, fk_stream_t stream);
+
+/* Right-hand side r_k = sum_j Y_j exp(-i pi <k, X_j> / 2L), ||k||_inf <= m (n v =
+ * Phi^* Y).  r_out: (2m+1)^d complex128.  Y: n values of X.dtype, contiguous.  If mu_out != NULL
+ * the moments are produced by the SAME pass over (X, Y) (one read of the data).  d in {1, 2}. */
+fk_status fk_rhs_type1(fk_points X, const void* Y, double L, int m, double eps, double* r_out, double* mu_out, int flags,
+                       void* ws, size_t ws_bytes, int* d_status, fk_stream_t stream);
+
+/* Additive-model cross moments for every feature pair l1 < l2 in lexicographic pair order
+ * (P:505-512): G[p][a][b] = sum_j exp(-i pi (a X_{j,l1} - b X_{j,l2}) / 2L), a, b in {-m..m}:
+ * the 2-D type-1 sum of unit weights at the points (X_{l1}, -X_{l2}).  G_out: d(d-1)/2 blocks of
+ * (2m+1)^2 complex128, b fastest.  2 <= d <= 32. */
+fk_status fk_additive_cross_moments(fk_points X, double L, int m, double eps, double* G_out, int flags, void* ws,
+                                    size_t ws_bytes, int* d_status, fk_stream_t stream);
+
+typedef enum fk_kind {
+  FK_SOBOLEV = 0,  /* M = S, S_kk^2 = 1 + ||k||_2^{2s} */
+  FK_LOWBIAS = 1,  /* M = I */
+  FK_PIK_BOX = 2,  /* Sobolev + mu_pde D^* C D, Omega a box in [-L,L]^d          (reading R3) */
+  FK_ADDITIVE = 3  /* low-bias additive block system, theta in C^{d(2m+1)} */
+} fk_kind;
+
+typedef struct fk_problem {
+  int32_t d, m, kind, n_terms;
+  double n_total; /* total number of samples the moments were summed over (all shards) */
+  double L, s, lambda, mu_pde;
+  const int32_t* alpha;      /* host, n_terms x d multi-indices of D = sum a_alpha d^alpha (PIK_BOX) */
+  const double* a_alpha;     /* host, n_terms coefficients (PIK_BOX) */
+  const double* box;         /* host, 2d values [a_0, b_0, a_1, b_1, ...], Omega = prod [a_l, b_l] (PIK_BOX) */
+  const double* mu_moments;  /* device: (4m+1)^d complex128; ADDITIVE: d x (4m+1) (per-feature 1-D moments) */
+  const double* rhs;         /* device: (2m+1)^d complex128; ADDITIVE: d x (2m+1) (per-feature 1-D rhs) */
+  const double* cross;       /* device: ADDITIVE only, d(d-1)/2 x (2m+1)^2 from fk_additive_cross_moments */
+} fk_problem;
+
+typedef struct fk_solve_report {
+  double backward_err; /* ||A theta - r/n|| / ||r/n|| with A re-evaluated from the moments (reading R8) */
+  double ms;           /* device time of the solve (assembly + factorisation + solves) */
+  int32_t info;        /* Cholesky info (0 = success) */
+  int32_t n_unknowns;  /* D */
+} fk_solve_report;
+
+/* theta = A^{-1} r / n by dense Hermitian Cholesky in fp64 (P:513 for the additive block
+ * system; reading R9 for why not CG).  theta_out: D complex128, D = (2m+1)^d (d(2m+1) for
+ * ADDITIVE).  rep may be NULL (no synchronisation); otherwise the call synchronises `stream`
+ * and fills *rep.  Returns FK_E_SOLVE if A is not numerically positive definite. */
+fk_status fk_solve(const fk_problem* P, double* theta_out, fk_solve_report* rep, void* ws, size_t ws_bytes,
+                   fk_stream_t stream);
+
+/* Prediction by the type-2 sum: out_j = Re sum_k theta_k exp(+i pi <k, Xq_j> / 2L);
+ * additive != 0: out_j = sum_l Re sum_a theta_{l,a} exp(+i pi a Xq_{j,l} / 2L).
+ * out: Xq.n values of Xq.dtype.  d in {1, 2} (any d for additive). */
+fk_status fk_predict_type2(const double* theta, int d, int m, double L, int additive, fk_points Xq, double eps, void* out,
+                           void* ws, size_t ws_bytes, int* d_status, fk_stream_t stream);
+
+typedef enum fk_entry {
+  FK_ENTRY_MOMENTS = 0,
+  FK_ENTRY_RHS = 1,
+  FK_ENTRY_CROSS = 2,
+  FK_ENTRY_SOLVE = 3,
+  FK_ENTRY_PREDICT = 4
+} fk_entry;
+
+/* Workspace bytes the call `entry` needs for (d, m, eps, dtype, n, kind) on the current device
+ * (kind: fk_kind for SOLVE, the additive flag for PREDICT, ignored otherwise).  0 on error. */
+size_t fk_workspace_bytes(int entry, int d, int m, double eps, int dtype, int64_t n, int kind);
+
+/* Last error message of the calling thread ("" if none). */
+const char* fk_last_error(void);
+
+/* Library version string. */
+const char* fk_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FK_H */

@@ -1,0 +1,139 @@
+// fk_api.cu -- the extern "C" entry points of libfk (include/fk.h): argument validation on the
+// host, then dispatch to the stream-ordered implementations.
+#include <cmath>
+
+#include "fk_internal.cuh"
+
+namespace fk {
+const char* last_error_cstr();
+}
+
+using namespace fk;
+
+namespace {
+
+fk_status check_eps(double eps) {
+  if (!(eps >= 1e-14 && eps <= 1e-1)) return fail(FK_E_EPS, "eps must lie in [1e-14, 1e-1]");
+  return FK_OK;
+}
+
+fk_status check_points(const fk_points& X, int dmin, int dmax, const char* who) {
+  if (X.n < 0) return fail(FK_E_ARG, std::string(who) + ": n < 0");
+  if (X.d < dmin || X.d > dmax) return fail(FK_E_UNSUPPORTED, std::string(who) + ": unsupported dimension d = " + std::to_string(X.d));
+  if (X.dtype != FK_F32 && X.dtype != FK_F64) return fail(FK_E_ARG, std::string(who) + ": dtype must be FK_F32 or FK_F64");
+  if (X.n > 0 && X.ptr == nullptr) return fail(FK_E_ARG, std::string(who) + ": null points");
+  if (X.stride_n < 0 || X.stride_d < 0 || (X.n > 1 && X.stride_n == 0)) return fail(FK_E_ARG, std::string(who) + ": bad strides");
+  return FK_OK;
+}
+
+fk_status check_common(double L, int m, double eps, const char* who) {
+  if (!(L > 0.0) || !std::isfinite(L)) return fail(FK_E_ARG, std::string(who) + ": L must be positive");
+  if (m < 1 || m > (1 << 20)) return fail(FK_E_ARG, std::string(who) + ": m must be >= 1");
+  return check_eps(eps);
+}
+
+fk_status type1_entry(const fk_points& X, const void* Y, double L, int m, double eps, double* r_out, double* mu_out, int flags,
+                      void* ws, size_t ws_bytes, int* d_status, cudaStream_t s, const char* who) {
+  set_error("");
+  FK_TRY(check_common(L, m, eps, who));
+  FK_TRY(check_points(X, 1, 1, who));
+  if (!r_out && !mu_out) return fail(FK_E_ARG, std::string(who) + ": no output requested");
+  if (r_out && X.n > 0 && Y == nullptr) return fail(FK_E_ARG, std::string(who) + ": Y is null");
+  Plan1 p;
+  FK_TRY(make_plan1(X.d, m, eps, mu_out != nullptr, r_out != nullptr, &p));
+  Type1Out out{mu_out, r_out, (flags & FK_ACCUMULATE) != 0};
+  return type1_run(p, X, Y, L, out, ws, ws_bytes, d_status, s);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fk_last_error(void) { return last_error_cstr(); }
+
+const char* fk_version(void) { return "fk 0.1 (sm_100a)"; }
+
+fk_status fk_moments_type1(fk_points X, double L, int m, double eps, double* mu_out, int flags, void* ws, size_t ws_bytes,
+                           int* d_status, fk_stream_t stream) {
+  if (!mu_out) return fail(FK_E_ARG, "fk_moments_type1: mu_out is null");
+  return type1_entry(X, nullptr, L, m, eps, nullptr, mu_out, flags, ws, ws_bytes, d_status, (cudaStream_t)stream, "fk_moments_type1");
+}
+
+fk_status fk_rhs_type1(fk_points X, const void* Y, double L, int m, double eps, double* r_out, double* mu_out, int flags, void* ws,
+                       size_t ws_bytes, int* d_status, fk_stream_t stream) {
+  if (!r_out) return fail(FK_E_ARG, "fk_rhs_type1: r_out is null");
+  return type1_entry(X, Y, L, m, eps, r_out, mu_out, flags, ws, ws_bytes, d_status, (cudaStream_t)stream, "fk_rhs_type1");
+}
+
+fk_status fk_additive_cross_moments(fk_points X, double L, int m, double eps, double* G_out, int flags, void* ws, size_t ws_bytes,
+                                    int* d_status, fk_stream_t stream) {
+  set_error("");
+  FK_TRY(check_common(L, m, eps, "fk_additive_cross_moments"));
+  FK_TRY(check_points(X, 2, 32, "fk_additive_cross_moments"));
+  if (!G_out) return fail(FK_E_ARG, "fk_additive_cross_moments: G_out is null");
+  return cross_run(X, L, m, eps, G_out, (flags & FK_ACCUMULATE) != 0, ws, ws_bytes, d_status, (cudaStream_t)stream);
+}
+
+fk_status fk_solve(const fk_problem* P, double* theta_out, fk_solve_report* rep, void* ws, size_t ws_bytes, fk_stream_t stream) {
+  set_error("");
+  if (!P || !theta_out) return fail(FK_E_ARG, "fk_solve: null problem or output");
+  if (P->m < 1 || P->d < 1) return fail(FK_E_ARG, "fk_solve: d, m must be >= 1");
+  if (!(P->lambda > 0.0)) return fail(FK_E_ARG, "fk_solve: lambda must be > 0");
+  if (!(P->n_total > 0.0)) return fail(FK_E_ARG, "fk_solve: n_total must be > 0");
+  if (!(P->L > 0.0)) return fail(FK_E_ARG, "fk_solve: L must be > 0");
+  if (P->kind < FK_SOBOLEV || P->kind > FK_ADDITIVE) return fail(FK_E_ARG, "fk_solve: unknown kind");
+  if (!P->mu_moments || !P->rhs) return fail(FK_E_ARG, "fk_solve: null moments or rhs");
+  if (P->kind == FK_ADDITIVE && P->d > 1 && !P->cross) return fail(FK_E_ARG, "fk_solve: ADDITIVE needs cross moments");
+  if (P->kind != FK_ADDITIVE && P->d > 3) return fail(FK_E_UNSUPPORTED, "fk_solve: d <= 3 for the dense tensor-grid system");
+  if ((P->kind == FK_SOBOLEV || P->kind == FK_PIK_BOX) && !(P->s > 0.0)) return fail(FK_E_ARG, "fk_solve: s must be > 0");
+  if (P->kind == FK_PIK_BOX) {
+    if (P->n_terms < 1 || !P->alpha || !P->a_alpha || !P->box) return fail(FK_E_ARG, "fk_solve: PIK_BOX needs alpha, a_alpha, box");
+    for (int l = 0; l < P->d; ++l) {
+      const double a = P->box[2 * l], b = P->box[2 * l + 1];
+      if (!(a < b) || a < -P->L || b > P->L) return fail(FK_E_ARG, "fk_solve: box must satisfy -L <= a < b <= L");
+    }
+  }
+  // dense systems above ~2.5e4 unknowns exceed a sensible workspace
+  long D = P->kind == FK_ADDITIVE ? (long)P->d * (2 * P->m + 1) : (long)std::pow(2.0 * P->m + 1, P->d);
+  if (D > 40000) return fail(FK_E_UNSUPPORTED, "fk_solve: dense system too large (D = " + std::to_string(D) + ")");
+  return solve_run(P, theta_out, rep, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+fk_status fk_predict_type2(const double* theta, int d, int m, double L, int additive, fk_points Xq, double eps, void* out, void* ws,
+                           size_t ws_bytes, int* d_status, fk_stream_t stream) {
+  set_error("");
+  FK_TRY(check_common(L, m, eps, "fk_predict_type2"));
+  FK_TRY(check_points(Xq, 1, 32, "fk_predict_type2"));
+  if (Xq.d != d) return fail(FK_E_ARG, "fk_predict_type2: Xq.d != d");
+  if (!theta || (Xq.n > 0 && !out)) return fail(FK_E_ARG, "fk_predict_type2: null theta or out");
+  return predict_run(theta, d, m, L, additive, Xq, eps, out, ws, ws_bytes, d_status, (cudaStream_t)stream);
+}
+
+size_t fk_workspace_bytes(int entry, int d, int m, double eps, int dtype, int64_t n, int kind) {
+  set_error("");
+  (void)dtype;
+  if (m < 1 || d < 1 || !(eps >= 1e-14 && eps <= 1e-1)) {
+    set_error("fk_workspace_bytes: bad arguments");
+    return 0;
+  }
+  switch (entry) {
+    case FK_ENTRY_MOMENTS:
+    case FK_ENTRY_RHS: {
+      Plan1 p;
+      const bool mu = true, r = entry == FK_ENTRY_RHS;
+      if (make_plan1(d, m, eps, mu, r, &p) != FK_OK) return 0;
+      return type1_ws_bytes(p, mu, r);
+    }
+    case FK_ENTRY_CROSS:
+      return cross_ws_bytes(d, m, eps, n);
+    case FK_ENTRY_SOLVE:
+      return solve_ws_bytes(d, m, kind);
+    case FK_ENTRY_PREDICT:
+      return predict_ws_bytes(d, m, eps, kind);
+    default:
+      set_error("fk_workspace_bytes: unknown entry");
+      return 0;
+  }
+}
+
+}  // extern "C"

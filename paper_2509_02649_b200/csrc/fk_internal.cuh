@@ -1,0 +1,140 @@
+// fk_internal.cuh -- internal declarations of libfk (not installed; include/fk.h is the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cufft.h>
+#include <cstdint>
+#include <cstddef>
+#include <string>
+
+#include "../../include/fk.h"
+
+namespace fk {
+
+// ------------------------------------------------------------------------------------------
+// errors
+// ------------------------------------------------------------------------------------------
+void set_error(const std::string& msg);
+fk_status fail(fk_status st, const std::string& msg);
+#define FK_CUDA_TRY(expr)                                                                       \
+  do {                                                                                          \
+    cudaError_t _e = (expr);                                                                    \
+    if (_e != cudaSuccess)                                                                      \
+      return ::fk::fail(FK_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));          \
+  } while (0)
+#define FK_CUFFT_TRY(expr)                                                                      \
+  do {                                                                                          \
+    cufftResult _r = (expr);                                                                    \
+    if (_r != CUFFT_SUCCESS) return ::fk::fail(FK_E_CUDA, std::string(#expr) + ": cufft error " + std::to_string((int)_r)); \
+  } while (0)
+#define FK_TRY(expr)                  \
+  do {                                \
+    fk_status _s = (expr);            \
+    if (_s != FK_OK) return _s;       \
+  } while (0)
+
+int device_sm_count();
+
+// ------------------------------------------------------------------------------------------
+// workspace: a bump allocator over the caller's buffer (256-byte aligned slices)
+// ------------------------------------------------------------------------------------------
+struct Bump {
+  char* base;
+  size_t used = 0;
+  size_t cap;
+  explicit Bump(void* b, size_t c) : base((char*)b), cap(c) {}
+  void* take(size_t bytes) {
+    size_t off = (used + 255) & ~(size_t)255;
+    used = off + bytes;
+    return base ? (void*)(base + off) : nullptr;
+  }
+  bool ok() const { return used <= cap; }
+};
+
+// ------------------------------------------------------------------------------------------
+// spreading plans
+// ------------------------------------------------------------------------------------------
+enum KerKind { KER_BS3 = 0, KER_ES = 1 };
+
+// One fine grid of one channel along one dimension: period nf, cells [off, off + G) held locally.
+struct Geo {
+  int nf = 0;
+  int off = 0;
+  int G = 0;
+};
+
+struct EsParams {
+  int w = 0;
+  double beta = 0.0;
+};
+
+// Plan of a type-1 pass: window, precision and the two fine grids (moments: modes 4m+1,
+// rhs: modes 2m+1, nf_r = nf_mu / 2 so the rhs cell is the moment cell halved).
+struct Plan1 {
+  int d = 1;
+  int m = 0;
+  KerKind ker = KER_BS3;
+  bool fp64 = false;      // fp64 accumulation path (ES window)
+  EsParams es;
+  int nf_mu = 0, nf_r = 0;  // per dimension
+  Geo gA, gB;             // per-dimension geometry of the moment / rhs grids
+  bool smem = true;       // grids held in shared memory (else global accumulation)
+  int threads = 1024;
+  int ctas = 0;
+  size_t smem_bytes = 0;
+};
+
+fk_status make_plan1(int d, int m, double eps, bool need_mu, bool need_r, Plan1* p);
+int fft_friendly(int n);  // smallest 2^a 3^b 5^c >= n, even, multiple of 8
+
+// ES window Fourier transform table phihat[k] = psi-hat(k / nf), k = 0..K (computed on device).
+fk_status es_phihat_table(const EsParams& es, int nf, int K, double* d_tab, cudaStream_t s);
+
+// cuFFT plan cache (plans own no memory; the work area comes from the workspace)
+struct FftPlan {
+  cufftHandle h = 0;
+  size_t work = 0;
+};
+fk_status fft_plan(int rank, const int* dims, int batch, cufftType type, FftPlan* out);
+fk_status fft_exec_d2z(const FftPlan& p, double* in, cufftDoubleComplex* out, void* work, cudaStream_t s);
+fk_status fft_exec_z2d(const FftPlan& p, cufftDoubleComplex* in, double* out, void* work, cudaStream_t s);
+
+// ------------------------------------------------------------------------------------------
+// d = 1 pass (spread1d.cu)
+// ------------------------------------------------------------------------------------------
+struct Type1Out {
+  double* mu;  // (4m+1)^d complex or null
+  double* r;   // (2m+1)^d complex or null
+  bool accumulate;
+};
+size_t type1_ws_bytes(const Plan1& p, bool need_mu, bool need_r);
+fk_status type1_run(const Plan1& p, const fk_points& X, const void* Y, double L, const Type1Out& out, void* ws, size_t ws_bytes,
+                    int* d_status, cudaStream_t s);
+
+// ------------------------------------------------------------------------------------------
+// solve (solve.cu), predict (predict.cu), additive (additive.cu)
+// ------------------------------------------------------------------------------------------
+size_t solve_ws_bytes(int d, int m, int kind);
+fk_status solve_run(const fk_problem* P, double* theta, fk_solve_report* rep, void* ws, size_t ws_bytes, cudaStream_t s);
+
+size_t predict_ws_bytes(int d, int m, double eps, int additive);
+fk_status predict_run(const double* theta, int d, int m, double L, int additive, const fk_points& Xq, double eps, void* out,
+                      void* ws, size_t ws_bytes, int* d_status, cudaStream_t s);
+
+size_t cross_ws_bytes(int d, int m, double eps, int64_t n);
+fk_status cross_run(const fk_points& X, double L, int m, double eps, double* G, bool accumulate, void* ws, size_t ws_bytes,
+                    int* d_status, cudaStream_t s);
+
+// ------------------------------------------------------------------------------------------
+// device helpers
+// ------------------------------------------------------------------------------------------
+#define FK_MAGIC 12582912.0f        // 1.5 * 2^23: x + MAGIC rounds x to an integer in the low mantissa bits
+#define FK_MAGIC_BITS 0x4B400000
+
+__host__ __device__ inline double sinc_pi(double x) {  // sin(pi x) / (pi x)
+  if (x == 0.0) return 1.0;
+  const double a = 3.14159265358979323846 * x;
+  return sin(a) / a;
+}
+
+}  // namespace fk

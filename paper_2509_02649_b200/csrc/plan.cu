@@ -1,0 +1,197 @@
+// plan.cu -- errors, plans (window / precision / fine-grid geometry), cuFFT plan cache,
+// and the ES window transform table.
+#include <cmath>
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <vector>
+
+#include "fk_internal.cuh"
+
+namespace fk {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+fk_status fail(fk_status st, const std::string& msg) {
+  g_last_error = msg;
+  return st;
+}
+const char* last_error_cstr() { return g_last_error.c_str(); }
+
+int device_sm_count() {
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+  return sms;
+}
+
+static int max_smem_optin() {
+  int dev = 0, v = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  return v > 0 ? v : 232448;
+}
+
+int fft_friendly(int n) {
+  int best = 1 << 30;
+  for (long a = 8; a < 2L * n + 64; a *= 2)
+    for (long b = a; b < 2L * n + 64; b *= 3)
+      for (long c = b; c < 2L * n + 64; c *= 5)
+        if (c >= n && c < best) best = (int)c;
+  return best;
+}
+
+// fp32 path: cubic B-spline window.  Its transform is sinc^4, so the aliased copies at k +- nf
+// are damped by (k/(nf-k))^4 <= (2 sigma - 1)^-4 at the edge mode:
+// sigma = ((1/eps)^{1/4} + 1) / 2 puts the edge-mode error near eps.
+static double bs3_sigma(double eps) { return std::max(4.0, 0.5 * (std::pow(1.0 / eps, 0.25) + 1.0)); }
+
+fk_status make_plan1(int d, int m, double eps, bool need_mu, bool need_r, Plan1* p) {
+  if (d != 1) return fail(FK_E_UNSUPPORTED, "make_plan1: only d = 1 here");
+  Plan1 q;
+  q.d = d;
+  q.m = m;
+  const int sms = device_sm_count();
+  if (sms <= 0) return fail(FK_E_CUDA, "no CUDA device");
+  const int smem_cap = max_smem_optin();
+  const int modes_mu = 4 * m + 1;
+  bool fp32 = eps >= 1e-7;
+  if (fp32) {
+    const double sigma = bs3_sigma(eps);
+    q.ker = KER_BS3;
+    q.fp64 = false;
+    q.nf_mu = fft_friendly((int)std::ceil(sigma * modes_mu));
+    q.nf_r = q.nf_mu / 2;
+    q.gA = {q.nf_mu, q.nf_mu / 4 - 1, q.nf_mu / 2 + 4};
+    q.gB = {q.nf_r, q.nf_r / 4 - 1, q.nf_r / 2 + 4};
+    size_t bytes = (size_t)((need_mu ? q.gA.G : 0) + (need_r ? q.gB.G : 0)) * 4;
+    if (bytes > (size_t)smem_cap) fp32 = false;  // too large for one CTA: take the fp64 path
+    else {
+      q.smem_bytes = bytes;
+      q.smem = true;
+    }
+  }
+  if (!fp32) {
+    q.ker = KER_ES;
+    q.fp64 = true;
+    int w = (int)std::ceil(std::log10(1.0 / eps)) + 2;
+    w = std::min(16, std::max(4, w));
+    q.es.w = w;
+    q.es.beta = 2.30 * w;  // ES shape for sigma = 2
+    q.nf_mu = fft_friendly(2 * modes_mu);
+    q.nf_r = q.nf_mu / 2;
+    q.gA = {q.nf_mu, q.nf_mu / 4 - w / 2 - 2, q.nf_mu / 2 + w + 4};
+    q.gB = {q.nf_r, q.nf_r / 4 - w / 2 - 2, q.nf_r / 2 + w + 4};
+    size_t bytes = (size_t)((need_mu ? q.gA.G : 0) + (need_r ? q.gB.G : 0)) * 8;
+    q.smem = bytes <= (size_t)smem_cap;
+    q.smem_bytes = q.smem ? bytes : 0;
+  }
+  // launch shape: persistent CTAs, as many per SM as shared memory and 2048 threads allow
+  q.threads = 1024;
+  int per_sm = 2;
+  if (q.smem && q.smem_bytes > 0) per_sm = std::max(1, std::min(2, (int)((smem_cap + 1024) / (q.smem_bytes + 1024))));
+  if (!q.smem) per_sm = 2;
+  q.ctas = sms * per_sm;
+  *p = q;
+  return FK_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// ES window transform: psi(z) = exp(beta (sqrt(1 - z^2) - 1)), |z| <= 1, z = x / (w/2).
+// psi-hat(k/nf) = int psi(2x/w) e^{-2 pi i k x / nf} dx = w int_0^1 psi(z) cos(pi k w z / nf) dz,
+// by 96-point Gauss-Legendre on [0, 1].
+// ------------------------------------------------------------------------------------------
+struct GL96 {
+  double x[96];
+  double w[96];
+};
+
+static void gauss_legendre01(int n, double* x, double* w) {
+  for (int i = 0; i < n; ++i) {
+    double z = std::cos(3.14159265358979323846 * (i + 0.75) / (n + 0.5));
+    double pp = 0.0;
+    for (int it = 0; it < 100; ++it) {
+      double p1 = 1.0, p2 = 0.0;
+      for (int j = 1; j <= n; ++j) {
+        double p3 = p2;
+        p2 = p1;
+        p1 = ((2.0 * j - 1.0) * z * p2 - (j - 1.0) * p3) / j;
+      }
+      pp = n * (z * p1 - p2) / (z * z - 1.0);
+      double z1 = z;
+      z = z1 - p1 / pp;
+      if (std::fabs(z - z1) < 1e-15) break;
+    }
+    x[i] = 0.5 * (1.0 - z);  // map [-1,1] -> [0,1]
+    w[i] = 1.0 / ((1.0 - z * z) * pp * pp);  // = 2/((1-z^2)pp^2) * 1/2
+  }
+}
+
+__global__ void k_es_phihat(GL96 gl, int w, double beta, int nf, int K, double* tab) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k > K) return;
+  double s = 0.0;
+  for (int i = 0; i < 96; ++i) {
+    const double z = gl.x[i];
+    const double psi = exp(beta * (sqrt(1.0 - z * z) - 1.0));
+    s += gl.w[i] * psi * cos(3.14159265358979323846 * (double)k * w * z / nf);
+  }
+  tab[k] = w * s;
+}
+
+fk_status es_phihat_table(const EsParams& es, int nf, int K, double* d_tab, cudaStream_t s) {
+  static GL96 gl;
+  static std::once_flag once;
+  std::call_once(once, [] { gauss_legendre01(96, gl.x, gl.w); });
+  k_es_phihat<<<(K + 1 + 127) / 128, 128, 0, s>>>(gl, es.w, es.beta, nf, K, d_tab);
+  FK_CUDA_TRY(cudaGetLastError());
+  return FK_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// cuFFT plan cache.  Plans are created once per (device, rank, dims, batch, type) with
+// auto-allocation off; each execution binds the caller's stream and workspace under a lock.
+// ------------------------------------------------------------------------------------------
+static std::mutex g_fft_mu;
+static std::map<std::tuple<int, int, int, int, int, int>, FftPlan> g_fft_plans;
+
+fk_status fft_plan(int rank, const int* dims, int batch, cufftType type, FftPlan* out) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  auto key = std::make_tuple(dev, rank, dims[0], rank > 1 ? dims[1] : 0, batch, (int)type);
+  std::lock_guard<std::mutex> lk(g_fft_mu);
+  auto it = g_fft_plans.find(key);
+  if (it != g_fft_plans.end()) {
+    *out = it->second;
+    return FK_OK;
+  }
+  FftPlan p;
+  FK_CUFFT_TRY(cufftCreate(&p.h));
+  FK_CUFFT_TRY(cufftSetAutoAllocation(p.h, 0));
+  int n[2] = {dims[0], rank > 1 ? dims[1] : 0};
+  size_t work = 0;
+  FK_CUFFT_TRY(cufftMakePlanMany(p.h, rank, n, nullptr, 1, 0, nullptr, 1, 0, type, batch, &work));
+  p.work = work;
+  g_fft_plans[key] = p;
+  *out = p;
+  return FK_OK;
+}
+
+fk_status fft_exec_d2z(const FftPlan& p, double* in, cufftDoubleComplex* out, void* work, cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(g_fft_mu);
+  FK_CUFFT_TRY(cufftSetStream(p.h, s));
+  FK_CUFFT_TRY(cufftSetWorkArea(p.h, work));
+  FK_CUFFT_TRY(cufftExecD2Z(p.h, in, out));
+  return FK_OK;
+}
+
+fk_status fft_exec_z2d(const FftPlan& p, cufftDoubleComplex* in, double* out, void* work, cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(g_fft_mu);
+  FK_CUFFT_TRY(cufftSetStream(p.h, s));
+  FK_CUFFT_TRY(cufftSetWorkArea(p.h, work));
+  FK_CUFFT_TRY(cufftExecZ2D(p.h, in, out));
+  return FK_OK;
+}
+
+}  // namespace fk

@@ -1,0 +1,247 @@
+// predict.cu -- prediction by the type-2 sum (additive :463-468):
+//   f(x) = Re sum_{|k|<=m} theta_k exp(+i k t(x))
+// Since only the real part is returned, theta is replaced by its Hermitian part
+// h_k = (theta_k + conj theta_{-k}) / 2, so the fine grid
+//   g_l = sum_k h_k (-1)^k / psi-hat(k/nf) exp(+2 pi i k l / nf)       (one cuFFT Z2D)
+// is real, and f(x) = sum_l g_l psi(u(x) - l) is a w-tap gather from the occupied half of the
+// grid, held in shared memory (fp32 path: cubic B-spline, 4 taps; fp64 path: ES window).
+// The gather streams Xq once and writes f once: 8 B per query in fp32 (HBM-bound).
+#include <cmath>
+
+#include "fk_internal.cuh"
+#include "window.cuh"
+
+namespace fk {
+namespace {
+
+struct PredPlan {
+  int d, m, nfeat;
+  bool additive;
+  KerKind ker;
+  bool fp64;
+  EsParams es;
+  int nf;
+  Geo g;
+  size_t smem;
+  bool in_smem;
+};
+
+static double bs3_sigma_p(double eps) { return std::max(4.0, 0.5 * (std::pow(1.0 / eps, 0.25) + 1.0)); }
+
+static fk_status make_pred_plan(int d, int m, double eps, int additive, PredPlan* p) {
+  PredPlan q{};
+  q.d = d;
+  q.m = m;
+  q.additive = additive != 0;
+  q.nfeat = q.additive ? d : 1;
+  if (!q.additive && d != 1) return fail(FK_E_UNSUPPORTED, "fk_predict_type2: d = 1 or additive in this build");
+  q.fp64 = eps < 1e-7;
+  int smem_cap = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&smem_cap, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (!q.fp64) {
+    q.ker = KER_BS3;
+    q.nf = fft_friendly((int)std::ceil(bs3_sigma_p(eps) * (2 * m + 1)));
+    q.g = {q.nf, q.nf / 4 - 1, q.nf / 2 + 4};
+    q.smem = (size_t)q.nfeat * q.g.G * 4;
+  } else {
+    q.ker = KER_ES;
+    int w = (int)std::ceil(std::log10(1.0 / eps)) + 2;
+    w = std::min(16, std::max(4, w));
+    q.es.w = w;
+    q.es.beta = 2.30 * w;
+    q.nf = fft_friendly(2 * (2 * m + 1));
+    q.g = {q.nf, q.nf / 4 - w / 2 - 2, q.nf / 2 + w + 4};
+    q.smem = (size_t)q.nfeat * q.g.G * 8;
+  }
+  q.in_smem = q.smem <= (size_t)smem_cap;
+  if (!q.in_smem) q.smem = 0;
+  *p = q;
+  return FK_OK;
+}
+
+__global__ void k_pred_prep(const double2* __restrict__ theta, int nfeat, int m, int nf, int ker, const double* __restrict__ tab,
+                            double2* __restrict__ H) {
+  const int half = nf / 2 + 1;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)nfeat * half) return;
+  const int f = (int)(t / half), k = (int)(t % half);
+  double2 h = make_double2(0.0, 0.0);
+  if (k <= m) {
+    const double2 a = theta[(int64_t)f * (2 * m + 1) + m + k];
+    const double2 b = theta[(int64_t)f * (2 * m + 1) + m - k];
+    double ph;
+    if (ker == KER_BS3) {
+      const double s = sinc_pi((double)k / nf);
+      ph = (s * s) * (s * s);
+    } else {
+      ph = tab[k];
+    }
+    const double sc = 0.5 * ((k & 1) ? -1.0 : 1.0) / ph;
+    h = make_double2((a.x + b.x) * sc, (a.y - b.y) * sc);
+    if (k == 0) h.y = 0.0;
+  }
+  H[t] = h;
+}
+
+template <typename XT, bool EXACT>
+__global__ void __launch_bounds__(512) k_gather_bs3(const XT* __restrict__ Xq, int64_t n, int nfeat, int64_t sn, int64_t sd,
+                                                   const double* __restrict__ grid, int nf, int off, int G, float a_hi,
+                                                   float a_lo, double a_d, int in_smem, XT* __restrict__ out,
+                                                   int* __restrict__ d_status) {
+  extern __shared__ float sg[];
+  const float* gs = sg;
+  if (in_smem) {
+    for (int64_t i = threadIdx.x; i < (int64_t)nfeat * G; i += blockDim.x) {
+      const int f = (int)(i / G), c = (int)(i % G);
+      sg[i] = (float)grid[(int64_t)f * nf + off + c];
+    }
+    __syncthreads();
+  }
+  const int nq = nf / 4;
+  bool bad = false;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    float acc = 0.0f;
+    bool ok = true;
+    for (int f = 0; f < nfeat; ++f) {
+      int t;
+      float fr;
+      if (sizeof(XT) == 8) {
+        const double p = (double)Xq[j * sn + f * sd] * a_d;
+        const double fl = floor(p);
+        fr = (float)(p - fl);
+        t = (p == p && fabs(p) < 1e9) ? (int)fl + nq : -1;
+        if (fr >= 1.0f) { fr = 0.0f; t += 1; }
+      } else {
+        pos1_f32<EXACT>((float)Xq[j * sn + f * sd], a_hi, a_lo, nq, t, fr);
+      }
+      if ((unsigned)t > (unsigned)(G - 4)) {
+        ok = false;
+        continue;
+      }
+      float w[4];
+      bs3_float(fr, w);
+      if (in_smem) {
+        const float* c = gs + (int64_t)f * G + t;
+        acc += w[0] * c[0] + w[1] * c[1] + w[2] * c[2] + w[3] * c[3];
+      } else {
+        const double* c = grid + (int64_t)f * nf + off + t;
+        acc += w[0] * (float)c[0] + w[1] * (float)c[1] + w[2] * (float)c[2] + w[3] * (float)c[3];
+      }
+    }
+    if (!ok) bad = true;
+    out[j] = ok ? (XT)acc : (XT)NAN;
+  }
+  if (bad && d_status) atomicOr(d_status, (int)FK_E_RANGE);
+}
+
+template <typename XT>
+__global__ void __launch_bounds__(512) k_gather_es(const XT* __restrict__ Xq, int64_t n, int nfeat, int64_t sn, int64_t sd,
+                                                  const double* __restrict__ grid, int nf, int off, int G, double a, int w,
+                                                  double beta, int in_smem, XT* __restrict__ out, int* __restrict__ d_status) {
+  extern __shared__ double sgd[];
+  if (in_smem) {
+    for (int64_t i = threadIdx.x; i < (int64_t)nfeat * G; i += blockDim.x) {
+      const int f = (int)(i / G), c = (int)(i % G);
+      sgd[i] = grid[(int64_t)f * nf + off + c];
+    }
+    __syncthreads();
+  }
+  bool bad = false;
+  const double inv = 2.0 / w;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    bool ok = true;
+    for (int f = 0; f < nfeat; ++f) {
+      const double ul = (double)Xq[j * sn + f * sd] * a + 0.5 * nf - off;
+      const int l0 = (int)ceil(ul - 0.5 * w);
+      if (!(ul == ul) || l0 < 0 || l0 + w > G) {
+        ok = false;
+        continue;
+      }
+      const double* c = in_smem ? sgd + (int64_t)f * G : grid + (int64_t)f * nf + off;
+      for (int i = 0; i < w; ++i) {
+        const double z = ((double)(l0 + i) - ul) * inv;
+        const double v = 1.0 - z * z;
+        if (v > 0.0) acc += exp(beta * (sqrt(v) - 1.0)) * c[l0 + i];
+      }
+    }
+    if (!ok) bad = true;
+    out[j] = ok ? (XT)acc : (XT)NAN;
+  }
+  if (bad && d_status) atomicOr(d_status, (int)FK_E_RANGE);
+}
+
+struct PredWs {
+  double2* H;
+  double* grid;
+  double* tab;
+  void* work;
+};
+
+static fk_status pred_layout(const PredPlan& p, Bump& b, PredWs& w) {
+  FftPlan fp;
+  FK_TRY(fft_plan(1, &p.nf, p.nfeat, CUFFT_Z2D, &fp));
+  w.H = (double2*)b.take((size_t)p.nfeat * (p.nf / 2 + 1) * 16);
+  w.grid = (double*)b.take((size_t)p.nfeat * p.nf * 8);
+  w.tab = (double*)b.take((size_t)(p.m + 1) * 8);
+  w.work = b.take(std::max<size_t>(fp.work, 256));
+  return FK_OK;
+}
+
+template <typename XT>
+static fk_status gather(const PredPlan& p, const fk_points& Xq, double L, const PredWs& w, void* out, int* d_status, cudaStream_t s) {
+  const int sms = device_sm_count();
+  const double a = (double)p.nf / (4.0 * L);
+  if (p.ker == KER_BS3) {
+    const float a_hi = (float)a, a_lo = (float)(a - (double)a_hi);
+    int ex = 0;
+    const bool exact = std::frexp(a, &ex) == 0.5;
+    auto k = exact ? k_gather_bs3<XT, true> : k_gather_bs3<XT, false>;
+    if (p.smem) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+    const int per_sm = p.smem ? std::max(1, std::min(4, (int)(200000 / (p.smem + 1024)))) : 4;
+    k<<<sms * per_sm, 512, p.smem, s>>>((const XT*)Xq.ptr, Xq.n, p.nfeat, Xq.stride_n, Xq.stride_d, w.grid, p.nf, p.g.off, p.g.G,
+                                        a_hi, a_lo, a, p.in_smem ? 1 : 0, (XT*)out, d_status);
+  } else {
+    auto k = k_gather_es<XT>;
+    if (p.smem) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+    const int per_sm = p.smem ? std::max(1, std::min(4, (int)(200000 / (p.smem + 1024)))) : 4;
+    k<<<sms * per_sm, 512, p.smem, s>>>((const XT*)Xq.ptr, Xq.n, p.nfeat, Xq.stride_n, Xq.stride_d, w.grid, p.nf, p.g.off, p.g.G, a,
+                                        p.es.w, p.es.beta, p.in_smem ? 1 : 0, (XT*)out, d_status);
+  }
+  FK_CUDA_TRY(cudaGetLastError());
+  return FK_OK;
+}
+
+}  // namespace
+
+size_t predict_ws_bytes(int d, int m, double eps, int additive) {
+  PredPlan p;
+  if (make_pred_plan(d, m, eps, additive, &p) != FK_OK) return 0;
+  Bump b(nullptr, 0);
+  PredWs w;
+  if (pred_layout(p, b, w) != FK_OK) return 0;
+  return b.used + 256;
+}
+
+fk_status predict_run(const double* theta, int d, int m, double L, int additive, const fk_points& Xq, double eps, void* out, void* ws,
+                      size_t ws_bytes, int* d_status, cudaStream_t s) {
+  PredPlan p;
+  FK_TRY(make_pred_plan(d, m, eps, additive, &p));
+  Bump b(ws, ws_bytes);
+  PredWs w;
+  FK_TRY(pred_layout(p, b, w));
+  if (!b.ok()) return fail(FK_E_WORKSPACE, "fk_predict_type2: workspace too small");
+  if (p.ker == KER_ES) FK_TRY(es_phihat_table(p.es, p.nf, p.m, w.tab, s));
+  const int64_t tot = (int64_t)p.nfeat * (p.nf / 2 + 1);
+  k_pred_prep<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>((const double2*)theta, p.nfeat, m, p.nf, p.ker, w.tab, w.H);
+  FK_CUDA_TRY(cudaGetLastError());
+  FftPlan fp;
+  FK_TRY(fft_plan(1, &p.nf, p.nfeat, CUFFT_Z2D, &fp));
+  FK_TRY(fft_exec_z2d(fp, (cufftDoubleComplex*)w.H, w.grid, w.work, s));
+  if (Xq.n == 0) return FK_OK;
+  if (Xq.dtype == FK_F32) return gather<float>(p, Xq, L, w, out, d_status, s);
+  return gather<double>(p, Xq, L, w, out, d_status, s);
+}
+
+}  // namespace fk

@@ -1,0 +1,294 @@
+// solve.cu -- assembly and dense solve of the regularised Fourier system (PAPER.md:107 eq.
+// kenrel_reg, :252 Sobolev, :316 low-bias, :396 physics-informed box domain, :476-487 additive).
+//
+//   A[k1,k2] = mu_{k1-k2}/n + lambda R_{k1} delta_{k1 k2} (+ mu_pde conj(d_{k1}) B(k2-k1) d_{k2})
+//   A theta  = r / n
+//
+// A is Hermitian positive definite for lambda > 0; it is factorised by cuSOLVER zpotrf (fp64
+// Cholesky) and solved by zpotrs.  CG is not used: cond(A) is 1e6..1e11 at the
+// BASELINE configurations and Jacobi-preconditioned CG would need 1e3+ iterations (DESIGN.md
+// reading R9).  The backward error of the report re-evaluates A from the moments on the fly.
+#include <cusolverDn.h>
+
+#include <cmath>
+#include <map>
+#include <mutex>
+
+#include "fk_internal.cuh"
+
+namespace fk {
+namespace {
+
+constexpr int kMaxTerms = 8, kMaxD = 4;
+
+struct SysArgs {
+  int d, m, kind, D;
+  double inv_n, lambda, s, mu_pde, c;  // c = pi / (2L)
+  double inv4L;
+  int n_terms;
+  int alpha[kMaxTerms][kMaxD];
+  double a_alpha[kMaxTerms];
+  double box[kMaxD][2];
+  const double2* mu;
+  const double2* cross;
+};
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) { return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+
+__device__ void decode(int idx, int d, int m, int* k) {
+  const int side = 2 * m + 1;
+  for (int l = d - 1; l >= 0; --l) {
+    k[l] = idx % side - m;
+    idx /= side;
+  }
+}
+
+// symbol of D on exp(+i <k, t(x)>): d_k = sum_a a_alpha prod_l (i c k_l)^{alpha_l}  (reading R3)
+__device__ double2 pde_symbol(const SysArgs& g, const int* k) {
+  double2 acc = make_double2(0.0, 0.0);
+  for (int t = 0; t < g.n_terms; ++t) {
+    double2 term = make_double2(g.a_alpha[t], 0.0);
+    for (int l = 0; l < g.d; ++l) {
+      const double2 ik = make_double2(0.0, g.c * k[l]);
+      for (int e = 0; e < g.alpha[t][l]; ++e) term = cmul(term, ik);
+    }
+    acc.x += term.x;
+    acc.y += term.y;
+  }
+  return acc;
+}
+
+// B(q) = (4L)^{-d} int_box exp(+i c <q, x>) dx  (index order of reading R3)
+__device__ double2 box_fourier(const SysArgs& g, const int* q) {
+  double2 acc = make_double2(1.0, 0.0);
+  for (int l = 0; l < g.d; ++l) {
+    const double a = g.box[l][0], b = g.box[l][1];
+    double2 v;
+    if (q[l] == 0) {
+      v = make_double2(b - a, 0.0);
+    } else {
+      const double w = g.c * q[l];
+      double sb, cb, sa, ca;
+      sincos(w * b, &sb, &cb);
+      sincos(w * a, &sa, &ca);
+      // (e^{iwb} - e^{iwa}) / (i w) = ((sb - sa) - i (cb - ca)) / w
+      v = make_double2((sb - sa) / w, -(cb - ca) / w);
+    }
+    acc = cmul(acc, make_double2(v.x * g.inv4L, v.y * g.inv4L));
+  }
+  return acc;
+}
+
+__device__ double2 entry(const SysArgs& g, int i, int j) {
+  double2 v;
+  if (g.kind == FK_ADDITIVE) {
+    const int side = 2 * g.m + 1;
+    const int l1 = i / side, a = i % side - g.m;
+    const int l2 = j / side, b = j % side - g.m;
+    if (l1 == l2) {
+      v = g.mu[(int64_t)l1 * (4 * g.m + 1) + (a - b + 2 * g.m)];
+    } else if (l1 < l2) {
+      const int p = l1 * g.d - l1 * (l1 + 1) / 2 + (l2 - l1 - 1);
+      v = g.cross[((int64_t)p * side + (a + g.m)) * side + (b + g.m)];
+    } else {
+      const int p = l2 * g.d - l2 * (l2 + 1) / 2 + (l1 - l2 - 1);
+      v = cconj(g.cross[((int64_t)p * side + (b + g.m)) * side + (a + g.m)]);
+    }
+    v.x *= g.inv_n;
+    v.y *= g.inv_n;
+    if (i == j) v.x += g.lambda;
+    return v;
+  }
+  int k1[kMaxD], k2[kMaxD];
+  decode(i, g.d, g.m, k1);
+  decode(j, g.d, g.m, k2);
+  int64_t qi = 0;
+  const int qside = 4 * g.m + 1;
+  for (int l = 0; l < g.d; ++l) qi = qi * qside + (k1[l] - k2[l] + 2 * g.m);
+  v = g.mu[qi];
+  v.x *= g.inv_n;
+  v.y *= g.inv_n;
+  if (i == j) {
+    double R = 1.0;
+    if (g.kind != FK_LOWBIAS) {
+      double nk2 = 0.0;
+      for (int l = 0; l < g.d; ++l) nk2 += (double)k1[l] * k1[l];
+      R = 1.0 + pow(nk2, g.s);
+    }
+    v.x += g.lambda * R;
+  }
+  if (g.kind == FK_PIK_BOX && g.mu_pde != 0.0) {
+    int q[kMaxD];
+    for (int l = 0; l < g.d; ++l) q[l] = k2[l] - k1[l];
+    const double2 t = cmul(cmul(cconj(pde_symbol(g, k1)), box_fourier(g, q)), pde_symbol(g, k2));
+    v.x += g.mu_pde * t.x;
+    v.y += g.mu_pde * t.y;
+  }
+  return v;
+}
+
+__global__ void k_assemble(SysArgs g, double2* __restrict__ A) {  // column-major, lower triangle + diagonal
+  const int64_t D = g.D;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < D * D; t += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(t / D), i = (int)(t % D);
+    if (i >= j) A[t] = entry(g, i, j);
+  }
+}
+
+__global__ void k_scale_copy(const double2* __restrict__ r, double inv_n, int D, double2* __restrict__ b) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < D) b[i] = make_double2(r[i].x * inv_n, r[i].y * inv_n);
+}
+
+// res[0] += ||A theta - b||^2, res[1] += ||b||^2, with A evaluated on the fly (one warp per row)
+__global__ void k_residual(SysArgs g, const double2* __restrict__ theta, const double2* __restrict__ r, double* __restrict__ res) {
+  const int lane = threadIdx.x & 31;
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (row >= g.D) return;
+  double sx = 0.0, sy = 0.0;
+  for (int j = lane; j < g.D; j += 32) {
+    const double2 a = entry(g, row, j);
+    const double2 t = theta[j];
+    sx += a.x * t.x - a.y * t.y;
+    sy += a.x * t.y + a.y * t.x;
+  }
+  for (int o = 16; o; o >>= 1) {
+    sx += __shfl_xor_sync(0xffffffffu, sx, o);
+    sy += __shfl_xor_sync(0xffffffffu, sy, o);
+  }
+  if (lane == 0) {
+    const double bx = r[row].x * g.inv_n, by = r[row].y * g.inv_n;
+    atomicAdd(res, (sx - bx) * (sx - bx) + (sy - by) * (sy - by));
+    atomicAdd(res + 1, bx * bx + by * by);
+  }
+}
+
+std::mutex g_sol_mu;
+std::map<int, cusolverDnHandle_t> g_handles;
+
+fk_status handle_for_device(cusolverDnHandle_t* h) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  auto it = g_handles.find(dev);
+  if (it != g_handles.end()) {
+    *h = it->second;
+    return FK_OK;
+  }
+  cusolverDnHandle_t nh;
+  if (cusolverDnCreate(&nh) != CUSOLVER_STATUS_SUCCESS) return fail(FK_E_CUDA, "cusolverDnCreate failed");
+  g_handles[dev] = nh;
+  *h = nh;
+  return FK_OK;
+}
+
+int unknowns(int d, int m, int kind) {
+  if (kind == FK_ADDITIVE) return d * (2 * m + 1);
+  int D = 1;
+  for (int l = 0; l < d; ++l) D *= 2 * m + 1;
+  return D;
+}
+
+fk_status lwork_for(int D, int* lwork) {
+  std::lock_guard<std::mutex> lk(g_sol_mu);
+  cusolverDnHandle_t h;
+  FK_TRY(handle_for_device(&h));
+  if (cusolverDnZpotrf_bufferSize(h, CUBLAS_FILL_MODE_LOWER, D, nullptr, D, lwork) != CUSOLVER_STATUS_SUCCESS)
+    return fail(FK_E_CUDA, "cusolverDnZpotrf_bufferSize failed");
+  return FK_OK;
+}
+
+}  // namespace
+
+size_t solve_ws_bytes(int d, int m, int kind) {
+  const int D = unknowns(d, m, kind);
+  int lwork = 0;
+  if (lwork_for(D, &lwork) != FK_OK) return 0;
+  Bump b(nullptr, 0);
+  b.take((size_t)D * D * 16);
+  b.take((size_t)lwork * 16);
+  b.take(64);
+  return b.used + 256;
+}
+
+fk_status solve_run(const fk_problem* P, double* theta, fk_solve_report* rep, void* ws, size_t ws_bytes, cudaStream_t s) {
+  SysArgs g{};
+  g.d = P->d;
+  g.m = P->m;
+  g.kind = P->kind;
+  g.D = unknowns(P->d, P->m, P->kind);
+  g.inv_n = 1.0 / P->n_total;
+  g.lambda = P->lambda;
+  g.s = P->s;
+  g.mu_pde = P->mu_pde;
+  g.c = 3.14159265358979323846 / (2.0 * P->L);
+  g.inv4L = 1.0 / (4.0 * P->L);
+  g.mu = (const double2*)P->mu_moments;
+  g.cross = (const double2*)P->cross;
+  if (P->kind == FK_PIK_BOX) {
+    if (P->n_terms < 0 || P->n_terms > kMaxTerms || P->d > kMaxD) return fail(FK_E_ARG, "fk_solve: at most 8 PDE terms, d <= 4");
+    g.n_terms = P->n_terms;
+    for (int t = 0; t < P->n_terms; ++t) {
+      g.a_alpha[t] = P->a_alpha[t];
+      for (int l = 0; l < P->d; ++l) g.alpha[t][l] = P->alpha[t * P->d + l];
+    }
+    for (int l = 0; l < P->d; ++l) {
+      g.box[l][0] = P->box[2 * l];
+      g.box[l][1] = P->box[2 * l + 1];
+    }
+  }
+  const int D = g.D;
+  int lwork = 0;
+  FK_TRY(lwork_for(D, &lwork));
+  Bump b(ws, ws_bytes);
+  double2* A = (double2*)b.take((size_t)D * D * 16);
+  double2* work = (double2*)b.take((size_t)lwork * 16);
+  int* info = (int*)b.take(16);
+  double* res = (double*)(info + 4);
+  if (!b.ok()) return fail(FK_E_WORKSPACE, "fk_solve: workspace too small");
+
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (rep) {
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, s);
+  }
+  const int sms = device_sm_count();
+  k_assemble<<<sms * 8, 256, 0, s>>>(g, A);
+  k_scale_copy<<<(D + 255) / 256, 256, 0, s>>>((const double2*)P->rhs, g.inv_n, D, (double2*)theta);
+  FK_CUDA_TRY(cudaGetLastError());
+  {
+    std::lock_guard<std::mutex> lk(g_sol_mu);
+    cusolverDnHandle_t h;
+    FK_TRY(handle_for_device(&h));
+    if (cusolverDnSetStream(h, s) != CUSOLVER_STATUS_SUCCESS) return fail(FK_E_CUDA, "cusolverDnSetStream failed");
+    if (cusolverDnZpotrf(h, CUBLAS_FILL_MODE_LOWER, D, (cuDoubleComplex*)A, D, (cuDoubleComplex*)work, lwork, info) !=
+        CUSOLVER_STATUS_SUCCESS)
+      return fail(FK_E_CUDA, "cusolverDnZpotrf failed");
+    if (cusolverDnZpotrs(h, CUBLAS_FILL_MODE_LOWER, D, 1, (const cuDoubleComplex*)A, D, (cuDoubleComplex*)theta, D, info) !=
+        CUSOLVER_STATUS_SUCCESS)
+      return fail(FK_E_CUDA, "cusolverDnZpotrs failed");
+  }
+  if (rep) {
+    cudaEventRecord(e1, s);
+    FK_CUDA_TRY(cudaMemsetAsync(res, 0, 16, s));
+    k_residual<<<(D * 32 + 255) / 256, 256, 0, s>>>(g, (const double2*)theta, (const double2*)P->rhs, res);
+    int hinfo = 0;
+    double hres[2] = {0, 0};
+    FK_CUDA_TRY(cudaMemcpyAsync(&hinfo, info, 4, cudaMemcpyDeviceToHost, s));
+    FK_CUDA_TRY(cudaMemcpyAsync(hres, res, 16, cudaMemcpyDeviceToHost, s));
+    FK_CUDA_TRY(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    rep->info = hinfo;
+    rep->ms = ms;
+    rep->n_unknowns = D;
+    rep->backward_err = hres[1] > 0 ? std::sqrt(hres[0] / hres[1]) : 0.0;
+    if (hinfo != 0) return fail(FK_E_SOLVE, "fk_solve: Cholesky failed, info = " + std::to_string(hinfo));
+  }
+  return FK_OK;
+}
+
+}  // namespace fk

@@ -1,0 +1,528 @@
+// spread1d.cu -- the d = 1 type-1 pass over all samples (sec. 2.3):
+//   mu_q = sum_j exp(-i q t_j),  |q| <= 2m      r_k = sum_j Y_j exp(-i k t_j),  |k| <= m
+// computed as: spread every sample onto an oversampled periodic fine grid on t in [-pi, pi)
+// (points occupy its middle half), FFT the grid, deconvolve by the window transform and keep
+// the needed modes.  DESIGN.md §"Kernels" derives the design; summary:
+//
+//   fp32 path (eps >= 1e-7): cubic B-spline window (4 taps, no transcendental), moment grid
+//     nf_mu ~ sigma (4m+1) with sigma ~ 16, rhs grid nf_r = nf_mu / 2; both grids' occupied
+//     halves live in ONE CTA's shared memory as int32 fixed point (native ATOMS.ADD; fp32 smem
+//     atomics are CAS loops on sm_100a).  Partition of unity is exact in fixed point.  A cell
+//     that reaches 2^30 is drained into an fp64 global carry grid (atomicExch), so no periodic
+//     flush is needed and no overflow is possible.  The rhs channel uses a per-CTA power-of-two
+//     scale from the CTA's first 4096 |Y|; |Y| outliers (and NaN) take an exact fp64 slow path.
+//   fp64 path: exponential-of-semicircle window (sigma = 2, w ~ log10(1/eps) + 2) accumulated in
+//     fp64 (shared memory when it fits, else global).
+//
+// X and Y are streamed once from HBM with 128-bit evict-first loads, software-pipelined one
+// iteration ahead; CTAs are persistent (1-2 per SM) over contiguous sample ranges.
+#include <cmath>
+
+#include "fk_internal.cuh"
+#include "window.cuh"
+
+namespace fk {
+namespace {
+
+constexpr float kSA = 2097152.0f;  // 2^21: density fixed-point scale (tap weights <= 2/3)
+constexpr double kInvSA = 1.0 / 2097152.0;
+constexpr int kYProbe = 4096;      // samples used to pick a CTA's rhs scale
+
+__device__ __forceinline__ float4 ld_stream(const float4* p) { return __ldcs(p); }
+
+__device__ __noinline__ void drain_cells(int* G, int t0, double* carry, double inv_scale) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int v = atomicExch(G + t0 + k, 0);
+    if (v) atomicAdd(carry + t0 + k, (double)v * inv_scale);
+  }
+}
+
+__device__ __noinline__ void rhs_slow(float y, float fB, double* carryB, int tB0) {
+  double w[4];
+  bs3_exact(fB, w);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) atomicAdd(carryB + tB0 + k, w[k] * (double)y);
+}
+
+struct Bs3Args {
+  int64_t n, stride, per;
+  float a_hi, a_lo;
+  double a_d;
+  int nqA, GA, nqB, GB;
+  int* partA;
+  int* partB;
+  int* escale;
+  double* carryA;
+  double* carryB;
+  int* d_status;
+};
+
+template <bool MU, bool R>
+__device__ __forceinline__ void bs3_sample(int* __restrict__ A, int* __restrict__ B, const Bs3Args& g, int tA, int tB, float fA,
+                                           float fB, float y, float SY, float invSY_unused, double invSY, bool& bad) {
+  if ((unsigned)tA > (unsigned)(g.GA - 4)) {  // |X| > L (beyond rounding) or NaN: skip, flag
+    bad = true;
+    return;
+  }
+  if (MU) {
+    int i0, i1, i2, i3;
+    bs3_fixed(fA, kSA * (1.0f / 6.0f), (int)kSA, i0, i1, i2, i3);
+    int* c = A + tA;
+    const int o0 = atomicAdd(c, i0), o1 = atomicAdd(c + 1, i1), o2 = atomicAdd(c + 2, i2), o3 = atomicAdd(c + 3, i3);
+    if ((o0 | o1 | o2 | o3) & 0x40000000) drain_cells(A, tA, g.carryA, kInvSA);
+  }
+  if (R) {
+    const float ys = y * SY;
+    if (fabsf(ys) < 2097152.0f) {
+      int j0, j1, j2, j3;
+      const int jS = __float_as_int(ys + FK_MAGIC) - FK_MAGIC_BITS;
+      bs3_fixed(fB, ys * (1.0f / 6.0f), jS, j0, j1, j2, j3);
+      int* c = B + tB;
+      const unsigned p0 = (unsigned)atomicAdd(c, j0), p1 = (unsigned)atomicAdd(c + 1, j1);
+      const unsigned p2 = (unsigned)atomicAdd(c + 2, j2), p3 = (unsigned)atomicAdd(c + 3, j3);
+      const unsigned T = 1u << 30;
+      if (((p0 + T) | (p1 + T) | (p2 + T) | (p3 + T)) & 0x80000000u) drain_cells(B, tB, g.carryB, invSY);
+    } else {
+      rhs_slow(y, fB, g.carryB, tB);
+    }
+  }
+}
+
+template <typename XT, bool MU, bool R, bool VEC, bool EXACT>
+__global__ void __launch_bounds__(1024, 1) k_spread1d_bs3(const XT* __restrict__ X, const XT* __restrict__ Y, Bs3Args g) {
+  extern __shared__ int sm[];
+  int* A = sm;
+  int* B = sm + (MU ? g.GA : 0);
+  const int nsm = (MU ? g.GA : 0) + (R ? g.GB : 0);
+  for (int i = threadIdx.x; i < nsm; i += blockDim.x) sm[i] = 0;
+
+  const int64_t beg = (int64_t)blockIdx.x * g.per;
+  const int64_t end = min(g.n, beg + g.per);
+
+  // rhs scale of this CTA: 2^E with max|Y| 2^E in [2^19, 2^20) over its first kYProbe samples
+  float SY = 0.0f;
+  double invSY = 0.0;
+  int E = 19;
+  if (R) {
+    __shared__ float red[32];
+    __shared__ int sE;
+    float mx = 0.0f;
+    const int64_t cnt = max((int64_t)0, min(end - beg, (int64_t)kYProbe));
+    for (int64_t i = threadIdx.x; i < cnt; i += blockDim.x) mx = fmaxf(mx, fabsf((float)Y[beg + i]));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float t = 0.0f;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t = fmaxf(t, red[w]);
+      int e2 = 0;
+      int Eloc = 19;
+      if (t > 0.0f && t <= 3.0e38f) {
+        frexpf(t, &e2);  // t = mant * 2^e2, mant in [0.5, 1)
+        Eloc = 20 - e2;
+      }
+      Eloc = max(-100, min(110, Eloc));
+      sE = Eloc;
+      g.escale[blockIdx.x] = Eloc;
+    }
+    __syncthreads();
+    E = sE;
+    SY = ldexpf(1.0f, E);
+    invSY = ldexp(1.0, -E);
+  }
+  __syncthreads();
+
+  bool bad = false;
+  if (VEC) {
+    // 4 samples per thread per step; float4 streaming loads, prefetched one step ahead
+    const float4* X4 = reinterpret_cast<const float4*>(X);
+    const float4* Y4 = reinterpret_cast<const float4*>(Y);
+    const int64_t b4 = beg >> 2, e4 = end >> 2;
+    int64_t i = b4 + threadIdx.x;
+    float4 xv = make_float4(0, 0, 0, 0), yv = make_float4(0, 0, 0, 0);
+    if (i < e4) {
+      xv = ld_stream(X4 + i);
+      if (R) yv = ld_stream(Y4 + i);
+    }
+    while (i < e4) {
+      const int64_t inx = i + blockDim.x;
+      float4 xn = make_float4(0, 0, 0, 0), yn = make_float4(0, 0, 0, 0);
+      if (inx < e4) {
+        xn = ld_stream(X4 + inx);
+        if (R) yn = ld_stream(Y4 + inx);
+      }
+      const float xs[4] = {xv.x, xv.y, xv.z, xv.w};
+      const float ys[4] = {yv.x, yv.y, yv.z, yv.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        int tA, tB;
+        float fA, fB;
+        pos_f32<EXACT>(xs[q], g.a_hi, g.a_lo, g.nqA, g.nqB, tA, tB, fA, fB);
+        bs3_sample<MU, R>(A, B, g, tA, tB, fA, fB, ys[q], SY, 0.f, invSY, bad);
+      }
+      xv = xn;
+      yv = yn;
+      i = inx;
+    }
+    // tail (< 4 samples, last CTA only)
+    for (int64_t j = (e4 << 2) + threadIdx.x; j < end; j += blockDim.x) {
+      if (j < beg) continue;
+      int tA, tB;
+      float fA, fB;
+      pos_f32<EXACT>((float)X[j], g.a_hi, g.a_lo, g.nqA, g.nqB, tA, tB, fA, fB);
+      bs3_sample<MU, R>(A, B, g, tA, tB, fA, fB, R ? (float)Y[j] : 0.f, SY, 0.f, invSY, bad);
+    }
+  } else {
+    for (int64_t j = beg + threadIdx.x; j < end; j += blockDim.x) {
+      int tA, tB;
+      float fA, fB;
+      if (sizeof(XT) == 8) pos_f64((double)X[j * g.stride], g.a_d, g.nqA, g.nqB, tA, tB, fA, fB);
+      else pos_f32<EXACT>((float)X[j * g.stride], g.a_hi, g.a_lo, g.nqA, g.nqB, tA, tB, fA, fB);
+      bs3_sample<MU, R>(A, B, g, tA, tB, fA, fB, R ? (float)Y[j] : 0.f, SY, 0.f, invSY, bad);
+    }
+  }
+  if (bad && g.d_status) atomicOr(g.d_status, (int)FK_E_RANGE);
+  __syncthreads();
+  if (MU) {
+    int* dst = g.partA + (int64_t)blockIdx.x * g.GA;
+    for (int i = threadIdx.x; i < g.GA; i += blockDim.x) dst[i] = A[i];
+  }
+  if (R) {
+    int* dst = g.partB + (int64_t)blockIdx.x * g.GB;
+    for (int i = threadIdx.x; i < g.GB; i += blockDim.x) dst[i] = B[i];
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// fp64 path: exponential-of-semicircle window, fp64 accumulation
+// ------------------------------------------------------------------------------------------
+struct EsArgs {
+  int64_t n, stride, per;
+  double a;  // nf_mu / (4L)
+  int w;
+  double beta;
+  int nfA, offA, GA, nfB, offB, GB;
+  double* partA;
+  double* partB;
+  int* d_status;
+};
+
+__device__ __forceinline__ void es_spread(double* G, double ul, int w, double beta, double c) {
+  const int l0 = (int)ceil(ul - 0.5 * w);
+  const double inv = 2.0 / w;
+  for (int i = 0; i < w; ++i) {
+    const double z = ((double)(l0 + i) - ul) * inv;
+    const double v = 1.0 - z * z;
+    const double psi = v > 0.0 ? exp(beta * (sqrt(v) - 1.0)) : 0.0;
+    atomicAdd(G + l0 + i, c * psi);
+  }
+}
+
+template <typename XT, bool MU, bool R, bool SMEM>
+__global__ void __launch_bounds__(1024, 1) k_spread1d_es(const XT* __restrict__ X, const XT* __restrict__ Y, EsArgs g) {
+  extern __shared__ double smd[];
+  double* A = SMEM ? smd : g.partA;
+  double* B = SMEM ? smd + (MU ? g.GA : 0) : g.partB;
+  if (SMEM) {
+    const int nsm = (MU ? g.GA : 0) + (R ? g.GB : 0);
+    for (int i = threadIdx.x; i < nsm; i += blockDim.x) smd[i] = 0.0;
+    __syncthreads();
+  }
+  const int64_t beg = (int64_t)blockIdx.x * g.per;
+  const int64_t end = min(g.n, beg + g.per);
+  bool bad = false;
+  for (int64_t j = beg + threadIdx.x; j < end; j += blockDim.x) {
+    const double x = (double)X[j * g.stride];
+    const double u = x * g.a + 0.5 * g.nfA;  // moment-grid coordinate (cells), t = -pi at 0
+    const double ulA = u - g.offA;
+    const int l0 = (int)ceil(ulA - 0.5 * g.w);
+    if (!(ulA == ulA) || l0 < 0 || l0 + g.w > g.GA) {
+      bad = true;
+      continue;
+    }
+    if (MU) es_spread(A, ulA, g.w, g.beta, 1.0);
+    if (R) es_spread(B, 0.5 * u - g.offB, g.w, g.beta, (double)Y[j]);
+  }
+  if (bad && g.d_status) atomicOr(g.d_status, (int)FK_E_RANGE);
+  if (SMEM) {
+    __syncthreads();
+    if (MU) {
+      double* dst = g.partA + (int64_t)blockIdx.x * g.GA;
+      for (int i = threadIdx.x; i < g.GA; i += blockDim.x) dst[i] = A[i];
+    }
+    if (R) {
+      double* dst = g.partB + (int64_t)blockIdx.x * g.GB;
+      for (int i = threadIdx.x; i < g.GB; i += blockDim.x) dst[i] = B[i];
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// per-CTA partial grids -> one fp64 fine grid (full period, zero outside the occupied band),
+// summed over CTAs in a fixed order (the fixed-point path is exact, hence bitwise deterministic)
+// ------------------------------------------------------------------------------------------
+__global__ void k_reduce_fixed(const int* __restrict__ part, const int* __restrict__ escale, int ncta, int G, int off, int nf,
+                               double uniform_inv, const double* __restrict__ carry, double* __restrict__ fine) {
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= nf) return;
+  const int i = l - off;
+  double s = 0.0;
+  if (i >= 0 && i < G) {
+    if (escale) {
+      for (int c = 0; c < ncta; ++c) s += (double)part[(int64_t)c * G + i] * ldexp(1.0, -escale[c]);
+    } else {
+      for (int c = 0; c < ncta; ++c) s += (double)part[(int64_t)c * G + i];
+      s *= uniform_inv;
+    }
+    s += carry[i];
+  }
+  fine[l] = s;
+}
+
+__global__ void k_reduce_f64(const double* __restrict__ part, int ncta, int G, int off, int nf, double* __restrict__ fine) {
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= nf) return;
+  const int i = l - off;
+  double s = 0.0;
+  if (i >= 0 && i < G)
+    for (int c = 0; c < ncta; ++c) s += part[(int64_t)c * G + i];
+  fine[l] = s;
+}
+
+// mode q of the window-convolved grid: F_q = sum_l b_l e^{-2 pi i q l / nf}; the grid origin is
+// t = -pi, so e^{-i q (t + pi)} = (-1)^q e^{-i q t}: mu_q = (-1)^q F_q / psi-hat(q / nf).
+__global__ void k_deconv1d(const double2* __restrict__ F, int nf, int K, int ker, const double* __restrict__ tab,
+                           double2* __restrict__ out, int acc) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx > 2 * K) return;
+  const int q = idx - K;
+  const int aq = q < 0 ? -q : q;
+  double2 v = F[aq];
+  if (q < 0) v.y = -v.y;
+  double ph;
+  if (ker == KER_BS3) {
+    const double s = sinc_pi((double)aq / nf);
+    ph = (s * s) * (s * s);
+  } else {
+    ph = tab[aq];
+  }
+  const double sc = ((aq & 1) ? -1.0 : 1.0) / ph;
+  v.x *= sc;
+  v.y *= sc;
+  if (acc) {
+    out[idx].x += v.x;
+    out[idx].y += v.y;
+  } else {
+    out[idx] = v;
+  }
+}
+
+struct Ws1 {
+  void* partA = nullptr;
+  void* partB = nullptr;
+  int* escale = nullptr;
+  double* carryA = nullptr;
+  double* carryB = nullptr;
+  double* fineA = nullptr;
+  double* fineB = nullptr;
+  double2* specA = nullptr;
+  double2* specB = nullptr;
+  double* tabA = nullptr;
+  double* tabB = nullptr;
+  void* fftwork = nullptr;
+};
+
+static fk_status layout1(const Plan1& p, bool mu, bool r, Bump& b, Ws1& w, size_t* fftwork) {
+  const size_t esz = p.fp64 ? 8 : 4;
+  const int nparts = p.smem ? p.ctas : 1;
+  FftPlan pa, pb;
+  size_t fw = 0;
+  if (mu) {
+    FK_TRY(fft_plan(1, &p.nf_mu, 1, CUFFT_D2Z, &pa));
+    fw = std::max(fw, pa.work);
+  }
+  if (r) {
+    FK_TRY(fft_plan(1, &p.nf_r, 1, CUFFT_D2Z, &pb));
+    fw = std::max(fw, pb.work);
+  }
+  if (mu) {
+    w.partA = b.take((size_t)nparts * p.gA.G * esz);
+    w.fineA = (double*)b.take((size_t)p.nf_mu * 8);
+    w.specA = (double2*)b.take((size_t)(p.nf_mu / 2 + 1) * 16);
+    if (!p.fp64) w.carryA = (double*)b.take((size_t)p.gA.G * 8);
+    if (p.ker == KER_ES) w.tabA = (double*)b.take((size_t)(2 * p.m + 1) * 8);
+  }
+  if (r) {
+    w.partB = b.take((size_t)nparts * p.gB.G * esz);
+    w.fineB = (double*)b.take((size_t)p.nf_r * 8);
+    w.specB = (double2*)b.take((size_t)(p.nf_r / 2 + 1) * 16);
+    if (!p.fp64) {
+      w.carryB = (double*)b.take((size_t)p.gB.G * 8);
+      w.escale = (int*)b.take((size_t)p.ctas * 4);
+    }
+    if (p.ker == KER_ES) w.tabB = (double*)b.take((size_t)(p.m + 1) * 8);
+  }
+  w.fftwork = b.take(std::max<size_t>(fw, 256));
+  if (fftwork) *fftwork = fw;
+  return FK_OK;
+}
+
+template <typename XT, bool MU, bool R>
+static void launch_bs3(const Plan1& p, const XT* X, const XT* Y, const Bs3Args& a, bool vec, bool exact, cudaStream_t s) {
+  auto run = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
+    kern<<<p.ctas, p.threads, p.smem_bytes, s>>>(X, Y, a);
+  };
+  if (sizeof(XT) == 8) {
+    run(k_spread1d_bs3<XT, MU, R, false, false>);
+  } else if (vec) {
+    if (exact) run(k_spread1d_bs3<XT, MU, R, true, true>);
+    else run(k_spread1d_bs3<XT, MU, R, true, false>);
+  } else {
+    if (exact) run(k_spread1d_bs3<XT, MU, R, false, true>);
+    else run(k_spread1d_bs3<XT, MU, R, false, false>);
+  }
+}
+
+template <typename XT, bool MU, bool R>
+static void launch_es(const Plan1& p, const XT* X, const XT* Y, const EsArgs& a, cudaStream_t s) {
+  if (p.smem) {
+    auto k = k_spread1d_es<XT, MU, R, true>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
+    k<<<p.ctas, p.threads, p.smem_bytes, s>>>(X, Y, a);
+  } else {
+    k_spread1d_es<XT, MU, R, false><<<p.ctas, p.threads, 0, s>>>(X, Y, a);
+  }
+}
+
+template <typename XT>
+static fk_status spread_dispatch(const Plan1& p, const fk_points& Xp, const void* Yv, double L, bool mu, bool r, const Ws1& w,
+                                 int* d_status, cudaStream_t s) {
+  const XT* X = (const XT*)Xp.ptr;
+  const XT* Y = (const XT*)Yv;
+  const int64_t n = Xp.n;
+  if (!p.fp64) {
+    Bs3Args a{};
+    a.n = n;
+    a.stride = Xp.stride_n;
+    const double ad = (double)p.nf_mu / (4.0 * L);
+    a.a_d = ad;
+    a.a_hi = (float)ad;
+    a.a_lo = (float)(ad - (double)a.a_hi);
+    int ex = 0;
+    const bool exact = (std::frexp(ad, &ex) == 0.5);  // power of two: X * a is exact in fp32
+    a.nqA = p.nf_mu / 4;
+    a.nqB = p.nf_r / 4;
+    a.GA = p.gA.G;
+    a.GB = p.gB.G;
+    const bool vec = sizeof(XT) == 4 && Xp.stride_n == 1 && ((uintptr_t)X % 16 == 0) && (!r || ((uintptr_t)Y % 16 == 0));
+    int64_t per = (n + p.ctas - 1) / p.ctas;
+    per = (per + 3) & ~(int64_t)3;
+    a.per = per;
+    a.partA = (int*)w.partA;
+    a.partB = (int*)w.partB;
+    a.escale = w.escale;
+    a.carryA = w.carryA;
+    a.carryB = w.carryB;
+    a.d_status = d_status;
+    if (mu && r) launch_bs3<XT, true, true>(p, X, Y, a, vec, exact, s);
+    else if (mu) launch_bs3<XT, true, false>(p, X, Y, a, vec, exact, s);
+    else launch_bs3<XT, false, true>(p, X, Y, a, vec, exact, s);
+  } else {
+    EsArgs a{};
+    a.n = n;
+    a.stride = Xp.stride_n;
+    a.a = (double)p.nf_mu / (4.0 * L);
+    a.w = p.es.w;
+    a.beta = p.es.beta;
+    a.nfA = p.nf_mu;
+    a.offA = p.gA.off;
+    a.GA = p.gA.G;
+    a.nfB = p.nf_r;
+    a.offB = p.gB.off;
+    a.GB = p.gB.G;
+    a.per = (n + p.ctas - 1) / p.ctas;
+    a.partA = (double*)w.partA;
+    a.partB = (double*)w.partB;
+    a.d_status = d_status;
+    if (mu && r) launch_es<XT, true, true>(p, X, Y, a, s);
+    else if (mu) launch_es<XT, true, false>(p, X, Y, a, s);
+    else launch_es<XT, false, true>(p, X, Y, a, s);
+  }
+  FK_CUDA_TRY(cudaGetLastError());
+  return FK_OK;
+}
+
+}  // namespace
+
+size_t type1_ws_bytes(const Plan1& p, bool need_mu, bool need_r) {
+  Bump b(nullptr, 0);
+  Ws1 w;
+  if (layout1(p, need_mu, need_r, b, w, nullptr) != FK_OK) return 0;
+  return b.used + 256;
+}
+
+fk_status type1_run(const Plan1& p, const fk_points& X, const void* Y, double L, const Type1Out& out, void* ws, size_t ws_bytes,
+                    int* d_status, cudaStream_t s) {
+  const bool mu = out.mu != nullptr, r = out.r != nullptr;
+  Bump b(ws, ws_bytes);
+  Ws1 w;
+  size_t fw = 0;
+  FK_TRY(layout1(p, mu, r, b, w, &fw));
+  if (!b.ok()) return fail(FK_E_WORKSPACE, "workspace too small: need " + std::to_string(b.used + 256) + " bytes");
+  // zero what is accumulated globally
+  if (!p.fp64) {
+    if (mu) FK_CUDA_TRY(cudaMemsetAsync(w.carryA, 0, (size_t)p.gA.G * 8, s));
+    if (r) FK_CUDA_TRY(cudaMemsetAsync(w.carryB, 0, (size_t)p.gB.G * 8, s));
+  } else if (!p.smem) {
+    if (mu) FK_CUDA_TRY(cudaMemsetAsync(w.partA, 0, (size_t)p.gA.G * 8, s));
+    if (r) FK_CUDA_TRY(cudaMemsetAsync(w.partB, 0, (size_t)p.gB.G * 8, s));
+  }
+  if (X.n > 0) {
+    if (X.dtype == FK_F32) FK_TRY(spread_dispatch<float>(p, X, Y, L, mu, r, w, d_status, s));
+    else FK_TRY(spread_dispatch<double>(p, X, Y, L, mu, r, w, d_status, s));
+  } else if (!p.fp64 || p.smem) {
+    // no samples: partials are all zero
+    const size_t esz = p.fp64 ? 8 : 4;
+    if (mu) FK_CUDA_TRY(cudaMemsetAsync(w.partA, 0, (size_t)p.ctas * p.gA.G * esz, s));
+    if (r) FK_CUDA_TRY(cudaMemsetAsync(w.partB, 0, (size_t)p.ctas * p.gB.G * esz, s));
+    if (r && w.escale) FK_CUDA_TRY(cudaMemsetAsync(w.escale, 0, (size_t)p.ctas * 4, s));
+  }
+  const int nparts = p.smem ? p.ctas : 1;
+  const int TB = 256;
+  if (mu) {
+    if (!p.fp64)
+      k_reduce_fixed<<<(p.nf_mu + TB - 1) / TB, TB, 0, s>>>((const int*)w.partA, nullptr, nparts, p.gA.G, p.gA.off, p.nf_mu, kInvSA,
+                                                            w.carryA, w.fineA);
+    else
+      k_reduce_f64<<<(p.nf_mu + TB - 1) / TB, TB, 0, s>>>((const double*)w.partA, nparts, p.gA.G, p.gA.off, p.nf_mu, w.fineA);
+    FK_CUDA_TRY(cudaGetLastError());
+    FftPlan pa;
+    FK_TRY(fft_plan(1, &p.nf_mu, 1, CUFFT_D2Z, &pa));
+    FK_TRY(fft_exec_d2z(pa, w.fineA, (cufftDoubleComplex*)w.specA, w.fftwork, s));
+    if (p.ker == KER_ES) FK_TRY(es_phihat_table(p.es, p.nf_mu, 2 * p.m, w.tabA, s));
+    k_deconv1d<<<(4 * p.m + 1 + TB - 1) / TB, TB, 0, s>>>(w.specA, p.nf_mu, 2 * p.m, p.ker, w.tabA, (double2*)out.mu,
+                                                          out.accumulate ? 1 : 0);
+    FK_CUDA_TRY(cudaGetLastError());
+  }
+  if (r) {
+    if (!p.fp64)
+      k_reduce_fixed<<<(p.nf_r + TB - 1) / TB, TB, 0, s>>>((const int*)w.partB, w.escale, nparts, p.gB.G, p.gB.off, p.nf_r, 1.0,
+                                                           w.carryB, w.fineB);
+    else
+      k_reduce_f64<<<(p.nf_r + TB - 1) / TB, TB, 0, s>>>((const double*)w.partB, nparts, p.gB.G, p.gB.off, p.nf_r, w.fineB);
+    FK_CUDA_TRY(cudaGetLastError());
+    FftPlan pb;
+    FK_TRY(fft_plan(1, &p.nf_r, 1, CUFFT_D2Z, &pb));
+    FK_TRY(fft_exec_d2z(pb, w.fineB, (cufftDoubleComplex*)w.specB, w.fftwork, s));
+    if (p.ker == KER_ES) FK_TRY(es_phihat_table(p.es, p.nf_r, p.m, w.tabB, s));
+    k_deconv1d<<<(2 * p.m + 1 + TB - 1) / TB, TB, 0, s>>>(w.specB, p.nf_r, p.m, p.ker, w.tabB, (double2*)out.r,
+                                                          out.accumulate ? 1 : 0);
+    FK_CUDA_TRY(cudaGetLastError());
+  }
+  return FK_OK;
+}
+
+}  // namespace fk

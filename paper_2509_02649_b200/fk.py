@@ -1,0 +1,248 @@
+"""Thin Python binding of libfk (include/fk.h): argument marshalling only.
+
+Every step of the fit path runs in libfk's CUDA kernels; this module turns torch CUDA tensors
+into the C ABI's plain pointers / sizes / strides, allocates outputs and the workspace with
+torch (device memory plumbing), calls the C entry point on the current torch stream and turns a
+non-zero status into an exception.  The names are the C names.  There is no fallback: importing
+this module on a box without the built library raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfk.so")
+
+FK_OK, FK_E_ARG, FK_E_RANGE, FK_E_EPS, FK_E_CUDA, FK_E_WORKSPACE, FK_E_SOLVE, FK_E_UNSUPPORTED = range(8)
+FK_F32, FK_F64 = 0, 1
+FK_ACCUMULATE = 1
+FK_SOBOLEV, FK_LOWBIAS, FK_PIK_BOX, FK_ADDITIVE = 0, 1, 2, 3
+KINDS = {"sobolev": FK_SOBOLEV, "lowbias": FK_LOWBIAS, "pik_box": FK_PIK_BOX, "additive": FK_ADDITIVE}
+FK_ENTRY_MOMENTS, FK_ENTRY_RHS, FK_ENTRY_CROSS, FK_ENTRY_SOLVE, FK_ENTRY_PREDICT = range(5)
+_STATUS = {1: "FK_E_ARG", 2: "FK_E_RANGE", 3: "FK_E_EPS", 4: "FK_E_CUDA", 5: "FK_E_WORKSPACE", 6: "FK_E_SOLVE", 7: "FK_E_UNSUPPORTED"}
+
+
+class FkError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class fk_points(ctypes.Structure):
+    _fields_ = [("ptr", ctypes.c_void_p), ("dtype", ctypes.c_int32), ("d", ctypes.c_int32), ("n", ctypes.c_int64),
+                ("stride_n", ctypes.c_int64), ("stride_d", ctypes.c_int64)]
+
+
+class fk_problem(ctypes.Structure):
+    _fields_ = [("d", ctypes.c_int32), ("m", ctypes.c_int32), ("kind", ctypes.c_int32), ("n_terms", ctypes.c_int32),
+                ("n_total", ctypes.c_double), ("L", ctypes.c_double), ("s", ctypes.c_double), ("lam", ctypes.c_double),
+                ("mu_pde", ctypes.c_double), ("alpha", ctypes.POINTER(ctypes.c_int32)), ("a_alpha", ctypes.POINTER(ctypes.c_double)),
+                ("box", ctypes.POINTER(ctypes.c_double)), ("mu_moments", ctypes.c_void_p), ("rhs", ctypes.c_void_p),
+                ("cross", ctypes.c_void_p)]
+
+
+class fk_solve_report(ctypes.Structure):
+    _fields_ = [("backward_err", ctypes.c_double), ("ms", ctypes.c_double), ("info", ctypes.c_int32), ("n_unknowns", ctypes.c_int32)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libfk.so (raises if it was not built: there is no CPU path)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"libfk.so not found at {LIB_PATH}; build it with `python -m paper_2509_02649_b200.build`")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, dp, ip, sz = ctypes.c_void_p, ctypes.c_double, ctypes.c_int, ctypes.c_size_t
+        L.fk_moments_type1.argtypes = [fk_points, dp, ip, dp, vp, ip, vp, sz, vp, vp]
+        L.fk_rhs_type1.argtypes = [fk_points, vp, dp, ip, dp, vp, vp, ip, vp, sz, vp, vp]
+        L.fk_additive_cross_moments.argtypes = [fk_points, dp, ip, dp, vp, ip, vp, sz, vp, vp]
+        L.fk_solve.argtypes = [ctypes.POINTER(fk_problem), vp, ctypes.POINTER(fk_solve_report), vp, sz, vp]
+        L.fk_predict_type2.argtypes = [vp, ip, ip, dp, ip, fk_points, dp, vp, vp, sz, vp, vp]
+        L.fk_workspace_bytes.argtypes = [ip, ip, ip, dp, ip, ctypes.c_int64, ip]
+        L.fk_workspace_bytes.restype = ctypes.c_size_t
+        L.fk_last_error.restype = ctypes.c_char_p
+        L.fk_version.restype = ctypes.c_char_p
+        for f in ("fk_moments_type1", "fk_rhs_type1", "fk_additive_cross_moments", "fk_solve", "fk_predict_type2"):
+            getattr(L, f).restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _check(status: int):
+    if status != FK_OK:
+        raise FkError(status, lib().fk_last_error().decode())
+
+
+def _stream(stream: Optional[torch.cuda.Stream]) -> ctypes.c_void_p:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _points(X: torch.Tensor) -> fk_points:
+    if not X.is_cuda:
+        raise ValueError("points must be a CUDA tensor")
+    if X.dtype not in (torch.float32, torch.float64):
+        raise ValueError("points must be float32 or float64")
+    if X.dim() == 1:
+        n, d, sn, sd = X.shape[0], 1, X.stride(0), 1
+    elif X.dim() == 2:
+        n, d = X.shape
+        sn, sd = X.stride()
+    else:
+        raise ValueError("points must be (n,) or (n, d)")
+    return fk_points(X.data_ptr(), FK_F32 if X.dtype == torch.float32 else FK_F64, d, n, sn, sd)
+
+
+_ws_cache = {}
+
+
+def _workspace(nbytes: int, device) -> torch.Tensor:
+    key = (device.index if device.index is not None else torch.cuda.current_device())
+    buf = _ws_cache.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
+        _ws_cache[key] = buf
+    return buf
+
+
+def fk_workspace_bytes(entry: int, d: int, m: int, eps: float, dtype: int = FK_F32, n: int = 0, kind: int = 0) -> int:
+    nb = lib().fk_workspace_bytes(entry, d, m, eps, dtype, n, kind)
+    if nb == 0:
+        raise FkError(FK_E_ARG, lib().fk_last_error().decode())
+    return int(nb)
+
+
+def _dstatus(d_status, device):
+    if d_status is None:
+        d_status = torch.zeros(1, dtype=torch.int32, device=device)
+    return d_status
+
+
+def raise_on_status(d_status: torch.Tensor):
+    v = int(d_status.item())
+    if v & FK_E_RANGE:
+        raise FkError(FK_E_RANGE, "a coordinate outside [-L, L] (or NaN) was skipped")
+
+
+def fk_moments_type1(X: torch.Tensor, L: float, m: int, eps: float = 1e-6, mu_out: Optional[torch.Tensor] = None,
+                     accumulate: bool = False, d_status: Optional[torch.Tensor] = None, stream=None, check: bool = True) -> torch.Tensor:
+    """mu_q = sum_j exp(-i pi <q, X_j>/2L), |q|_inf <= 2m (complex128, shape (4m+1,)*d)."""
+    P = _points(X)
+    if mu_out is None:
+        mu_out = torch.zeros((4 * m + 1,) * P.d, dtype=torch.complex128, device=X.device)
+    nb = fk_workspace_bytes(FK_ENTRY_MOMENTS, P.d, m, eps, P.dtype, P.n)
+    ws = _workspace(nb, X.device)
+    ds = _dstatus(d_status, X.device)
+    _check(lib().fk_moments_type1(P, L, m, eps, mu_out.data_ptr(), FK_ACCUMULATE if accumulate else 0, ws.data_ptr(), ws.numel(),
+                                  ds.data_ptr(), _stream(stream)))
+    if check and d_status is None:
+        raise_on_status(ds)
+    return mu_out
+
+
+def fk_rhs_type1(X: torch.Tensor, Y: torch.Tensor, L: float, m: int, eps: float = 1e-6, r_out: Optional[torch.Tensor] = None,
+                 mu_out: Optional[torch.Tensor] = None, with_moments: bool = True, accumulate: bool = False,
+                 d_status: Optional[torch.Tensor] = None, stream=None, check: bool = True):
+    """(r, mu): r_k = sum_j Y_j exp(-i pi <k, X_j>/2L), |k| <= m, and (same pass) the moments."""
+    P = _points(X)
+    if Y.dtype != X.dtype or not Y.is_cuda or Y.dim() != 1 or Y.shape[0] != P.n or (P.n > 1 and Y.stride(0) != 1):
+        raise ValueError("Y must be a contiguous CUDA vector of X's dtype and length")
+    if r_out is None:
+        r_out = torch.zeros((2 * m + 1,) * P.d, dtype=torch.complex128, device=X.device)
+    if with_moments and mu_out is None:
+        mu_out = torch.zeros((4 * m + 1,) * P.d, dtype=torch.complex128, device=X.device)
+    entry = FK_ENTRY_RHS
+    nb = fk_workspace_bytes(entry, P.d, m, eps, P.dtype, P.n)
+    ws = _workspace(nb, X.device)
+    ds = _dstatus(d_status, X.device)
+    _check(lib().fk_rhs_type1(P, Y.data_ptr(), L, m, eps, r_out.data_ptr(), mu_out.data_ptr() if mu_out is not None else None,
+                              FK_ACCUMULATE if accumulate else 0, ws.data_ptr(), ws.numel(), ds.data_ptr(), _stream(stream)))
+    if check and d_status is None:
+        raise_on_status(ds)
+    return r_out, mu_out
+
+
+def fk_additive_cross_moments(X: torch.Tensor, L: float, m: int, eps: float = 1e-6, G_out: Optional[torch.Tensor] = None,
+                              accumulate: bool = False, d_status: Optional[torch.Tensor] = None, stream=None,
+                              check: bool = True) -> torch.Tensor:
+    """G[p, a, b] = sum_j exp(-i pi (a X_{j,l1} - b X_{j,l2})/2L) for pairs l1 < l2."""
+    P = _points(X)
+    npairs = P.d * (P.d - 1) // 2
+    if G_out is None:
+        G_out = torch.zeros((npairs, 2 * m + 1, 2 * m + 1), dtype=torch.complex128, device=X.device)
+    nb = fk_workspace_bytes(FK_ENTRY_CROSS, P.d, m, eps, P.dtype, P.n)
+    ws = _workspace(nb, X.device)
+    ds = _dstatus(d_status, X.device)
+    _check(lib().fk_additive_cross_moments(P, L, m, eps, G_out.data_ptr(), FK_ACCUMULATE if accumulate else 0, ws.data_ptr(),
+                                           ws.numel(), ds.data_ptr(), _stream(stream)))
+    if check and d_status is None:
+        raise_on_status(ds)
+    return G_out
+
+
+def fk_solve(mu: torch.Tensor, r: torch.Tensor, n_total: float, d: int, m: int, L: float, lam: float, kind: str = "sobolev",
+             s: float = 1.0, mu_pde: float = 0.0, alpha: Optional[Sequence] = None, a_alpha: Optional[Sequence[float]] = None,
+             box: Optional[Sequence] = None, cross: Optional[torch.Tensor] = None, theta_out: Optional[torch.Tensor] = None,
+             report: bool = True, stream=None):
+    """theta = A^{-1} r/n (dense fp64 Cholesky).  Returns (theta complex128, report dict or None)."""
+    k = KINDS[kind] if isinstance(kind, str) else int(kind)
+    D = d * (2 * m + 1) if k == FK_ADDITIVE else (2 * m + 1) ** d
+    if theta_out is None:
+        theta_out = torch.empty(D, dtype=torch.complex128, device=mu.device)
+    prob = fk_problem()
+    prob.d, prob.m, prob.kind = d, m, k
+    prob.n_total, prob.L, prob.s, prob.lam, prob.mu_pde = float(n_total), float(L), float(s), float(lam), float(mu_pde)
+    keep = []
+    if k == FK_PIK_BOX:
+        al = (ctypes.c_int32 * (len(alpha) * d))(*[int(v) for row in alpha for v in row])
+        aa = (ctypes.c_double * len(a_alpha))(*[float(v) for v in a_alpha])
+        bx = (ctypes.c_double * (2 * d))(*[float(v) for row in box for v in row])
+        keep += [al, aa, bx]
+        prob.n_terms = len(a_alpha)
+        prob.alpha = ctypes.cast(al, ctypes.POINTER(ctypes.c_int32))
+        prob.a_alpha = ctypes.cast(aa, ctypes.POINTER(ctypes.c_double))
+        prob.box = ctypes.cast(bx, ctypes.POINTER(ctypes.c_double))
+    mu = mu.contiguous()
+    r = r.contiguous()
+    prob.mu_moments = mu.data_ptr()
+    prob.rhs = r.data_ptr()
+    prob.cross = cross.contiguous().data_ptr() if cross is not None else None
+    nb = fk_workspace_bytes(FK_ENTRY_SOLVE, d, m, 1e-6, FK_F64, 0, k)
+    ws = _workspace(nb, mu.device)
+    rep = fk_solve_report()
+    _check(lib().fk_solve(ctypes.byref(prob), theta_out.data_ptr(), ctypes.byref(rep) if report else None, ws.data_ptr(), ws.numel(),
+                          _stream(stream)))
+    del keep
+    out = None
+    if report:
+        out = {"backward_err": rep.backward_err, "ms": rep.ms, "info": rep.info, "n_unknowns": rep.n_unknowns}
+    return theta_out, out
+
+
+def fk_predict_type2(theta: torch.Tensor, d: int, m: int, L: float, Xq: torch.Tensor, eps: float = 1e-6, additive: bool = False,
+                     out: Optional[torch.Tensor] = None, d_status: Optional[torch.Tensor] = None, stream=None,
+                     check: bool = True) -> torch.Tensor:
+    """f(x) = Re sum_k theta_k exp(+i pi <k, x>/2L) at the rows of Xq (additive: sum over features)."""
+    P = _points(Xq)
+    if out is None:
+        out = torch.empty(P.n, dtype=Xq.dtype, device=Xq.device)
+    nb = fk_workspace_bytes(FK_ENTRY_PREDICT, d, m, eps, P.dtype, P.n, 1 if additive else 0)
+    ws = _workspace(nb, Xq.device)
+    ds = _dstatus(d_status, Xq.device)
+    theta = theta.contiguous()
+    _check(lib().fk_predict_type2(theta.data_ptr(), d, m, L, 1 if additive else 0, P, eps, out.data_ptr(), ws.data_ptr(), ws.numel(),
+                                  ds.data_ptr(), _stream(stream)))
+    if check and d_status is None:
+        raise_on_status(ds)
+    return out
+
+
+def version() -> str:
+    return lib().fk_version().decode()

@@ -1,0 +1,225 @@
+"""GPU parity of the d = 1 type-1 pass, solve and predict (through the C ABI) against the oracle.
+
+Gates (BASELINE.json north_star; readings R7, R8):
+  moments / rhs relative l2 <= 1e-5 with fp32 spreading at eps = 1e-6, <= 1e-10 in fp64 mode;
+  theta and predictions <= 1e-4 relative (fp64 mode); fp32 mode: predictions <= 1e-4 and the
+  backward error of theta in the oracle's system <= 1e-5.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import datagen
+from gpu_util import dev, fk, gen_dataset, gen_equispaced, host, rel
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def F():
+    assert torch.cuda.is_available(), "GPU tests need CUDA"
+    return fk()
+
+
+def _run(F, X, Y, m, eps, dtype):
+    Xd = dev(X.reshape(-1), dtype)
+    Yd = dev(Y, dtype)
+    r, mu = F.fk_rhs_type1(Xd, Yd, 1.0, m, eps)
+    torch.cuda.synchronize()
+    return host(mu), host(r)
+
+
+@pytest.mark.parametrize("n,m,xkind", [(100_000, 50, "uniform"), (50_003, 1000, "uniform"), (40_001, 300, "gaussian"), (4_099, 7, "uniform")])
+def test_type1_fp32_matches_oracle(F, oracle, n, m, xkind):
+    X, Y = datagen.dataset(n, xkind=xkind, seed=11)
+    mu, r = _run(F, X, Y, m, 1e-6, torch.float32)
+    mu_o = oracle.moments(X, 1.0, m)
+    r_o = oracle.rhs(X, Y, 1.0, m)
+    e_mu, e_r = rel(mu, mu_o), rel(r, r_o)
+    print(f"fp32 n={n} m={m} {xkind}: mu {e_mu:.2e} r {e_r:.2e}")
+    assert e_mu <= 1e-5 and e_r <= 1e-5
+    assert mu[2 * m] == n  # mu_0 = n exactly (fixed-point partition of unity)
+
+
+@pytest.mark.parametrize("n,m", [(30_001, 50), (20_000, 1000)])
+def test_type1_fp64_matches_oracle(F, oracle, n, m):
+    X, Y = datagen.dataset(n, seed=12)
+    X = X.astype(np.float64) * (1 - 2.0 ** -30)  # genuinely fp64 coordinates
+    Y = Y.astype(np.float64) + 1e-9
+    mu, r = _run(F, X, Y, m, 1e-10, torch.float64)
+    e_mu, e_r = rel(mu, oracle.moments(X, 1.0, m)), rel(r, oracle.rhs(X, Y, 1.0, m))
+    print(f"fp64 n={n} m={m}: mu {e_mu:.2e} r {e_r:.2e}")
+    assert e_mu <= 1e-10 and e_r <= 1e-10
+
+
+def test_edge_cases(F, oracle):
+    m = 20
+    # n = 0: all zero
+    mu = F.fk_moments_type1(torch.zeros(0, device="cuda"), 1.0, m)
+    assert float(mu.abs().max()) == 0.0
+    # n = 1 at the origin: every moment is 1
+    mu = host(F.fk_moments_type1(torch.zeros(1, device="cuda"), 1.0, m))
+    assert np.max(np.abs(mu - 1.0)) < 1e-6
+    # all samples identical (coherent fixed-point rounding) and all samples at the box edges
+    for x in (0.123456789, 1.0, -1.0):
+        X = np.full(10_000, x, dtype=np.float32)
+        Y = np.linspace(-2, 3, 10_000).astype(np.float32)
+        mu, r = _run(F, X, Y, m, 1e-6, torch.float32)
+        assert rel(mu, oracle.moments(X, 1.0, m)) <= 1e-5
+        assert rel(r, oracle.rhs(X, Y, 1.0, m)) <= 1e-5
+    # general L (non power-of-two scale: compensated position) and unaligned / strided views
+    X, Y = datagen.dataset(20_001, seed=13, L=2.7)
+    Xd, Yd = dev(X.reshape(-1)), dev(Y)
+    r, mu = F.fk_rhs_type1(Xd[1:], Yd[1:], 2.7, 64, 1e-6)  # 4-byte misaligned start
+    assert rel(host(mu), oracle.moments(X[1:], 2.7, 64)) <= 1e-5
+    assert rel(host(r), oracle.rhs(X[1:], Y[1:], 2.7, 64)) <= 1e-5
+    X2 = dev(np.stack([X.reshape(-1), -X.reshape(-1)], 1))  # column 0 of a row-major (n, 2): stride 2
+    mu2 = F.fk_moments_type1(X2[:, :1], 2.7, 64)
+    assert rel(host(mu2), oracle.moments(X, 2.7, 64)) <= 1e-5
+
+
+def test_y_scale_extremes(F, oracle):
+    X, Y = datagen.dataset(30_000, seed=14)
+    for scale in (1e-12, 1e9):
+        Ys = (Y.astype(np.float64) * scale).astype(np.float32)
+        _, r = _run(F, X, Ys, 40, 1e-6, torch.float32)
+        assert rel(r, oracle.rhs(X, Ys, 1.0, 40)) <= 1e-5
+    # outliers 1000x the CTA's probe maximum take the exact slow path
+    Yo = Y.copy()
+    Yo[-50:] *= 1000.0
+    _, r = _run(F, X, Yo, 40, 1e-6, torch.float32)
+    assert rel(r, oracle.rhs(X, Yo, 1.0, 40)) <= 1e-5
+
+
+def test_shard_additivity_and_moments_only(F):
+    """fk(X) == fk(X[:a]) + fk(X[a:]) via FK_ACCUMULATE, and moments-only == fused."""
+    X, Y = datagen.dataset(100_000, seed=15)
+    Xd, Yd = dev(X.reshape(-1)), dev(Y)
+    r, mu = F.fk_rhs_type1(Xd, Yd, 1.0, 100, 1e-6)
+    r2, mu2 = F.fk_rhs_type1(Xd[:37_000], Yd[:37_000], 1.0, 100, 1e-6)
+    F.fk_rhs_type1(Xd[37_000:], Yd[37_000:], 1.0, 100, 1e-6, r_out=r2, mu_out=mu2, accumulate=True)
+    assert rel(host(mu2), host(mu)) < 1e-12 and rel(host(r2), host(r)) < 1e-7
+    mu3 = F.fk_moments_type1(Xd, 1.0, 100, 1e-6)
+    assert torch.equal(mu3, mu)  # identical fixed-point pass: bitwise equal
+
+
+def test_deterministic(F):
+    X, Y = datagen.dataset(200_000, seed=16)
+    Xd, Yd = dev(X.reshape(-1)), dev(Y)
+    a = F.fk_rhs_type1(Xd, Yd, 1.0, 500, 1e-6)
+    b = F.fk_rhs_type1(Xd, Yd, 1.0, 500, 1e-6)
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+
+
+def test_range_flag(F):
+    X = torch.tensor([0.1, 1.5, -0.2, float("nan")], device="cuda")
+    with pytest.raises(F.FkError):
+        F.fk_moments_type1(X, 1.0, 5)
+    ds = torch.zeros(1, dtype=torch.int32, device="cuda")
+    mu = F.fk_moments_type1(X, 1.0, 5, d_status=ds)
+    assert int(ds.item()) & F.FK_E_RANGE
+    assert abs(float(mu[10].real) - 2.0) < 1e-6  # the two valid samples only
+
+
+def test_argument_errors(F):
+    X = torch.zeros(10, device="cuda")
+    with pytest.raises(F.FkError, match="FK_E_EPS"):
+        F.fk_moments_type1(X, 1.0, 5, eps=1e-16)
+    with pytest.raises(F.FkError, match="FK_E_ARG"):
+        F.fk_moments_type1(X, -1.0, 5)
+    with pytest.raises(F.FkError, match="FK_E_ARG"):
+        F.fk_moments_type1(X, 1.0, 0)
+
+
+# ---------------------------------------------------------------------------------------------
+# solve + predict
+# ---------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("m,kind,s,lam", [(50, "sobolev", 2.0, 1e-4), (1000, "sobolev", 1.0, 1e10 ** (-2 / 3)), (60, "lowbias", 2.0, 1e-3)])
+def test_solve_matches_oracle(F, oracle, m, kind, s, lam):
+    """Same (oracle) moments into fk_solve and into numpy: theta within 1e-8 relative."""
+    X, Y = datagen.dataset(20_000, seed=17)
+    mu = oracle.moments(X, 1.0, m)
+    r = oracle.rhs(X, Y, 1.0, m)
+    th_o = oracle.solve(mu, r, 20_000, 1, m, lam, kind, s)
+    th, rep = F.fk_solve(dev(mu.reshape(-1)), dev(r.reshape(-1)), 20_000, 1, m, 1.0, lam, kind, s)
+    A = oracle.assemble(mu, 20_000, 1, m, lam, kind, s)
+    print(f"solve m={m} {kind}: rel {rel(host(th), th_o):.2e} backward {rep['backward_err']:.2e} cond {np.linalg.cond(A):.1e} ms {rep['ms']:.2f}")
+    assert rep["info"] == 0
+    assert rep["backward_err"] < 1e-12
+    assert oracle.backward_error(A, host(th), r.reshape(-1) / 20_000) < 1e-12
+    assert rel(host(th), th_o) < 1e-6
+
+
+@pytest.mark.parametrize("m,eps", [(50, 1e-6), (1000, 1e-6), (50, 1e-10), (700, 1e-11)])
+def test_predict_matches_oracle(F, oracle, m, eps):
+    rng = np.random.default_rng(3)
+    k = np.arange(-m, m + 1)
+    th = (rng.normal(size=2 * m + 1) + 1j * rng.normal(size=2 * m + 1)) / (1.0 + np.abs(k)) ** 2
+    Xq = datagen.dataset(20_001, seed=18)[0]
+    dt = torch.float32 if eps >= 1e-7 else torch.float64
+    out = host(F.fk_predict_type2(dev(th), 1, m, 1.0, dev(Xq.reshape(-1), dt), eps))
+    ref = oracle.predict(th, Xq, 1.0, m)
+    err = rel(out, ref)
+    print(f"predict m={m} eps={eps}: {err:.2e}")
+    assert err <= (1e-5 if eps >= 1e-7 else 1e-10)
+
+
+@pytest.mark.parametrize("mode", ["fp32", "fp64"])
+def test_fit_end_to_end(F, oracle, mode):
+    """Whole GPU fit (moments + rhs + solve) then predict vs the oracle fit (config C1 shape)."""
+    n, m, s, lam = 100_000, 50, 2.0, 1e-4
+    X, Y = datagen.dataset(n, seed=19)
+    Xq = datagen.dataset(10_000, seed=20)[0]
+    th_o, mu_o, r_o = oracle.fit(X, Y, 1.0, m, lam, "sobolev", s)
+    f_o = oracle.predict(th_o, Xq, 1.0, m)
+    dt = torch.float32 if mode == "fp32" else torch.float64
+    eps = 1e-6 if mode == "fp32" else 1e-10
+    r, mu = F.fk_rhs_type1(dev(X.reshape(-1), dt), dev(Y, dt), 1.0, m, eps)
+    th, rep = F.fk_solve(mu.reshape(-1), r.reshape(-1), n, 1, m, 1.0, lam, "sobolev", s)
+    f = host(F.fk_predict_type2(th, 1, m, 1.0, dev(Xq.reshape(-1), dt), eps))
+    A = oracle.assemble(mu_o, n, 1, m, lam, "sobolev", s)
+    bw = oracle.backward_error(A, host(th), r_o.reshape(-1) / n)
+    print(f"fit {mode}: theta {rel(host(th), th_o):.2e} pred {rel(f, f_o):.2e} backward {bw:.2e}")
+    assert rel(f, f_o) <= 1e-4
+    if mode == "fp64":
+        assert rel(host(th), th_o) <= 1e-4
+    else:
+        assert bw <= 1e-5
+
+
+# ---------------------------------------------------------------------------------------------
+# full size (BASELINE C2, n ~ 1e10) in the bench's launch configuration: closed-form pin P1/P2
+# ---------------------------------------------------------------------------------------------
+def test_full_size_equispaced_closed_form(F):
+    N = 1 << 24
+    reps = 596
+    n = reps * N  # 9,999,220,736
+    m = 1000
+    free, _ = torch.cuda.mem_get_info()
+    if free < n * 8 + (4 << 30):
+        pytest.skip("needs ~84 GB of free device memory")
+    X = torch.empty(n, dtype=torch.float32, device="cuda")
+    Y = torch.empty(n, dtype=torch.float32, device="cuda")
+    gen_equispaced(X, Y, n, 0, n, 1000003, 12345)
+    r, mu = F.fk_rhs_type1(X, Y, 1.0, m, 1e-6)
+    torch.cuda.synchronize()
+    del X, Y
+    mu, r = host(mu), host(r)
+    q = np.arange(-2 * m, 2 * m + 1)
+    mu_c = np.zeros(q.shape, np.complex128)
+    odd = np.abs(q) % 2 == 1
+    mu_c[odd] = reps * (-1.0) ** ((np.abs(q[odd]) - 1) // 2) / np.sin(np.abs(q[odd]) * np.pi / (2 * N))
+    mu_c[q == 0] = n
+    k = np.arange(-m, m + 1).astype(np.float64)
+    r_c = np.zeros(k.shape, np.complex128)
+    ko = np.abs(k) % 2 == 1
+    kk = k[ko]
+    r_c[ko] = reps * np.exp(1j * kk * np.pi / 2) * np.exp(-1j * kk * np.pi / (2 * N)) * 2.0 / (1 - np.exp(-2j * np.pi * kk / N))
+    r_c[k == 0] = n / 2
+    e_mu, e_r = rel(mu, mu_c), rel(r, r_c)
+    print(f"full size n={n}: mu {e_mu:.2e} r {e_r:.2e}")
+    assert mu[2 * m] == n and r[m] == n / 2  # exact totals
+    assert e_mu <= 1e-5 and e_r <= 1e-5
