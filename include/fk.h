@@ -149,6 +149,14 @@ const char* fk_last_error(void);
 /* Library version string. */
 const char* fk_version(void);
 
+/* Diagnostics (not part of the method; used by bench.py for the roofline line):
+ * fk_profile_enable(1) brackets every spreading-kernel launch with CUDA events recorded on the
+ * launching stream; fk_profile_read() waits for the recorded events, returns the summed
+ * spreading-kernel device time (ms) and launch count since the last read, and the number of
+ * kernels libfk itself launched (cuFFT / cuSOLVER internals excluded), then resets all three. */
+void fk_profile_enable(int on);
+int fk_profile_read(double* spread_ms, int64_t* spread_launches, int64_t* kernel_launches);
+
 #ifdef __cplusplus
 }
 #endif

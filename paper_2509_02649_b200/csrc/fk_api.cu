@@ -6,6 +6,8 @@
 
 namespace fk {
 const char* last_error_cstr();
+int profile_read(double* ms, int64_t* launches, int64_t* kernels);
+void profile_enable(int on);
 }
 
 using namespace fk;
@@ -52,6 +54,12 @@ extern "C" {
 const char* fk_last_error(void) { return last_error_cstr(); }
 
 const char* fk_version(void) { return "fk 0.1 (sm_100a)"; }
+
+void fk_profile_enable(int on) { profile_enable(on); }
+
+int fk_profile_read(double* spread_ms, int64_t* spread_launches, int64_t* kernel_launches) {
+  return profile_read(spread_ms, spread_launches, kernel_launches);
+}
 
 fk_status fk_moments_type1(fk_points X, double L, int m, double eps, double* mu_out, int flags, void* ws, size_t ws_bytes,
                            int* d_status, fk_stream_t stream) {

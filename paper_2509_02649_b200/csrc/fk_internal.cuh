@@ -35,6 +35,11 @@ fk_status fail(fk_status st, const std::string& msg);
 
 int device_sm_count();
 
+// diagnostics: kernel-launch counter and spreading-kernel event brackets (fk_profile_*)
+void count_launch(int k = 1);
+void prof_spread_begin(cudaStream_t s);
+void prof_spread_end(cudaStream_t s);
+
 // ------------------------------------------------------------------------------------------
 // workspace: a bump allocator over the caller's buffer (256-byte aligned slices)
 // ------------------------------------------------------------------------------------------

@@ -1,5 +1,6 @@
 // plan.cu -- errors, plans (window / precision / fine-grid geometry), cuFFT plan cache,
 // and the ES window transform table.
+#include <atomic>
 #include <cmath>
 #include <map>
 #include <mutex>
@@ -18,6 +19,50 @@ fk_status fail(fk_status st, const std::string& msg) {
   return st;
 }
 const char* last_error_cstr() { return g_last_error.c_str(); }
+
+static std::atomic<int64_t> g_kernels{0};
+static std::atomic<bool> g_prof_on{false};
+static std::mutex g_prof_mu;
+static std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_prof_ev;
+static thread_local cudaEvent_t g_prof_open = nullptr;
+
+void count_launch(int k) { g_kernels.fetch_add(k, std::memory_order_relaxed); }
+
+void prof_spread_begin(cudaStream_t s) {
+  if (!g_prof_on.load()) return;
+  cudaEventCreate(&g_prof_open);
+  cudaEventRecord(g_prof_open, s);
+}
+
+void prof_spread_end(cudaStream_t s) {
+  if (!g_prof_on.load() || !g_prof_open) return;
+  cudaEvent_t e1;
+  cudaEventCreate(&e1);
+  cudaEventRecord(e1, s);
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof_ev.emplace_back(g_prof_open, e1);
+  g_prof_open = nullptr;
+}
+
+int profile_read(double* ms, int64_t* launches, int64_t* kernels) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  double tot = 0.0;
+  for (auto& pr : g_prof_ev) {
+    cudaEventSynchronize(pr.second);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, pr.first, pr.second);
+    tot += t;
+    cudaEventDestroy(pr.first);
+    cudaEventDestroy(pr.second);
+  }
+  if (ms) *ms = tot;
+  if (launches) *launches = (int64_t)g_prof_ev.size();
+  if (kernels) *kernels = g_kernels.exchange(0);
+  g_prof_ev.clear();
+  return 0;
+}
+
+void profile_enable(int on) { g_prof_on.store(on != 0); }
 
 int device_sm_count() {
   int dev = 0, sms = 0;
@@ -145,6 +190,7 @@ fk_status es_phihat_table(const EsParams& es, int nf, int K, double* d_tab, cuda
   static std::once_flag once;
   std::call_once(once, [] { gauss_legendre01(96, gl.x, gl.w); });
   k_es_phihat<<<(K + 1 + 127) / 128, 128, 0, s>>>(gl, es.w, es.beta, nf, K, d_tab);
+  count_launch();
   FK_CUDA_TRY(cudaGetLastError());
   return FK_OK;
 }

@@ -210,6 +210,7 @@ static fk_status gather(const PredPlan& p, const fk_points& Xq, double L, const 
                                         p.es.w, p.es.beta, p.in_smem ? 1 : 0, (XT*)out, d_status);
   }
   FK_CUDA_TRY(cudaGetLastError());
+  count_launch();
   return FK_OK;
 }
 
@@ -236,6 +237,7 @@ fk_status predict_run(const double* theta, int d, int m, double L, int additive,
   const int64_t tot = (int64_t)p.nfeat * (p.nf / 2 + 1);
   k_pred_prep<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>((const double2*)theta, p.nfeat, m, p.nf, p.ker, w.tab, w.H);
   FK_CUDA_TRY(cudaGetLastError());
+  count_launch();
   FftPlan fp;
   FK_TRY(fft_plan(1, &p.nf, p.nfeat, CUFFT_Z2D, &fp));
   FK_TRY(fft_exec_z2d(fp, (cufftDoubleComplex*)w.H, w.grid, w.work, s));

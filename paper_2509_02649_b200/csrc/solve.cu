@@ -257,6 +257,7 @@ fk_status solve_run(const fk_problem* P, double* theta, fk_solve_report* rep, vo
   k_assemble<<<sms * 8, 256, 0, s>>>(g, A);
   k_scale_copy<<<(D + 255) / 256, 256, 0, s>>>((const double2*)P->rhs, g.inv_n, D, (double2*)theta);
   FK_CUDA_TRY(cudaGetLastError());
+  count_launch(2);
   {
     std::lock_guard<std::mutex> lk(g_sol_mu);
     cusolverDnHandle_t h;
@@ -273,6 +274,7 @@ fk_status solve_run(const fk_problem* P, double* theta, fk_solve_report* rep, vo
     cudaEventRecord(e1, s);
     FK_CUDA_TRY(cudaMemsetAsync(res, 0, 16, s));
     k_residual<<<(D * 32 + 255) / 256, 256, 0, s>>>(g, (const double2*)theta, (const double2*)P->rhs, res);
+    count_launch();
     int hinfo = 0;
     double hres[2] = {0, 0};
     FK_CUDA_TRY(cudaMemcpyAsync(&hinfo, info, 4, cudaMemcpyDeviceToHost, s));

@@ -373,7 +373,10 @@ template <typename XT, bool MU, bool R>
 static void launch_bs3(const Plan1& p, const XT* X, const XT* Y, const Bs3Args& a, bool vec, bool exact, cudaStream_t s) {
   auto run = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
+    prof_spread_begin(s);
     kern<<<p.ctas, p.threads, p.smem_bytes, s>>>(X, Y, a);
+    prof_spread_end(s);
+    count_launch();
   };
   if (sizeof(XT) == 8) {
     run(k_spread1d_bs3<XT, MU, R, false, false>);
@@ -391,10 +394,15 @@ static void launch_es(const Plan1& p, const XT* X, const XT* Y, const EsArgs& a,
   if (p.smem) {
     auto k = k_spread1d_es<XT, MU, R, true>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
+    prof_spread_begin(s);
     k<<<p.ctas, p.threads, p.smem_bytes, s>>>(X, Y, a);
+    prof_spread_end(s);
   } else {
+    prof_spread_begin(s);
     k_spread1d_es<XT, MU, R, false><<<p.ctas, p.threads, 0, s>>>(X, Y, a);
+    prof_spread_end(s);
   }
+  count_launch();
 }
 
 template <typename XT>
@@ -499,6 +507,7 @@ fk_status type1_run(const Plan1& p, const fk_points& X, const void* Y, double L,
     else
       k_reduce_f64<<<(p.nf_mu + TB - 1) / TB, TB, 0, s>>>((const double*)w.partA, nparts, p.gA.G, p.gA.off, p.nf_mu, w.fineA);
     FK_CUDA_TRY(cudaGetLastError());
+    count_launch();
     FftPlan pa;
     FK_TRY(fft_plan(1, &p.nf_mu, 1, CUFFT_D2Z, &pa));
     FK_TRY(fft_exec_d2z(pa, w.fineA, (cufftDoubleComplex*)w.specA, w.fftwork, s));
@@ -506,6 +515,7 @@ fk_status type1_run(const Plan1& p, const fk_points& X, const void* Y, double L,
     k_deconv1d<<<(4 * p.m + 1 + TB - 1) / TB, TB, 0, s>>>(w.specA, p.nf_mu, 2 * p.m, p.ker, w.tabA, (double2*)out.mu,
                                                           out.accumulate ? 1 : 0);
     FK_CUDA_TRY(cudaGetLastError());
+    count_launch();
   }
   if (r) {
     if (!p.fp64)
@@ -514,6 +524,7 @@ fk_status type1_run(const Plan1& p, const fk_points& X, const void* Y, double L,
     else
       k_reduce_f64<<<(p.nf_r + TB - 1) / TB, TB, 0, s>>>((const double*)w.partB, nparts, p.gB.G, p.gB.off, p.nf_r, w.fineB);
     FK_CUDA_TRY(cudaGetLastError());
+    count_launch();
     FftPlan pb;
     FK_TRY(fft_plan(1, &p.nf_r, 1, CUFFT_D2Z, &pb));
     FK_TRY(fft_exec_d2z(pb, w.fineB, (cufftDoubleComplex*)w.specB, w.fftwork, s));
@@ -521,6 +532,7 @@ fk_status type1_run(const Plan1& p, const fk_points& X, const void* Y, double L,
     k_deconv1d<<<(2 * p.m + 1 + TB - 1) / TB, TB, 0, s>>>(w.specB, p.nf_r, p.m, p.ker, w.tabB, (double2*)out.r,
                                                           out.accumulate ? 1 : 0);
     FK_CUDA_TRY(cudaGetLastError());
+    count_launch();
   }
   return FK_OK;
 }

@@ -1,0 +1,118 @@
+"""High-level fit / predict built on the C ABI (plumbing only: streams, copies, process groups).
+
+  fit(X, Y, ...)              one GPU: fk_rhs_type1 (moments + rhs in one pass) -> fk_solve
+  fit_distributed(...)        one process per GPU: each rank passes its sample shard, the small
+                              unnormalised [mu | r] vector is all-reduced (sum) over NCCL, rank 0
+                              solves and broadcasts theta (shard additivity R5)
+  fit_host(X_host, Y_host)    host (pinned) inputs streamed to the device in chunks on a copy
+                              stream, overlapped with the spreading of the previous chunk; the
+                              per-chunk outputs accumulate (FK_ACCUMULATE)
+All arithmetic of the method runs in libfk; this module only moves memory and calls it.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+
+from . import fk
+
+
+@dataclass
+class FitResult:
+    theta: torch.Tensor        # complex128, (2m+1)^d
+    mu: torch.Tensor           # complex128 moments, (4m+1,)*d (unnormalised, all shards)
+    r: torch.Tensor            # complex128 rhs, (2m+1,)*d
+    n_total: int
+    report: Optional[dict] = None
+
+
+def _moment_buffers(d: int, m: int, device):
+    nmu, nr = (4 * m + 1) ** d, (2 * m + 1) ** d
+    buf = torch.zeros(nmu + nr, dtype=torch.complex128, device=device)
+    return buf, buf[:nmu].view((4 * m + 1,) * d), buf[nmu:].view((2 * m + 1,) * d)
+
+
+def fit(X: torch.Tensor, Y: torch.Tensor, L: float, m: int, lam: float, kind: str = "sobolev", s: float = 1.0,
+        eps: float = 1e-6, report: bool = False, **pi) -> FitResult:
+    d = 1 if X.dim() == 1 else X.shape[1]
+    _, mu, r = _moment_buffers(d, m, X.device)
+    fk.fk_rhs_type1(X, Y, L, m, eps, r_out=r, mu_out=mu, check=False)
+    theta, rep = fk.fk_solve(mu.reshape(-1), r.reshape(-1), X.shape[0], d, m, L, lam, kind, s, report=report, **pi)
+    return FitResult(theta, mu, r, X.shape[0], rep)
+
+
+def fit_distributed(X_shard: torch.Tensor, Y_shard: torch.Tensor, n_total: int, L: float, m: int, lam: float,
+                    kind: str = "sobolev", s: float = 1.0, eps: float = 1e-6, group=None, buffers=None, theta_out=None,
+                    report: bool = False) -> FitResult:
+    """Data-parallel fit: call on every rank with that rank's shard (one process per GPU)."""
+    import torch.distributed as dist
+
+    d = 1 if X_shard.dim() == 1 else X_shard.shape[1]
+    buf, mu, r = buffers if buffers is not None else _moment_buffers(d, m, X_shard.device)
+    fk.fk_rhs_type1(X_shard, Y_shard, L, m, eps, r_out=r, mu_out=mu, check=False)
+    ws = dist.get_world_size(group) if dist.is_initialized() else 1
+    if ws > 1:
+        dist.all_reduce(torch.view_as_real(buf), op=dist.ReduceOp.SUM, group=group)
+    D = (2 * m + 1) ** d
+    if theta_out is None:
+        theta_out = torch.empty(D, dtype=torch.complex128, device=X_shard.device)
+    rep = None
+    if ws == 1 or dist.get_rank(group) == 0:
+        _, rep = fk.fk_solve(mu.reshape(-1), r.reshape(-1), n_total, d, m, L, lam, kind, s, theta_out=theta_out, report=report)
+    if ws > 1:
+        dist.broadcast(torch.view_as_real(theta_out), src=0, group=group)
+    return FitResult(theta_out, mu, r, n_total, rep)
+
+
+class HostStreamer:
+    """Streams pinned host (X, Y) to the device in fixed-size chunks, double-buffered on a copy
+    stream, and runs the one-pass moments + rhs on each chunk as it lands."""
+
+    def __init__(self, chunk: int, d: int, dtype, device):
+        self.chunk = chunk
+        self.dev = device
+        shape = (chunk,) if d == 1 else (chunk, d)
+        self.xb = [torch.empty(shape, dtype=dtype, device=device) for _ in range(2)]
+        self.yb = [torch.empty(chunk, dtype=dtype, device=device) for _ in range(2)]
+        self.copy_stream = torch.cuda.Stream(device)
+        self.copied = [torch.cuda.Event() for _ in range(2)]
+        self.consumed = [torch.cuda.Event() for _ in range(2)]
+
+    def moments(self, Xh: torch.Tensor, Yh: torch.Tensor, L: float, m: int, eps: float, mu, r):
+        n = Xh.shape[0]
+        comp = torch.cuda.current_stream(self.dev)
+        nchunks = (n + self.chunk - 1) // self.chunk
+        for i in range(nchunks):
+            b = i & 1
+            lo, hi = i * self.chunk, min(n, (i + 1) * self.chunk)
+            with torch.cuda.stream(self.copy_stream):
+                if i >= 2:
+                    self.copy_stream.wait_event(self.consumed[b])
+                self.xb[b][: hi - lo].copy_(Xh[lo:hi], non_blocking=True)
+                self.yb[b][: hi - lo].copy_(Yh[lo:hi], non_blocking=True)
+                self.copied[b].record(self.copy_stream)
+            comp.wait_event(self.copied[b])
+            fk.fk_rhs_type1(self.xb[b][: hi - lo], self.yb[b][: hi - lo], L, m, eps, r_out=r, mu_out=mu, accumulate=i > 0,
+                            check=False)
+            self.consumed[b].record(comp)
+        if nchunks == 0:
+            mu.zero_()
+            r.zero_()
+
+
+def fit_host(Xh: torch.Tensor, Yh: torch.Tensor, L: float, m: int, lam: float, kind: str = "sobolev", s: float = 1.0,
+             eps: float = 1e-6, chunk: int = 1 << 26, streamer: Optional[HostStreamer] = None, device=None):
+    """Fit from host (ideally pinned) buffers; returns theta on the HOST (complex128 numpy array)."""
+    device = device or torch.device("cuda", torch.cuda.current_device())
+    d = 1 if Xh.dim() == 1 else Xh.shape[1]
+    st = streamer or HostStreamer(min(chunk, max(1, Xh.shape[0])), d, Xh.dtype, device)
+    _, mu, r = _moment_buffers(d, m, device)
+    st.moments(Xh, Yh, L, m, eps, mu, r)
+    theta, _ = fk.fk_solve(mu.reshape(-1), r.reshape(-1), Xh.shape[0], d, m, L, lam, kind, s, report=False)
+    return theta.cpu().numpy()
+
+
+def predict(theta: torch.Tensor, d: int, m: int, L: float, Xq: torch.Tensor, eps: float = 1e-6, additive: bool = False):
+    return fk.fk_predict_type2(theta, d, m, L, Xq, eps, additive=additive)

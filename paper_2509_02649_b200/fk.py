@@ -113,10 +113,9 @@ def _workspace(nbytes: int, device) -> torch.Tensor:
 
 
 def fk_workspace_bytes(entry: int, d: int, m: int, eps: float, dtype: int = FK_F32, n: int = 0, kind: int = 0) -> int:
-    nb = lib().fk_workspace_bytes(entry, d, m, eps, dtype, n, kind)
-    if nb == 0:
-        raise FkError(FK_E_ARG, lib().fk_last_error().decode())
-    return int(nb)
+    """Workspace bytes for a call; 0 when the arguments are invalid (the call itself then returns
+    the precise status, so callers pass a minimal buffer and let the entry point report it)."""
+    return int(lib().fk_workspace_bytes(entry, d, m, eps, dtype, n, kind))
 
 
 def _dstatus(d_status, device):
@@ -246,3 +245,17 @@ def fk_predict_type2(theta: torch.Tensor, d: int, m: int, L: float, Xq: torch.Te
 
 def version() -> str:
     return lib().fk_version().decode()
+
+
+def profile_enable(on: bool = True):
+    """Bracket every spreading-kernel launch with CUDA events on its stream (diagnostics)."""
+    lib().fk_profile_enable(1 if on else 0)
+
+
+def profile_read():
+    """(spread_ms_total, spread_launches, kernel_launches) since the last read; resets them."""
+    ms = ctypes.c_double(0.0)
+    nl = ctypes.c_int64(0)
+    nk = ctypes.c_int64(0)
+    lib().fk_profile_read(ctypes.byref(ms), ctypes.byref(nl), ctypes.byref(nk))
+    return ms.value, nl.value, nk.value
