@@ -43,6 +43,29 @@ def fit(X: torch.Tensor, Y: torch.Tensor, L: float, m: int, lam: float, kind: st
     return FitResult(theta, mu, r, X.shape[0], rep)
 
 
+def _world(group=None) -> int:
+    import torch.distributed as dist
+
+    return dist.get_world_size(group) if dist.is_initialized() else 1
+
+
+def reduce_moments(buf: torch.Tensor, group=None) -> None:
+    """Sum the ranks' unnormalised [mu | r (| G)] complex128 buffers in place (one all-reduce;
+    exact by shard additivity, R5).  No-op on one rank."""
+    import torch.distributed as dist
+
+    if _world(group) > 1:
+        dist.all_reduce(torch.view_as_real(buf), op=dist.ReduceOp.SUM, group=group)
+
+
+def broadcast_theta(theta: torch.Tensor, group=None, src: int = 0) -> None:
+    """Send rank src's solution to every rank (for sharded prediction).  No-op on one rank."""
+    import torch.distributed as dist
+
+    if _world(group) > 1:
+        dist.broadcast(torch.view_as_real(theta), src=src, group=group)
+
+
 def fit_distributed(X_shard: torch.Tensor, Y_shard: torch.Tensor, n_total: int, L: float, m: int, lam: float,
                     kind: str = "sobolev", s: float = 1.0, eps: float = 1e-6, group=None, buffers=None, theta_out=None,
                     report: bool = False) -> FitResult:
@@ -52,17 +75,14 @@ def fit_distributed(X_shard: torch.Tensor, Y_shard: torch.Tensor, n_total: int, 
     d = 1 if X_shard.dim() == 1 else X_shard.shape[1]
     buf, mu, r = buffers if buffers is not None else _moment_buffers(d, m, X_shard.device)
     fk.fk_rhs_type1(X_shard, Y_shard, L, m, eps, r_out=r, mu_out=mu, check=False)
-    ws = dist.get_world_size(group) if dist.is_initialized() else 1
-    if ws > 1:
-        dist.all_reduce(torch.view_as_real(buf), op=dist.ReduceOp.SUM, group=group)
+    reduce_moments(buf, group)
     D = (2 * m + 1) ** d
     if theta_out is None:
         theta_out = torch.empty(D, dtype=torch.complex128, device=X_shard.device)
     rep = None
-    if ws == 1 or dist.get_rank(group) == 0:
+    if _world(group) == 1 or dist.get_rank(group) == 0:
         _, rep = fk.fk_solve(mu.reshape(-1), r.reshape(-1), n_total, d, m, L, lam, kind, s, theta_out=theta_out, report=report)
-    if ws > 1:
-        dist.broadcast(torch.view_as_real(theta_out), src=0, group=group)
+    broadcast_theta(theta_out, group)
     return FitResult(theta_out, mu, r, n_total, rep)
 
 

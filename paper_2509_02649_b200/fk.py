@@ -259,3 +259,15 @@ def profile_read():
     nk = ctypes.c_int64(0)
     lib().fk_profile_read(ctypes.byref(ms), ctypes.byref(nl), ctypes.byref(nk))
     return ms.value, nl.value, nk.value
+
+
+fk_profile_enable = profile_enable
+fk_profile_read = profile_read
+
+
+def fk_version() -> str:
+    return version()
+
+
+def fk_last_error() -> str:
+    return lib().fk_last_error().decode()
