@@ -38,9 +38,10 @@ fk_status type1_entry(const fk_points& X, const void* Y, double L, int m, double
                       void* ws, size_t ws_bytes, int* d_status, cudaStream_t s, const char* who) {
   set_error("");
   FK_TRY(check_common(L, m, eps, who));
-  FK_TRY(check_points(X, 1, 1, who));
+  FK_TRY(check_points(X, 1, 2, who));
   if (!r_out && !mu_out) return fail(FK_E_ARG, std::string(who) + ": no output requested");
   if (r_out && X.n > 0 && Y == nullptr) return fail(FK_E_ARG, std::string(who) + ": Y is null");
+  if (X.d == 2) return type1_2d_run(m, eps, X, Y, L, mu_out, r_out, (flags & FK_ACCUMULATE) != 0, ws, ws_bytes, d_status, s);
   Plan1 p;
   FK_TRY(make_plan1(X.d, m, eps, mu_out != nullptr, r_out != nullptr, &p));
   Type1Out out{mu_out, r_out, (flags & FK_ACCUMULATE) != 0};
@@ -119,7 +120,6 @@ fk_status fk_predict_type2(const double* theta, int d, int m, double L, int addi
 
 size_t fk_workspace_bytes(int entry, int d, int m, double eps, int dtype, int64_t n, int kind) {
   set_error("");
-  (void)dtype;
   if (m < 1 || d < 1 || !(eps >= 1e-14 && eps <= 1e-1)) {
     set_error("fk_workspace_bytes: bad arguments");
     return 0;
@@ -127,13 +127,14 @@ size_t fk_workspace_bytes(int entry, int d, int m, double eps, int dtype, int64_
   switch (entry) {
     case FK_ENTRY_MOMENTS:
     case FK_ENTRY_RHS: {
+      if (d == 2) return type1_2d_ws_bytes(m, eps, true, entry == FK_ENTRY_RHS, dtype);
       Plan1 p;
       const bool mu = true, r = entry == FK_ENTRY_RHS;
       if (make_plan1(d, m, eps, mu, r, &p) != FK_OK) return 0;
       return type1_ws_bytes(p, mu, r);
     }
     case FK_ENTRY_CROSS:
-      return cross_ws_bytes(d, m, eps, n);
+      return cross_ws_bytes(d, m, eps, n, dtype);
     case FK_ENTRY_SOLVE:
       return solve_ws_bytes(d, m, kind);
     case FK_ENTRY_PREDICT:

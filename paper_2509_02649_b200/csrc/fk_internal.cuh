@@ -126,7 +126,10 @@ size_t predict_ws_bytes(int d, int m, double eps, int additive);
 fk_status predict_run(const double* theta, int d, int m, double L, int additive, const fk_points& Xq, double eps, void* out,
                       void* ws, size_t ws_bytes, int* d_status, cudaStream_t s);
 
-size_t cross_ws_bytes(int d, int m, double eps, int64_t n);
+size_t cross_ws_bytes(int d, int m, double eps, int64_t n, int dtype);
+size_t type1_2d_ws_bytes(int m, double eps, bool mu, bool r, int dtype);
+fk_status type1_2d_run(int m, double eps, const fk_points& X, const void* Y, double L, double* mu_out, double* r_out, bool acc, void* ws,
+                       size_t ws_bytes, int* d_status, cudaStream_t s);
 fk_status cross_run(const fk_points& X, double L, int m, double eps, double* G, bool accumulate, void* ws, size_t ws_bytes,
                     int* d_status, cudaStream_t s);
 

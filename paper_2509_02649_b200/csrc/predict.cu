@@ -34,12 +34,21 @@ static fk_status make_pred_plan(int d, int m, double eps, int additive, PredPlan
   q.m = m;
   q.additive = additive != 0;
   q.nfeat = q.additive ? d : 1;
-  if (!q.additive && d != 1) return fail(FK_E_UNSUPPORTED, "fk_predict_type2: d = 1 or additive in this build");
+  if (!q.additive && d > 2) return fail(FK_E_UNSUPPORTED, "fk_predict_type2: d <= 2 (or additive) in this build");
   q.fp64 = eps < 1e-7;
   int smem_cap = 0, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&smem_cap, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  if (!q.fp64) {
+  if (!q.additive && d == 2) {  // 2-D: ES window on a sigma = 2 grid (the B-spline grid would be ~8x larger per dim)
+    q.ker = KER_ES;
+    int w = (int)std::ceil(std::log10(1.0 / eps)) + (q.fp64 ? 2 : 1);
+    w = std::min(16, std::max(4, w));
+    q.es.w = w;
+    q.es.beta = 2.30 * w;
+    q.nf = fft_friendly(2 * (2 * m + 1));
+    q.g = {q.nf, q.nf / 4 - w / 2 - 2, q.nf / 2 + w + 4};
+    q.smem = (size_t)q.g.G * q.g.G * (q.fp64 ? 8 : 4);
+  } else if (!q.fp64) {
     q.ker = KER_BS3;
     q.nf = fft_friendly((int)std::ceil(bs3_sigma_p(eps) * (2 * m + 1)));
     q.g = {q.nf, q.nf / 4 - 1, q.nf / 2 + 4};
@@ -172,6 +181,89 @@ __global__ void __launch_bounds__(512) k_gather_es(const XT* __restrict__ Xq, in
   if (bad && d_status) atomicOr(d_status, (int)FK_E_RANGE);
 }
 
+// ---- d = 2: H[k0 mod nf][k1], 0 <= k1 <= nf/2, from the Hermitian part of theta ----
+__global__ void k_pred_prep2d(const double2* __restrict__ theta, int m, int nf, const double* __restrict__ tab,
+                              double2* __restrict__ H) {
+  const int half = nf / 2 + 1;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)nf * half) return;
+  const int row = (int)(t / half), k1 = (int)(t % half);
+  const int k0 = row <= nf / 2 ? row : row - nf;
+  double2 h = make_double2(0.0, 0.0);
+  if (k1 <= m && k0 >= -m && k0 <= m) {
+    const int side = 2 * m + 1;
+    const double2 a = theta[(int64_t)(k0 + m) * side + (k1 + m)];
+    const double2 b = theta[(int64_t)(-k0 + m) * side + (-k1 + m)];
+    const double sc = 0.5 * (((k0 + k1) & 1) ? -1.0 : 1.0) / (tab[k0 < 0 ? -k0 : k0] * tab[k1]);
+    h = make_double2((a.x + b.x) * sc, (a.y - b.y) * sc);
+  }
+  H[t] = h;
+}
+
+// one coordinate on an ES grid: first tap (local index) and the offset f of the point
+__device__ __forceinline__ void es_place(double x, double a, int K, int w, int& l0, double& f) {
+  const double p = x * a;
+  const double P = floor(p);
+  f = p - P;
+  const int d0 = (w & 1) ? (f > 0.5 ? 1 : 0) - (w >> 1) : (f > 0.0 ? 1 : 0) - (w >> 1);
+  l0 = (fabs(p) < 1e8) ? (int)P + K + d0 : -1000000;
+  f = f - d0;  // tap i sits at offset (i - f) cells
+}
+
+template <typename XT, typename GT>
+__global__ void __launch_bounds__(256) k_gather2d(const XT* __restrict__ Xq, int64_t n, int64_t sn, int64_t sd,
+                                                 const double* __restrict__ grid, int nf, int off, int G, int K, double a, int w,
+                                                 double beta, int in_smem, XT* __restrict__ out, int* __restrict__ d_status) {
+  extern __shared__ unsigned char sgraw[];
+  GT* sg = reinterpret_cast<GT*>(sgraw);
+  if (in_smem) {
+    for (int64_t i = threadIdx.x; i < (int64_t)G * G; i += blockDim.x) {
+      const int r = (int)(i / G), c = (int)(i % G);
+      sg[i] = (GT)grid[(int64_t)(off + r) * nf + off + c];
+    }
+    __syncthreads();
+  }
+  bool bad = false;
+  const GT inv = (GT)2.0 / (GT)w;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    int l0, l1;
+    double f0, f1;
+    es_place((double)Xq[j * sn], a, K, w, l0, f0);
+    es_place((double)Xq[j * sn + sd], a, K, w, l1, f1);
+    if (l0 < 0 || l1 < 0 || l0 + w > G || l1 + w > G) {
+      bad = true;
+      out[j] = (XT)NAN;
+      continue;
+    }
+    GT px[16];
+    for (int i = 0; i < 16; ++i) {
+      if (i < w) {
+        const GT z = ((GT)i - (GT)f1) * inv;
+        const GT v = (GT)1 - z * z;
+        px[i] = v > (GT)0 ? (GT)exp((double)beta * (sqrt((double)v) - 1.0)) : (GT)0;
+      }
+    }
+    GT acc = 0;
+    for (int r = 0; r < w; ++r) {
+      const GT z = ((GT)r - (GT)f0) * inv;
+      const GT v = (GT)1 - z * z;
+      if (!(v > (GT)0)) continue;
+      const GT wy = (GT)exp((double)beta * (sqrt((double)v) - 1.0));
+      GT racc = 0;
+      if (in_smem) {
+        const GT* row = sg + (int64_t)(l0 + r) * G + l1;
+        for (int c = 0; c < w; ++c) racc += px[c] * row[c];
+      } else {
+        const double* row = grid + (int64_t)(off + l0 + r) * nf + off + l1;
+        for (int c = 0; c < w; ++c) racc += px[c] * (GT)row[c];
+      }
+      acc += wy * racc;
+    }
+    out[j] = (XT)acc;
+  }
+  if (bad && d_status) atomicOr(d_status, (int)FK_E_RANGE);
+}
+
 struct PredWs {
   double2* H;
   double* grid;
@@ -179,13 +271,44 @@ struct PredWs {
   void* work;
 };
 
+static bool is2d(const PredPlan& p) { return !p.additive && p.d == 2; }
+
 static fk_status pred_layout(const PredPlan& p, Bump& b, PredWs& w) {
   FftPlan fp;
-  FK_TRY(fft_plan(1, &p.nf, p.nfeat, CUFFT_Z2D, &fp));
-  w.H = (double2*)b.take((size_t)p.nfeat * (p.nf / 2 + 1) * 16);
-  w.grid = (double*)b.take((size_t)p.nfeat * p.nf * 8);
+  if (is2d(p)) {
+    int dims[2] = {p.nf, p.nf};
+    FK_TRY(fft_plan(2, dims, 1, CUFFT_Z2D, &fp));
+    w.H = (double2*)b.take((size_t)p.nf * (p.nf / 2 + 1) * 16);
+    w.grid = (double*)b.take((size_t)p.nf * p.nf * 8);
+  } else {
+    FK_TRY(fft_plan(1, &p.nf, p.nfeat, CUFFT_Z2D, &fp));
+    w.H = (double2*)b.take((size_t)p.nfeat * (p.nf / 2 + 1) * 16);
+    w.grid = (double*)b.take((size_t)p.nfeat * p.nf * 8);
+  }
   w.tab = (double*)b.take((size_t)(p.m + 1) * 8);
   w.work = b.take(std::max<size_t>(fp.work, 256));
+  return FK_OK;
+}
+
+template <typename XT>
+static fk_status gather2d(const PredPlan& p, const fk_points& Xq, double L, const PredWs& w, void* out, int* d_status, cudaStream_t s) {
+  const int sms = device_sm_count();
+  const double a = (double)p.nf / (4.0 * L);
+  const int K = p.nf / 2 - p.g.off;
+  const int per_sm = p.smem ? std::max(1, std::min(4, (int)(200000 / (p.smem + 1024)))) : 4;
+  if (p.fp64) {
+    auto k = k_gather2d<XT, double>;
+    if (p.smem) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+    k<<<sms * per_sm, 256, p.smem, s>>>((const XT*)Xq.ptr, Xq.n, Xq.stride_n, Xq.stride_d, w.grid, p.nf, p.g.off, p.g.G, K, a, p.es.w,
+                                        p.es.beta, p.in_smem ? 1 : 0, (XT*)out, d_status);
+  } else {
+    auto k = k_gather2d<XT, float>;
+    if (p.smem) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+    k<<<sms * per_sm, 256, p.smem, s>>>((const XT*)Xq.ptr, Xq.n, Xq.stride_n, Xq.stride_d, w.grid, p.nf, p.g.off, p.g.G, K, a, p.es.w,
+                                        p.es.beta, p.in_smem ? 1 : 0, (XT*)out, d_status);
+  }
+  FK_CUDA_TRY(cudaGetLastError());
+  count_launch();
   return FK_OK;
 }
 
@@ -234,6 +357,19 @@ fk_status predict_run(const double* theta, int d, int m, double L, int additive,
   FK_TRY(pred_layout(p, b, w));
   if (!b.ok()) return fail(FK_E_WORKSPACE, "fk_predict_type2: workspace too small");
   if (p.ker == KER_ES) FK_TRY(es_phihat_table(p.es, p.nf, p.m, w.tab, s));
+  if (is2d(p)) {
+    const int64_t tot2 = (int64_t)p.nf * (p.nf / 2 + 1);
+    k_pred_prep2d<<<(unsigned)((tot2 + 255) / 256), 256, 0, s>>>((const double2*)theta, m, p.nf, w.tab, w.H);
+    FK_CUDA_TRY(cudaGetLastError());
+    count_launch();
+    FftPlan fp2;
+    int dims[2] = {p.nf, p.nf};
+    FK_TRY(fft_plan(2, dims, 1, CUFFT_Z2D, &fp2));
+    FK_TRY(fft_exec_z2d(fp2, (cufftDoubleComplex*)w.H, w.grid, w.work, s));
+    if (Xq.n == 0) return FK_OK;
+    if (Xq.dtype == FK_F32) return gather2d<float>(p, Xq, L, w, out, d_status, s);
+    return gather2d<double>(p, Xq, L, w, out, d_status, s);
+  }
   const int64_t tot = (int64_t)p.nfeat * (p.nf / 2 + 1);
   k_pred_prep<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>((const double2*)theta, p.nfeat, m, p.nf, p.ker, w.tab, w.H);
   FK_CUDA_TRY(cudaGetLastError());

@@ -1,0 +1,863 @@
+// spread2d.cu -- d = 2 type-1 passes (PAPER.md:212-220 d-level moments, :203-208 rhs) and the
+// additive model's cross moments (2-D unit-weight sums at (X_l1, -X_l2)).
+//
+// Window: exponential of semicircle psi(z) = exp(beta (sqrt(1 - z^2) - 1)), sigma = 2 (fine grid
+// nf >= 2 x modes per dimension), w = ceil(log10 1/eps) + 1 taps per dimension (+1 in fp64),
+// beta = 2.30 w.  A 2-D grid's occupied quarter does not fit one CTA at C3 (299^2 + 155^2
+// cells), so the occupied rows are split into T row tiles ("binned subproblems"): tile t owns
+// the samples whose first tap row lies in its row range and keeps those rows plus a (w-1)-row
+// halo in shared memory; CTA (chunk, t) streams its chunk of samples and spreads the ones it
+// owns.  Accumulation: int32 fixed point (weights x 2^21, rhs with a per-CTA power-of-two scale,
+// native ATOMS.ADD, drain-at-2^30 into fp64 carry grids) on the fp32 path; fp64 smem atomics on
+// the fp64 path.  Partials are reduced per fine-grid cell in a fixed CTA order, FFT'd (cuFFT 2-D
+// D2Z, batched over pairs) and deconvolved by psi-hat(q0) psi-hat(q1).
+#include <cmath>
+
+#include "fk_internal.cuh"
+
+namespace fk {
+namespace {
+
+constexpr int kW = 16;  // max taps per dimension
+constexpr float kS2 = 2097152.0f;  // 2^21
+constexpr double kInvS2 = 1.0 / 2097152.0;
+
+// Exact position of a coordinate on a grid: p = x * a (compensated when a is not a power of
+// two), P = floor(p), f = p - P in [0,1).  The first tap of a w-tap ES window centred at the
+// point is P + d0 where d0 = 1 - w/2 (w even, f > 0) / -w/2 (w even, f = 0) / etc., and tap i
+// sits at offset (d0 + i - f) cells from the point -- exact in fp32.
+struct P1 {
+  int P;
+  float f;
+};
+
+template <bool EXACT>
+__device__ __forceinline__ P1 place_f32(float x, float a_hi, float a_lo) {
+  float p = x * a_hi;
+  float fl = floorf(p);
+  float f = p - fl;
+  if (!EXACT) {
+    const float e = fmaf(x, a_hi, -p) + x * a_lo;
+    f += e;
+    if (f < 0.0f) { f += 1.0f; fl -= 1.0f; }
+    if (f >= 1.0f) { f -= 1.0f; fl += 1.0f; }
+  }
+  P1 r;
+  r.P = (__float_as_int(fl + FK_MAGIC) - FK_MAGIC_BITS);
+  r.f = f;
+  return r;
+}
+
+__device__ __forceinline__ P1 halve(P1 a, float e_unused) {  // position on the half-resolution grid
+  P1 r;
+  const int odd = a.P & 1;
+  r.P = (a.P - odd) / 2;  // floor(P/2) for any sign
+  if (a.P < 0 && odd) r.P = (a.P - 1) / 2;
+  r.f = 0.5f * (a.f + (float)odd);
+  return r;
+}
+
+// first-tap offset d0 so that taps d0..d0+w-1 cover [f - w/2, f + w/2]
+__device__ __forceinline__ int first_tap(float f, int w) {
+  // ceil(f - w/2) with f in [0,1)
+  return (w & 1) ? (f > 0.5f ? 1 : 0) - (w >> 1) : (f > 0.0f ? 1 : 0) - (w >> 1);
+}
+
+__device__ __forceinline__ int first_tap_d(double f, int w) {
+  return (w & 1) ? (f > 0.5 ? 1 : 0) - (w >> 1) : (f > 0.0 ? 1 : 0) - (w >> 1);
+}
+
+__device__ __forceinline__ void es_taps_f32(float f, int d0, int w, float beta, float* psi) {
+  const float inv = 2.0f / (float)w;
+#pragma unroll
+  for (int i = 0; i < kW; ++i) {
+    if (i < w) {
+      const float z = ((float)(d0 + i) - f) * inv;
+      const float v = 1.0f - z * z;
+      psi[i] = v > 0.0f ? __expf(beta * (sqrtf(v) - 1.0f)) : 0.0f;
+    } else {
+      psi[i] = 0.0f;
+    }
+  }
+}
+
+__device__ __forceinline__ void es_taps_f64(double f, int d0, int w, double beta, double* psi) {
+  const double inv = 2.0 / (double)w;
+#pragma unroll
+  for (int i = 0; i < kW; ++i) {
+    if (i < w) {
+      const double z = ((double)(d0 + i) - f) * inv;
+      const double v = 1.0 - z * z;
+      psi[i] = v > 0.0 ? exp(beta * (sqrt(v) - 1.0)) : 0.0;
+    } else {
+      psi[i] = 0.0;
+    }
+  }
+}
+
+__device__ __noinline__ void drain_row(int* row, int w, double* carry_row, double inv_scale) {
+  for (int b = 0; b < w; ++b) {
+    const int v = atomicExch(row + b, 0);
+    if (v) atomicAdd(carry_row + b, (double)v * inv_scale);
+  }
+}
+
+// One 2-D tile of one grid: rows [r0, r0 + rows) of the occupied G x G region, in smem.
+struct Tile {
+  int G;     // occupied cells per dimension (local coordinates 0..G-1)
+  int K;     // local index of the grid centre offset: local = P + K (+ tap offset)
+  int R;     // rows owned per tile
+  int rows;  // rows stored = R + w - 1
+};
+
+// fixed-point spread of one sample into a tile (fp32 path); returns false if out of range
+template <bool SIGNED>
+__device__ __forceinline__ void spread_fixed(int* T, const Tile& g, int lr /*local first row*/, int lc, const float* py,
+                                             const float* px, int w, float scale, double* carry, int tile_r0, double inv_scale) {
+  for (int a = 0; a < kW; ++a) {
+    if (a >= w) break;
+    const float wy = py[a] * scale;
+    int* row = T + (lr - tile_r0 + a) * g.G + lc;
+    unsigned orr = 0;
+#pragma unroll
+    for (int b = 0; b < kW; ++b) {
+      if (b < w) {
+        const int v = __float_as_int(fmaf(wy, px[b], FK_MAGIC)) - FK_MAGIC_BITS;
+        const unsigned o = (unsigned)atomicAdd(row + b, v);
+        orr |= SIGNED ? (o + (1u << 30)) : o;
+      }
+    }
+    if (SIGNED ? (orr & 0x80000000u) : (orr & 0x40000000u))
+      drain_row(row, w, carry + (int64_t)(lr + a) * g.G + lc, inv_scale);
+  }
+}
+
+__device__ __forceinline__ void spread_f64(double* T, const Tile& g, int lr, int lc, const double* py, const double* px, int w,
+                                           double c, int tile_r0) {
+  for (int a = 0; a < kW; ++a) {
+    if (a >= w) break;
+    double* row = T + (lr - tile_r0 + a) * g.G + lc;
+    const double wy = py[a] * c;
+    for (int b = 0; b < w; ++b) atomicAdd(row + b, wy * px[b]);
+  }
+}
+
+struct Args2 {
+  int64_t n, sn, sd, per;
+  int w;
+  float beta_f;
+  double beta_d;
+  float a_hi, a_lo;  // nf_mu / (4L)
+  double a_d;
+  int T;             // row tiles
+  Tile gA, gB;
+  int KA, KB;        // centre offsets (local index of the grid centre)
+  void* partA;
+  void* partB;
+  int* escale;
+  double* carryA;
+  double* carryB;
+  int* d_status;
+};
+
+// moments (grid A) and rhs (grid B) of d = 2 points, fp32 fixed-point path
+template <bool MU, bool R, bool EXACT>
+__global__ void __launch_bounds__(512) k_spread2d_fixed(const float* __restrict__ X, const float* __restrict__ Y, Args2 g) {
+  extern __shared__ int sm2[];
+  int* A = sm2;
+  int* B = sm2 + (MU ? g.gA.rows * g.gA.G : 0);
+  const int tile = blockIdx.x % g.T;
+  const int chunk = blockIdx.x / g.T;
+  const int nsm = (MU ? g.gA.rows * g.gA.G : 0) + (R ? g.gB.rows * g.gB.G : 0);
+  for (int i = threadIdx.x; i < nsm; i += blockDim.x) sm2[i] = 0;
+  const int64_t beg = (int64_t)chunk * g.per;
+  const int64_t end = min(g.n, beg + g.per);
+  float SY = 0.f;
+  double invSY = 0.0;
+  if (R) {
+    __shared__ float red[32];
+    __shared__ int sE;
+    float mx = 0.0f;
+    const int64_t cnt = max((int64_t)0, min(end - beg, (int64_t)4096));
+    for (int64_t i = threadIdx.x; i < cnt; i += blockDim.x) mx = fmaxf(mx, fabsf(Y[beg + i]));
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float t = 0.0f;
+      for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t = fmaxf(t, red[i]);
+      int e2 = 0, E = 19;
+      if (t > 0.0f && t <= 3.0e38f) {
+        frexpf(t, &e2);
+        E = 20 - e2;
+      }
+      E = max(-100, min(110, E));
+      sE = E;
+      g.escale[blockIdx.x] = E;
+    }
+    __syncthreads();
+    SY = ldexpf(1.0f, sE);
+    invSY = ldexp(1.0, -sE);
+  }
+  __syncthreads();
+  const int rA0 = tile * g.gA.R, rB0 = tile * g.gB.R;
+  bool bad = false;
+  float px[kW], py[kW];
+  for (int64_t j = beg + threadIdx.x; j < end; j += blockDim.x) {
+    const float x0 = X[j * g.sn], x1 = X[j * g.sn + g.sd];
+    const P1 q0 = place_f32<EXACT>(x0, g.a_hi, g.a_lo);
+    const P1 q1 = place_f32<EXACT>(x1, g.a_hi, g.a_lo);
+    // range check on the moment grid (both coordinates): |X| <= L
+    const int d00 = first_tap(q0.f, g.w), d01 = first_tap(q1.f, g.w);
+    const int lrA = q0.P + g.KA + d00, lcA = q1.P + g.KA + d01;
+    if ((unsigned)lrA > (unsigned)(g.gA.G - g.w) || (unsigned)lcA > (unsigned)(g.gA.G - g.w) || x0 != x0 || x1 != x1) {
+      if (tile == 0) bad = true;
+      continue;
+    }
+    if (MU && lrA >= rA0 && lrA < rA0 + g.gA.R) {
+      es_taps_f32(q0.f, d00, g.w, g.beta_f, py);
+      es_taps_f32(q1.f, d01, g.w, g.beta_f, px);
+      spread_fixed<false>(A, g.gA, lrA, lcA, py, px, g.w, kS2, g.carryA, rA0, kInvS2);
+    }
+    if (R) {
+      const P1 h0 = halve(q0, 0.f), h1 = halve(q1, 0.f);
+      const int e0 = first_tap(h0.f, g.w), e1 = first_tap(h1.f, g.w);
+      const int lrB = h0.P + g.KB + e0, lcB = h1.P + g.KB + e1;
+      if (lrB >= rB0 && lrB < rB0 + g.gB.R) {
+        const float y = Y[j];
+        es_taps_f32(h0.f, e0, g.w, g.beta_f, py);
+        es_taps_f32(h1.f, e1, g.w, g.beta_f, px);
+        const float ys = y * SY;
+        if (fabsf(ys) < 1048576.0f) {
+          spread_fixed<true>(B, g.gB, lrB, lcB, py, px, g.w, ys, g.carryB, rB0, invSY);
+        } else {  // outlier / NaN: exact fp64 path straight into the carry grid
+          for (int a = 0; a < g.w; ++a)
+            for (int b = 0; b < g.w; ++b)
+              atomicAdd(g.carryB + (int64_t)(lrB + a) * g.gB.G + lcB + b, (double)py[a] * px[b] * (double)y);
+        }
+      }
+    }
+  }
+  if (bad && g.d_status) atomicOr(g.d_status, (int)FK_E_RANGE);
+  __syncthreads();
+  if (MU) {
+    int* dst = (int*)g.partA + (int64_t)blockIdx.x * g.gA.rows * g.gA.G;
+    for (int i = threadIdx.x; i < g.gA.rows * g.gA.G; i += blockDim.x) dst[i] = A[i];
+  }
+  if (R) {
+    int* dst = (int*)g.partB + (int64_t)blockIdx.x * g.gB.rows * g.gB.G;
+    for (int i = threadIdx.x; i < g.gB.rows * g.gB.G; i += blockDim.x) dst[i] = B[i];
+  }
+}
+
+// fp64 path (any input dtype): fp64 window, fp64 smem atomics
+template <typename XT, bool MU, bool R>
+__global__ void __launch_bounds__(256) k_spread2d_f64(const XT* __restrict__ X, const XT* __restrict__ Y, Args2 g) {
+  extern __shared__ double smd2[];
+  double* A = smd2;
+  double* B = smd2 + (MU ? g.gA.rows * g.gA.G : 0);
+  const int tile = blockIdx.x % g.T;
+  const int chunk = blockIdx.x / g.T;
+  const int nsm = (MU ? g.gA.rows * g.gA.G : 0) + (R ? g.gB.rows * g.gB.G : 0);
+  for (int i = threadIdx.x; i < nsm; i += blockDim.x) smd2[i] = 0.0;
+  __syncthreads();
+  const int64_t beg = (int64_t)chunk * g.per;
+  const int64_t end = min(g.n, beg + g.per);
+  const int rA0 = tile * g.gA.R, rB0 = tile * g.gB.R;
+  bool bad = false;
+  double px[kW], py[kW];
+  for (int64_t j = beg + threadIdx.x; j < end; j += blockDim.x) {
+    const double x0 = (double)X[j * g.sn], x1 = (double)X[j * g.sn + g.sd];
+    const double p0 = x0 * g.a_d, p1 = x1 * g.a_d;
+    const double P0 = floor(p0), P1_ = floor(p1);
+    const double f0 = p0 - P0, f1 = p1 - P1_;
+    if (!(fabs(p0) < 1e8 && fabs(p1) < 1e8)) {
+      if (tile == 0) bad = true;
+      continue;
+    }
+    const int d00 = first_tap_d(f0, g.w);
+    const int d01 = first_tap_d(f1, g.w);
+    const int lrA = (int)P0 + g.KA + d00, lcA = (int)P1_ + g.KA + d01;
+    if ((unsigned)lrA > (unsigned)(g.gA.G - g.w) || (unsigned)lcA > (unsigned)(g.gA.G - g.w)) {
+      if (tile == 0) bad = true;
+      continue;
+    }
+    if (MU && lrA >= rA0 && lrA < rA0 + g.gA.R) {
+      es_taps_f64(f0, d00, g.w, g.beta_d, py);
+      es_taps_f64(f1, d01, g.w, g.beta_d, px);
+      spread_f64(A, g.gA, lrA, lcA, py, px, g.w, 1.0, rA0);
+    }
+    if (R) {
+      const double h0 = 0.5 * p0, h1 = 0.5 * p1;
+      const double H0 = floor(h0), H1 = floor(h1);
+      const double g0 = h0 - H0, g1 = h1 - H1;
+      const int e0 = first_tap_d(g0, g.w);
+      const int e1 = first_tap_d(g1, g.w);
+      const int lrB = (int)H0 + g.KB + e0, lcB = (int)H1 + g.KB + e1;
+      if (lrB >= rB0 && lrB < rB0 + g.gB.R) {
+        es_taps_f64(g0, e0, g.w, g.beta_d, py);
+        es_taps_f64(g1, e1, g.w, g.beta_d, px);
+        spread_f64(B, g.gB, lrB, lcB, py, px, g.w, (double)Y[j], rB0);
+      }
+    }
+  }
+  if (bad && g.d_status) atomicOr(g.d_status, (int)FK_E_RANGE);
+  __syncthreads();
+  if (MU) {
+    double* dst = (double*)g.partA + (int64_t)blockIdx.x * g.gA.rows * g.gA.G;
+    for (int i = threadIdx.x; i < g.gA.rows * g.gA.G; i += blockDim.x) dst[i] = A[i];
+  }
+  if (R) {
+    double* dst = (double*)g.partB + (int64_t)blockIdx.x * g.gB.rows * g.gB.G;
+    for (int i = threadIdx.x; i < g.gB.rows * g.gB.G; i += blockDim.x) dst[i] = B[i];
+  }
+}
+
+// Cross moments: grid per pair, points (X_l1, -X_l2), unit weight; CTA = (chunk, pair group).
+struct ArgsX {
+  int64_t n, sn, sd, per;
+  int w;
+  float beta_f;
+  double beta_d;
+  float a_hi, a_lo;
+  double a_d;
+  int K;       // centre offset
+  int G;       // occupied cells per dim
+  int npairs, per_cta, ngroups;
+  int pl1[528], pl2[528];
+  void* part;
+  double* carry;  // npairs x G x G
+  int* d_status;
+};
+
+template <bool EXACT>
+__global__ void __launch_bounds__(512) k_cross2d_fixed(const float* __restrict__ X, const ArgsX* __restrict__ gp) {
+  extern __shared__ int smx[];
+  const ArgsX& g = *gp;
+  const int grp = blockIdx.x % g.ngroups;
+  const int chunk = blockIdx.x / g.ngroups;
+  const int p0 = grp * g.per_cta;
+  const int np = min(g.per_cta, g.npairs - p0);
+  const int cells = g.G * g.G;
+  for (int i = threadIdx.x; i < np * cells; i += blockDim.x) smx[i] = 0;
+  __syncthreads();
+  const int64_t beg = (int64_t)chunk * g.per;
+  const int64_t end = min(g.n, beg + g.per);
+  Tile t{g.G, g.K, g.G, g.G};
+  bool bad = false;
+  float px[kW], py[kW];
+  for (int64_t j = beg + threadIdx.x; j < end; j += blockDim.x) {
+    for (int q = 0; q < np; ++q) {
+      const int l1 = g.pl1[p0 + q], l2 = g.pl2[p0 + q];
+      const float x0 = X[j * g.sn + l1 * g.sd];
+      const float x1 = -X[j * g.sn + l2 * g.sd];
+      const P1 q0 = place_f32<EXACT>(x0, g.a_hi, g.a_lo);
+      const P1 q1 = place_f32<EXACT>(x1, g.a_hi, g.a_lo);
+      const int d00 = first_tap(q0.f, g.w), d01 = first_tap(q1.f, g.w);
+      const int lr = q0.P + g.K + d00, lc = q1.P + g.K + d01;
+      if ((unsigned)lr > (unsigned)(g.G - g.w) || (unsigned)lc > (unsigned)(g.G - g.w) || x0 != x0 || x1 != x1) {
+        bad = true;
+        continue;
+      }
+      es_taps_f32(q0.f, d00, g.w, g.beta_f, py);
+      es_taps_f32(q1.f, d01, g.w, g.beta_f, px);
+      spread_fixed<false>(smx + q * cells, t, lr, lc, py, px, g.w, kS2, g.carry + (int64_t)(p0 + q) * cells, 0, kInvS2);
+    }
+  }
+  if (bad && g.d_status) atomicOr(g.d_status, (int)FK_E_RANGE);
+  __syncthreads();
+  int* dst = (int*)g.part + ((int64_t)chunk * g.npairs + p0) * cells;
+  for (int i = threadIdx.x; i < np * cells; i += blockDim.x) dst[i] = smx[i];
+}
+
+template <typename XT>
+__global__ void __launch_bounds__(256) k_cross2d_f64(const XT* __restrict__ X, const ArgsX* __restrict__ gp) {
+  extern __shared__ double smxd[];
+  const ArgsX& g = *gp;
+  const int grp = blockIdx.x % g.ngroups;
+  const int chunk = blockIdx.x / g.ngroups;
+  const int p0 = grp * g.per_cta;
+  const int np = min(g.per_cta, g.npairs - p0);
+  const int cells = g.G * g.G;
+  for (int i = threadIdx.x; i < np * cells; i += blockDim.x) smxd[i] = 0.0;
+  __syncthreads();
+  const int64_t beg = (int64_t)chunk * g.per;
+  const int64_t end = min(g.n, beg + g.per);
+  Tile t{g.G, g.K, g.G, g.G};
+  bool bad = false;
+  double px[kW], py[kW];
+  for (int64_t j = beg + threadIdx.x; j < end; j += blockDim.x) {
+    for (int q = 0; q < np; ++q) {
+      const int l1 = g.pl1[p0 + q], l2 = g.pl2[p0 + q];
+      const double pa = (double)X[j * g.sn + l1 * g.sd] * g.a_d, pb = -(double)X[j * g.sn + l2 * g.sd] * g.a_d;
+      if (!(fabs(pa) < 1e8 && fabs(pb) < 1e8)) {
+        bad = true;
+        continue;
+      }
+      const double Pa = floor(pa), Pb = floor(pb), fa = pa - Pa, fb = pb - Pb;
+      const int d00 = first_tap_d(fa, g.w);
+      const int d01 = first_tap_d(fb, g.w);
+      const int lr = (int)Pa + g.K + d00, lc = (int)Pb + g.K + d01;
+      if ((unsigned)lr > (unsigned)(g.G - g.w) || (unsigned)lc > (unsigned)(g.G - g.w)) {
+        bad = true;
+        continue;
+      }
+      es_taps_f64(fa, d00, g.w, g.beta_d, py);
+      es_taps_f64(fb, d01, g.w, g.beta_d, px);
+      spread_f64(smxd + q * cells, t, lr, lc, py, px, g.w, 1.0, 0);
+    }
+  }
+  if (bad && g.d_status) atomicOr(g.d_status, (int)FK_E_RANGE);
+  __syncthreads();
+  double* dst = (double*)g.part + ((int64_t)chunk * g.npairs + p0) * cells;
+  for (int i = threadIdx.x; i < np * cells; i += blockDim.x) dst[i] = smxd[i];
+}
+
+// ------------------------------------------------------------------------------------------
+// partial tiles -> full-period fp64 grid (fixed order), per batch item
+// ------------------------------------------------------------------------------------------
+// tiles: cta = chunk*T + t holds rows [t R, t R + rows) of the G x G occupied block
+__global__ void k_reduce2d(const void* __restrict__ part, int is_fixed, const int* __restrict__ escale, int nchunks, int T, int R,
+                           int rows, int G, int off, int nf, double uniform_inv, const double* __restrict__ carry,
+                           double* __restrict__ fine, int batch, int64_t part_batch_stride, int64_t part_cta_stride) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t per = (int64_t)nf * nf;
+  if (t >= per * batch) return;
+  const int bi = (int)(t / per);
+  const int64_t c = t % per;
+  const int r = (int)(c / nf) - off, col = (int)(c % nf) - off;
+  double s = 0.0;
+  if (r >= 0 && r < G && col >= 0 && col < G) {
+    for (int tt = 0; tt < T; ++tt) {
+      const int lr = r - tt * R;
+      if (lr < 0 || lr >= rows) continue;
+      for (int ch = 0; ch < nchunks; ++ch) {
+        const int64_t cta = (int64_t)ch * T + tt;
+        const int64_t idx = bi * part_batch_stride + cta * part_cta_stride + (int64_t)lr * G + col;
+        if (is_fixed) {
+          const double v = (double)((const int*)part)[idx];
+          s += escale ? v * ldexp(1.0, -escale[cta]) : v * uniform_inv;
+        } else {
+          s += ((const double*)part)[idx];
+        }
+      }
+    }
+    if (carry) s += carry[(int64_t)bi * G * G + (int64_t)r * G + col];
+  }
+  fine[t] = s;
+}
+
+// out[q0][q1] = (-1)^(q0+q1) F[q0 mod nf][q1 mod nf] / (psi-hat(q0) psi-hat(q1)), |q| <= K,
+// F the D2Z output [nf][nf/2+1] (Hermitian: F[a][-b] = conj F[-a][b]).
+__global__ void k_deconv2d(const double2* __restrict__ F, int nf, int K, const double* __restrict__ tab, double2* __restrict__ out,
+                           int acc, int batch, int flip1) {
+  const int side = 2 * K + 1;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)side * side * batch) return;
+  const int bi = (int)(t / ((int64_t)side * side));
+  const int rem = (int)(t % ((int64_t)side * side));
+  const int q0 = rem / side - K, q1 = rem % side - K;
+  const int half = nf / 2 + 1;
+  const double2* Fb = F + (int64_t)bi * nf * half;
+  double2 v;
+  if (q1 >= 0) {
+    v = Fb[(int64_t)((q0 % nf + nf) % nf) * half + q1];
+  } else {
+    v = Fb[(int64_t)(((-q0) % nf + nf) % nf) * half + (-q1)];
+    v.y = -v.y;
+  }
+  const double sc = (((q0 + q1) & 1) ? -1.0 : 1.0) / (tab[q0 < 0 ? -q0 : q0] * tab[q1 < 0 ? -q1 : q1]);
+  v.x *= sc;
+  v.y *= sc;
+  (void)flip1;
+  if (acc) {
+    out[t].x += v.x;
+    out[t].y += v.y;
+  } else {
+    out[t] = v;
+  }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------------------------
+// host side
+// ------------------------------------------------------------------------------------------
+struct Plan2 {
+  int m, w;
+  double beta;
+  bool fp64;
+  int nfA, nfB;
+  Tile gA, gB;
+  int offA, offB, KA, KB;
+  int T, chunks, threads;
+  size_t smem;
+};
+
+static int max_optin() {
+  int dev = 0, v = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  return v > 0 ? v : 232448;
+}
+
+static int es_width(double eps, bool fp64) {
+  int w = (int)std::ceil(std::log10(1.0 / eps)) + (fp64 ? 2 : 1);
+  return std::min(kW, std::max(4, w));
+}
+
+// Geometry of one ES grid: local index = global - off, centre nf/2 at local K, occupied G cells.
+static void es_geo(int nf, int w, int* off, int* K, int* G) {
+  *off = nf / 4 - w / 2 - 2;
+  *K = nf / 2 - *off;
+  *G = nf / 2 + w + 4;
+}
+
+// fp64 = fp64 accumulation (and fp64 window): eps < 1e-7 or fp64 input coordinates
+static fk_status make_plan2(int m, double eps, bool mu, bool r, int dtype, Plan2* p) {
+  Plan2 q{};
+  q.m = m;
+  q.fp64 = eps < 1e-7 || dtype == FK_F64;
+  q.w = es_width(eps, eps < 1e-7);
+  q.beta = 2.30 * q.w;
+  q.nfA = fft_friendly(2 * (4 * m + 1));
+  q.nfB = q.nfA / 2;
+  int GA, GB;
+  es_geo(q.nfA, q.w, &q.offA, &q.KA, &GA);
+  es_geo(q.nfB, q.w, &q.offB, &q.KB, &GB);
+  const size_t esz = q.fp64 ? 8 : 4;
+  const size_t cap = (size_t)max_optin() - 2048;
+  for (int T = 1; T <= 64; ++T) {
+    const int RA = (GA + T - 1) / T, RB = (GB + T - 1) / T;
+    const size_t bytes = ((mu ? (size_t)(RA + q.w - 1) * GA : 0) + (r ? (size_t)(RB + q.w - 1) * GB : 0)) * esz;
+    if (bytes <= cap) {
+      q.T = T;
+      q.gA = {GA, q.KA, RA, RA + q.w - 1};
+      q.gB = {GB, q.KB, RB, RB + q.w - 1};
+      q.smem = bytes;
+      break;
+    }
+  }
+  if (q.T == 0) return fail(FK_E_UNSUPPORTED, "d=2 grid too large for 64 row tiles");
+  q.threads = q.fp64 ? 256 : 512;
+  const int sms = device_sm_count();
+  const int per_sm = std::max(1, std::min(4, (int)(cap / (q.smem + 1024))));
+  q.chunks = std::max(1, (sms * per_sm) / q.T);
+  *p = q;
+  return FK_OK;
+}
+
+struct Ws2 {
+  void* partA = nullptr;
+  void* partB = nullptr;
+  int* escale = nullptr;
+  double* carryA = nullptr;
+  double* carryB = nullptr;
+  double* fineA = nullptr;
+  double* fineB = nullptr;
+  double2* specA = nullptr;
+  double2* specB = nullptr;
+  double* tabA = nullptr;
+  double* tabB = nullptr;
+  void* work = nullptr;
+};
+
+static fk_status layout2(const Plan2& p, bool mu, bool r, Bump& b, Ws2& w) {
+  const size_t esz = p.fp64 ? 8 : 4;
+  const int ctas = p.chunks * p.T;
+  size_t fw = 0;
+  FftPlan pa, pb;
+  int dA[2] = {p.nfA, p.nfA}, dB[2] = {p.nfB, p.nfB};
+  if (mu) {
+    FK_TRY(fft_plan(2, dA, 1, CUFFT_D2Z, &pa));
+    fw = std::max(fw, pa.work);
+    w.partA = b.take((size_t)ctas * p.gA.rows * p.gA.G * esz);
+    w.fineA = (double*)b.take((size_t)p.nfA * p.nfA * 8);
+    w.specA = (double2*)b.take((size_t)p.nfA * (p.nfA / 2 + 1) * 16);
+    w.tabA = (double*)b.take((size_t)(2 * p.m + 1) * 8);
+    if (!p.fp64) w.carryA = (double*)b.take((size_t)p.gA.G * p.gA.G * 8);
+  }
+  if (r) {
+    FK_TRY(fft_plan(2, dB, 1, CUFFT_D2Z, &pb));
+    fw = std::max(fw, pb.work);
+    w.partB = b.take((size_t)ctas * p.gB.rows * p.gB.G * esz);
+    w.fineB = (double*)b.take((size_t)p.nfB * p.nfB * 8);
+    w.specB = (double2*)b.take((size_t)p.nfB * (p.nfB / 2 + 1) * 16);
+    w.tabB = (double*)b.take((size_t)(p.m + 1) * 8);
+    if (!p.fp64) {
+      w.carryB = (double*)b.take((size_t)p.gB.G * p.gB.G * 8);
+      w.escale = (int*)b.take((size_t)ctas * 4);
+    }
+  }
+  w.work = b.take(std::max<size_t>(fw, 256));
+  return FK_OK;
+}
+
+size_t type1_2d_ws_bytes(int m, double eps, bool mu, bool r, int dtype) {
+  Plan2 p;
+  if (make_plan2(m, eps, mu, r, dtype, &p) != FK_OK) return 0;
+  Bump b(nullptr, 0);
+  Ws2 w;
+  if (layout2(p, mu, r, b, w) != FK_OK) return 0;
+  return b.used + 256;
+}
+
+fk_status type1_2d_run(int m, double eps, const fk_points& X, const void* Y, double L, double* mu_out, double* r_out, bool acc, void* ws,
+                       size_t ws_bytes, int* d_status, cudaStream_t s) {
+  const bool mu = mu_out != nullptr, r = r_out != nullptr;
+  Plan2 p;
+  FK_TRY(make_plan2(m, eps, mu, r, X.dtype, &p));
+  Bump b(ws, ws_bytes);
+  Ws2 w;
+  FK_TRY(layout2(p, mu, r, b, w));
+  if (!b.ok()) return fail(FK_E_WORKSPACE, "workspace too small");
+  const int ctas = p.chunks * p.T;
+  const size_t esz = p.fp64 ? 8 : 4;
+  if (mu && w.carryA) FK_CUDA_TRY(cudaMemsetAsync(w.carryA, 0, (size_t)p.gA.G * p.gA.G * 8, s));
+  if (r && w.carryB) FK_CUDA_TRY(cudaMemsetAsync(w.carryB, 0, (size_t)p.gB.G * p.gB.G * 8, s));
+  Args2 a{};
+  a.n = X.n;
+  a.sn = X.stride_n;
+  a.sd = X.stride_d;
+  a.per = (X.n + p.chunks - 1) / p.chunks;
+  a.w = p.w;
+  a.beta_f = (float)p.beta;
+  a.beta_d = p.beta;
+  const double ad = (double)p.nfA / (4.0 * L);
+  a.a_d = ad;
+  a.a_hi = (float)ad;
+  a.a_lo = (float)(ad - (double)a.a_hi);
+  int ex = 0;
+  const bool exact = std::frexp(ad, &ex) == 0.5;
+  a.T = p.T;
+  a.gA = p.gA;
+  a.gB = p.gB;
+  a.KA = p.KA;
+  a.KB = p.KB;
+  a.partA = w.partA;
+  a.partB = w.partB;
+  a.escale = w.escale;
+  a.carryA = w.carryA;
+  a.carryB = w.carryB;
+  a.d_status = d_status;
+  if (X.n > 0) {
+    if (!p.fp64) {
+      const float* Xf = (const float*)X.ptr;
+      const float* Yf = (const float*)Y;
+      auto go = [&](auto k) {
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+        prof_spread_begin(s);
+        k<<<ctas, p.threads, p.smem, s>>>(Xf, Yf, a);
+        prof_spread_end(s);
+      };
+      if (mu && r) exact ? go(k_spread2d_fixed<true, true, true>) : go(k_spread2d_fixed<true, true, false>);
+      else if (mu) exact ? go(k_spread2d_fixed<true, false, true>) : go(k_spread2d_fixed<true, false, false>);
+      else exact ? go(k_spread2d_fixed<false, true, true>) : go(k_spread2d_fixed<false, true, false>);
+    } else {
+      auto go = [&](auto k, auto* Xp, auto* Yp) {
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+        prof_spread_begin(s);
+        k<<<ctas, p.threads, p.smem, s>>>(Xp, Yp, a);
+        prof_spread_end(s);
+      };
+      if (X.dtype == FK_F32) {
+        const float* Xf = (const float*)X.ptr;
+        const float* Yf = (const float*)Y;
+        if (mu && r) go(k_spread2d_f64<float, true, true>, Xf, Yf);
+        else if (mu) go(k_spread2d_f64<float, true, false>, Xf, Yf);
+        else go(k_spread2d_f64<float, false, true>, Xf, Yf);
+      } else {
+        const double* Xd = (const double*)X.ptr;
+        const double* Yd = (const double*)Y;
+        if (mu && r) go(k_spread2d_f64<double, true, true>, Xd, Yd);
+        else if (mu) go(k_spread2d_f64<double, true, false>, Xd, Yd);
+        else go(k_spread2d_f64<double, false, true>, Xd, Yd);
+      }
+    }
+    FK_CUDA_TRY(cudaGetLastError());
+    count_launch();
+  } else {
+    if (mu) FK_CUDA_TRY(cudaMemsetAsync(w.partA, 0, (size_t)ctas * p.gA.rows * p.gA.G * esz, s));
+    if (r) FK_CUDA_TRY(cudaMemsetAsync(w.partB, 0, (size_t)ctas * p.gB.rows * p.gB.G * esz, s));
+    if (r && w.escale) FK_CUDA_TRY(cudaMemsetAsync(w.escale, 0, (size_t)ctas * 4, s));
+  }
+  // the fp64 kernel is also used for fp32 inputs when the fp64 path is selected, and for fp64
+  // inputs on the fp32 path (its partials are then doubles)
+  const bool fixed = !p.fp64;
+  EsParams es{p.w, p.beta};
+  const int TB = 256;
+  auto finish = [&](void* part, int* esc, const Tile& g, int off, int nf, double* carry, double* fine, double2* spec, double* tab,
+                    int K, double* out) -> fk_status {
+    const int64_t tot = (int64_t)nf * nf;
+    k_reduce2d<<<(unsigned)((tot + TB - 1) / TB), TB, 0, s>>>(part, fixed ? 1 : 0, esc, p.chunks, p.T, g.R, g.rows, g.G, off, nf,
+                                                             kInvS2, fixed ? carry : nullptr, fine, 1, 0,
+                                                             (int64_t)g.rows * g.G);
+    FK_CUDA_TRY(cudaGetLastError());
+    FftPlan fp;
+    int dims[2] = {nf, nf};
+    FK_TRY(fft_plan(2, dims, 1, CUFFT_D2Z, &fp));
+    FK_TRY(fft_exec_d2z(fp, fine, (cufftDoubleComplex*)spec, w.work, s));
+    FK_TRY(es_phihat_table(es, nf, K, tab, s));
+    const int64_t nout = (int64_t)(2 * K + 1) * (2 * K + 1);
+    k_deconv2d<<<(unsigned)((nout + TB - 1) / TB), TB, 0, s>>>(spec, nf, K, tab, (double2*)out, acc ? 1 : 0, 1, 0);
+    FK_CUDA_TRY(cudaGetLastError());
+    count_launch(2);
+    return FK_OK;
+  };
+  if (mu) FK_TRY(finish(w.partA, nullptr, p.gA, p.offA, p.nfA, w.carryA, w.fineA, w.specA, w.tabA, 2 * m, mu_out));
+  if (r) FK_TRY(finish(w.partB, w.escale, p.gB, p.offB, p.nfB, w.carryB, w.fineB, w.specB, w.tabB, m, r_out));
+  return FK_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// additive cross moments
+// ------------------------------------------------------------------------------------------
+struct PlanX {
+  int m, w, nf, off, K, G, npairs, per_cta, ngroups, chunks, threads;
+  double beta;
+  bool fp64;
+  size_t smem;
+};
+
+static fk_status make_planx(int d, int m, double eps, int dtype, PlanX* p) {
+  PlanX q{};
+  q.m = m;
+  q.fp64 = eps < 1e-7 || dtype == FK_F64;
+  q.w = es_width(eps, eps < 1e-7);
+  q.beta = 2.30 * q.w;
+  q.nf = fft_friendly(2 * (2 * m + 1));
+  es_geo(q.nf, q.w, &q.off, &q.K, &q.G);
+  q.npairs = d * (d - 1) / 2;
+  const size_t esz = q.fp64 ? 8 : 4;
+  const size_t cap = (size_t)max_optin() - 2048;
+  const size_t per = (size_t)q.G * q.G * esz;
+  if (per > cap) return fail(FK_E_UNSUPPORTED, "fk_additive_cross_moments: m too large for one pair grid per CTA");
+  q.per_cta = (int)std::min<size_t>(q.npairs, cap / per);
+  q.ngroups = (q.npairs + q.per_cta - 1) / q.per_cta;
+  q.smem = (size_t)q.per_cta * per;
+  q.threads = q.fp64 ? 256 : 512;
+  const int sms = device_sm_count();
+  const int per_sm = std::max(1, std::min(4, (int)(cap / (q.smem + 1024))));
+  q.chunks = std::max(1, (sms * per_sm + q.ngroups - 1) / q.ngroups);
+  *p = q;
+  return FK_OK;
+}
+
+static fk_status layoutx(const PlanX& p, Bump& b, void** part, double** carry, double** fine, double2** spec, double** tab, void** work,
+                         ArgsX** args) {
+  FftPlan fp;
+  int dims[2] = {p.nf, p.nf};
+  FK_TRY(fft_plan(2, dims, p.npairs, CUFFT_D2Z, &fp));
+  const size_t esz = p.fp64 ? 8 : 4;
+  *part = b.take((size_t)p.chunks * p.npairs * p.G * p.G * esz);
+  *carry = (double*)b.take((size_t)p.npairs * p.G * p.G * 8);
+  *fine = (double*)b.take((size_t)p.npairs * p.nf * p.nf * 8);
+  *spec = (double2*)b.take((size_t)p.npairs * p.nf * (p.nf / 2 + 1) * 16);
+  *tab = (double*)b.take((size_t)(p.m + 1) * 8);
+  *args = (ArgsX*)b.take(sizeof(ArgsX));
+  *work = b.take(std::max<size_t>(fp.work, 256));
+  return FK_OK;
+}
+
+size_t cross_ws_bytes(int d, int m, double eps, int64_t n, int dtype) {
+  (void)n;
+  if (d < 2) return 0;
+  PlanX p;
+  if (make_planx(d, m, eps, dtype, &p) != FK_OK) return 0;
+  Bump b(nullptr, 0);
+  void *part, *work;
+  double *carry, *fine, *tab;
+  double2* spec;
+  ArgsX* args;
+  if (layoutx(p, b, &part, &carry, &fine, &spec, &tab, &work, &args) != FK_OK) return 0;
+  return b.used + 256;
+}
+
+fk_status cross_run(const fk_points& X, double L, int m, double eps, double* G, bool accumulate, void* ws, size_t ws_bytes,
+                    int* d_status, cudaStream_t s) {
+  PlanX p;
+  FK_TRY(make_planx(X.d, m, eps, X.dtype, &p));
+  if (p.npairs > 528) return fail(FK_E_UNSUPPORTED, "fk_additive_cross_moments: at most 528 pairs");
+  Bump b(ws, ws_bytes);
+  void *part, *work;
+  double *carry, *fine, *tab;
+  double2* spec;
+  ArgsX* dargs;
+  FK_TRY(layoutx(p, b, &part, &carry, &fine, &spec, &tab, &work, &dargs));
+  if (!b.ok()) return fail(FK_E_WORKSPACE, "workspace too small");
+  const bool fixed = !p.fp64;
+  static thread_local ArgsX a;  // host staging for the argument block (copied to the workspace)
+  a = ArgsX{};
+  a.n = X.n;
+  a.sn = X.stride_n;
+  a.sd = X.stride_d;
+  a.per = (X.n + p.chunks - 1) / p.chunks;
+  a.w = p.w;
+  a.beta_f = (float)p.beta;
+  a.beta_d = p.beta;
+  const double ad = (double)p.nf / (4.0 * L);
+  a.a_d = ad;
+  a.a_hi = (float)ad;
+  a.a_lo = (float)(ad - (double)a.a_hi);
+  int ex = 0;
+  const bool exact = std::frexp(ad, &ex) == 0.5;
+  a.K = p.K;
+  a.G = p.G;
+  a.npairs = p.npairs;
+  a.per_cta = p.per_cta;
+  a.ngroups = p.ngroups;
+  int q = 0;
+  for (int l1 = 0; l1 < X.d; ++l1)
+    for (int l2 = l1 + 1; l2 < X.d; ++l2) {
+      a.pl1[q] = l1;
+      a.pl2[q] = l2;
+      ++q;
+    }
+  a.part = part;
+  a.carry = carry;
+  a.d_status = d_status;
+  FK_CUDA_TRY(cudaMemsetAsync(carry, 0, (size_t)p.npairs * p.G * p.G * 8, s));
+  FK_CUDA_TRY(cudaMemcpyAsync(dargs, &a, sizeof(ArgsX), cudaMemcpyHostToDevice, s));
+  const int ctas = p.chunks * p.ngroups;
+  const size_t esz = p.fp64 ? 8 : 4;
+  if (X.n > 0) {
+    auto go = [&](auto k, auto* Xp, int threads) {
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+      prof_spread_begin(s);
+      k<<<ctas, threads, p.smem, s>>>(Xp, dargs);
+      prof_spread_end(s);
+    };
+    if (fixed) {
+      if (exact) go(k_cross2d_fixed<true>, (const float*)X.ptr, 512);
+      else go(k_cross2d_fixed<false>, (const float*)X.ptr, 512);
+    } else if (X.dtype == FK_F32) {
+      go(k_cross2d_f64<float>, (const float*)X.ptr, 256);  // fp32 points, fp64 accuracy
+    } else {
+      go(k_cross2d_f64<double>, (const double*)X.ptr, 256);
+    }
+    FK_CUDA_TRY(cudaGetLastError());
+    count_launch();
+  } else {
+    FK_CUDA_TRY(cudaMemsetAsync(part, 0, (size_t)p.chunks * p.npairs * p.G * p.G * esz, s));
+  }
+  const int TB = 256;
+  const int64_t tot = (int64_t)p.npairs * p.nf * p.nf;
+  // part layout: [chunk][pair][G][G] -> batch stride G*G, "cta" stride npairs*G*G, T = 1
+  k_reduce2d<<<(unsigned)((tot + TB - 1) / TB), TB, 0, s>>>(part, fixed ? 1 : 0, nullptr, p.chunks, 1, p.G, p.G, p.G, p.off, p.nf,
+                                                           kInvS2, fixed ? carry : nullptr, fine, p.npairs, (int64_t)p.G * p.G,
+                                                           (int64_t)p.npairs * p.G * p.G);
+  FK_CUDA_TRY(cudaGetLastError());
+  FftPlan fp;
+  int dims[2] = {p.nf, p.nf};
+  FK_TRY(fft_plan(2, dims, p.npairs, CUFFT_D2Z, &fp));
+  FK_TRY(fft_exec_d2z(fp, fine, (cufftDoubleComplex*)spec, work, s));
+  EsParams es{p.w, p.beta};
+  FK_TRY(es_phihat_table(es, p.nf, m, tab, s));
+  const int64_t nout = (int64_t)p.npairs * (2 * m + 1) * (2 * m + 1);
+  k_deconv2d<<<(unsigned)((nout + TB - 1) / TB), TB, 0, s>>>(spec, p.nf, m, tab, (double2*)G, accumulate ? 1 : 0, p.npairs, 0);
+  FK_CUDA_TRY(cudaGetLastError());
+  count_launch(2);
+  return FK_OK;
+}
+
+}  // namespace fk

@@ -1,0 +1,130 @@
+"""GPU parity of the d = 2 pass (C3/C4 shapes), the physics-informed and Sobolev d = 2 solves,
+2-D prediction, and the additive model (cross moments, block solve, additive prediction)."""
+import numpy as np
+import pytest
+
+import datagen
+from gpu_util import dev, fk, host, rel
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def F():
+    assert torch.cuda.is_available()
+    return fk()
+
+
+HEAT = dict(alpha=[[1, 0], [0, 2]], a_alpha=[1.0, -1.0], box=[[-1.0, 1.0], [-1.0, 1.0]])  # d_tau f - d_xx f (DESIGN R6)
+
+
+@pytest.mark.parametrize("n,m,eps,dt", [(20_001, 8, 1e-6, "f32"), (20_000, 32, 1e-6, "f32"), (6_000, 64, 1e-6, "f32"),
+                                        (5_000, 16, 1e-10, "f64"), (4_001, 12, 1e-6, "f64")])
+def test_type1_2d_matches_oracle(F, oracle, n, m, eps, dt):
+    X, Y = datagen.dataset(n, d=2, ykind="expcos", seed=21)
+    t = torch.float32 if dt == "f32" else torch.float64
+    if dt == "f64":
+        X = X.astype(np.float64) * (1 - 2.0 ** -31)
+        Y = Y.astype(np.float64)
+    r, mu = F.fk_rhs_type1(dev(X, t), dev(Y, t), 1.0, m, eps)
+    mu_o, r_o = oracle.moments(X, 1.0, m), oracle.rhs(X, Y, 1.0, m)
+    e_mu, e_r = rel(host(mu), mu_o), rel(host(r), r_o)
+    print(f"d=2 n={n} m={m} eps={eps} {dt}: mu {e_mu:.2e} r {e_r:.2e}")
+    tol = 1e-5 if eps >= 1e-7 else 1e-10
+    assert e_mu <= tol and e_r <= tol
+
+
+def test_2d_edges_and_views(F, oracle):
+    m = 10
+    X = np.array([[1.0, 1.0], [-1.0, -1.0], [1.0, -1.0], [-1.0, 1.0], [0.3, -0.7]] * 300, dtype=np.float32)
+    Y = np.linspace(-1, 2, X.shape[0]).astype(np.float32)
+    r, mu = F.fk_rhs_type1(dev(X), dev(Y), 1.0, m, 1e-6)
+    assert rel(host(mu), oracle.moments(X, 1.0, m)) <= 1e-5
+    assert rel(host(r), oracle.rhs(X, Y, 1.0, m)) <= 1e-5
+    # SoA view (column pitch != d) and general L
+    X2, Y2 = datagen.dataset(7_003, d=2, seed=22, L=1.9)
+    soa = dev(np.ascontiguousarray(X2.T))  # (2, n)
+    mu2 = F.fk_moments_type1(soa.t(), 1.9, m, 1e-6)
+    assert rel(host(mu2), oracle.moments(X2, 1.9, m)) <= 1e-5
+
+
+@pytest.mark.parametrize("kind,m", [("sobolev", 16), ("pik_box", 12)])
+def test_solve_2d_matches_oracle(F, oracle, kind, m):
+    X, Y = datagen.dataset(20_000, d=2, ykind="expcos", seed=23)
+    mu, r = oracle.moments(X, 1.0, m), oracle.rhs(X, Y, 1.0, m)
+    kw = dict(mu_pde=1.0, L=1.0, **HEAT) if kind == "pik_box" else {}
+    th_o = oracle.solve(mu, r, 20_000, 2, m, 1e-6, kind, 2.0, **kw)
+    kw2 = dict(mu_pde=1.0, **HEAT) if kind == "pik_box" else {}
+    th, rep = F.fk_solve(dev(mu.reshape(-1)), dev(r.reshape(-1)), 20_000, 2, m, 1.0, 1e-6, kind, 2.0, **kw2)
+    print(f"solve d=2 {kind} m={m}: {rel(host(th), th_o):.2e} backward {rep['backward_err']:.1e} ms {rep['ms']:.1f}")
+    assert rep["backward_err"] < 1e-11
+    assert rel(host(th), th_o) < 1e-6
+
+
+@pytest.mark.parametrize("m,eps", [(20, 1e-6), (64, 1e-6), (16, 1e-10)])
+def test_predict_2d_matches_oracle(F, oracle, m, eps):
+    rng = np.random.default_rng(4)
+    k = oracle.mode_grid(2, m)
+    D = k.shape[0]
+    th = (rng.normal(size=D) + 1j * rng.normal(size=D)) / (1.0 + np.sum(k * k, 1))
+    Xq = datagen.dataset(5_001, d=2, seed=24)[0]
+    t = torch.float32 if eps >= 1e-7 else torch.float64
+    out = host(F.fk_predict_type2(dev(th), 2, m, 1.0, dev(Xq, t), eps))
+    err = rel(out, oracle.predict(th, Xq, 1.0, m))
+    print(f"predict d=2 m={m} eps={eps}: {err:.2e}")
+    assert err <= (1e-5 if eps >= 1e-7 else 1e-10)
+
+
+def test_pi_fit_end_to_end(F, oracle):
+    """C4 shape (PI space-time heat equation, d = 2, m = 16 here): GPU fit vs oracle fit."""
+    n, m, s, lam = 30_000, 16, 2.0, 30_000 ** (-2 / 3)
+    X, Y = datagen.dataset(n, d=2, ykind="expcos", seed=25)
+    Xq = datagen.dataset(3_000, d=2, seed=26)[0]
+    th_o, _, _ = oracle.fit(X, Y, 1.0, m, lam, "pik_box", s, mu_pde=1.0, L=1.0, **HEAT)
+    r, mu = F.fk_rhs_type1(dev(X), dev(Y), 1.0, m, 1e-6)
+    th, rep = F.fk_solve(mu.reshape(-1), r.reshape(-1), n, 2, m, 1.0, lam, "pik_box", s, mu_pde=1.0, **HEAT)
+    f = host(F.fk_predict_type2(th, 2, m, 1.0, dev(Xq), 1e-6))
+    f_o = oracle.predict(th_o, Xq, 1.0, m)
+    print(f"PI fit: pred {rel(f, f_o):.2e}")
+    assert rel(f, f_o) <= 1e-4
+
+
+@pytest.mark.parametrize("d,m,n,eps", [(3, 10, 20_000, 1e-6), (10, 50, 2_000, 1e-6), (4, 8, 5_000, 1e-10)])
+def test_cross_moments_match_oracle(F, oracle, d, m, n, eps):
+    X, _ = datagen.dataset(n, d=d, ykind="additive", seed=27)
+    t = torch.float32 if eps >= 1e-7 else torch.float64
+    Xs = X if eps >= 1e-7 else X.astype(np.float64)
+    G = host(F.fk_additive_cross_moments(dev(Xs, t), 1.0, m, eps))
+    G_o = oracle.cross_moments(Xs, 1.0, m)
+    errs = [rel(G[p], G_o[p]) for p in range(G.shape[0])]
+    print(f"cross d={d} m={m} n={n} eps={eps}: max pair err {max(errs):.2e}")
+    assert max(errs) <= (1e-5 if eps >= 1e-7 else 1e-10)
+
+
+def test_additive_fit_end_to_end(F, oracle):
+    """C5 shape (d = 10 features, m = 20 here): per-feature moments/rhs (fk_rhs_type1 on column
+    views), cross moments, block solve, additive prediction vs the oracle."""
+    n, d, m, lam = 10_000, 10, 20, 10_000 ** (-0.8)
+    X, Y = datagen.dataset(n, d=d, ykind="additive", seed=28)
+    Xq = datagen.dataset(2_000, d=d, seed=29)[0]
+    Xd, Yd = dev(X), dev(Y)
+    mus = torch.zeros((d, 4 * m + 1), dtype=torch.complex128, device="cuda")
+    rs = torch.zeros((d, 2 * m + 1), dtype=torch.complex128, device="cuda")
+    for l in range(d):
+        F.fk_rhs_type1(Xd[:, l], Yd, 1.0, m, 1e-6, r_out=rs[l], mu_out=mus[l])
+    G = F.fk_additive_cross_moments(Xd, 1.0, m, 1e-6)
+    th, rep = F.fk_solve(mus, rs, n, d, m, 1.0, lam, "additive", cross=G)
+    mu_l = [oracle.moments(X[:, l], 1.0, m) for l in range(d)]
+    r_l = [oracle.rhs(X[:, l], Y, 1.0, m) for l in range(d)]
+    th_o = oracle.solve_additive(mu_l, r_l, oracle.cross_moments(X, 1.0, m), n, d, m, lam)
+    f = host(F.fk_predict_type2(th, d, m, 1.0, dev(Xq), 1e-6, additive=True))
+    f_o = oracle.predict_additive(th_o, Xq, 1.0, m)
+    print(f"additive fit: theta {rel(host(th), th_o):.2e} pred {rel(f, f_o):.2e} backward {rep['backward_err']:.1e}")
+    assert rel(f, f_o) <= 1e-4
+    # theta itself through the same (oracle) inputs: the block solve
+    th2, _ = F.fk_solve(dev(np.stack(mu_l)), dev(np.stack(r_l)), n, d, m, 1.0, lam, "additive", cross=dev(oracle.cross_moments(X, 1.0, m)))
+    assert rel(host(th2), th_o) < 1e-8
+    # additive prediction alone
+    f2 = host(F.fk_predict_type2(dev(th_o), d, m, 1.0, dev(Xq), 1e-6, additive=True))
+    assert rel(f2, f_o) <= 1e-5
