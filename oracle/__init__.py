@@ -260,5 +260,7 @@ def fit(X, Y, L: float, m: int, lam: float, kind: str = "sobolev", s: float = 1.
     d = X.shape[1]
     mu = moments(X, L, m)
     r = rhs(X, Y, L, m)
+    if kind == "pik_box":
+        pi = dict(pi, L=L)
     theta = solve(mu, r, X.shape[0], d, m, lam, kind, s, **pi)
     return theta, mu, r

@@ -81,7 +81,7 @@ def test_pi_fit_end_to_end(F, oracle):
     n, m, s, lam = 30_000, 16, 2.0, 30_000 ** (-2 / 3)
     X, Y = datagen.dataset(n, d=2, ykind="expcos", seed=25)
     Xq = datagen.dataset(3_000, d=2, seed=26)[0]
-    th_o, _, _ = oracle.fit(X, Y, 1.0, m, lam, "pik_box", s, mu_pde=1.0, L=1.0, **HEAT)
+    th_o, _, _ = oracle.fit(X, Y, 1.0, m, lam, "pik_box", s, mu_pde=1.0, **HEAT)
     r, mu = F.fk_rhs_type1(dev(X), dev(Y), 1.0, m, 1e-6)
     th, rep = F.fk_solve(mu.reshape(-1), r.reshape(-1), n, 2, m, 1.0, lam, "pik_box", s, mu_pde=1.0, **HEAT)
     f = host(F.fk_predict_type2(th, 2, m, 1.0, dev(Xq), 1e-6))
