@@ -7,16 +7,16 @@
 A step = one whole fit over the configuration's n samples, which are generated on the device
 (seeded, counter-based: datagen/gen.cu) BEFORE the timed region and stay resident in HBM.
 Multi-GPU is strong scaling: rank r owns samples [r n/N, (r+1) n/N) of the same global dataset,
-spreads them, the 6002-entry complex128 [mu | r] vector is all-reduced over NCCL, rank 0 solves,
+spreads them, the small complex128 [mu | r (| G)] vector is all-reduced over NCCL, rank 0 solves,
 theta is broadcast.  Time = CUDA events on the launching stream between barriers, max over ranks.
+Default workload: BASELINE config C2 (d=1, m=1000, n=1e10), which fits one B200 (80 GB).
 
-Rank 0 prints ONE JSON line (see DESIGN.md §Measurement for every key).
+Rank 0 prints ONE JSON line (DESIGN.md §6 explains every key).
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import statistics
 import subprocess
@@ -28,15 +28,23 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "samples/sec fit (moments+solve) at 1/2/4/8 B200; HBM GB/s vs 8 TB/s"
+HEAT = dict(alpha=[[1, 0], [0, 2]], a_alpha=[1.0, -1.0], box=[[-1.0, 1.0], [-1.0, 1.0]])
 
-# BASELINE.json configs (C1..C5); s, lambda per the paper's schedules (reading R6)
+# BASELINE.json configs C1..C5; s, lambda, mu, PDE per the paper's schedules (reading R6)
 CONFIGS = {
     "c1": dict(d=1, m=50, n=100_000, s=2.0, lam=1e5 ** -0.8, kind="sobolev", xkind=0, ykind=0,
                desc="C1 Sobolev d=1 s=2 m=50 n=1e5 uniform X on [-1,1], Y=sin-like+N(0,1)"),
     "c2": dict(d=1, m=1000, n=10_000_000_000, s=1.0, lam=1e10 ** (-2.0 / 3.0), kind="sobolev", xkind=0, ykind=0,
                desc="C2 Sobolev d=1 s=1 m=1000 n=1e10 uniform X on [-1,1], Y=sin-like+N(0,1)"),
+    "c3": dict(d=2, m=64, n=1_000_000_000, s=2.0, lam=1e-6, kind="sobolev", xkind=0, ykind=1,
+               desc="C3 Sobolev d=2 s=2 m=64 (129^2 modes, 257^2 moments) n=1e9 uniform X, Y=exp(x1)cos(x2)-like+N(0,1)"),
+    "c4": dict(d=2, m=32, n=100_000_000, s=2.0, lam=1e8 ** (-2.0 / 3.0), kind="pik_box", xkind=0, ykind=1, mu_pde=1.0,
+               desc="C4 physics-informed d=2 space-time heat penalty d_t f - d_xx f on [-1,1]^2, mu=1, s=2, m=32, n=1e8"),
+    "c5": dict(d=10, m=50, n=1_000_000_000, s=2.0, lam=1e9 ** -0.8, kind="additive", xkind=0, ykind=2,
+               desc="C5 low-bias additive d=10 m=50 n=1e9 (10 1-D moment/rhs passes + 45 pairwise 2-D cross moments), X SoA"),
 }
 NOMINAL_HBM_GBS = 8000.0
+ATOMS_RANDOM_PEAK = 2.604e12  # measured random-address int32 ATOMS lane-ops/s, chip-wide (profiles/r01_microbench_spread.log)
 
 
 def parse():
@@ -46,7 +54,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="fk", choices=["fk", "reference"])
-    ap.add_argument("--n", type=float, default=None, help="override n (parity/profiling runs only)")
+    ap.add_argument("--n", type=float, default=None, help="override n (profiling runs only)")
     ap.add_argument("--eps", type=float, default=1e-6)
     ap.add_argument("--xkind", default=None, choices=[None, "uniform", "gaussian"])
     ap.add_argument("--no-e2e", action="store_true")
@@ -56,33 +64,51 @@ def parse():
     return ap.parse_args()
 
 
+def pi_kwargs(cfg):
+    return dict(mu_pde=cfg["mu_pde"], **HEAT) if cfg["kind"] == "pik_box" else {}
+
+
 # ---------------------------------------------------------------------------------------------
 # CPU oracle timing (cpu_baseline leg and --impl reference); the only place bench runs oracle/
 # ---------------------------------------------------------------------------------------------
 def oracle_fit_rate(cfg, target_s: float):
-    import numpy as np
-
+    """(samples/s, sample size, seconds, threads, note) of the fp64 oracle on a bounded sample."""
     import datagen
     import oracle
 
     oracle.build()
     d, m = cfg["d"], cfg["m"]
     xk = "uniform" if cfg["xkind"] == 0 else "gaussian"
+    yk = {0: "sin", 1: "expcos", 2: "additive"}[cfg["ykind"]]
+    D = d * (2 * m + 1) if cfg["kind"] == "additive" else (2 * m + 1) ** d
+    with_solve = D <= 5000
+    note = "moments+rhs by fp64 direct sum" + (" + dense solve" if with_solve else "; the dense solve (D=%d) is not timed on CPU" % D)
 
     def one(n):
-        X, Y = datagen.dataset(n, d=d, xkind=xk, seed=0)
+        X, Y = datagen.dataset(n, d=d, xkind=xk, ykind=yk, seed=0)
         t0 = time.perf_counter()
-        mu = oracle.moments(X, 1.0, m)
-        r = oracle.rhs(X, Y, 1.0, m)
-        oracle.solve(mu, r, n, d, m, cfg["lam"], cfg["kind"], cfg["s"])
+        if cfg["kind"] == "additive":
+            mu_l = [oracle.moments(X[:, l], 1.0, m) for l in range(d)]
+            r_l = [oracle.rhs(X[:, l], Y, 1.0, m) for l in range(d)]
+            G = oracle.cross_moments(X, 1.0, m)
+            if with_solve:
+                oracle.solve_additive(mu_l, r_l, G, n, d, m, cfg["lam"])
+        else:
+            mu = oracle.moments(X, 1.0, m)
+            r = oracle.rhs(X, Y, 1.0, m)
+            if with_solve:
+                kw = dict(pi_kwargs(cfg), L=1.0) if cfg["kind"] == "pik_box" else {}
+                oracle.solve(mu, r, n, d, m, cfg["lam"], cfg["kind"], cfg["s"], **kw)
         return time.perf_counter() - t0
 
-    n0 = 2000
-    t0 = one(n0)
-    n1 = int(max(n0, min(5_000_000, n0 * target_s / max(t0, 1e-3))))
-    t1 = one(n1)
-    cores = oracle.num_threads()
-    return n1 / t1, n1, t1, cores
+    n, t = 256, one(256)
+    while t < target_s / 4 and n < 20_000_000:
+        n *= 4
+        t = one(n)
+    if t < target_s * 0.6:
+        n = int(n * target_s / max(t, 1e-3))
+        t = one(n)
+    return n / t, n, t, oracle.num_threads(), note
 
 
 def cpu_model():
@@ -99,11 +125,10 @@ def run_reference(args, cfg, rank, world):
     if rank != 0:
         return 0
     rates = []
-    n_s = None
-    cores = None
+    n_s = cores = note = None
     target = max(2.0, min(10.0, 150.0 / max(1, args.steps + args.warmup)))
     for i in range(args.warmup + args.steps):
-        rate, n_s, t, cores = oracle_fit_rate(cfg, target)
+        rate, n_s, t, cores, note = oracle_fit_rate(cfg, target)
         if i >= args.warmup:
             rates.append(rate)
     v = statistics.median(rates)
@@ -112,9 +137,9 @@ def run_reference(args, cfg, rank, world):
         "warmup": args.warmup, "ms_per_step": 1e3 * n_s / v, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg["desc"], "n": cfg["n"], "d": cfg["d"], "m": cfg["m"], "s": cfg["s"], "lambda": cfg["lam"],
-                   "sample_per_step": n_s, "note": "fp64 direct-sum oracle (oracle/direct.c, OpenMP) + numpy dense solve on a bounded sample"},
+                   "sample_per_step": n_s, "note": "CPU oracle (oracle/direct.c OpenMP + numpy) on a bounded sample: " + note},
         "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cores, "kind": "oracle",
-                         "sample": f"{n_s} samples of the same workload per step ({cpu_model()})"},
+                         "sample": f"{n_s} samples of the same workload per step ({cpu_model()}); {note}"},
         "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -184,10 +209,15 @@ def measured_peaks():
 def ncu_traffic(config: str):
     """dram bytes per sample of the spreading kernel from the committed ncu --set full capture."""
     try:
-        t = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-        return t.get(config)
+        return json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(config)
     except (OSError, ValueError):
         return None
+
+
+def es_width(eps):
+    import math
+
+    return min(16, max(4, int(math.ceil(math.log10(1.0 / eps))) + 1))
 
 
 # ---------------------------------------------------------------------------------------------
@@ -209,9 +239,9 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_2509_02649_b200 import build, fk
-    from paper_2509_02649_b200.fit import HostStreamer, _moment_buffers, fit_distributed
     from datagen.device import gen_dataset
+    from paper_2509_02649_b200 import build, fk
+    from paper_2509_02649_b200.fit import _moment_buffers, additive_buffers, fit_additive_distributed, fit_distributed
 
     if not os.path.exists(fk.LIB_PATH):
         build.build()
@@ -224,14 +254,26 @@ def main():
     lo = n * rank // world
     hi = n * (rank + 1) // world
     n_loc = hi - lo
-    X = torch.empty((n_loc,) if d == 1 else (n_loc, d), dtype=torch.float32, device=dev)
+    additive = cfg["kind"] == "additive"
     Y = torch.empty(n_loc, dtype=torch.float32, device=dev)
-    gen_dataset(X, Y, n_loc, d, i0=lo, xkind=cfg["xkind"], ykind=cfg["ykind"], seed=0)
-    buffers = _moment_buffers(d, m, dev)
-    theta = torch.empty((2 * m + 1) ** d, dtype=torch.complex128, device=dev)
+    if additive:  # SoA: one contiguous column per feature
+        Xsoa = torch.empty((d, n_loc), dtype=torch.float32, device=dev)
+        gen_dataset(Xsoa, Y, n_loc, d, i0=lo, xkind=cfg["xkind"], ykind=cfg["ykind"], seed=0, stride_n=1, stride_d=n_loc)
+        X = Xsoa.t()
+        buffers = additive_buffers(d, m, dev)
+        theta = torch.empty(d * (2 * m + 1), dtype=torch.complex128, device=dev)
+    else:
+        X = torch.empty((n_loc,) if d == 1 else (n_loc, d), dtype=torch.float32, device=dev)
+        gen_dataset(X, Y, n_loc, d, i0=lo, xkind=cfg["xkind"], ykind=cfg["ykind"], seed=0)
+        buffers = _moment_buffers(d, m, dev)
+        theta = torch.empty((2 * m + 1) ** d, dtype=torch.complex128, device=dev)
+    pik = pi_kwargs(cfg)
 
     def step():
-        fit_distributed(X, Y, n, L, m, cfg["lam"], cfg["kind"], cfg["s"], eps, buffers=buffers, theta_out=theta)
+        if additive:
+            fit_additive_distributed(X, Y, n, L, m, cfg["lam"], eps, buffers=buffers, theta_out=theta)
+        else:
+            fit_distributed(X, Y, n, L, m, cfg["lam"], cfg["kind"], cfg["s"], eps, buffers=buffers, theta_out=theta, **pik)
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -262,28 +304,48 @@ def main():
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    ms_step = ms_max / args.steps
+    ms_step = float(t.item()) / args.steps
     value = n / (ms_step * 1e-3)
 
-    # roofline of the dominant kernel (the spread): algorithmic bytes = 8 B per local sample
-    bytes_launch = n_loc * 8
-    avg_spread_ms = spread_ms / max(1, spread_launches)
-    achieved = bytes_launch / (avg_spread_ms * 1e-3) / 1e9
     peaks = measured_peaks()
-    peak = peaks.get("hbm_gbs", 6650.0)
-    tr = ncu_traffic(args.config)
-    traffic = None if tr is None else tr["dram_bytes_per_sample"] * n_loc
+    spread_per_step_ms = spread_ms / args.steps
+    bytes_step = n_loc * (d + 1) * 4 if not additive else n_loc * (d + 1) * 4
+    if d == 1:
+        # dominant kernel = the one-pass spread: algorithmic 8 B per local sample
+        avg = spread_ms / max(1, spread_launches)
+        achieved = n_loc * 8 / (avg * 1e-3) / 1e9
+        peak = peaks.get("hbm_gbs", 6650.0)
+        tr = ncu_traffic(args.config)
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": None if tr is None else tr["dram_bytes_per_sample"] * n_loc,
+                "kernel": "k_spread1d_bs3 (one pass over X, Y)",
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s",
+                "frac_of_nominal_8tbs": achieved / NOMINAL_HBM_GBS, "spread_ms_avg": avg, "bytes_per_launch": n_loc * 8,
+                "spread_share_of_step": spread_per_step_ms / ms_step}
+    else:
+        # d >= 2 / additive: bound by random-address shared-memory atomics (2 w^2 per sample for d = 2,
+        # npairs w^2 + 2 d x 4 per sample for the additive model); peak = the measured random ATOMS rate
+        w = es_width(eps)
+        if additive:
+            atoms = n_loc * (d * (d - 1) // 2 * w * w + d * 8)
+        else:
+            atoms = n_loc * 2 * w * w
+        achieved = atoms / (spread_per_step_ms * 1e-3) / 1e9
+        roof = {"bound": "alu", "achieved": achieved, "peak": ATOMS_RANDOM_PEAK / 1e9, "unit": "Gatomic/s",
+                "frac": achieved * 1e9 / ATOMS_RANDOM_PEAK, "traffic": None,
+                "kernel": "spreading kernels (shared-memory int32 atomics)",
+                "peak_source": "measured random-address ATOMS.ADD rate, profiles/r01_microbench_spread.log",
+                "hbm_gbs": bytes_step / (spread_per_step_ms * 1e-3) / 1e9, "spread_ms_per_step": spread_per_step_ms,
+                "spread_share_of_step": spread_per_step_ms / ms_step, "atomics_per_step": atoms}
 
-    # end-to-end through the public API from pinned host buffers (bounded n, same metric)
     e2e = None
-    if not args.no_e2e and rank == 0:
+    if not args.no_e2e and rank == 0 and not additive:
         e2e = run_e2e(args, cfg, dev, eps)
     cpu = None
     if not args.no_cpu and rank == 0 and world == 1:
-        rate, n_s, t_s, cores = oracle_fit_rate(cfg, args.cpu_seconds)
+        rate, n_s, t_s, cores, note = oracle_fit_rate(cfg, args.cpu_seconds)
         cpu = {"value": rate, "unit": "samples/s", "cores": cores, "kind": "oracle",
-               "sample": f"{n_s} samples of {args.config} (moments+rhs by fp64 direct sum, dense solve) in {t_s:.1f} s on {cpu_model()}"}
+               "sample": f"{n_s} samples of {args.config} in {t_s:.1f} s on {cpu_model()}: {note}"}
     if world > 1:
         dist.barrier()
     if rank == 0:
@@ -291,17 +353,12 @@ def main():
             "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": cfg["desc"], "n": n, "d": d, "m": m, "s": cfg["s"], "lambda": cfg["lam"], "eps": eps,
-                       "L": L, "xkind": "uniform" if cfg["xkind"] == 0 else "gaussian",
-                       "parallelism": f"dp{world}: sample shards, NCCL all-reduce of [mu|r], solve on rank 0",
-                       "cache": f"inputs {n_loc * 8 / 1e9:.1f} GB/GPU >> 126 MB L2 (no flush needed)"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic, "kernel": "k_spread1d_bs3 (one pass over X, Y)",
-                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s",
-                         "frac_of_nominal_8tbs": achieved / NOMINAL_HBM_GBS, "spread_ms_avg": avg_spread_ms,
-                         "spread_share_of_step": avg_spread_ms / ms_step if world == 1 else None,
-                         "bytes_per_launch": bytes_launch},
-            "hbm_gbs_fit": n * 8 / (ms_step * 1e-3) / 1e9 / world,
+            "config": {"workload": cfg["desc"], "n": n, "d": d, "m": m, "s": cfg["s"], "lambda": cfg["lam"], "eps": eps, "L": L,
+                       "kind": cfg["kind"], "xkind": "uniform" if cfg["xkind"] == 0 else "gaussian",
+                       "parallelism": f"dp{world}: sample shards, NCCL all-reduce of the moment vector, solve on rank 0",
+                       "cache": f"inputs {bytes_step / 1e9:.1f} GB/GPU >> 126 MB L2 (no flush needed)"},
+            "roofline": roof,
+            "hbm_gbs_fit": n_loc * (d + 1) * 4 / (ms_step * 1e-3) / 1e9,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": kernels,
@@ -315,18 +372,19 @@ def main():
 
 
 def run_e2e(args, cfg, dev, eps):
+    """Same metric through the public API from pinned HOST buffers: chunked H2D (copy stream,
+    overlapped with the spreading of the previous chunk) + fk_solve + theta D2H, every step."""
     import torch
 
-    from paper_2509_02649_b200.fit import HostStreamer, _moment_buffers
-    from paper_2509_02649_b200 import fk
     from datagen.device import gen_dataset
+    from paper_2509_02649_b200 import fk
+    from paper_2509_02649_b200.fit import HostStreamer, _moment_buffers
 
     d, m = cfg["d"], cfg["m"]
     n = int(min(args.e2e_n, cfg["n"]))
     chunk = 1 << 26
     Xh = torch.empty((n,) if d == 1 else (n, d), dtype=torch.float32, pin_memory=True)
     Yh = torch.empty(n, dtype=torch.float32, pin_memory=True)
-    # fill the pinned host buffers chunk by chunk with the same seeded generator
     tmpx = torch.empty((chunk,) if d == 1 else (chunk, d), dtype=torch.float32, device=dev)
     tmpy = torch.empty(chunk, dtype=torch.float32, device=dev)
     for lo in range(0, n, chunk):
@@ -337,11 +395,13 @@ def run_e2e(args, cfg, dev, eps):
     del tmpx, tmpy
     st = HostStreamer(chunk, d, torch.float32, dev)
     _, mu, r = _moment_buffers(d, m, dev)
-    theta_h = torch.empty((2 * m + 1) ** d, dtype=torch.complex128, pin_memory=True)
+    D = (2 * m + 1) ** d
+    theta_h = torch.empty(D, dtype=torch.complex128, pin_memory=True)
+    pik = pi_kwargs(cfg)
 
     def step():
         st.moments(Xh, Yh, 1.0, m, eps, mu, r)
-        th, _ = fk.fk_solve(mu.reshape(-1), r.reshape(-1), n, d, m, 1.0, cfg["lam"], cfg["kind"], cfg["s"], report=False)
+        th, _ = fk.fk_solve(mu.reshape(-1), r.reshape(-1), n, d, m, 1.0, cfg["lam"], cfg["kind"], cfg["s"], report=False, **pik)
         theta_h.copy_(th, non_blocking=True)
 
     step()
@@ -355,9 +415,9 @@ def run_e2e(args, cfg, dev, eps):
     e1.record(s)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
-    return {"value": n / (ms * 1e-3), "unit": "samples/s", "h2d_bytes_per_step": n * (d + 1) * 4,
-            "d2h_bytes_per_step": (2 * m + 1) ** d * 16, "n": n, "ms_per_step": ms,
-            "path": "paper_2509_02649_b200.fit.HostStreamer + fk_solve: pinned host X,Y -> chunked H2D on a copy stream overlapped with fk_rhs_type1; theta D2H"}
+    return {"value": n / (ms * 1e-3), "unit": "samples/s", "h2d_bytes_per_step": n * (d + 1) * 4, "d2h_bytes_per_step": D * 16,
+            "n": n, "ms_per_step": ms,
+            "path": "fit.HostStreamer + fk_solve: pinned host X,Y -> chunked H2D on a copy stream overlapped with fk_rhs_type1; theta D2H"}
 
 
 if __name__ == "__main__":

@@ -128,19 +128,6 @@ __device__ double2 entry(const SysArgs& g, int i, int j) {
   return v;
 }
 
-__global__ void k_assemble(SysArgs g, double2* __restrict__ A) {  // column-major, lower triangle + diagonal
-  const int64_t D = g.D;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < D * D; t += (int64_t)gridDim.x * blockDim.x) {
-    const int j = (int)(t / D), i = (int)(t % D);
-    if (i >= j) A[t] = entry(g, i, j);
-  }
-}
-
-__global__ void k_scale_copy(const double2* __restrict__ r, double inv_n, int D, double2* __restrict__ b) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < D) b[i] = make_double2(r[i].x * inv_n, r[i].y * inv_n);
-}
-
 // res[0] += ||A theta - b||^2, res[1] += ||b||^2, with A evaluated on the fly (one warp per row)
 __global__ void k_residual(SysArgs g, const double2* __restrict__ theta, const double2* __restrict__ r, double* __restrict__ res) {
   const int lane = threadIdx.x & 31;
@@ -189,12 +176,112 @@ int unknowns(int d, int m, int kind) {
   return D;
 }
 
+// ---- real form of the Hermitian system (DESIGN.md §5 "Solve") ----
+// For real Y the solution is Hermitian, theta_{-k} = conj theta_k, so theta = P z with z real:
+// z = (a_0, a_1, b_1, a_2, b_2, ...) over the centre and the positive half of the mode grid
+// (per feature block for the additive model), theta_k = a_k + i b_k, theta_{-k} = a_k - i b_k.
+// Then P^* A P z = P^* r/n is real symmetric positive definite with the same unique solution
+// and a quarter of the complex Cholesky's flops.  Column u of P has at most two entries.
+struct PCol {
+  int i[2];
+  double2 a[2];
+  int cnt;
+};
+
+__device__ __forceinline__ int neg_index(const SysArgs& g, int i) {
+  if (g.kind == FK_ADDITIVE) {
+    const int S = 2 * g.m + 1, l = i / S;
+    return l * S + (S - 1 - (i - l * S));
+  }
+  return g.D - 1 - i;
+}
+
+__device__ __forceinline__ PCol pcol(const SysArgs& g, int u) {
+  PCol p;
+  int base, c0, v;
+  if (g.kind == FK_ADDITIVE) {
+    const int S = 2 * g.m + 1;
+    base = (u / S) * S;
+    c0 = base + g.m;
+    v = u % S;
+  } else {
+    base = 0;
+    c0 = (g.D - 1) / 2;
+    v = u;
+  }
+  if (v == 0) {
+    p.cnt = 1;
+    p.i[0] = c0;
+    p.a[0] = make_double2(1.0, 0.0);
+    return p;
+  }
+  const int t = (v + 1) >> 1;
+  const int i = c0 + t;
+  p.cnt = 2;
+  p.i[0] = i;
+  p.i[1] = neg_index(g, i);
+  if (v & 1) {  // a_k: e_k + e_{-k}
+    p.a[0] = make_double2(1.0, 0.0);
+    p.a[1] = make_double2(1.0, 0.0);
+  } else {      // b_k: i e_k - i e_{-k}
+    p.a[0] = make_double2(0.0, 1.0);
+    p.a[1] = make_double2(0.0, -1.0);
+  }
+  (void)base;
+  return p;
+}
+
+__global__ void k_assemble_real(SysArgs g, double* __restrict__ M) {  // column-major, lower triangle
+  const int64_t D = g.D;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < D * D; t += (int64_t)gridDim.x * blockDim.x) {
+    const int v = (int)(t / D), u = (int)(t % D);
+    if (u < v) continue;
+    const PCol pu = pcol(g, u), pv = pcol(g, v);
+    double s = 0.0;
+    for (int x = 0; x < pu.cnt; ++x)
+      for (int y = 0; y < pv.cnt; ++y) {
+        const double2 a = entry(g, pu.i[x], pv.i[y]);
+        const double2 c = cmul(cmul(cconj(pu.a[x]), a), pv.a[y]);
+        s += c.x;
+      }
+    M[t] = s;
+  }
+}
+
+__global__ void k_rhs_real(SysArgs g, const double2* __restrict__ r, double* __restrict__ c) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= g.D) return;
+  const PCol p = pcol(g, u);
+  double s = 0.0;
+  for (int x = 0; x < p.cnt; ++x) {
+    const double2 b = make_double2(r[p.i[x]].x * g.inv_n, r[p.i[x]].y * g.inv_n);
+    s += cmul(cconj(p.a[x]), b).x;
+  }
+  c[u] = s;
+}
+
+__global__ void k_theta_from_real(SysArgs g, const double* __restrict__ z, double2* __restrict__ theta) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= g.D) return;
+  const int v = g.kind == FK_ADDITIVE ? u % (2 * g.m + 1) : u;
+  const int base = g.kind == FK_ADDITIVE ? u - v : 0;
+  if (v == 0) {
+    const int c0 = g.kind == FK_ADDITIVE ? base + g.m : (g.D - 1) / 2;
+    theta[c0] = make_double2(z[u], 0.0);
+  } else if (v & 1) {
+    const PCol p = pcol(g, u);
+    const double a = z[u], b = z[u + 1];
+    theta[p.i[0]] = make_double2(a, b);
+    theta[p.i[1]] = make_double2(a, -b);
+  }
+}
+
 fk_status lwork_for(int D, int* lwork) {
   std::lock_guard<std::mutex> lk(g_sol_mu);
   cusolverDnHandle_t h;
   FK_TRY(handle_for_device(&h));
-  if (cusolverDnZpotrf_bufferSize(h, CUBLAS_FILL_MODE_LOWER, D, nullptr, D, lwork) != CUSOLVER_STATUS_SUCCESS)
-    return fail(FK_E_CUDA, "cusolverDnZpotrf_bufferSize failed");
+  if (cusolverDnDpotrf_bufferSize(h, CUBLAS_FILL_MODE_LOWER, D, nullptr, D, lwork) != CUSOLVER_STATUS_SUCCESS)
+    return fail(FK_E_CUDA, "cusolverDnDpotrf_bufferSize failed");
   return FK_OK;
 }
 
@@ -205,8 +292,9 @@ size_t solve_ws_bytes(int d, int m, int kind) {
   int lwork = 0;
   if (lwork_for(D, &lwork) != FK_OK) return 0;
   Bump b(nullptr, 0);
-  b.take((size_t)D * D * 16);
-  b.take((size_t)lwork * 16);
+  b.take((size_t)D * D * 8);
+  b.take((size_t)lwork * 8);
+  b.take((size_t)D * 8);
   b.take(64);
   return b.used + 256;
 }
@@ -241,8 +329,9 @@ fk_status solve_run(const fk_problem* P, double* theta, fk_solve_report* rep, vo
   int lwork = 0;
   FK_TRY(lwork_for(D, &lwork));
   Bump b(ws, ws_bytes);
-  double2* A = (double2*)b.take((size_t)D * D * 16);
-  double2* work = (double2*)b.take((size_t)lwork * 16);
+  double* M = (double*)b.take((size_t)D * D * 8);
+  double* work = (double*)b.take((size_t)lwork * 8);
+  double* z = (double*)b.take((size_t)D * 8);
   int* info = (int*)b.take(16);
   double* res = (double*)(info + 4);
   if (!b.ok()) return fail(FK_E_WORKSPACE, "fk_solve: workspace too small");
@@ -254,8 +343,8 @@ fk_status solve_run(const fk_problem* P, double* theta, fk_solve_report* rep, vo
     cudaEventRecord(e0, s);
   }
   const int sms = device_sm_count();
-  k_assemble<<<sms * 8, 256, 0, s>>>(g, A);
-  k_scale_copy<<<(D + 255) / 256, 256, 0, s>>>((const double2*)P->rhs, g.inv_n, D, (double2*)theta);
+  k_assemble_real<<<sms * 8, 256, 0, s>>>(g, M);
+  k_rhs_real<<<(D + 255) / 256, 256, 0, s>>>(g, (const double2*)P->rhs, z);
   FK_CUDA_TRY(cudaGetLastError());
   count_launch(2);
   {
@@ -263,13 +352,14 @@ fk_status solve_run(const fk_problem* P, double* theta, fk_solve_report* rep, vo
     cusolverDnHandle_t h;
     FK_TRY(handle_for_device(&h));
     if (cusolverDnSetStream(h, s) != CUSOLVER_STATUS_SUCCESS) return fail(FK_E_CUDA, "cusolverDnSetStream failed");
-    if (cusolverDnZpotrf(h, CUBLAS_FILL_MODE_LOWER, D, (cuDoubleComplex*)A, D, (cuDoubleComplex*)work, lwork, info) !=
-        CUSOLVER_STATUS_SUCCESS)
-      return fail(FK_E_CUDA, "cusolverDnZpotrf failed");
-    if (cusolverDnZpotrs(h, CUBLAS_FILL_MODE_LOWER, D, 1, (const cuDoubleComplex*)A, D, (cuDoubleComplex*)theta, D, info) !=
-        CUSOLVER_STATUS_SUCCESS)
-      return fail(FK_E_CUDA, "cusolverDnZpotrs failed");
+    if (cusolverDnDpotrf(h, CUBLAS_FILL_MODE_LOWER, D, M, D, work, lwork, info) != CUSOLVER_STATUS_SUCCESS)
+      return fail(FK_E_CUDA, "cusolverDnDpotrf failed");
+    if (cusolverDnDpotrs(h, CUBLAS_FILL_MODE_LOWER, D, 1, M, D, z, D, info) != CUSOLVER_STATUS_SUCCESS)
+      return fail(FK_E_CUDA, "cusolverDnDpotrs failed");
   }
+  k_theta_from_real<<<(D + 255) / 256, 256, 0, s>>>(g, z, (double2*)theta);
+  FK_CUDA_TRY(cudaGetLastError());
+  count_launch();
   if (rep) {
     cudaEventRecord(e1, s);
     FK_CUDA_TRY(cudaMemsetAsync(res, 0, 16, s));

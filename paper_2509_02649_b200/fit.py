@@ -68,8 +68,9 @@ def broadcast_theta(theta: torch.Tensor, group=None, src: int = 0) -> None:
 
 def fit_distributed(X_shard: torch.Tensor, Y_shard: torch.Tensor, n_total: int, L: float, m: int, lam: float,
                     kind: str = "sobolev", s: float = 1.0, eps: float = 1e-6, group=None, buffers=None, theta_out=None,
-                    report: bool = False) -> FitResult:
-    """Data-parallel fit: call on every rank with that rank's shard (one process per GPU)."""
+                    report: bool = False, **pi) -> FitResult:
+    """Data-parallel fit: call on every rank with that rank's shard (one process per GPU).
+    pi: mu_pde, alpha, a_alpha, box for kind = "pik_box"."""
     import torch.distributed as dist
 
     d = 1 if X_shard.dim() == 1 else X_shard.shape[1]
@@ -81,9 +82,40 @@ def fit_distributed(X_shard: torch.Tensor, Y_shard: torch.Tensor, n_total: int, 
         theta_out = torch.empty(D, dtype=torch.complex128, device=X_shard.device)
     rep = None
     if _world(group) == 1 or dist.get_rank(group) == 0:
-        _, rep = fk.fk_solve(mu.reshape(-1), r.reshape(-1), n_total, d, m, L, lam, kind, s, theta_out=theta_out, report=report)
+        _, rep = fk.fk_solve(mu.reshape(-1), r.reshape(-1), n_total, d, m, L, lam, kind, s, theta_out=theta_out, report=report, **pi)
     broadcast_theta(theta_out, group)
     return FitResult(theta_out, mu, r, n_total, rep)
+
+
+def additive_buffers(d: int, m: int, device):
+    """One complex128 buffer [mu_l (d x (4m+1)) | r_l (d x (2m+1)) | G (pairs x (2m+1)^2)] and its views."""
+    npairs = d * (d - 1) // 2
+    a, b, c = d * (4 * m + 1), d * (2 * m + 1), npairs * (2 * m + 1) ** 2
+    buf = torch.zeros(a + b + c, dtype=torch.complex128, device=device)
+    return buf, buf[:a].view(d, 4 * m + 1), buf[a:a + b].view(d, 2 * m + 1), buf[a + b:].view(npairs, 2 * m + 1, 2 * m + 1)
+
+
+def fit_additive_distributed(X_shard: torch.Tensor, Y_shard: torch.Tensor, n_total: int, L: float, m: int, lam: float,
+                             eps: float = 1e-6, group=None, buffers=None, theta_out=None, report: bool = False) -> FitResult:
+    """Low-bias additive model: per-feature 1-D moments / rhs (one fk_rhs_type1 pass
+    per feature column), all pairwise cross moments (fk_additive_cross_moments), one all-reduce
+    of everything, block solve on rank 0, broadcast.  X_shard: (n, d), any strides (SoA is
+    coalesced for both kernels)."""
+    import torch.distributed as dist
+
+    d = X_shard.shape[1]
+    buf, mus, rs, G = buffers if buffers is not None else additive_buffers(d, m, X_shard.device)
+    for l in range(d):
+        fk.fk_rhs_type1(X_shard[:, l], Y_shard, L, m, eps, r_out=rs[l], mu_out=mus[l], check=False)
+    fk.fk_additive_cross_moments(X_shard, L, m, eps, G_out=G, check=False)
+    reduce_moments(buf, group)
+    if theta_out is None:
+        theta_out = torch.empty(d * (2 * m + 1), dtype=torch.complex128, device=X_shard.device)
+    rep = None
+    if _world(group) == 1 or dist.get_rank(group) == 0:
+        _, rep = fk.fk_solve(mus, rs, n_total, d, m, L, lam, "additive", cross=G, theta_out=theta_out, report=report)
+    broadcast_theta(theta_out, group)
+    return FitResult(theta_out, mus, rs, n_total, rep)
 
 
 class HostStreamer:
