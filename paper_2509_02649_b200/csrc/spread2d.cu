@@ -12,6 +12,7 @@
 // the fp64 path.  Partials are reduced per fine-grid cell in a fixed CTA order, FFT'd (cuFFT 2-D
 // D2Z, batched over pairs) and deconvolved by psi-hat(q0) psi-hat(q1).
 #include <cmath>
+#include <type_traits>
 
 #include "fk_internal.cuh"
 
@@ -67,31 +68,25 @@ __device__ __forceinline__ int first_tap_d(double f, int w) {
   return (w & 1) ? (f > 0.5 ? 1 : 0) - (w >> 1) : (f > 0.0 ? 1 : 0) - (w >> 1);
 }
 
-__device__ __forceinline__ void es_taps_f32(float f, int d0, int w, float beta, float* psi) {
-  const float inv = 2.0f / (float)w;
+template <int W>
+__device__ __forceinline__ void es_taps_f32(float f, int d0, float beta, float* psi) {
+  const float inv = 2.0f / (float)W;
 #pragma unroll
-  for (int i = 0; i < kW; ++i) {
-    if (i < w) {
-      const float z = ((float)(d0 + i) - f) * inv;
-      const float v = 1.0f - z * z;
-      psi[i] = v > 0.0f ? __expf(beta * (sqrtf(v) - 1.0f)) : 0.0f;
-    } else {
-      psi[i] = 0.0f;
-    }
+  for (int i = 0; i < W; ++i) {
+    const float z = ((float)(d0 + i) - f) * inv;
+    const float v = 1.0f - z * z;
+    psi[i] = v > 0.0f ? __expf(beta * (sqrtf(v) - 1.0f)) : 0.0f;
   }
 }
 
-__device__ __forceinline__ void es_taps_f64(double f, int d0, int w, double beta, double* psi) {
-  const double inv = 2.0 / (double)w;
+template <int W>
+__device__ __forceinline__ void es_taps_f64(double f, int d0, double beta, double* psi) {
+  const double inv = 2.0 / (double)W;
 #pragma unroll
-  for (int i = 0; i < kW; ++i) {
-    if (i < w) {
-      const double z = ((double)(d0 + i) - f) * inv;
-      const double v = 1.0 - z * z;
-      psi[i] = v > 0.0 ? exp(beta * (sqrt(v) - 1.0)) : 0.0;
-    } else {
-      psi[i] = 0.0;
-    }
+  for (int i = 0; i < W; ++i) {
+    const double z = ((double)(d0 + i) - f) * inv;
+    const double v = 1.0 - z * z;
+    psi[i] = v > 0.0 ? exp(beta * (sqrt(v) - 1.0)) : 0.0;
   }
 }
 
@@ -111,34 +106,34 @@ struct Tile {
 };
 
 // fixed-point spread of one sample into a tile (fp32 path); returns false if out of range
-template <bool SIGNED>
+template <bool SIGNED, int W>
 __device__ __forceinline__ void spread_fixed(int* T, const Tile& g, int lr /*local first row*/, int lc, const float* py,
-                                             const float* px, int w, float scale, double* carry, int tile_r0, double inv_scale) {
-  for (int a = 0; a < kW; ++a) {
-    if (a >= w) break;
-    const float wy = py[a] * scale;
-    int* row = T + (lr - tile_r0 + a) * g.G + lc;
-    unsigned orr = 0;
+                                             const float* px, float scale, double* carry, int tile_r0, double inv_scale) {
+  int* row = T + (lr - tile_r0) * g.G + lc;
+  unsigned orr = 0;
 #pragma unroll
-    for (int b = 0; b < kW; ++b) {
-      if (b < w) {
-        const int v = __float_as_int(fmaf(wy, px[b], FK_MAGIC)) - FK_MAGIC_BITS;
-        const unsigned o = (unsigned)atomicAdd(row + b, v);
-        orr |= SIGNED ? (o + (1u << 30)) : o;
-      }
+  for (int a = 0; a < W; ++a) {
+    const float wy = py[a] * scale;
+#pragma unroll
+    for (int b = 0; b < W; ++b) {
+      const int v = __float_as_int(fmaf(wy, px[b], FK_MAGIC)) - FK_MAGIC_BITS;
+      const unsigned o = (unsigned)atomicAdd(row + a * g.G + b, v);
+      orr |= SIGNED ? (o + (1u << 30)) : o;
     }
-    if (SIGNED ? (orr & 0x80000000u) : (orr & 0x40000000u))
-      drain_row(row, w, carry + (int64_t)(lr + a) * g.G + lc, inv_scale);
   }
+  if (SIGNED ? (orr & 0x80000000u) : (orr & 0x40000000u))
+    for (int a = 0; a < W; ++a) drain_row(row + a * g.G, W, carry + (int64_t)(lr + a) * g.G + lc, inv_scale);
 }
 
-__device__ __forceinline__ void spread_f64(double* T, const Tile& g, int lr, int lc, const double* py, const double* px, int w,
-                                           double c, int tile_r0) {
-  for (int a = 0; a < kW; ++a) {
-    if (a >= w) break;
+template <int W>
+__device__ __forceinline__ void spread_f64(double* T, const Tile& g, int lr, int lc, const double* py, const double* px, double c,
+                                           int tile_r0) {
+#pragma unroll
+  for (int a = 0; a < W; ++a) {
     double* row = T + (lr - tile_r0 + a) * g.G + lc;
     const double wy = py[a] * c;
-    for (int b = 0; b < w; ++b) atomicAdd(row + b, wy * px[b]);
+#pragma unroll
+    for (int b = 0; b < W; ++b) atomicAdd(row + b, wy * px[b]);
   }
 }
 
@@ -161,7 +156,7 @@ struct Args2 {
 };
 
 // moments (grid A) and rhs (grid B) of d = 2 points, fp32 fixed-point path
-template <bool MU, bool R, bool EXACT>
+template <int W, bool MU, bool R, bool EXACT>
 __global__ void __launch_bounds__(512) k_spread2d_fixed(const float* __restrict__ X, const float* __restrict__ Y, Args2 g) {
   extern __shared__ int sm2[];
   int* A = sm2;
@@ -202,37 +197,37 @@ __global__ void __launch_bounds__(512) k_spread2d_fixed(const float* __restrict_
   __syncthreads();
   const int rA0 = tile * g.gA.R, rB0 = tile * g.gB.R;
   bool bad = false;
-  float px[kW], py[kW];
+  float px[W], py[W];
   for (int64_t j = beg + threadIdx.x; j < end; j += blockDim.x) {
     const float x0 = X[j * g.sn], x1 = X[j * g.sn + g.sd];
     const P1 q0 = place_f32<EXACT>(x0, g.a_hi, g.a_lo);
     const P1 q1 = place_f32<EXACT>(x1, g.a_hi, g.a_lo);
     // range check on the moment grid (both coordinates): |X| <= L
-    const int d00 = first_tap(q0.f, g.w), d01 = first_tap(q1.f, g.w);
+    const int d00 = first_tap(q0.f, W), d01 = first_tap(q1.f, W);
     const int lrA = q0.P + g.KA + d00, lcA = q1.P + g.KA + d01;
-    if ((unsigned)lrA > (unsigned)(g.gA.G - g.w) || (unsigned)lcA > (unsigned)(g.gA.G - g.w) || x0 != x0 || x1 != x1) {
+    if ((unsigned)lrA > (unsigned)(g.gA.G - W) || (unsigned)lcA > (unsigned)(g.gA.G - W) || x0 != x0 || x1 != x1) {
       if (tile == 0) bad = true;
       continue;
     }
     if (MU && lrA >= rA0 && lrA < rA0 + g.gA.R) {
-      es_taps_f32(q0.f, d00, g.w, g.beta_f, py);
-      es_taps_f32(q1.f, d01, g.w, g.beta_f, px);
-      spread_fixed<false>(A, g.gA, lrA, lcA, py, px, g.w, kS2, g.carryA, rA0, kInvS2);
+      es_taps_f32<W>(q0.f, d00, g.beta_f, py);
+      es_taps_f32<W>(q1.f, d01, g.beta_f, px);
+      spread_fixed<false, W>(A, g.gA, lrA, lcA, py, px, kS2, g.carryA, rA0, kInvS2);
     }
     if (R) {
       const P1 h0 = halve(q0, 0.f), h1 = halve(q1, 0.f);
-      const int e0 = first_tap(h0.f, g.w), e1 = first_tap(h1.f, g.w);
+      const int e0 = first_tap(h0.f, W), e1 = first_tap(h1.f, W);
       const int lrB = h0.P + g.KB + e0, lcB = h1.P + g.KB + e1;
       if (lrB >= rB0 && lrB < rB0 + g.gB.R) {
         const float y = Y[j];
-        es_taps_f32(h0.f, e0, g.w, g.beta_f, py);
-        es_taps_f32(h1.f, e1, g.w, g.beta_f, px);
+        es_taps_f32<W>(h0.f, e0, g.beta_f, py);
+        es_taps_f32<W>(h1.f, e1, g.beta_f, px);
         const float ys = y * SY;
         if (fabsf(ys) < 1048576.0f) {
-          spread_fixed<true>(B, g.gB, lrB, lcB, py, px, g.w, ys, g.carryB, rB0, invSY);
+          spread_fixed<true, W>(B, g.gB, lrB, lcB, py, px, ys, g.carryB, rB0, invSY);
         } else {  // outlier / NaN: exact fp64 path straight into the carry grid
-          for (int a = 0; a < g.w; ++a)
-            for (int b = 0; b < g.w; ++b)
+          for (int a = 0; a < W; ++a)
+            for (int b = 0; b < W; ++b)
               atomicAdd(g.carryB + (int64_t)(lrB + a) * g.gB.G + lcB + b, (double)py[a] * px[b] * (double)y);
         }
       }
@@ -251,8 +246,8 @@ __global__ void __launch_bounds__(512) k_spread2d_fixed(const float* __restrict_
 }
 
 // fp64 path (any input dtype): fp64 window, fp64 smem atomics
-template <typename XT, bool MU, bool R>
-__global__ void __launch_bounds__(256) k_spread2d_f64(const XT* __restrict__ X, const XT* __restrict__ Y, Args2 g) {
+template <int W, typename XT>
+__global__ void __launch_bounds__(256) k_spread2d_f64(const XT* __restrict__ X, const XT* __restrict__ Y, Args2 g, bool MU, bool R) {
   extern __shared__ double smd2[];
   double* A = smd2;
   double* B = smd2 + (MU ? g.gA.rows * g.gA.G : 0);
@@ -265,7 +260,7 @@ __global__ void __launch_bounds__(256) k_spread2d_f64(const XT* __restrict__ X, 
   const int64_t end = min(g.n, beg + g.per);
   const int rA0 = tile * g.gA.R, rB0 = tile * g.gB.R;
   bool bad = false;
-  double px[kW], py[kW];
+  double px[W], py[W];
   for (int64_t j = beg + threadIdx.x; j < end; j += blockDim.x) {
     const double x0 = (double)X[j * g.sn], x1 = (double)X[j * g.sn + g.sd];
     const double p0 = x0 * g.a_d, p1 = x1 * g.a_d;
@@ -275,29 +270,29 @@ __global__ void __launch_bounds__(256) k_spread2d_f64(const XT* __restrict__ X, 
       if (tile == 0) bad = true;
       continue;
     }
-    const int d00 = first_tap_d(f0, g.w);
-    const int d01 = first_tap_d(f1, g.w);
+    const int d00 = first_tap_d(f0, W);
+    const int d01 = first_tap_d(f1, W);
     const int lrA = (int)P0 + g.KA + d00, lcA = (int)P1_ + g.KA + d01;
-    if ((unsigned)lrA > (unsigned)(g.gA.G - g.w) || (unsigned)lcA > (unsigned)(g.gA.G - g.w)) {
+    if ((unsigned)lrA > (unsigned)(g.gA.G - W) || (unsigned)lcA > (unsigned)(g.gA.G - W)) {
       if (tile == 0) bad = true;
       continue;
     }
     if (MU && lrA >= rA0 && lrA < rA0 + g.gA.R) {
-      es_taps_f64(f0, d00, g.w, g.beta_d, py);
-      es_taps_f64(f1, d01, g.w, g.beta_d, px);
-      spread_f64(A, g.gA, lrA, lcA, py, px, g.w, 1.0, rA0);
+      es_taps_f64<W>(f0, d00, g.beta_d, py);
+      es_taps_f64<W>(f1, d01, g.beta_d, px);
+      spread_f64<W>(A, g.gA, lrA, lcA, py, px, 1.0, rA0);
     }
     if (R) {
       const double h0 = 0.5 * p0, h1 = 0.5 * p1;
       const double H0 = floor(h0), H1 = floor(h1);
       const double g0 = h0 - H0, g1 = h1 - H1;
-      const int e0 = first_tap_d(g0, g.w);
-      const int e1 = first_tap_d(g1, g.w);
+      const int e0 = first_tap_d(g0, W);
+      const int e1 = first_tap_d(g1, W);
       const int lrB = (int)H0 + g.KB + e0, lcB = (int)H1 + g.KB + e1;
       if (lrB >= rB0 && lrB < rB0 + g.gB.R) {
-        es_taps_f64(g0, e0, g.w, g.beta_d, py);
-        es_taps_f64(g1, e1, g.w, g.beta_d, px);
-        spread_f64(B, g.gB, lrB, lcB, py, px, g.w, (double)Y[j], rB0);
+        es_taps_f64<W>(g0, e0, g.beta_d, py);
+        es_taps_f64<W>(g1, e1, g.beta_d, px);
+        spread_f64<W>(B, g.gB, lrB, lcB, py, px, (double)Y[j], rB0);
       }
     }
   }
@@ -330,7 +325,7 @@ struct ArgsX {
   int* d_status;
 };
 
-template <bool EXACT>
+template <int W, bool EXACT>
 __global__ void __launch_bounds__(512) k_cross2d_fixed(const float* __restrict__ X, const ArgsX* __restrict__ gp) {
   extern __shared__ int smx[];
   const ArgsX& g = *gp;
@@ -345,7 +340,7 @@ __global__ void __launch_bounds__(512) k_cross2d_fixed(const float* __restrict__
   const int64_t end = min(g.n, beg + g.per);
   Tile t{g.G, g.K, g.G, g.G};
   bool bad = false;
-  float px[kW], py[kW];
+  float px[W], py[W];
   for (int64_t j = beg + threadIdx.x; j < end; j += blockDim.x) {
     for (int q = 0; q < np; ++q) {
       const int l1 = g.pl1[p0 + q], l2 = g.pl2[p0 + q];
@@ -353,15 +348,15 @@ __global__ void __launch_bounds__(512) k_cross2d_fixed(const float* __restrict__
       const float x1 = -X[j * g.sn + l2 * g.sd];
       const P1 q0 = place_f32<EXACT>(x0, g.a_hi, g.a_lo);
       const P1 q1 = place_f32<EXACT>(x1, g.a_hi, g.a_lo);
-      const int d00 = first_tap(q0.f, g.w), d01 = first_tap(q1.f, g.w);
+      const int d00 = first_tap(q0.f, W), d01 = first_tap(q1.f, W);
       const int lr = q0.P + g.K + d00, lc = q1.P + g.K + d01;
-      if ((unsigned)lr > (unsigned)(g.G - g.w) || (unsigned)lc > (unsigned)(g.G - g.w) || x0 != x0 || x1 != x1) {
+      if ((unsigned)lr > (unsigned)(g.G - W) || (unsigned)lc > (unsigned)(g.G - W) || x0 != x0 || x1 != x1) {
         bad = true;
         continue;
       }
-      es_taps_f32(q0.f, d00, g.w, g.beta_f, py);
-      es_taps_f32(q1.f, d01, g.w, g.beta_f, px);
-      spread_fixed<false>(smx + q * cells, t, lr, lc, py, px, g.w, kS2, g.carry + (int64_t)(p0 + q) * cells, 0, kInvS2);
+      es_taps_f32<W>(q0.f, d00, g.beta_f, py);
+      es_taps_f32<W>(q1.f, d01, g.beta_f, px);
+      spread_fixed<false, W>(smx + q * cells, t, lr, lc, py, px, kS2, g.carry + (int64_t)(p0 + q) * cells, 0, kInvS2);
     }
   }
   if (bad && g.d_status) atomicOr(g.d_status, (int)FK_E_RANGE);
@@ -370,7 +365,7 @@ __global__ void __launch_bounds__(512) k_cross2d_fixed(const float* __restrict__
   for (int i = threadIdx.x; i < np * cells; i += blockDim.x) dst[i] = smx[i];
 }
 
-template <typename XT>
+template <int W, typename XT>
 __global__ void __launch_bounds__(256) k_cross2d_f64(const XT* __restrict__ X, const ArgsX* __restrict__ gp) {
   extern __shared__ double smxd[];
   const ArgsX& g = *gp;
@@ -385,7 +380,7 @@ __global__ void __launch_bounds__(256) k_cross2d_f64(const XT* __restrict__ X, c
   const int64_t end = min(g.n, beg + g.per);
   Tile t{g.G, g.K, g.G, g.G};
   bool bad = false;
-  double px[kW], py[kW];
+  double px[W], py[W];
   for (int64_t j = beg + threadIdx.x; j < end; j += blockDim.x) {
     for (int q = 0; q < np; ++q) {
       const int l1 = g.pl1[p0 + q], l2 = g.pl2[p0 + q];
@@ -395,16 +390,16 @@ __global__ void __launch_bounds__(256) k_cross2d_f64(const XT* __restrict__ X, c
         continue;
       }
       const double Pa = floor(pa), Pb = floor(pb), fa = pa - Pa, fb = pb - Pb;
-      const int d00 = first_tap_d(fa, g.w);
-      const int d01 = first_tap_d(fb, g.w);
+      const int d00 = first_tap_d(fa, W);
+      const int d01 = first_tap_d(fb, W);
       const int lr = (int)Pa + g.K + d00, lc = (int)Pb + g.K + d01;
-      if ((unsigned)lr > (unsigned)(g.G - g.w) || (unsigned)lc > (unsigned)(g.G - g.w)) {
+      if ((unsigned)lr > (unsigned)(g.G - W) || (unsigned)lc > (unsigned)(g.G - W)) {
         bad = true;
         continue;
       }
-      es_taps_f64(fa, d00, g.w, g.beta_d, py);
-      es_taps_f64(fb, d01, g.w, g.beta_d, px);
-      spread_f64(smxd + q * cells, t, lr, lc, py, px, g.w, 1.0, 0);
+      es_taps_f64<W>(fa, d00, g.beta_d, py);
+      es_taps_f64<W>(fb, d01, g.beta_d, px);
+      spread_f64<W>(smxd + q * cells, t, lr, lc, py, px, 1.0, 0);
     }
   }
   if (bad && g.d_status) atomicOr(g.d_status, (int)FK_E_RANGE);
@@ -483,6 +478,20 @@ __global__ void k_deconv2d(const double2* __restrict__ F, int nf, int K, const d
 // ------------------------------------------------------------------------------------------
 // host side
 // ------------------------------------------------------------------------------------------
+template <typename F>
+static void dispatch_w64(int w, F&& f) {
+  switch (w) {
+    case 9: f(std::integral_constant<int, 9>{}); break;
+    case 10: f(std::integral_constant<int, 10>{}); break;
+    case 11: f(std::integral_constant<int, 11>{}); break;
+    case 12: f(std::integral_constant<int, 12>{}); break;
+    case 13: f(std::integral_constant<int, 13>{}); break;
+    case 14: f(std::integral_constant<int, 14>{}); break;
+    case 15: f(std::integral_constant<int, 15>{}); break;
+    default: f(std::integral_constant<int, 16>{}); break;
+  }
+}
+
 struct Plan2 {
   int m, w;
   double beta;
@@ -501,9 +510,11 @@ static int max_optin() {
   return v > 0 ? v : 232448;
 }
 
-static int es_width(double eps, bool fp64) {
-  int w = (int)std::ceil(std::log10(1.0 / eps)) + (fp64 ? 2 : 1);
-  return std::min(kW, std::max(4, w));
+// taps per dimension: fp32 fixed-point path 5..8 (eps >= 1e-7), fp64 path 9..16
+static int es_width(double eps, bool fp64acc) {
+  if (!fp64acc) return std::min(8, std::max(5, (int)std::ceil(std::log10(1.0 / eps)) + 1));
+  if (eps >= 1e-7) return 9;
+  return std::min(kW, std::max(9, (int)std::ceil(std::log10(1.0 / eps)) + 2));
 }
 
 // Geometry of one ES grid: local index = global - off, centre nf/2 at local K, occupied G cells.
@@ -518,7 +529,7 @@ static fk_status make_plan2(int m, double eps, bool mu, bool r, int dtype, Plan2
   Plan2 q{};
   q.m = m;
   q.fp64 = eps < 1e-7 || dtype == FK_F64;
-  q.w = es_width(eps, eps < 1e-7);
+  q.w = es_width(eps, q.fp64);
   q.beta = 2.30 * q.w;
   q.nfA = fft_friendly(2 * (4 * m + 1));
   q.nfB = q.nfA / 2;
@@ -650,29 +661,31 @@ fk_status type1_2d_run(int m, double eps, const fk_points& X, const void* Y, dou
         k<<<ctas, p.threads, p.smem, s>>>(Xf, Yf, a);
         prof_spread_end(s);
       };
-      if (mu && r) exact ? go(k_spread2d_fixed<true, true, true>) : go(k_spread2d_fixed<true, true, false>);
-      else if (mu) exact ? go(k_spread2d_fixed<true, false, true>) : go(k_spread2d_fixed<true, false, false>);
-      else exact ? go(k_spread2d_fixed<false, true, true>) : go(k_spread2d_fixed<false, true, false>);
+      auto byw = [&](auto wtag) {
+        constexpr int WW = decltype(wtag)::value;
+        if (mu && r) exact ? go(k_spread2d_fixed<WW, true, true, true>) : go(k_spread2d_fixed<WW, true, true, false>);
+        else if (mu) exact ? go(k_spread2d_fixed<WW, true, false, true>) : go(k_spread2d_fixed<WW, true, false, false>);
+        else exact ? go(k_spread2d_fixed<WW, false, true, true>) : go(k_spread2d_fixed<WW, false, true, false>);
+      };
+      switch (p.w) {
+        case 5: byw(std::integral_constant<int, 5>{}); break;
+        case 6: byw(std::integral_constant<int, 6>{}); break;
+        case 7: byw(std::integral_constant<int, 7>{}); break;
+        default: byw(std::integral_constant<int, 8>{}); break;
+      }
     } else {
       auto go = [&](auto k, auto* Xp, auto* Yp) {
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
         prof_spread_begin(s);
-        k<<<ctas, p.threads, p.smem, s>>>(Xp, Yp, a);
+        k<<<ctas, p.threads, p.smem, s>>>(Xp, Yp, a, mu, r);
         prof_spread_end(s);
       };
-      if (X.dtype == FK_F32) {
-        const float* Xf = (const float*)X.ptr;
-        const float* Yf = (const float*)Y;
-        if (mu && r) go(k_spread2d_f64<float, true, true>, Xf, Yf);
-        else if (mu) go(k_spread2d_f64<float, true, false>, Xf, Yf);
-        else go(k_spread2d_f64<float, false, true>, Xf, Yf);
-      } else {
-        const double* Xd = (const double*)X.ptr;
-        const double* Yd = (const double*)Y;
-        if (mu && r) go(k_spread2d_f64<double, true, true>, Xd, Yd);
-        else if (mu) go(k_spread2d_f64<double, true, false>, Xd, Yd);
-        else go(k_spread2d_f64<double, false, true>, Xd, Yd);
-      }
+      auto byw = [&](auto wtag) {
+        constexpr int WW = decltype(wtag)::value;
+        if (X.dtype == FK_F32) go(k_spread2d_f64<WW, float>, (const float*)X.ptr, (const float*)Y);
+        else go(k_spread2d_f64<WW, double>, (const double*)X.ptr, (const double*)Y);
+      };
+      dispatch_w64(p.w, byw);
     }
     FK_CUDA_TRY(cudaGetLastError());
     count_launch();
@@ -723,7 +736,7 @@ static fk_status make_planx(int d, int m, double eps, int dtype, PlanX* p) {
   PlanX q{};
   q.m = m;
   q.fp64 = eps < 1e-7 || dtype == FK_F64;
-  q.w = es_width(eps, eps < 1e-7);
+  q.w = es_width(eps, q.fp64);
   q.beta = 2.30 * q.w;
   q.nf = fft_friendly(2 * (2 * m + 1));
   es_geo(q.nf, q.w, &q.off, &q.K, &q.G);
@@ -828,12 +841,24 @@ fk_status cross_run(const fk_points& X, double L, int m, double eps, double* G, 
       prof_spread_end(s);
     };
     if (fixed) {
-      if (exact) go(k_cross2d_fixed<true>, (const float*)X.ptr, 512);
-      else go(k_cross2d_fixed<false>, (const float*)X.ptr, 512);
-    } else if (X.dtype == FK_F32) {
-      go(k_cross2d_f64<float>, (const float*)X.ptr, 256);  // fp32 points, fp64 accuracy
+      auto byw = [&](auto wtag) {
+        constexpr int WW = decltype(wtag)::value;
+        if (exact) go(k_cross2d_fixed<WW, true>, (const float*)X.ptr, 512);
+        else go(k_cross2d_fixed<WW, false>, (const float*)X.ptr, 512);
+      };
+      switch (p.w) {
+        case 5: byw(std::integral_constant<int, 5>{}); break;
+        case 6: byw(std::integral_constant<int, 6>{}); break;
+        case 7: byw(std::integral_constant<int, 7>{}); break;
+        default: byw(std::integral_constant<int, 8>{}); break;
+      }
     } else {
-      go(k_cross2d_f64<double>, (const double*)X.ptr, 256);
+      auto byw = [&](auto wtag) {
+        constexpr int WW = decltype(wtag)::value;
+        if (X.dtype == FK_F32) go(k_cross2d_f64<WW, float>, (const float*)X.ptr, 256);  // fp32 points, fp64 accuracy
+        else go(k_cross2d_f64<WW, double>, (const double*)X.ptr, 256);
+      };
+      dispatch_w64(p.w, byw);
     }
     FK_CUDA_TRY(cudaGetLastError());
     count_launch();
