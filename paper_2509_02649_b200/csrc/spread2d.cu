@@ -198,40 +198,97 @@ __global__ void __launch_bounds__(512) k_spread2d_fixed(const float* __restrict_
   const int rA0 = tile * g.gA.R, rB0 = tile * g.gB.R;
   bool bad = false;
   float px[W], py[W];
-  for (int64_t j = beg + threadIdx.x; j < end; j += blockDim.x) {
-    const float x0 = X[j * g.sn], x1 = X[j * g.sn + g.sd];
-    const P1 q0 = place_f32<EXACT>(x0, g.a_hi, g.a_lo);
-    const P1 q1 = place_f32<EXACT>(x1, g.a_hi, g.a_lo);
-    // range check on the moment grid (both coordinates): |X| <= L
+  // A tile owns ~1/T of the samples it reads; spreading them straight from the read loop would
+  // run every 49-atomic spread with ~1/T of the lanes active.  Owned samples are therefore
+  // compacted into a per-warp queue (ballot + popc) and spread 32 at a time.
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  float2* qa = reinterpret_cast<float2*>(sm2 + ((nsm + 3) & ~3)) + warp * 64;
+  float2* qb = reinterpret_cast<float2*>(sm2 + ((nsm + 3) & ~3)) + nwarps * 64 + warp * 64;
+  float* qy = reinterpret_cast<float*>(reinterpret_cast<float2*>(sm2 + ((nsm + 3) & ~3)) + 2 * nwarps * 64) + warp * 64;
+  int cA = 0, cB = 0;
+  auto spreadA = [&](float x0, float x1) {
+    const P1 q0 = place_f32<EXACT>(x0, g.a_hi, g.a_lo), q1 = place_f32<EXACT>(x1, g.a_hi, g.a_lo);
     const int d00 = first_tap(q0.f, W), d01 = first_tap(q1.f, W);
-    const int lrA = q0.P + g.KA + d00, lcA = q1.P + g.KA + d01;
-    if ((unsigned)lrA > (unsigned)(g.gA.G - W) || (unsigned)lcA > (unsigned)(g.gA.G - W) || x0 != x0 || x1 != x1) {
-      if (tile == 0) bad = true;
-      continue;
+    es_taps_f32<W>(q0.f, d00, g.beta_f, py);
+    es_taps_f32<W>(q1.f, d01, g.beta_f, px);
+    spread_fixed<false, W>(A, g.gA, q0.P + g.KA + d00, q1.P + g.KA + d01, py, px, kS2, g.carryA, rA0, kInvS2);
+  };
+  auto spreadB = [&](float x0, float x1, float y) {
+    const P1 h0 = halve(place_f32<EXACT>(x0, g.a_hi, g.a_lo), 0.f), h1 = halve(place_f32<EXACT>(x1, g.a_hi, g.a_lo), 0.f);
+    const int e0 = first_tap(h0.f, W), e1 = first_tap(h1.f, W);
+    const int lrB = h0.P + g.KB + e0, lcB = h1.P + g.KB + e1;
+    es_taps_f32<W>(h0.f, e0, g.beta_f, py);
+    es_taps_f32<W>(h1.f, e1, g.beta_f, px);
+    const float ys = y * SY;
+    if (fabsf(ys) < 1048576.0f) {
+      spread_fixed<true, W>(B, g.gB, lrB, lcB, py, px, ys, g.carryB, rB0, invSY);
+    } else {  // outlier / NaN: exact fp64 path straight into the carry grid
+      for (int a = 0; a < W; ++a)
+        for (int b = 0; b < W; ++b) atomicAdd(g.carryB + (int64_t)(lrB + a) * g.gB.G + lcB + b, (double)py[a] * px[b] * (double)y);
     }
-    if (MU && lrA >= rA0 && lrA < rA0 + g.gA.R) {
-      es_taps_f32<W>(q0.f, d00, g.beta_f, py);
-      es_taps_f32<W>(q1.f, d01, g.beta_f, px);
-      spread_fixed<false, W>(A, g.gA, lrA, lcA, py, px, kS2, g.carryA, rA0, kInvS2);
-    }
-    if (R) {
-      const P1 h0 = halve(q0, 0.f), h1 = halve(q1, 0.f);
-      const int e0 = first_tap(h0.f, W), e1 = first_tap(h1.f, W);
-      const int lrB = h0.P + g.KB + e0, lcB = h1.P + g.KB + e1;
-      if (lrB >= rB0 && lrB < rB0 + g.gB.R) {
-        const float y = Y[j];
-        es_taps_f32<W>(h0.f, e0, g.beta_f, py);
-        es_taps_f32<W>(h1.f, e1, g.beta_f, px);
-        const float ys = y * SY;
-        if (fabsf(ys) < 1048576.0f) {
-          spread_fixed<true, W>(B, g.gB, lrB, lcB, py, px, ys, g.carryB, rB0, invSY);
-        } else {  // outlier / NaN: exact fp64 path straight into the carry grid
-          for (int a = 0; a < W; ++a)
-            for (int b = 0; b < W; ++b)
-              atomicAdd(g.carryB + (int64_t)(lrB + a) * g.gB.G + lcB + b, (double)py[a] * px[b] * (double)y);
+  };
+  for (int64_t j0 = beg + (int64_t)warp * 32; j0 < end; j0 += (int64_t)nwarps * 32) {  // warp-uniform trip count
+    const int64_t j = j0 + lane;
+    bool ownA = false, ownB = false;
+    float x0 = 0.f, x1 = 0.f, y = 0.f;
+    if (j < end) {
+      x0 = X[j * g.sn];
+      x1 = X[j * g.sn + g.sd];
+      const P1 q0 = place_f32<EXACT>(x0, g.a_hi, g.a_lo);
+      const P1 q1 = place_f32<EXACT>(x1, g.a_hi, g.a_lo);
+      // range check on the moment grid (both coordinates): |X| <= L
+      const int lrA = q0.P + g.KA + first_tap(q0.f, W), lcA = q1.P + g.KA + first_tap(q1.f, W);
+      if ((unsigned)lrA > (unsigned)(g.gA.G - W) || (unsigned)lcA > (unsigned)(g.gA.G - W) || x0 != x0 || x1 != x1) {
+        if (tile == 0) bad = true;
+      } else {
+        ownA = MU && lrA >= rA0 && lrA < rA0 + g.gA.R;
+        if (R) {
+          const P1 h0 = halve(q0, 0.f);
+          const int lrB = h0.P + g.KB + first_tap(h0.f, W);
+          ownB = lrB >= rB0 && lrB < rB0 + g.gB.R;
+          if (ownB) y = Y[j];
         }
       }
     }
+    if (MU) {
+      const unsigned msk = __ballot_sync(0xffffffffu, ownA);
+      if (ownA) qa[cA + __popc(msk & lt)] = make_float2(x0, x1);
+      cA += __popc(msk);
+      if (cA >= 32) {
+        __syncwarp();
+        const float2 v = qa[cA - 32 + lane];
+        cA -= 32;
+        __syncwarp();
+        spreadA(v.x, v.y);
+      }
+    }
+    if (R) {
+      const unsigned msk = __ballot_sync(0xffffffffu, ownB);
+      if (ownB) {
+        const int at = cB + __popc(msk & lt);
+        qb[at] = make_float2(x0, x1);
+        qy[at] = y;
+      }
+      cB += __popc(msk);
+      if (cB >= 32) {
+        __syncwarp();
+        const float2 v = qb[cB - 32 + lane];
+        const float vy = qy[cB - 32 + lane];
+        cB -= 32;
+        __syncwarp();
+        spreadB(v.x, v.y, vy);
+      }
+    }
+  }
+  __syncwarp();
+  if (MU && lane < cA) {
+    const float2 v = qa[lane];
+    spreadA(v.x, v.y);
+  }
+  if (R && lane < cB) {
+    const float2 v = qb[lane];
+    spreadB(v.x, v.y, qy[lane]);
   }
   if (bad && g.d_status) atomicOr(g.d_status, (int)FK_E_RANGE);
   __syncthreads();
@@ -538,9 +595,12 @@ static fk_status make_plan2(int m, double eps, bool mu, bool r, int dtype, Plan2
   es_geo(q.nfB, q.w, &q.offB, &q.KB, &GB);
   const size_t esz = q.fp64 ? 8 : 4;
   const size_t cap = (size_t)max_optin() - 2048;
+  // fp32 path: + per-warp compaction queues (16 warps x 64 x (float2 + float2 + float)), 16-byte aligned
+  const size_t queues = q.fp64 ? 0 : (size_t)16 * 64 * 20 + 16;
   for (int T = 1; T <= 64; ++T) {
     const int RA = (GA + T - 1) / T, RB = (GB + T - 1) / T;
-    const size_t bytes = ((mu ? (size_t)(RA + q.w - 1) * GA : 0) + (r ? (size_t)(RB + q.w - 1) * GB : 0)) * esz;
+    size_t bytes = ((mu ? (size_t)(RA + q.w - 1) * GA : 0) + (r ? (size_t)(RB + q.w - 1) * GB : 0)) * esz;
+    bytes = ((bytes + 15) & ~(size_t)15) + queues;
     if (bytes <= cap) {
       q.T = T;
       q.gA = {GA, q.KA, RA, RA + q.w - 1};
