@@ -110,7 +110,7 @@ fk_status make_plan1(int d, int m, double eps, bool need_mu, bool need_r, Plan1*
     q.nf_r = q.nf_mu / 2;
     q.gA = {q.nf_mu, q.nf_mu / 4 - 1, q.nf_mu / 2 + 4};
     q.gB = {q.nf_r, q.nf_r / 4 - 1, q.nf_r / 2 + 4};
-    size_t bytes = (size_t)((need_mu ? q.gA.G + 4 : 0) + (need_r ? q.gB.G + 4 : 0)) * 4;  // + 4 dummy cells each
+    size_t bytes = (size_t)((need_mu ? q.gA.G : 0) + (need_r ? q.gB.G : 0)) * 4;
     if (bytes > (size_t)smem_cap) fp32 = false;  // too large for one CTA: take the fp64 path
     else {
       q.smem_bytes = bytes;

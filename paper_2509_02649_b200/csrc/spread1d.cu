@@ -89,71 +89,12 @@ __device__ __forceinline__ void bs3_sample(int* __restrict__ A, int* __restrict_
   }
 }
 
-// ---- hot path (fp32 X, Y contiguous and 16-byte aligned, nf_mu / 4L a power of two, both
-// channels): branch-free per sample except one rare path, 32-bit shared addresses -----------
-__device__ __forceinline__ int atoms_add(unsigned addr, int v) {
-  int old;
-  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v) : "memory");
-  return old;
-}
-
-// everything that is not the common case: a coordinate outside the grid (flag; its atomics went
-// to the 4 dummy cells past the grid), an rhs outlier (exact fp64 contribution), and draining
-// cells that reached 2^30
-__device__ __noinline__ void bs3_rare(int* A, int* B, const Bs3Args& g, int tA, int tB, float fB, float y, bool ok, bool outlier,
-                                      bool drainA, bool drainB, double invSY, bool* bad) {
-  if (!ok) *bad = true;
-  if (ok && outlier) rhs_slow(y, fB, g.carryB, tB);
-  if (drainA) drain_cells(A, tA, g.carryA, kInvSA);
-  if (drainB) drain_cells(B, tB, g.carryB, invSY);
-}
-
-__device__ __forceinline__ void bs3_sample_fast(int* A, int* B, unsigned sA, unsigned sB, const Bs3Args& g, float x, float y, float SY,
-                                                double invSY, bool& bad) {
-  const float p = x * g.a_hi;  // exact: a is a power of two
-  const float fl = floorf(p);
-  const float f = p - fl;
-  const int ic = __float_as_int(fl + FK_MAGIC) - FK_MAGIC_BITS;
-  int tA = ic + g.nqA;
-  const bool ok = (unsigned)tA <= (unsigned)(g.GA - 4);
-  // rhs grid: half the cells, so its cell is floor(ic / 2) and its offset (f + (ic & 1)) / 2
-  const float fB = fmaf(f, 0.5f, (ic & 1) ? 0.5f : 0.0f);
-  int tB = (ic >> 1) + g.nqB;
-  tA = ok ? tA : g.GA;  // dummy cells GA..GA+3 / GB..GB+3
-  tB = ok ? tB : g.GB;
-  // moments: cubic B-spline taps x 2^21, partition of unity closed in integers
-  const float K = kSA * (1.0f / 6.0f);
-  const float g1 = 1.0f - f, f2 = f * f, f3 = f2 * f, g3 = g1 * g1 * g1;
-  const int b0 = __float_as_int(fmaf(g3, K, FK_MAGIC)), b3 = __float_as_int(fmaf(f3, K, FK_MAGIC));
-  const int b1 = __float_as_int(fmaf(f3, 3.0f * K, fmaf(f2, -6.0f * K, 4.0f * K)) + FK_MAGIC);
-  const int i2 = ((int)kSA + 3 * FK_MAGIC_BITS) - b0 - b1 - b3;
-  // rhs: taps x Y 2^E (outliers contribute through the rare path instead)
-  float ys = y * SY;
-  const bool outlier = !(fabsf(ys) < 2097152.0f);
-  ys = outlier ? 0.0f : ys;
-  const float yk = ys * (1.0f / 6.0f);
-  const float h1 = 1.0f - fB, fB2 = fB * fB, fB3 = fB2 * fB, h3 = h1 * h1 * h1;
-  const int c0 = __float_as_int(fmaf(h3, yk, FK_MAGIC)), c3 = __float_as_int(fmaf(fB3, yk, FK_MAGIC));
-  const int c1 = __float_as_int(fmaf(fmaf(fB3, 3.0f, fmaf(fB2, -6.0f, 4.0f)), yk, FK_MAGIC));
-  const int cS = __float_as_int(ys + FK_MAGIC);
-  const int j2 = cS + 2 * FK_MAGIC_BITS - c0 - c1 - c3;
-  const unsigned aA = sA + 4u * (unsigned)tA, aB = sB + 4u * (unsigned)tB;
-  const int o0 = atoms_add(aA, b0 - FK_MAGIC_BITS), o1 = atoms_add(aA + 4, b1 - FK_MAGIC_BITS);
-  const int o2 = atoms_add(aA + 8, i2), o3 = atoms_add(aA + 12, b3 - FK_MAGIC_BITS);
-  const unsigned T = 1u << 30;
-  const unsigned q0 = (unsigned)atoms_add(aB, c0 - FK_MAGIC_BITS) + T, q1 = (unsigned)atoms_add(aB + 4, c1 - FK_MAGIC_BITS) + T;
-  const unsigned q2 = (unsigned)atoms_add(aB + 8, j2) + T, q3 = (unsigned)atoms_add(aB + 12, c3 - FK_MAGIC_BITS) + T;
-  const bool drainA = ((o0 | o1 | o2 | o3) & 0x40000000) != 0;
-  const bool drainB = ((q0 | q1 | q2 | q3) & 0x80000000u) != 0;
-  if (!ok | outlier | drainA | drainB) bs3_rare(A, B, g, tA, tB, fB, y, ok, outlier, drainA, drainB, invSY, &bad);
-}
-
 template <typename XT, bool MU, bool R, bool VEC, bool EXACT>
 __global__ void __launch_bounds__(1024, 1) k_spread1d_bs3(const XT* __restrict__ X, const XT* __restrict__ Y, Bs3Args g) {
   extern __shared__ int sm[];
   int* A = sm;
-  int* B = sm + (MU ? g.GA + 4 : 0);
-  const int nsm = (MU ? g.GA + 4 : 0) + (R ? g.GB + 4 : 0);
+  int* B = sm + (MU ? g.GA : 0);
+  const int nsm = (MU ? g.GA : 0) + (R ? g.GB : 0);
   for (int i = threadIdx.x; i < nsm; i += blockDim.x) sm[i] = 0;
 
   const int64_t beg = (int64_t)blockIdx.x * g.per;
@@ -214,18 +155,12 @@ __global__ void __launch_bounds__(1024, 1) k_spread1d_bs3(const XT* __restrict__
       }
       const float xs[4] = {xv.x, xv.y, xv.z, xv.w};
       const float ys[4] = {yv.x, yv.y, yv.z, yv.w};
-      if (MU && R && EXACT) {
-        const unsigned sA = (unsigned)__cvta_generic_to_shared(A), sB = (unsigned)__cvta_generic_to_shared(B);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) bs3_sample_fast(A, B, sA, sB, g, xs[q], ys[q], SY, invSY, bad);
-      } else {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          int tA, tB;
-          float fA, fB;
-          pos_f32<EXACT>(xs[q], g.a_hi, g.a_lo, g.nqA, g.nqB, tA, tB, fA, fB);
-          bs3_sample<MU, R>(A, B, g, tA, tB, fA, fB, ys[q], SY, 0.f, invSY, bad);
-        }
+      for (int q = 0; q < 4; ++q) {
+        int tA, tB;
+        float fA, fB;
+        pos_f32<EXACT>(xs[q], g.a_hi, g.a_lo, g.nqA, g.nqB, tA, tB, fA, fB);
+        bs3_sample<MU, R>(A, B, g, tA, tB, fA, fB, ys[q], SY, 0.f, invSY, bad);
       }
       xv = xn;
       yv = yn;
@@ -416,7 +351,7 @@ static fk_status layout1(const Plan1& p, bool mu, bool r, Bump& b, Ws1& w, size_
     w.partA = b.take((size_t)nparts * p.gA.G * esz);
     w.fineA = (double*)b.take((size_t)p.nf_mu * 8);
     w.specA = (double2*)b.take((size_t)(p.nf_mu / 2 + 1) * 16);
-    if (!p.fp64) w.carryA = (double*)b.take((size_t)(p.gA.G + 4) * 8);  // + 4 dummy cells
+    if (!p.fp64) w.carryA = (double*)b.take((size_t)p.gA.G * 8);
     if (p.ker == KER_ES) w.tabA = (double*)b.take((size_t)(2 * p.m + 1) * 8);
   }
   if (r) {
@@ -424,7 +359,7 @@ static fk_status layout1(const Plan1& p, bool mu, bool r, Bump& b, Ws1& w, size_
     w.fineB = (double*)b.take((size_t)p.nf_r * 8);
     w.specB = (double2*)b.take((size_t)(p.nf_r / 2 + 1) * 16);
     if (!p.fp64) {
-      w.carryB = (double*)b.take((size_t)(p.gB.G + 4) * 8);
+      w.carryB = (double*)b.take((size_t)p.gB.G * 8);
       w.escale = (int*)b.take((size_t)p.ctas * 4);
     }
     if (p.ker == KER_ES) w.tabB = (double*)b.take((size_t)(p.m + 1) * 8);
@@ -547,8 +482,8 @@ fk_status type1_run(const Plan1& p, const fk_points& X, const void* Y, double L,
   if (!b.ok()) return fail(FK_E_WORKSPACE, "workspace too small: need " + std::to_string(b.used + 256) + " bytes");
   // zero what is accumulated globally
   if (!p.fp64) {
-    if (mu) FK_CUDA_TRY(cudaMemsetAsync(w.carryA, 0, (size_t)(p.gA.G + 4) * 8, s));
-    if (r) FK_CUDA_TRY(cudaMemsetAsync(w.carryB, 0, (size_t)(p.gB.G + 4) * 8, s));
+    if (mu) FK_CUDA_TRY(cudaMemsetAsync(w.carryA, 0, (size_t)p.gA.G * 8, s));
+    if (r) FK_CUDA_TRY(cudaMemsetAsync(w.carryB, 0, (size_t)p.gB.G * 8, s));
   } else if (!p.smem) {
     if (mu) FK_CUDA_TRY(cudaMemsetAsync(w.partA, 0, (size_t)p.gA.G * 8, s));
     if (r) FK_CUDA_TRY(cudaMemsetAsync(w.partB, 0, (size_t)p.gB.G * 8, s));
