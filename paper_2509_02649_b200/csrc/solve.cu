@@ -31,6 +31,8 @@ struct SysArgs {
   double box[kMaxD][2];
   const double2* mu;
   const double2* cross;
+  const double2* dsym;  // PI tables (k_pi_tables), or null
+  const double2* boxt;
 };
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) { return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
@@ -119,13 +121,39 @@ __device__ double2 entry(const SysArgs& g, int i, int j) {
     v.x += g.lambda * R;
   }
   if (g.kind == FK_PIK_BOX && g.mu_pde != 0.0) {
-    int q[kMaxD];
-    for (int l = 0; l < g.d; ++l) q[l] = k2[l] - k1[l];
-    const double2 t = cmul(cmul(cconj(pde_symbol(g, k1)), box_fourier(g, q)), pde_symbol(g, k2));
+    double2 t;
+    if (g.dsym) {  // tabulated: d_k per mode, box integral per dimension and difference q_l
+      double2 b = make_double2(1.0, 0.0);
+      for (int l = 0; l < g.d; ++l) b = cmul(b, g.boxt[l * (4 * g.m + 1) + (k2[l] - k1[l] + 2 * g.m)]);
+      t = cmul(cmul(cconj(g.dsym[i]), b), g.dsym[j]);
+    } else {
+      int q[kMaxD];
+      for (int l = 0; l < g.d; ++l) q[l] = k2[l] - k1[l];
+      t = cmul(cmul(cconj(pde_symbol(g, k1)), box_fourier(g, q)), pde_symbol(g, k2));
+    }
     v.x += g.mu_pde * t.x;
     v.y += g.mu_pde * t.y;
   }
   return v;
+}
+
+// PI tables: dsym[i] = d_{k_i} (symbol), boxt[l][q + 2m] = (4L)^{-1} int_{a_l}^{b_l} e^{i c q x} dx
+__global__ void k_pi_tables(SysArgs g, double2* __restrict__ dsym, double2* __restrict__ boxt) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < g.D) {
+    int k[kMaxD];
+    decode(t, g.d, g.m, k);
+    dsym[t] = pde_symbol(g, k);
+  }
+  const int nq = 4 * g.m + 1;
+  if (t < g.d * nq) {
+    const int l = t / nq, qv = t % nq - 2 * g.m;
+    SysArgs one = g;
+    one.d = 1;
+    one.box[0][0] = g.box[l][0];
+    one.box[0][1] = g.box[l][1];
+    boxt[t] = box_fourier(one, &qv);
+  }
 }
 
 // res[0] += ||A theta - b||^2, res[1] += ||b||^2, with A evaluated on the fly (one warp per row)
@@ -296,6 +324,10 @@ size_t solve_ws_bytes(int d, int m, int kind) {
   b.take((size_t)lwork * 8);
   b.take((size_t)D * 8);
   b.take(64);
+  if (kind == FK_PIK_BOX) {
+    b.take((size_t)D * 16);
+    b.take((size_t)d * (4 * m + 1) * 16);
+  }
   return b.used + 256;
 }
 
@@ -334,6 +366,12 @@ fk_status solve_run(const fk_problem* P, double* theta, fk_solve_report* rep, vo
   double* z = (double*)b.take((size_t)D * 8);
   int* info = (int*)b.take(16);
   double* res = (double*)(info + 4);
+  double2* dsym = nullptr;
+  double2* boxt = nullptr;
+  if (P->kind == FK_PIK_BOX) {
+    dsym = (double2*)b.take((size_t)D * 16);
+    boxt = (double2*)b.take((size_t)P->d * (4 * P->m + 1) * 16);
+  }
   if (!b.ok()) return fail(FK_E_WORKSPACE, "fk_solve: workspace too small");
 
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -343,6 +381,14 @@ fk_status solve_run(const fk_problem* P, double* theta, fk_solve_report* rep, vo
     cudaEventRecord(e0, s);
   }
   const int sms = device_sm_count();
+  if (P->kind == FK_PIK_BOX) {
+    const int nt = std::max(D, P->d * (4 * P->m + 1));
+    k_pi_tables<<<(nt + 255) / 256, 256, 0, s>>>(g, dsym, boxt);
+    FK_CUDA_TRY(cudaGetLastError());
+    count_launch();
+    g.dsym = dsym;
+    g.boxt = boxt;
+  }
   k_assemble_real<<<sms * 8, 256, 0, s>>>(g, M);
   k_rhs_real<<<(D + 255) / 256, 256, 0, s>>>(g, (const double2*)P->rhs, z);
   FK_CUDA_TRY(cudaGetLastError());
