@@ -139,6 +139,9 @@ fk_status cross_run(const fk_points& X, double L, int m, double eps, double* G, 
 #define FK_MAGIC 12582912.0f        // 1.5 * 2^23: x + MAGIC rounds x to an integer in the low mantissa bits
 #define FK_MAGIC_BITS 0x4B400000
 
+// exact 2^e for |e| < 1000 without the libm ldexp call
+__device__ inline double pow2(int e) { return __longlong_as_double((long long)(1023 + e) << 52); }
+
 __host__ __device__ inline double sinc_pi(double x) {  // sin(pi x) / (pi x)
   if (x == 0.0) return 1.0;
   const double a = 3.14159265358979323846 * x;

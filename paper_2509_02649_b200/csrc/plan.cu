@@ -173,23 +173,25 @@ static void gauss_legendre01(int n, double* x, double* w) {
   }
 }
 
-__global__ void k_es_phihat(GL96 gl, int w, double beta, int nf, int K, double* tab) {
-  int k = blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void k_es_phihat(GL96 gl, int w, double beta, int nf, int K, double* tab) {  // one warp per mode
+  const int k = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
   if (k > K) return;
   double s = 0.0;
-  for (int i = 0; i < 96; ++i) {
+  for (int i = lane; i < 96; i += 32) {
     const double z = gl.x[i];
     const double psi = exp(beta * (sqrt(1.0 - z * z) - 1.0));
     s += gl.w[i] * psi * cos(3.14159265358979323846 * (double)k * w * z / nf);
   }
-  tab[k] = w * s;
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) tab[k] = w * s;
 }
 
 fk_status es_phihat_table(const EsParams& es, int nf, int K, double* d_tab, cudaStream_t s) {
   static GL96 gl;
   static std::once_flag once;
   std::call_once(once, [] { gauss_legendre01(96, gl.x, gl.w); });
-  k_es_phihat<<<(K + 1 + 127) / 128, 128, 0, s>>>(gl, es.w, es.beta, nf, K, d_tab);
+  k_es_phihat<<<(unsigned)(((int64_t)(K + 1) * 32 + 255) / 256), 256, 0, s>>>(gl, es.w, es.beta, nf, K, d_tab);
   count_launch();
   FK_CUDA_TRY(cudaGetLastError());
   return FK_OK;

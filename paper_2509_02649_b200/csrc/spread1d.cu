@@ -271,7 +271,7 @@ __global__ void k_reduce_fixed(const int* __restrict__ part, const int* __restri
   double s = 0.0;
   if (i >= 0 && i < G) {
     if (escale) {
-      for (int c = 0; c < ncta; ++c) s += (double)part[(int64_t)c * G + i] * ldexp(1.0, -escale[c]);
+      for (int c = 0; c < ncta; ++c) s += (double)part[(int64_t)c * G + i] * pow2(-escale[c]);
     } else {
       for (int c = 0; c < ncta; ++c) s += (double)part[(int64_t)c * G + i];
       s *= uniform_inv;

@@ -488,7 +488,7 @@ __global__ void k_reduce2d(const void* __restrict__ part, int is_fixed, const in
         const int64_t idx = bi * part_batch_stride + cta * part_cta_stride + (int64_t)lr * G + col;
         if (is_fixed) {
           const double v = (double)((const int*)part)[idx];
-          s += escale ? v * ldexp(1.0, -escale[cta]) : v * uniform_inv;
+          s += escale ? v * pow2(-escale[cta]) : v * uniform_inv;
         } else {
           s += ((const double*)part)[idx];
         }
