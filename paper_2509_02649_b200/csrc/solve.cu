@@ -305,72 +305,6 @@ __global__ void k_theta_from_real(SysArgs g, const double* __restrict__ z, doubl
 }
 
 
-// ---- small dense SPD solve in one CTA: right-looking Cholesky in shared memory, then the two
-// triangular solves; M column-major (lower triangle used), z in / solution out, info as LAPACK.
-constexpr int kSmallD = 160;
-
-__global__ void __launch_bounds__(512) k_chol_small(const double* __restrict__ Mg, double* __restrict__ z, int D, int* info) {
-  extern __shared__ double S[];
-  double* a = S;          // D x D column-major
-  double* b = S + D * D;  // rhs
-  for (int t = threadIdx.x; t < D * D; t += blockDim.x) {
-    const int i = t % D, j = t / D;
-    a[t] = i >= j ? Mg[t] : 0.0;
-  }
-  for (int t = threadIdx.x; t < D; t += blockDim.x) b[t] = z[t];
-  __shared__ int fail_at;
-  if (threadIdx.x == 0) fail_at = 0;
-  __syncthreads();
-  for (int j = 0; j < D; ++j) {
-    const double pivot = a[j + j * D];
-    if (!(pivot > 0.0)) {
-      if (threadIdx.x == 0) fail_at = j + 1;
-      break;
-    }
-    const double ljj = sqrt(pivot);
-    const double inv = 1.0 / ljj;
-    __syncthreads();
-    if (threadIdx.x == 0) a[j + j * D] = ljj;
-    for (int i = j + 1 + threadIdx.x; i < D; i += blockDim.x) a[i + j * D] *= inv;
-    __syncthreads();
-    // trailing update of the lower triangle: a[i,k] -= l_ij l_kj, j < k <= i
-    const int r = D - j - 1;
-    for (int t = threadIdx.x; t < r * r; t += blockDim.x) {
-      const int ii = t % r, kk = t / r;
-      if (ii < kk) continue;
-      const int I = j + 1 + ii, Kc = j + 1 + kk;
-      a[I + Kc * D] -= a[I + j * D] * a[Kc + j * D];
-    }
-    __syncthreads();
-  }
-  __syncthreads();
-  if (fail_at) {
-    if (threadIdx.x == 0) *info = fail_at;
-    return;
-  }
-  // forward L y = b and backward L^T x = y, one warp (lanes split the dot products)
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    for (int j = 0; j < D; ++j) {
-      double sacc = 0.0;
-      for (int k = lane; k < j; k += 32) sacc += a[j + k * D] * b[k];
-      for (int o = 16; o; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
-      if (lane == 0) b[j] = (b[j] - sacc) / a[j + j * D];
-      __syncwarp();
-    }
-    for (int j = D - 1; j >= 0; --j) {
-      double sacc = 0.0;
-      for (int k = j + 1 + lane; k < D; k += 32) sacc += a[k + j * D] * b[k];
-      for (int o = 16; o; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
-      if (lane == 0) b[j] = (b[j] - sacc) / a[j + j * D];
-      __syncwarp();
-    }
-  }
-  __syncthreads();
-  for (int t = threadIdx.x; t < D; t += blockDim.x) z[t] = b[t];
-  if (threadIdx.x == 0) *info = 0;
-}
-
 fk_status lwork_for(int D, int* lwork) {
   std::lock_guard<std::mutex> lk(g_sol_mu);
   cusolverDnHandle_t h;
@@ -460,15 +394,7 @@ fk_status solve_run(const fk_problem* P, double* theta, fk_solve_report* rep, vo
   k_rhs_real<<<(D + 255) / 256, 256, 0, s>>>(g, (const double2*)P->rhs, z);
   FK_CUDA_TRY(cudaGetLastError());
   count_launch(2);
-  if (D <= kSmallD) {
-    // small systems (C1: D = 101): one CTA factors and solves in shared memory (cuSOLVER's
-    // single-CTA getrf path plus two trsv calls cost ~110 us at this size)
-    const size_t sm_bytes = ((size_t)D * D + D) * 8;
-    cudaFuncSetAttribute(k_chol_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_bytes);
-    k_chol_small<<<1, 512, sm_bytes, s>>>(M, z, D, info);
-    FK_CUDA_TRY(cudaGetLastError());
-    count_launch();
-  } else {
+  {
     std::lock_guard<std::mutex> lk(g_sol_mu);
     cusolverDnHandle_t h;
     FK_TRY(handle_for_device(&h));
