@@ -157,7 +157,7 @@ struct Args2 {
 
 // moments (grid A) and rhs (grid B) of d = 2 points, fp32 fixed-point path
 template <int W, bool MU, bool R, bool EXACT>
-__global__ void __launch_bounds__(512) k_spread2d_fixed(const float* __restrict__ X, const float* __restrict__ Y, Args2 g) {
+__global__ void __launch_bounds__(1024) k_spread2d_fixed(const float* __restrict__ X, const float* __restrict__ Y, Args2 g) {
   extern __shared__ int sm2[];
   int* A = sm2;
   int* B = sm2 + (MU ? g.gA.rows * g.gA.G : 0);
@@ -383,7 +383,7 @@ struct ArgsX {
 };
 
 template <int W, bool EXACT>
-__global__ void __launch_bounds__(512) k_cross2d_fixed(const float* __restrict__ X, const ArgsX* __restrict__ gp) {
+__global__ void __launch_bounds__(1024) k_cross2d_fixed(const float* __restrict__ X, const ArgsX* __restrict__ gp) {
   extern __shared__ int smx[];
   const ArgsX& g = *gp;
   const int grp = blockIdx.x % g.ngroups;
@@ -596,7 +596,7 @@ static fk_status make_plan2(int m, double eps, bool mu, bool r, int dtype, Plan2
   const size_t esz = q.fp64 ? 8 : 4;
   const size_t cap = (size_t)max_optin() - 2048;
   // fp32 path: + per-warp compaction queues (16 warps x 64 x (float2 + float2 + float)), 16-byte aligned
-  const size_t queues = q.fp64 ? 0 : (size_t)16 * 64 * 20 + 16;
+  const size_t queues = q.fp64 ? 0 : (size_t)32 * 64 * 20 + 16;  // 32 warps
   for (int T = 1; T <= 64; ++T) {
     const int RA = (GA + T - 1) / T, RB = (GB + T - 1) / T;
     size_t bytes = ((mu ? (size_t)(RA + q.w - 1) * GA : 0) + (r ? (size_t)(RB + q.w - 1) * GB : 0)) * esz;
@@ -610,7 +610,7 @@ static fk_status make_plan2(int m, double eps, bool mu, bool r, int dtype, Plan2
     }
   }
   if (q.T == 0) return fail(FK_E_UNSUPPORTED, "d=2 grid too large for 64 row tiles");
-  q.threads = q.fp64 ? 256 : 512;
+  q.threads = q.fp64 ? 256 : 1024;
   const int sms = device_sm_count();
   const int per_sm = std::max(1, std::min(4, (int)(cap / (q.smem + 1024))));
   q.chunks = std::max(1, (sms * per_sm) / q.T);
@@ -808,7 +808,7 @@ static fk_status make_planx(int d, int m, double eps, int dtype, PlanX* p) {
   q.per_cta = (int)std::min<size_t>(q.npairs, cap / per);
   q.ngroups = (q.npairs + q.per_cta - 1) / q.per_cta;
   q.smem = (size_t)q.per_cta * per;
-  q.threads = q.fp64 ? 256 : 512;
+  q.threads = q.fp64 ? 256 : 1024;
   const int sms = device_sm_count();
   const int per_sm = std::max(1, std::min(4, (int)(cap / (q.smem + 1024))));
   q.chunks = std::max(1, (sms * per_sm + q.ngroups - 1) / q.ngroups);
@@ -903,8 +903,8 @@ fk_status cross_run(const fk_points& X, double L, int m, double eps, double* G, 
     if (fixed) {
       auto byw = [&](auto wtag) {
         constexpr int WW = decltype(wtag)::value;
-        if (exact) go(k_cross2d_fixed<WW, true>, (const float*)X.ptr, 512);
-        else go(k_cross2d_fixed<WW, false>, (const float*)X.ptr, 512);
+        if (exact) go(k_cross2d_fixed<WW, true>, (const float*)X.ptr, 1024);
+        else go(k_cross2d_fixed<WW, false>, (const float*)X.ptr, 1024);
       };
       switch (p.w) {
         case 5: byw(std::integral_constant<int, 5>{}); break;
