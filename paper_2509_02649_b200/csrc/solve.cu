@@ -8,6 +8,7 @@
 // Cholesky) and solved by zpotrs.  CG is not used: cond(A) is 1e6..1e11 at the
 // BASELINE configurations and Jacobi-preconditioned CG would need 1e3+ iterations (DESIGN.md
 // reading R9).  The backward error of the report re-evaluates A from the moments on the fly.
+#include <cublas_v2.h>
 #include <cusolverDn.h>
 
 #include <cmath>
@@ -181,6 +182,22 @@ __global__ void k_residual(SysArgs g, const double2* __restrict__ theta, const d
 
 std::mutex g_sol_mu;
 std::map<int, cusolverDnHandle_t> g_handles;
+std::map<int, cublasHandle_t> g_blas;
+
+fk_status blas_for_device(cublasHandle_t* h) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  auto it = g_blas.find(dev);
+  if (it != g_blas.end()) {
+    *h = it->second;
+    return FK_OK;
+  }
+  cublasHandle_t nh;
+  if (cublasCreate(&nh) != CUBLAS_STATUS_SUCCESS) return fail(FK_E_CUDA, "cublasCreate failed");
+  g_blas[dev] = nh;
+  *h = nh;
+  return FK_OK;
+}
 
 fk_status handle_for_device(cusolverDnHandle_t* h) {
   int dev = 0;
@@ -259,8 +276,10 @@ __device__ __forceinline__ PCol pcol(const SysArgs& g, int u) {
   return p;
 }
 
-__global__ void k_assemble_real(SysArgs g, double* __restrict__ M) {  // column-major, lower triangle
-  const int64_t D = g.D;
+// M is the (D+1) x (D+1) column-major augmented matrix [[P*AP, c], [c^T, huge]] (lower triangle):
+// its Cholesky factor's last row is y = L^{-1} c, so only the backward solve L^T z = y remains.
+__global__ void k_assemble_real(SysArgs g, double* __restrict__ M) {
+  const int64_t D = g.D, N = g.D + 1;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < D * D; t += (int64_t)gridDim.x * blockDim.x) {
     const int v = (int)(t / D), u = (int)(t % D);
     if (u < v) continue;
@@ -272,12 +291,14 @@ __global__ void k_assemble_real(SysArgs g, double* __restrict__ M) {  // column-
         const double2 c = cmul(cmul(cconj(pu.a[x]), a), pv.a[y]);
         s += c.x;
       }
-    M[t] = s;
+    M[u + v * N] = s;
   }
 }
 
-__global__ void k_rhs_real(SysArgs g, const double2* __restrict__ r, double* __restrict__ c) {
+__global__ void k_rhs_real(SysArgs g, const double2* __restrict__ r, double* __restrict__ M) {  // last row of M
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t N = g.D + 1;
+  if (u == g.D) M[g.D + g.D * N] = 1e200;  // any value above c^T (P*AP)^{-1} c keeps it SPD
   if (u >= g.D) return;
   const PCol p = pcol(g, u);
   double s = 0.0;
@@ -285,20 +306,21 @@ __global__ void k_rhs_real(SysArgs g, const double2* __restrict__ r, double* __r
     const double2 b = make_double2(r[p.i[x]].x * g.inv_n, r[p.i[x]].y * g.inv_n);
     s += cmul(cconj(p.a[x]), b).x;
   }
-  c[u] = s;
+  M[g.D + u * N] = s;
 }
 
-__global__ void k_theta_from_real(SysArgs g, const double* __restrict__ z, double2* __restrict__ theta) {
+__global__ void k_theta_from_real(SysArgs g, const double* __restrict__ zs, int64_t zstride, double2* __restrict__ theta) {
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
   if (u >= g.D) return;
+  auto z = [&](int i) { return zs[(int64_t)i * zstride]; };
   const int v = g.kind == FK_ADDITIVE ? u % (2 * g.m + 1) : u;
   const int base = g.kind == FK_ADDITIVE ? u - v : 0;
   if (v == 0) {
     const int c0 = g.kind == FK_ADDITIVE ? base + g.m : (g.D - 1) / 2;
-    theta[c0] = make_double2(z[u], 0.0);
+    theta[c0] = make_double2(z(u), 0.0);
   } else if (v & 1) {
     const PCol p = pcol(g, u);
-    const double a = z[u], b = z[u + 1];
+    const double a = z(u), b = z(u + 1);
     theta[p.i[0]] = make_double2(a, b);
     theta[p.i[1]] = make_double2(a, -b);
   }
@@ -319,9 +341,9 @@ fk_status lwork_for(int D, int* lwork) {
 size_t solve_ws_bytes(int d, int m, int kind) {
   const int D = unknowns(d, m, kind);
   int lwork = 0;
-  if (lwork_for(D, &lwork) != FK_OK) return 0;
+  if (lwork_for(D + 1, &lwork) != FK_OK) return 0;
   Bump b(nullptr, 0);
-  b.take((size_t)D * D * 8);
+  b.take((size_t)(D + 1) * (D + 1) * 8);
   b.take((size_t)lwork * 8);
   b.take((size_t)D * 8);
   b.take(64);
@@ -360,11 +382,11 @@ fk_status solve_run(const fk_problem* P, double* theta, fk_solve_report* rep, vo
   }
   const int D = g.D;
   int lwork = 0;
-  FK_TRY(lwork_for(D, &lwork));
+  const int N = D + 1;
+  FK_TRY(lwork_for(N, &lwork));
   Bump b(ws, ws_bytes);
-  double* M = (double*)b.take((size_t)D * D * 8);
+  double* M = (double*)b.take((size_t)N * N * 8);
   double* work = (double*)b.take((size_t)lwork * 8);
-  double* z = (double*)b.take((size_t)D * 8);
   int* info = (int*)b.take(16);
   double* res = (double*)(info + 4);
   double2* dsym = nullptr;
@@ -391,7 +413,7 @@ fk_status solve_run(const fk_problem* P, double* theta, fk_solve_report* rep, vo
     g.boxt = boxt;
   }
   k_assemble_real<<<sms * 8, 256, 0, s>>>(g, M);
-  k_rhs_real<<<(D + 255) / 256, 256, 0, s>>>(g, (const double2*)P->rhs, z);
+  k_rhs_real<<<(N + 255) / 256, 256, 0, s>>>(g, (const double2*)P->rhs, M);
   FK_CUDA_TRY(cudaGetLastError());
   count_launch(2);
   {
@@ -399,12 +421,16 @@ fk_status solve_run(const fk_problem* P, double* theta, fk_solve_report* rep, vo
     cusolverDnHandle_t h;
     FK_TRY(handle_for_device(&h));
     if (cusolverDnSetStream(h, s) != CUSOLVER_STATUS_SUCCESS) return fail(FK_E_CUDA, "cusolverDnSetStream failed");
-    if (cusolverDnDpotrf(h, CUBLAS_FILL_MODE_LOWER, D, M, D, work, lwork, info) != CUSOLVER_STATUS_SUCCESS)
+    if (cusolverDnDpotrf(h, CUBLAS_FILL_MODE_LOWER, N, M, N, work, lwork, info) != CUSOLVER_STATUS_SUCCESS)
       return fail(FK_E_CUDA, "cusolverDnDpotrf failed");
-    if (cusolverDnDpotrs(h, CUBLAS_FILL_MODE_LOWER, D, 1, M, D, z, D, info) != CUSOLVER_STATUS_SUCCESS)
-      return fail(FK_E_CUDA, "cusolverDnDpotrs failed");
+    cublasHandle_t bh;
+    FK_TRY(blas_for_device(&bh));
+    if (cublasSetStream(bh, s) != CUBLAS_STATUS_SUCCESS) return fail(FK_E_CUDA, "cublasSetStream failed");
+    // y = L^{-1} c is the factor's last row (stride N); solve L^T z = y in place
+    if (cublasDtrsv(bh, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, D, M, N, M + D, N) != CUBLAS_STATUS_SUCCESS)
+      return fail(FK_E_CUDA, "cublasDtrsv failed");
   }
-  k_theta_from_real<<<(D + 255) / 256, 256, 0, s>>>(g, z, (double2*)theta);
+  k_theta_from_real<<<(D + 255) / 256, 256, 0, s>>>(g, M + D, N, (double2*)theta);
   FK_CUDA_TRY(cudaGetLastError());
   count_launch();
   if (rep) {
