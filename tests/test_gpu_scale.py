@@ -35,7 +35,8 @@ def _closed_mu1(N, q):
 
 def test_full_size_gaussian_shard_additivity(F):
     """C2 (ii) workload (truncated-Gaussian X, n = 4e9 here): mu_0 = n exactly, and the moments
-    of the whole set equal the sum over two shards bit for bit (fixed-point sums are exact)."""
+    of the whole set equal the sum over two shards (the fine grids are exact fixed-point sums; only
+    the two FFTs' fp64 rounding differs)."""
     n = 4_000_000_000
     if _free_gb() < n * 8 / 1e9 + 4:
         pytest.skip("not enough device memory")
@@ -50,7 +51,7 @@ def test_full_size_gaussian_shard_additivity(F):
     del X, Y
     mu, mu2, r, r2 = host(mu), host(mu2), host(r), host(r2)
     assert mu[2000] == n
-    assert np.array_equal(mu, mu2)
+    assert rel(mu2, mu) < 1e-13
     assert rel(r2, r) < 1e-9
     # Hermitian symmetry of the fp64 outputs
     assert np.max(np.abs(mu[::-1] - np.conj(mu))) / abs(mu[2000]) < 1e-12
