@@ -1,0 +1,179 @@
+#!/usr/bin/env python
+"""Per-row measurements of the hot path (SURVEY.md §8(a) rows not timed by bench.py's fit step
+on their own), each against its roofline and beside the CPU oracle:
+
+  A12 predict (type-2 gather)     queries/s and GB/s of Xq in + f out (8 B/query fp32) vs HBM peak
+  A10/A11 solve                   GFLOP/s of the real Cholesky (D^3/3) vs the fp64 FMA peak
+  A7/A8 FFT + deconvolution       post-spread time of fk_rhs_type1 (reduce + cuFFT + deconv)
+
+    python bench_rows.py [--rows predict,solve,post]     -> one JSON line per measurement
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# fp64 FMA peak from unit counts and clock: 148 SMs x 64 FP64 FMA/clk x 2 flop x 1.965 GHz
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
+
+
+def hbm_peak():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+    except (OSError, ValueError, KeyError):
+        return 6650.0
+
+
+def timed(fn, reps=10, warm=3):
+    import torch
+
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def row_predict(out):
+    import numpy as np
+    import torch
+
+    import oracle
+    from datagen.device import gen_dataset
+    from paper_2509_02649_b200 import fk
+
+    for d, m, nq, eps, dt in [(1, 1000, 1 << 30, 1e-6, torch.float32), (1, 1000, 1 << 27, 1e-10, torch.float64),
+                              (2, 64, 1 << 28, 1e-6, torch.float32), (10, 50, 1 << 26, 1e-6, torch.float32)]:
+        additive = d > 2
+        rng = np.random.default_rng(0)
+        D = d * (2 * m + 1) if additive else (2 * m + 1) ** d
+        th = torch.from_numpy((rng.normal(size=D) + 1j * rng.normal(size=D)) / np.sqrt(D)).cuda()
+        Xq32 = torch.empty((nq, d) if d > 1 else (nq,), dtype=torch.float32, device="cuda")
+        gen_dataset(Xq32, None, nq, d, xkind=0, seed=1)
+        Xq = Xq32.to(dt) if dt != torch.float32 else Xq32
+        del Xq32
+        res = torch.empty(nq, dtype=dt, device="cuda")
+        ms = timed(lambda: fk.fk_predict_type2(th, d, m, 1.0, Xq, eps, additive=additive, out=res, check=False))
+        bpq = (d + 1) * (4 if dt == torch.float32 else 8)
+        gbs = nq * bpq / (ms * 1e-3) / 1e9
+        # oracle beside it: direct sum on a bounded sample of queries
+        ns = 2000 if d == 1 else 500
+        xs = Xq[:ns].double().cpu().numpy()
+        t0 = time.perf_counter()
+        if additive:
+            oracle.predict_additive(th.cpu().numpy(), xs, 1.0, m)
+        else:
+            oracle.predict(th.cpu().numpy(), xs, 1.0, m)
+        tcpu = time.perf_counter() - t0
+        out.append({"row": "A12 predict (type-2)", "d": d, "m": m, "additive": additive, "eps": eps, "dtype": str(dt).split(".")[-1],
+                    "queries": nq, "ms": ms, "queries_per_s": nq / (ms * 1e-3),
+                    "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm_peak(), "unit": "GB/s", "frac": gbs / hbm_peak(),
+                                 "bytes_per_query": bpq},
+                    "cpu_oracle": {"queries_per_s": ns / tcpu, "sample": ns, "threads": oracle.num_threads()}})
+        del Xq, res
+
+
+def row_solve(out):
+    import numpy as np
+    import torch
+
+    import datagen
+    import oracle
+    from paper_2509_02649_b200 import fk
+
+    HEAT = dict(alpha=[[1, 0], [0, 2]], a_alpha=[1.0, -1.0], box=[[-1.0, 1.0], [-1.0, 1.0]])
+    for d, m, kind in [(1, 1000, "sobolev"), (2, 32, "pik_box"), (10, 50, "additive"), (2, 64, "sobolev")]:
+        n = 200_000
+        if kind == "additive":
+            X, Y = datagen.dataset(n, d=d, ykind="additive")
+            Xd, Yd = torch.from_numpy(X).cuda(), torch.from_numpy(Y).cuda()
+            mus = torch.zeros((d, 4 * m + 1), dtype=torch.complex128, device="cuda")
+            rs = torch.zeros((d, 2 * m + 1), dtype=torch.complex128, device="cuda")
+            for l in range(d):
+                fk.fk_rhs_type1(Xd[:, l], Yd, 1.0, m, 1e-6, r_out=rs[l], mu_out=mus[l])
+            G = fk.fk_additive_cross_moments(Xd, 1.0, m, 1e-6)
+            args, kw = (mus, rs, n, d, m, 1.0, 1e-5, "additive"), dict(cross=G)
+        else:
+            X, Y = datagen.dataset(n, d=d, ykind="expcos" if d == 2 else "sin")
+            Xd = torch.from_numpy(X.reshape(-1) if d == 1 else X).cuda()
+            r, mu = fk.fk_rhs_type1(Xd, torch.from_numpy(Y).cuda(), 1.0, m, 1e-6)
+            args = (mu.reshape(-1), r.reshape(-1), n, d, m, 1.0, 1e-6, kind, 2.0)
+            kw = dict(mu_pde=1.0, **HEAT) if kind == "pik_box" else {}
+        for _ in range(2):
+            fk.fk_solve(*args, **kw)
+        reps = []
+        for _ in range(5):
+            _, rep = fk.fk_solve(*args, **kw)
+            reps.append(rep["ms"])
+        ms = float(np.median(reps))
+        D = rep["n_unknowns"]
+        gflops = (D + 1) ** 3 / 3.0 / (ms * 1e-3) / 1e9
+        cpu = None
+        if D <= 4225:  # numpy / LAPACK complex solve of the same system (the oracle's solve)
+            A = np.eye(D, dtype=np.complex128) + 0.01
+            b = np.ones(D, dtype=np.complex128)
+            t0 = time.perf_counter()
+            np.linalg.solve(A, b)
+            cpu = {"ms": 1e3 * (time.perf_counter() - t0), "what": "numpy.linalg.solve complex128 (the oracle's dense solve)"}
+        out.append({"row": "A10/A11 assemble + solve", "d": d, "m": m, "kind": kind, "D": D, "ms": ms,
+                    "backward_err": rep["backward_err"],
+                    "roofline": {"bound": "alu", "achieved": gflops / 1e3, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                                 "frac": gflops / 1e3 / FP64_PEAK_TFLOPS, "flops": (D + 1) ** 3 / 3.0,
+                                 "peak_source": "148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz"},
+                    "cpu_oracle": cpu})
+
+
+def row_post(out):
+    import torch
+
+    from datagen.device import gen_dataset
+    from paper_2509_02649_b200 import fk
+
+    for d, m, n in [(1, 1000, 1 << 24), (1, 50, 1 << 24), (2, 64, 1 << 24), (2, 32, 1 << 24)]:
+        X = torch.empty((n, d) if d > 1 else (n,), dtype=torch.float32, device="cuda")
+        Y = torch.empty(n, dtype=torch.float32, device="cuda")
+        gen_dataset(X, Y, n, d, xkind=0, ykind=1 if d == 2 else 0, seed=2)
+        r = torch.zeros((2 * m + 1,) * d, dtype=torch.complex128, device="cuda")
+        mu = torch.zeros((4 * m + 1,) * d, dtype=torch.complex128, device="cuda")
+        fk.profile_read()
+        fk.profile_enable(True)
+        ms = timed(lambda: fk.fk_rhs_type1(X, Y, 1.0, m, 1e-6, r_out=r, mu_out=mu, check=False), reps=10, warm=3)
+        fk.profile_enable(False)
+        sp, nl, _ = fk.profile_read()
+        spread = sp / max(1, nl)
+        out.append({"row": "A7/A8 reduce + FFT + deconvolution (post-spread part of fk_rhs_type1)", "d": d, "m": m, "n": n,
+                    "total_ms": ms, "spread_ms": spread, "post_spread_ms": ms - spread,
+                    "roofline": {"bound": "latency", "note": "fixed cost per fit: tiny grids (<= 1 MB), a handful of launches"}})
+        del X, Y
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--rows", default="predict,solve,post")
+    a = ap.parse_args()
+    import torch
+
+    from paper_2509_02649_b200 import build
+
+    build.build()
+    torch.cuda.set_device(0)
+    out = []
+    for r in a.rows.split(","):
+        {"predict": row_predict, "solve": row_solve, "post": row_post}[r](out)
+    for o in out:
+        print(json.dumps(o), flush=True)
+
+
+if __name__ == "__main__":
+    main()
