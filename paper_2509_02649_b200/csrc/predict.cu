@@ -7,6 +7,7 @@
 // grid, held in shared memory (fp32 path: cubic B-spline, 4 taps; fp64 path: ES window).
 // The gather streams Xq once and writes f once: 8 B per query in fp32 (HBM-bound).
 #include <cmath>
+#include <type_traits>
 
 #include "fk_internal.cuh"
 #include "window.cuh"
@@ -144,6 +145,39 @@ __global__ void __launch_bounds__(512) k_gather_bs3(const XT* __restrict__ Xq, i
   if (bad && d_status) atomicOr(d_status, (int)FK_E_RANGE);
 }
 
+// d = 1, fp32, contiguous 16-byte-aligned Xq / out, grid in smem: 4 queries per thread per step,
+// 128-bit streaming loads and stores (the scalar kernel above handles every other case)
+template <bool EXACT>
+__global__ void __launch_bounds__(512) k_gather_bs3_vec(const float4* __restrict__ Xq4, int64_t n4, const double* __restrict__ grid,
+                                                       int nf, int off, int G, float a_hi, float a_lo, float4* __restrict__ out4,
+                                                       int* __restrict__ d_status) {
+  extern __shared__ float sgv[];
+  for (int i = threadIdx.x; i < G; i += blockDim.x) sgv[i] = (float)grid[off + i];
+  __syncthreads();
+  const int nq = nf / 4;
+  bool bad = false;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n4; j += (int64_t)gridDim.x * blockDim.x) {
+    const float4 xv = __ldcs(Xq4 + j);
+    const float xs[4] = {xv.x, xv.y, xv.z, xv.w};
+    float r[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      int t;
+      float fr;
+      pos1_f32<EXACT>(xs[q], a_hi, a_lo, nq, t, fr);
+      const bool ok = (unsigned)t <= (unsigned)(G - 4);
+      bad |= !ok;
+      t = ok ? t : 0;
+      float w[4];
+      bs3_float(fr, w);
+      const float* c = sgv + t;
+      r[q] = ok ? (w[0] * c[0] + w[1] * c[1] + w[2] * c[2] + w[3] * c[3]) : NAN;
+    }
+    __stcs(out4 + j, make_float4(r[0], r[1], r[2], r[3]));
+  }
+  if (bad && d_status) atomicOr(d_status, (int)FK_E_RANGE);
+}
+
 template <typename XT>
 __global__ void __launch_bounds__(512) k_gather_es(const XT* __restrict__ Xq, int64_t n, int nfeat, int64_t sn, int64_t sd,
                                                   const double* __restrict__ grid, int nf, int off, int G, double a, int w,
@@ -200,6 +234,13 @@ __global__ void k_pred_prep2d(const double2* __restrict__ theta, int m, int nf, 
   H[t] = h;
 }
 
+template <typename GT>
+__device__ __forceinline__ GT es_eval(double beta, GT v);
+template <>
+__device__ __forceinline__ float es_eval<float>(double beta, float v) { return __expf((float)beta * (sqrtf(v) - 1.0f)); }
+template <>
+__device__ __forceinline__ double es_eval<double>(double beta, double v) { return exp(beta * (sqrt(v) - 1.0)); }
+
 // one coordinate on an ES grid: first tap (local index) and the offset f of the point
 __device__ __forceinline__ void es_place(double x, double a, int K, int w, int& l0, double& f) {
   const double p = x * a;
@@ -210,10 +251,11 @@ __device__ __forceinline__ void es_place(double x, double a, int K, int w, int& 
   f = f - d0;  // tap i sits at offset (i - f) cells
 }
 
-template <typename XT, typename GT>
+template <typename XT, typename GT, int W>
 __global__ void __launch_bounds__(256) k_gather2d(const XT* __restrict__ Xq, int64_t n, int64_t sn, int64_t sd,
-                                                 const double* __restrict__ grid, int nf, int off, int G, int K, double a, int w,
+                                                 const double* __restrict__ grid, int nf, int off, int G, int K, double a, int w_unused,
                                                  double beta, int in_smem, XT* __restrict__ out, int* __restrict__ d_status) {
+  constexpr int w = W;
   extern __shared__ unsigned char sgraw[];
   GT* sg = reinterpret_cast<GT*>(sgraw);
   if (in_smem) {
@@ -235,27 +277,28 @@ __global__ void __launch_bounds__(256) k_gather2d(const XT* __restrict__ Xq, int
       out[j] = (XT)NAN;
       continue;
     }
-    GT px[16];
-    for (int i = 0; i < 16; ++i) {
-      if (i < w) {
-        const GT z = ((GT)i - (GT)f1) * inv;
-        const GT v = (GT)1 - z * z;
-        px[i] = v > (GT)0 ? (GT)exp((double)beta * (sqrt((double)v) - 1.0)) : (GT)0;
-      }
+    GT px[W];
+#pragma unroll
+    for (int i = 0; i < W; ++i) {
+      const GT z = ((GT)i - (GT)f1) * inv;
+      const GT v = (GT)1 - z * z;
+      px[i] = v > (GT)0 ? es_eval<GT>(beta, v) : (GT)0;
     }
     GT acc = 0;
-    for (int r = 0; r < w; ++r) {
+#pragma unroll
+    for (int r = 0; r < W; ++r) {
       const GT z = ((GT)r - (GT)f0) * inv;
       const GT v = (GT)1 - z * z;
-      if (!(v > (GT)0)) continue;
-      const GT wy = (GT)exp((double)beta * (sqrt((double)v) - 1.0));
+      const GT wy = v > (GT)0 ? es_eval<GT>(beta, v) : (GT)0;
       GT racc = 0;
       if (in_smem) {
         const GT* row = sg + (int64_t)(l0 + r) * G + l1;
-        for (int c = 0; c < w; ++c) racc += px[c] * row[c];
+#pragma unroll
+        for (int c = 0; c < W; ++c) racc += px[c] * row[c];
       } else {
         const double* row = grid + (int64_t)(off + l0 + r) * nf + off + l1;
-        for (int c = 0; c < w; ++c) racc += px[c] * (GT)row[c];
+#pragma unroll
+        for (int c = 0; c < W; ++c) racc += px[c] * (GT)row[c];
       }
       acc += wy * racc;
     }
@@ -296,16 +339,30 @@ static fk_status gather2d(const PredPlan& p, const fk_points& Xq, double L, cons
   const double a = (double)p.nf / (4.0 * L);
   const int K = p.nf / 2 - p.g.off;
   const int per_sm = p.smem ? std::max(1, std::min(4, (int)(200000 / (p.smem + 1024)))) : 4;
-  if (p.fp64) {
-    auto k = k_gather2d<XT, double>;
+  auto go = [&](auto k) {
     if (p.smem) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
     k<<<sms * per_sm, 256, p.smem, s>>>((const XT*)Xq.ptr, Xq.n, Xq.stride_n, Xq.stride_d, w.grid, p.nf, p.g.off, p.g.G, K, a, p.es.w,
                                         p.es.beta, p.in_smem ? 1 : 0, (XT*)out, d_status);
-  } else {
-    auto k = k_gather2d<XT, float>;
-    if (p.smem) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
-    k<<<sms * per_sm, 256, p.smem, s>>>((const XT*)Xq.ptr, Xq.n, Xq.stride_n, Xq.stride_d, w.grid, p.nf, p.g.off, p.g.G, K, a, p.es.w,
-                                        p.es.beta, p.in_smem ? 1 : 0, (XT*)out, d_status);
+  };
+  auto byw = [&](auto wtag) {
+    constexpr int WW = decltype(wtag)::value;
+    if (p.fp64) go(k_gather2d<XT, double, WW>);
+    else go(k_gather2d<XT, float, WW>);
+  };
+  switch (p.es.w) {
+    case 4: byw(std::integral_constant<int, 4>{}); break;
+    case 5: byw(std::integral_constant<int, 5>{}); break;
+    case 6: byw(std::integral_constant<int, 6>{}); break;
+    case 7: byw(std::integral_constant<int, 7>{}); break;
+    case 8: byw(std::integral_constant<int, 8>{}); break;
+    case 9: byw(std::integral_constant<int, 9>{}); break;
+    case 10: byw(std::integral_constant<int, 10>{}); break;
+    case 11: byw(std::integral_constant<int, 11>{}); break;
+    case 12: byw(std::integral_constant<int, 12>{}); break;
+    case 13: byw(std::integral_constant<int, 13>{}); break;
+    case 14: byw(std::integral_constant<int, 14>{}); break;
+    case 15: byw(std::integral_constant<int, 15>{}); break;
+    default: byw(std::integral_constant<int, 16>{}); break;
   }
   FK_CUDA_TRY(cudaGetLastError());
   count_launch();
@@ -320,9 +377,31 @@ static fk_status gather(const PredPlan& p, const fk_points& Xq, double L, const 
     const float a_hi = (float)a, a_lo = (float)(a - (double)a_hi);
     int ex = 0;
     const bool exact = std::frexp(a, &ex) == 0.5;
+    const int per_sm = p.smem ? std::max(1, std::min(4, (int)(200000 / (p.smem + 1024)))) : 4;
+    const bool vec = sizeof(XT) == 4 && p.nfeat == 1 && p.in_smem && Xq.stride_n == 1 && ((uintptr_t)Xq.ptr % 16 == 0) &&
+                     ((uintptr_t)out % 16 == 0) && Xq.n >= 4;
+    if (vec) {
+      const int64_t n4 = Xq.n / 4;
+      auto kv = exact ? k_gather_bs3_vec<true> : k_gather_bs3_vec<false>;
+      cudaFuncSetAttribute(kv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+      kv<<<sms * per_sm, 512, p.smem, s>>>((const float4*)Xq.ptr, n4, w.grid, p.nf, p.g.off, p.g.G, a_hi, a_lo, (float4*)out, d_status);
+      FK_CUDA_TRY(cudaGetLastError());
+      count_launch();
+      if (n4 * 4 == Xq.n) return FK_OK;
+      // tail (< 4 queries) through the scalar kernel
+      fk_points tail = Xq;
+      tail.ptr = (const float*)Xq.ptr + n4 * 4;
+      tail.n = Xq.n - n4 * 4;
+      auto ks = exact ? k_gather_bs3<float, true> : k_gather_bs3<float, false>;
+      cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+      ks<<<1, 512, p.smem, s>>>((const float*)tail.ptr, tail.n, 1, 1, 1, w.grid, p.nf, p.g.off, p.g.G, a_hi, a_lo, a, 1,
+                                (float*)out + n4 * 4, d_status);
+      FK_CUDA_TRY(cudaGetLastError());
+      count_launch();
+      return FK_OK;
+    }
     auto k = exact ? k_gather_bs3<XT, true> : k_gather_bs3<XT, false>;
     if (p.smem) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
-    const int per_sm = p.smem ? std::max(1, std::min(4, (int)(200000 / (p.smem + 1024)))) : 4;
     k<<<sms * per_sm, 512, p.smem, s>>>((const XT*)Xq.ptr, Xq.n, p.nfeat, Xq.stride_n, Xq.stride_d, w.grid, p.nf, p.g.off, p.g.G,
                                         a_hi, a_lo, a, p.in_smem ? 1 : 0, (XT*)out, d_status);
   } else {
