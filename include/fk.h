@@ -96,7 +96,9 @@ typedef enum fk_kind {
   FK_SOBOLEV = 0,  /* M = S, S_kk^2 = 1 + ||k||_2^{2s} */
   FK_LOWBIAS = 1,  /* M = I */
   FK_PIK_BOX = 2,  /* Sobolev + mu_pde D^* C D, Omega a box in [-L,L]^d          (reading R3) */
-  FK_ADDITIVE = 3  /* low-bias additive block system, theta in C^{d(2m+1)} */
+  FK_ADDITIVE = 3, /* low-bias additive block system, theta in C^{d(2m+1)} */
+  FK_PIK_COLLOC = 4 /* Sobolev + mu_pde n_r^{-1} D^* (Phi^r)^* Phi^r D from collocation points'
+                       moments, for domains without a closed-form Fourier matrix */
 } fk_kind;
 
 typedef struct fk_problem {
@@ -109,6 +111,9 @@ typedef struct fk_problem {
   const double* mu_moments;  /* device: (4m+1)^d complex128; ADDITIVE: d x (4m+1) (per-feature 1-D moments) */
   const double* rhs;         /* device: (2m+1)^d complex128; ADDITIVE: d x (2m+1) (per-feature 1-D rhs) */
   const double* cross;       /* device: ADDITIVE only, d(d-1)/2 x (2m+1)^2 from fk_additive_cross_moments */
+  const double* colloc_moments; /* device: PIK_COLLOC only, (4m+1)^d moments of the n_colloc collocation
+                                   points (fk_moments_type1 on them); D is given by alpha / a_alpha */
+  double n_colloc;              /* PIK_COLLOC: number of collocation points n_r */
 } fk_problem;
 
 typedef struct fk_solve_report {

@@ -193,11 +193,14 @@ def box_fourier_matrix(d: int, m: int, L: float, box) -> np.ndarray:
 # The regularised Fourier system and its solve
 # ---------------------------------------------------------------------------------------------
 def assemble(mu, n_total: float, d: int, m: int, lam: float, kind: str = "sobolev", s: float = 1.0,
-             mu_pde: float = 0.0, L: float = 1.0, alpha=None, a_alpha=None, box=None) -> np.ndarray:
+             mu_pde: float = 0.0, L: float = 1.0, alpha=None, a_alpha=None, box=None, mu_colloc=None,
+             n_colloc: float = 0.0) -> np.ndarray:
     """A = T(mu)/n + lam * M*M (+ mu_pde * D* B D) (P:107 eq. kenrel_reg; P:252 Sobolev M=S;
-    P:316 low-bias M=I; P:396 physics-informed, tractable box domain)."""
+    P:316 low-bias M=I; P:396 physics-informed, tractable box domain; P:413 physics-informed,
+    collocation: + mu_pde n_r^{-1} D* (Phi^r)* Phi^r D with (Phi^r)* Phi^r = T(mu_colloc), the
+    Toeplitz matrix of the collocation points' moments)."""
     A = toeplitz_from_moments(np.asarray(mu), d, m) / float(n_total)
-    if kind in ("sobolev", "pik_box"):
+    if kind in ("sobolev", "pik_box", "pik_colloc"):
         A = A + lam * np.diag(sobolev_weights(d, m, s))
     elif kind == "lowbias":
         A = A + lam * np.eye(A.shape[0])
@@ -206,6 +209,10 @@ def assemble(mu, n_total: float, d: int, m: int, lam: float, kind: str = "sobole
     if kind == "pik_box":
         dk = pde_symbol(d, m, L, alpha, a_alpha)
         A = A + mu_pde * (np.conj(dk)[:, None] * box_fourier_matrix(d, m, L, box) * dk[None, :])
+    if kind == "pik_colloc":
+        dk = pde_symbol(d, m, L, alpha, a_alpha)
+        Tr = toeplitz_from_moments(np.asarray(mu_colloc), d, m) / float(n_colloc)
+        A = A + mu_pde * (np.conj(dk)[:, None] * Tr * dk[None, :])
     return A
 
 
@@ -260,7 +267,10 @@ def fit(X, Y, L: float, m: int, lam: float, kind: str = "sobolev", s: float = 1.
     d = X.shape[1]
     mu = moments(X, L, m)
     r = rhs(X, Y, L, m)
-    if kind == "pik_box":
+    if kind in ("pik_box", "pik_colloc"):
         pi = dict(pi, L=L)
+    if kind == "pik_colloc":  # collocation points -> their moments
+        Xr = _points(pi.pop("X_colloc"))
+        pi = dict(pi, mu_colloc=moments(Xr, L, m), n_colloc=Xr.shape[0])
     theta = solve(mu, r, X.shape[0], d, m, lam, kind, s, **pi)
     return theta, mu, r

@@ -90,11 +90,16 @@ fk_status fk_solve(const fk_problem* P, double* theta_out, fk_solve_report* rep,
   if (!(P->lambda > 0.0)) return fail(FK_E_ARG, "fk_solve: lambda must be > 0");
   if (!(P->n_total > 0.0)) return fail(FK_E_ARG, "fk_solve: n_total must be > 0");
   if (!(P->L > 0.0)) return fail(FK_E_ARG, "fk_solve: L must be > 0");
-  if (P->kind < FK_SOBOLEV || P->kind > FK_ADDITIVE) return fail(FK_E_ARG, "fk_solve: unknown kind");
+  if (P->kind < FK_SOBOLEV || P->kind > FK_PIK_COLLOC) return fail(FK_E_ARG, "fk_solve: unknown kind");
   if (!P->mu_moments || !P->rhs) return fail(FK_E_ARG, "fk_solve: null moments or rhs");
   if (P->kind == FK_ADDITIVE && P->d > 1 && !P->cross) return fail(FK_E_ARG, "fk_solve: ADDITIVE needs cross moments");
   if (P->kind != FK_ADDITIVE && P->d > 3) return fail(FK_E_UNSUPPORTED, "fk_solve: d <= 3 for the dense tensor-grid system");
-  if ((P->kind == FK_SOBOLEV || P->kind == FK_PIK_BOX) && !(P->s > 0.0)) return fail(FK_E_ARG, "fk_solve: s must be > 0");
+  if ((P->kind == FK_SOBOLEV || P->kind == FK_PIK_BOX || P->kind == FK_PIK_COLLOC) && !(P->s > 0.0))
+    return fail(FK_E_ARG, "fk_solve: s must be > 0");
+  if (P->kind == FK_PIK_COLLOC) {
+    if (P->n_terms < 1 || !P->alpha || !P->a_alpha) return fail(FK_E_ARG, "fk_solve: PIK_COLLOC needs alpha, a_alpha");
+    if (!P->colloc_moments || !(P->n_colloc > 0.0)) return fail(FK_E_ARG, "fk_solve: PIK_COLLOC needs colloc_moments and n_colloc > 0");
+  }
   if (P->kind == FK_PIK_BOX) {
     if (P->n_terms < 1 || !P->alpha || !P->a_alpha || !P->box) return fail(FK_E_ARG, "fk_solve: PIK_BOX needs alpha, a_alpha, box");
     for (int l = 0; l < P->d; ++l) {

@@ -34,6 +34,8 @@ struct SysArgs {
   const double2* cross;
   const double2* dsym;  // PI tables (k_pi_tables), or null
   const double2* boxt;
+  const double2* mur;   // PIK_COLLOC: collocation moments
+  double inv_nr;        // PIK_COLLOC: 1 / n_colloc
 };
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) { return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
@@ -120,6 +122,15 @@ __device__ double2 entry(const SysArgs& g, int i, int j) {
       R = 1.0 + pow(nk2, g.s);
     }
     v.x += g.lambda * R;
+  }
+  if (g.kind == FK_PIK_COLLOC && g.mu_pde != 0.0) {
+    // mu_pde conj(d_k1) (T(mu_r))_{k1,k2} d_k2 / n_r
+    double2 tr = g.mur[qi];
+    tr.x *= g.inv_nr;
+    tr.y *= g.inv_nr;
+    const double2 t = cmul(cmul(cconj(g.dsym[i]), tr), g.dsym[j]);
+    v.x += g.mu_pde * t.x;
+    v.y += g.mu_pde * t.y;
   }
   if (g.kind == FK_PIK_BOX && g.mu_pde != 0.0) {
     double2 t;
@@ -347,7 +358,7 @@ size_t solve_ws_bytes(int d, int m, int kind) {
   b.take((size_t)lwork * 8);
   b.take((size_t)D * 8);
   b.take(64);
-  if (kind == FK_PIK_BOX) {
+  if (kind == FK_PIK_BOX || kind == FK_PIK_COLLOC) {
     b.take((size_t)D * 16);
     b.take((size_t)d * (4 * m + 1) * 16);
   }
@@ -368,14 +379,16 @@ fk_status solve_run(const fk_problem* P, double* theta, fk_solve_report* rep, vo
   g.inv4L = 1.0 / (4.0 * P->L);
   g.mu = (const double2*)P->mu_moments;
   g.cross = (const double2*)P->cross;
-  if (P->kind == FK_PIK_BOX) {
+  g.mur = (const double2*)P->colloc_moments;
+  g.inv_nr = P->n_colloc > 0 ? 1.0 / P->n_colloc : 0.0;
+  if (P->kind == FK_PIK_BOX || P->kind == FK_PIK_COLLOC) {
     if (P->n_terms < 0 || P->n_terms > kMaxTerms || P->d > kMaxD) return fail(FK_E_ARG, "fk_solve: at most 8 PDE terms, d <= 4");
     g.n_terms = P->n_terms;
     for (int t = 0; t < P->n_terms; ++t) {
       g.a_alpha[t] = P->a_alpha[t];
       for (int l = 0; l < P->d; ++l) g.alpha[t][l] = P->alpha[t * P->d + l];
     }
-    for (int l = 0; l < P->d; ++l) {
+    for (int l = 0; l < P->d && P->box; ++l) {
       g.box[l][0] = P->box[2 * l];
       g.box[l][1] = P->box[2 * l + 1];
     }
@@ -391,7 +404,7 @@ fk_status solve_run(const fk_problem* P, double* theta, fk_solve_report* rep, vo
   double* res = (double*)(info + 4);
   double2* dsym = nullptr;
   double2* boxt = nullptr;
-  if (P->kind == FK_PIK_BOX) {
+  if (P->kind == FK_PIK_BOX || P->kind == FK_PIK_COLLOC) {
     dsym = (double2*)b.take((size_t)D * 16);
     boxt = (double2*)b.take((size_t)P->d * (4 * P->m + 1) * 16);
   }
@@ -404,7 +417,7 @@ fk_status solve_run(const fk_problem* P, double* theta, fk_solve_report* rep, vo
     cudaEventRecord(e0, s);
   }
   const int sms = device_sm_count();
-  if (P->kind == FK_PIK_BOX) {
+  if (P->kind == FK_PIK_BOX || P->kind == FK_PIK_COLLOC) {
     const int nt = std::max(D, P->d * (4 * P->m + 1));
     k_pi_tables<<<(nt + 255) / 256, 256, 0, s>>>(g, dsym, boxt);
     FK_CUDA_TRY(cudaGetLastError());

@@ -20,8 +20,8 @@ LIB_PATH = os.path.join(_HERE, "libfk.so")
 FK_OK, FK_E_ARG, FK_E_RANGE, FK_E_EPS, FK_E_CUDA, FK_E_WORKSPACE, FK_E_SOLVE, FK_E_UNSUPPORTED = range(8)
 FK_F32, FK_F64 = 0, 1
 FK_ACCUMULATE = 1
-FK_SOBOLEV, FK_LOWBIAS, FK_PIK_BOX, FK_ADDITIVE = 0, 1, 2, 3
-KINDS = {"sobolev": FK_SOBOLEV, "lowbias": FK_LOWBIAS, "pik_box": FK_PIK_BOX, "additive": FK_ADDITIVE}
+FK_SOBOLEV, FK_LOWBIAS, FK_PIK_BOX, FK_ADDITIVE, FK_PIK_COLLOC = 0, 1, 2, 3, 4
+KINDS = {"sobolev": FK_SOBOLEV, "lowbias": FK_LOWBIAS, "pik_box": FK_PIK_BOX, "additive": FK_ADDITIVE, "pik_colloc": FK_PIK_COLLOC}
 FK_ENTRY_MOMENTS, FK_ENTRY_RHS, FK_ENTRY_CROSS, FK_ENTRY_SOLVE, FK_ENTRY_PREDICT = range(5)
 _STATUS = {1: "FK_E_ARG", 2: "FK_E_RANGE", 3: "FK_E_EPS", 4: "FK_E_CUDA", 5: "FK_E_WORKSPACE", 6: "FK_E_SOLVE", 7: "FK_E_UNSUPPORTED"}
 
@@ -42,7 +42,7 @@ class fk_problem(ctypes.Structure):
                 ("n_total", ctypes.c_double), ("L", ctypes.c_double), ("s", ctypes.c_double), ("lam", ctypes.c_double),
                 ("mu_pde", ctypes.c_double), ("alpha", ctypes.POINTER(ctypes.c_int32)), ("a_alpha", ctypes.POINTER(ctypes.c_double)),
                 ("box", ctypes.POINTER(ctypes.c_double)), ("mu_moments", ctypes.c_void_p), ("rhs", ctypes.c_void_p),
-                ("cross", ctypes.c_void_p)]
+                ("cross", ctypes.c_void_p), ("colloc_moments", ctypes.c_void_p), ("n_colloc", ctypes.c_double)]
 
 
 class fk_solve_report(ctypes.Structure):
@@ -189,7 +189,7 @@ def fk_additive_cross_moments(X: torch.Tensor, L: float, m: int, eps: float = 1e
 def fk_solve(mu: torch.Tensor, r: torch.Tensor, n_total: float, d: int, m: int, L: float, lam: float, kind: str = "sobolev",
              s: float = 1.0, mu_pde: float = 0.0, alpha: Optional[Sequence] = None, a_alpha: Optional[Sequence[float]] = None,
              box: Optional[Sequence] = None, cross: Optional[torch.Tensor] = None, theta_out: Optional[torch.Tensor] = None,
-             report: bool = True, stream=None):
+             report: bool = True, stream=None, colloc_moments: Optional[torch.Tensor] = None, n_colloc: float = 0.0):
     """theta = A^{-1} r/n (dense fp64 Cholesky).  Returns (theta complex128, report dict or None)."""
     k = KINDS[kind] if isinstance(kind, str) else int(kind)
     D = d * (2 * m + 1) if k == FK_ADDITIVE else (2 * m + 1) ** d
@@ -199,15 +199,22 @@ def fk_solve(mu: torch.Tensor, r: torch.Tensor, n_total: float, d: int, m: int, 
     prob.d, prob.m, prob.kind = d, m, k
     prob.n_total, prob.L, prob.s, prob.lam, prob.mu_pde = float(n_total), float(L), float(s), float(lam), float(mu_pde)
     keep = []
-    if k == FK_PIK_BOX:
+    if k in (FK_PIK_BOX, FK_PIK_COLLOC):
         al = (ctypes.c_int32 * (len(alpha) * d))(*[int(v) for row in alpha for v in row])
         aa = (ctypes.c_double * len(a_alpha))(*[float(v) for v in a_alpha])
-        bx = (ctypes.c_double * (2 * d))(*[float(v) for row in box for v in row])
-        keep += [al, aa, bx]
+        keep += [al, aa]
         prob.n_terms = len(a_alpha)
         prob.alpha = ctypes.cast(al, ctypes.POINTER(ctypes.c_int32))
         prob.a_alpha = ctypes.cast(aa, ctypes.POINTER(ctypes.c_double))
-        prob.box = ctypes.cast(bx, ctypes.POINTER(ctypes.c_double))
+        if box is not None:
+            bx = (ctypes.c_double * (2 * d))(*[float(v) for row in box for v in row])
+            keep.append(bx)
+            prob.box = ctypes.cast(bx, ctypes.POINTER(ctypes.c_double))
+    if k == FK_PIK_COLLOC:
+        colloc_moments = colloc_moments.contiguous()
+        keep.append(colloc_moments)
+        prob.colloc_moments = colloc_moments.data_ptr()
+        prob.n_colloc = float(n_colloc)
     mu = mu.contiguous()
     r = r.contiguous()
     prob.mu_moments = mu.data_ptr()

@@ -360,3 +360,42 @@ def test_schedules_golden(oracle):
         mm, ll = oracle.schedule(float(n), float(s), int(d))
         assert mm == int(m)
         assert abs(ll - float(lam)) / float(lam) < 1e-3
+
+
+# --------------------------------------------------------------------------------------------
+# P7': physics-informed penalty by collocation
+# --------------------------------------------------------------------------------------------
+def test_pi_collocation_quadratic_form(oracle):
+    """theta^* D^* T(mu_r) D theta / n_r == n_r^{-1} sum_i |D f_theta(X^r_i)|^2, with
+    D f evaluated by finite differences of f itself (independent of the symbol d_k)."""
+    d, m, L = 2, 3, 1.0
+    alpha, a_alpha = [[1, 0], [0, 2]], [1.0, -1.0]
+    Xr = RNG.uniform(-0.8, 0.9, size=(400, d))
+    k = oracle.mode_grid(d, m).astype(np.float64)
+    theta = RNG.normal(size=k.shape[0]) + 1j * RNG.normal(size=k.shape[0])
+    dk = oracle.pde_symbol(d, m, L, alpha, a_alpha)
+    Tr = oracle.toeplitz_from_moments(oracle.moments(Xr, L, m), d, m)
+    form = np.real(np.conj(theta * dk) @ Tr @ (theta * dk)) / Xr.shape[0]
+    fun = lambda x: _f_theta(theta, k, x, L)
+    Df = _fd(fun, Xr, 0, 1, 1e-3) - _fd(fun, Xr, 1, 2, 1e-3)
+    direct = np.mean(np.abs(Df) ** 2)
+    assert abs(form - direct) / direct < 1e-7
+
+
+def test_pi_collocation_matches_box_penalty(oracle):
+    """Collocation on a fine midpoint grid of the box Omega approximates the box penalty:
+    mu' n_r^{-1} sum |Df|^2 ~ mu' |Omega|^{-1} int |Df|^2, i.e. pik_colloc(mu') == pik_box(mu) for
+    mu' = mu |Omega| (4L)^{-d} (P:398-404 vs P:410-413)."""
+    d, m, L, s, lam = 2, 4, 1.0, 2.0, 1e-4
+    alpha, a_alpha = [[1, 0], [0, 2]], [1.0, -1.0]
+    box = [[-0.6, 0.7], [-0.9, 0.5]]
+    X, Y = datagen.dataset(3000, d=2, ykind="expcos", seed=41)
+    mu, r = oracle.moments(X, L, m), oracle.rhs(X, Y, L, m)
+    g = 200
+    ax = [np.linspace(a, b, g, endpoint=False) + (b - a) / (2 * g) for a, b in box]
+    Xr = np.stack(np.meshgrid(*ax, indexing="ij"), -1).reshape(-1, d)
+    vol = np.prod([b - a for a, b in box])
+    th_box = oracle.solve(mu, r, 3000, d, m, lam, "pik_box", s, mu_pde=1.0, L=L, alpha=alpha, a_alpha=a_alpha, box=box)
+    th_col = oracle.solve(mu, r, 3000, d, m, lam, "pik_colloc", s, mu_pde=vol / (4 * L) ** d, L=L, alpha=alpha, a_alpha=a_alpha,
+                          mu_colloc=oracle.moments(Xr, L, m), n_colloc=Xr.shape[0])
+    assert rel(th_col, th_box) < 1e-3
