@@ -5,8 +5,9 @@ on their own), each against its roofline and beside the CPU oracle:
   A12 predict (type-2 gather)     queries/s and GB/s of Xq in + f out (8 B/query fp32) vs HBM peak
   A10/A11 solve                   GFLOP/s of the real Cholesky (D^3/3) vs the fp64 FMA peak
   A7/A8 FFT + deconvolution       post-spread time of fk_rhs_type1 (reduce + cuFFT + deconv)
+  NEXT-1 lambda path              fk_solve_path over 300 lambdas vs 300 fk_solve calls
 
-    python bench_rows.py [--rows predict,solve,post]     -> one JSON line per measurement
+    python bench_rows.py [--rows predict,solve,post,path]     -> one JSON line per measurement
 """
 from __future__ import annotations
 
@@ -158,9 +159,46 @@ def row_post(out):
         del X, Y
 
 
+def row_path(out):
+    import numpy as np
+    import torch
+
+    import datagen
+    from paper_2509_02649_b200 import fk
+
+    lams = list(np.logspace(-9, -1, 300))
+    for d, m, kind in [(1, 1000, "sobolev"), (10, 50, "additive"), (2, 32, "sobolev")]:
+        n = 200_000
+        X, Y = datagen.dataset(n, d=d, ykind="additive" if kind == "additive" else ("expcos" if d == 2 else "sin"))
+        Xd, Yd = torch.from_numpy(X.reshape(-1) if d == 1 else X).cuda(), torch.from_numpy(Y).cuda()
+        kw = {}
+        if kind == "additive":
+            mu = torch.zeros((d, 4 * m + 1), dtype=torch.complex128, device="cuda")
+            r = torch.zeros((d, 2 * m + 1), dtype=torch.complex128, device="cuda")
+            for l in range(d):
+                fk.fk_rhs_type1(Xd[:, l], Yd, 1.0, m, 1e-6, r_out=r[l], mu_out=mu[l])
+            kw["cross"] = fk.fk_additive_cross_moments(Xd, 1.0, m, 1e-6)
+        else:
+            r, mu = fk.fk_rhs_type1(Xd, Yd, 1.0, m, 1e-6)
+            mu, r = mu.reshape(-1), r.reshape(-1)
+        th = torch.empty(len(lams), d * (2 * m + 1) if kind == "additive" else (2 * m + 1) ** d, dtype=torch.complex128, device="cuda")
+        ms_path = timed(lambda: fk.fk_solve_path(mu, r, n, d, m, 1.0, lams, kind, 2.0, theta_out=th, check=False, **kw), reps=3, warm=1)
+        one = th[0].clone()
+        ms_chol = timed(lambda: [fk.fk_solve(mu, r, n, d, m, 1.0, lam, kind, 2.0, theta_out=one, report=False, **kw) for lam in lams],
+                        reps=1, warm=1)
+        # agreement of the two methods at the median lambda
+        l = len(lams) // 2
+        ch, _ = fk.fk_solve(mu, r, n, d, m, 1.0, lams[l], kind, 2.0, **kw)
+        err = float(torch.linalg.norm(th[l] - ch) / torch.linalg.norm(ch))
+        out.append({"row": "NEXT-1 lambda path (one eigendecomposition, P:542-548)", "d": d, "m": m, "kind": kind,
+                    "D": th.shape[1], "n_lambda": len(lams), "path_ms": ms_path, "cholesky_per_lambda_ms": ms_chol,
+                    "speedup": ms_chol / ms_path, "rel_diff_vs_cholesky": err})
+        del Xd, Yd
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--rows", default="predict,solve,post")
+    ap.add_argument("--rows", default="predict,solve,post,path")
     a = ap.parse_args()
     import torch
 
@@ -170,7 +208,7 @@ def main():
     torch.cuda.set_device(0)
     out = []
     for r in a.rows.split(","):
-        {"predict": row_predict, "solve": row_solve, "post": row_post}[r](out)
+        {"predict": row_predict, "solve": row_solve, "post": row_post, "path": row_path}[r](out)
     for o in out:
         print(json.dumps(o), flush=True)
 

@@ -136,12 +136,34 @@ fk_status fk_solve(const fk_problem* P, double* theta_out, fk_solve_report* rep,
 fk_status fk_predict_type2(const double* theta, int d, int m, double L, int additive, fk_points Xq, double eps, void* out,
                            void* ws, size_t ws_bytes, int* d_status, fk_stream_t stream);
 
+/* Regularisation path (grid search over lambda reusing one pass over the data):
+ * theta_l = A(lambda_l)^{-1} r / n for nlam values lambdas[l] (host array), all other fields of *P
+ * as for fk_solve (P->lambda is ignored).  A(lambda) = A0 + lambda M^*M with the real-symmetric
+ * reduction of fk_solve; one eigendecomposition of Dg^{-1/2} A0 Dg^{-1/2} (Dg = the diagonal of
+ * M^*M in the real basis) then costs O(D^2) per lambda.  theta_out: nlam x D complex128 (device,
+ * row l = theta(lambda_l)).  If info != NULL the call synchronises `stream` and stores the
+ * eigensolver's info (0 = success; FK_E_SOLVE otherwise). */
+fk_status fk_solve_path(const fk_problem* P, const double* lambdas, int nlam, double* theta_out, int* info, void* ws,
+                        size_t ws_bytes, fk_stream_t stream);
+
+/* Held-out risk along a path (grid search; reading R11):
+ * risk_out[l] = (1/n_v) sum_j (Y_j - f_l(x_j))^2 over a validation set, f_l the predictor of
+ * theta[l] (nlam x D complex128, device, Hermitian as produced by fk_solve / fk_solve_path), computed
+ * WITHOUT predicting at the validation points: from the validation set's moments and rhs (the same
+ * type-1 calls on (X_v, Y_v)), Pv->mu_moments / rhs / cross / n_total = those sums and n_v, Pv->d, m,
+ * kind as for the fit (lambda, mu_pde and PI fields ignored).  sum_y2 = sum_j Y_j^2 (host scalar; it
+ * only shifts every risk equally).  risk_out: nlam doubles (device).  Asynchronous on `stream`. */
+fk_status fk_path_validate(const fk_problem* Pv, const double* theta, int nlam, double sum_y2, double* risk_out, void* ws,
+                           size_t ws_bytes, fk_stream_t stream);
+
 typedef enum fk_entry {
   FK_ENTRY_MOMENTS = 0,
   FK_ENTRY_RHS = 1,
   FK_ENTRY_CROSS = 2,
   FK_ENTRY_SOLVE = 3,
-  FK_ENTRY_PREDICT = 4
+  FK_ENTRY_PREDICT = 4,
+  FK_ENTRY_SOLVE_PATH = 5, /* n = number of lambdas */
+  FK_ENTRY_PATH_VALIDATE = 6 /* n = number of lambdas */
 } fk_entry;
 
 /* Workspace bytes the call `entry` needs for (d, m, eps, dtype, n, kind) on the current device

@@ -83,11 +83,10 @@ fk_status fk_additive_cross_moments(fk_points X, double L, int m, double eps, do
   return cross_run(X, L, m, eps, G_out, (flags & FK_ACCUMULATE) != 0, ws, ws_bytes, d_status, (cudaStream_t)stream);
 }
 
-fk_status fk_solve(const fk_problem* P, double* theta_out, fk_solve_report* rep, void* ws, size_t ws_bytes, fk_stream_t stream) {
-  set_error("");
-  if (!P || !theta_out) return fail(FK_E_ARG, "fk_solve: null problem or output");
+static fk_status check_problem(const fk_problem* P, bool need_lambda) {
+  if (!P) return fail(FK_E_ARG, "fk_solve: null problem");
   if (P->m < 1 || P->d < 1) return fail(FK_E_ARG, "fk_solve: d, m must be >= 1");
-  if (!(P->lambda > 0.0)) return fail(FK_E_ARG, "fk_solve: lambda must be > 0");
+  if (need_lambda && !(P->lambda > 0.0)) return fail(FK_E_ARG, "fk_solve: lambda must be > 0");
   if (!(P->n_total > 0.0)) return fail(FK_E_ARG, "fk_solve: n_total must be > 0");
   if (!(P->L > 0.0)) return fail(FK_E_ARG, "fk_solve: L must be > 0");
   if (P->kind < FK_SOBOLEV || P->kind > FK_PIK_COLLOC) return fail(FK_E_ARG, "fk_solve: unknown kind");
@@ -110,7 +109,37 @@ fk_status fk_solve(const fk_problem* P, double* theta_out, fk_solve_report* rep,
   // dense systems above ~2.5e4 unknowns exceed a sensible workspace
   long D = P->kind == FK_ADDITIVE ? (long)P->d * (2 * P->m + 1) : (long)std::pow(2.0 * P->m + 1, P->d);
   if (D > 40000) return fail(FK_E_UNSUPPORTED, "fk_solve: dense system too large (D = " + std::to_string(D) + ")");
+  return FK_OK;
+}
+
+fk_status fk_solve(const fk_problem* P, double* theta_out, fk_solve_report* rep, void* ws, size_t ws_bytes, fk_stream_t stream) {
+  set_error("");
+  if (!theta_out) return fail(FK_E_ARG, "fk_solve: null output");
+  FK_TRY(check_problem(P, true));
   return solve_run(P, theta_out, rep, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+fk_status fk_solve_path(const fk_problem* P, const double* lambdas, int nlam, double* theta_out, int* info, void* ws,
+                        size_t ws_bytes, fk_stream_t stream) {
+  set_error("");
+  if (!theta_out || !lambdas || nlam < 1) return fail(FK_E_ARG, "fk_solve_path: null output / lambdas or nlam < 1");
+  for (int l = 0; l < nlam; ++l)
+    if (!(lambdas[l] > 0.0)) return fail(FK_E_ARG, "fk_solve_path: every lambda must be > 0");
+  FK_TRY(check_problem(P, false));
+  return solve_path_run(P, lambdas, nlam, theta_out, info, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+fk_status fk_path_validate(const fk_problem* Pv, const double* theta, int nlam, double sum_y2, double* risk_out, void* ws,
+                           size_t ws_bytes, fk_stream_t stream) {
+  set_error("");
+  if (!theta || !risk_out || nlam < 1) return fail(FK_E_ARG, "fk_path_validate: null theta / risk_out or nlam < 1");
+  if (!Pv) return fail(FK_E_ARG, "fk_path_validate: null problem");
+  fk_problem q = *Pv;  // data part only: lambda, s and the PI fields are not used
+  if (q.kind == FK_PIK_BOX || q.kind == FK_PIK_COLLOC) q.kind = FK_SOBOLEV;
+  q.s = 1.0;
+  q.n_terms = 0;
+  FK_TRY(check_problem(&q, false));
+  return path_validate_run(&q, theta, nlam, sum_y2, risk_out, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 fk_status fk_predict_type2(const double* theta, int d, int m, double L, int additive, fk_points Xq, double eps, void* out, void* ws,
@@ -144,6 +173,10 @@ size_t fk_workspace_bytes(int entry, int d, int m, double eps, int dtype, int64_
       return solve_ws_bytes(d, m, kind);
     case FK_ENTRY_PREDICT:
       return predict_ws_bytes(d, m, eps, kind);
+    case FK_ENTRY_PATH_VALIDATE:
+      return path_validate_ws_bytes(d, m, kind, (int)std::min<int64_t>(n, 1 << 20));
+    case FK_ENTRY_SOLVE_PATH:
+      return solve_path_ws_bytes(d, m, kind, (int)std::min<int64_t>(n, 1 << 20));
     default:
       set_error("fk_workspace_bytes: unknown entry");
       return 0;

@@ -120,6 +120,12 @@ fk_status type1_run(const Plan1& p, const fk_points& X, const void* Y, double L,
 // solve (solve.cu), predict (predict.cu), additive (additive.cu)
 // ------------------------------------------------------------------------------------------
 size_t solve_ws_bytes(int d, int m, int kind);
+size_t solve_path_ws_bytes(int d, int m, int kind, int nlam);
+fk_status solve_path_run(const fk_problem* P, const double* lambdas, int nlam, double* theta, int* info, void* ws, size_t ws_bytes,
+                         cudaStream_t s);
+size_t path_validate_ws_bytes(int d, int m, int kind, int nlam);
+fk_status path_validate_run(const fk_problem* Pv, const double* theta, int nlam, double sum_y2, double* risk_out, void* ws,
+                            size_t ws_bytes, cudaStream_t s);
 fk_status solve_run(const fk_problem* P, double* theta, fk_solve_report* rep, void* ws, size_t ws_bytes, cudaStream_t s);
 
 size_t predict_ws_bytes(int d, int m, double eps, int additive);

@@ -4,10 +4,14 @@
 //   A[k1,k2] = mu_{k1-k2}/n + lambda R_{k1} delta_{k1 k2} (+ mu_pde conj(d_{k1}) B(k2-k1) d_{k2})
 //   A theta  = r / n
 //
-// A is Hermitian positive definite for lambda > 0; it is factorised by cuSOLVER zpotrf (fp64
-// Cholesky) and solved by zpotrs.  CG is not used: cond(A) is 1e6..1e11 at the
-// BASELINE configurations and Jacobi-preconditioned CG would need 1e3+ iterations (DESIGN.md
-// reading R9).  The backward error of the report re-evaluates A from the moments on the fly.
+// A is Hermitian positive definite for lambda > 0.  For real Y, theta is Hermitian (theta_{-k} =
+// conj theta_k), so theta = P z with z real and P*AP z = P*r/n real SPD (1/4 of the complex
+// flops).  The real system is assembled with the rhs as an extra row (N = D + 1) so that cuSOLVER
+// dpotrf's last row holds L^{-1} c and one dtrsv finishes the solve.  CG is not used:
+// cond(A) is 1e6..1e11 at the BASELINE configurations and Jacobi-preconditioned CG would need 1e3+
+// iterations (reading R9).  The backward error of the report re-evaluates the complex A
+// from the moments on the fly.  The lambda path (fk_solve_path) and the held-out risk
+// (fk_path_validate) reuse the same real assembly.
 #include <cublas_v2.h>
 #include <cusolverDn.h>
 
@@ -363,6 +367,285 @@ size_t solve_ws_bytes(int d, int m, int kind) {
     b.take((size_t)d * (4 * m + 1) * 16);
   }
   return b.used + 256;
+}
+
+static fk_status fill_sysargs(const fk_problem* P, SysArgs* out) {
+  SysArgs g{};
+  g.d = P->d;
+  g.m = P->m;
+  g.kind = P->kind;
+  g.D = unknowns(P->d, P->m, P->kind);
+  g.inv_n = 1.0 / P->n_total;
+  g.lambda = P->lambda;
+  g.s = P->s;
+  g.mu_pde = P->mu_pde;
+  g.c = 3.14159265358979323846 / (2.0 * P->L);
+  g.inv4L = 1.0 / (4.0 * P->L);
+  g.mu = (const double2*)P->mu_moments;
+  g.cross = (const double2*)P->cross;
+  g.mur = (const double2*)P->colloc_moments;
+  g.inv_nr = P->n_colloc > 0 ? 1.0 / P->n_colloc : 0.0;
+  if (P->kind == FK_PIK_BOX || P->kind == FK_PIK_COLLOC) {
+    if (P->n_terms < 0 || P->n_terms > kMaxTerms || P->d > kMaxD) return fail(FK_E_ARG, "fk_solve: at most 8 PDE terms, d <= 4");
+    g.n_terms = P->n_terms;
+    for (int t = 0; t < P->n_terms; ++t) {
+      g.a_alpha[t] = P->a_alpha[t];
+      for (int l = 0; l < P->d; ++l) g.alpha[t][l] = P->alpha[t * P->d + l];
+    }
+    for (int l = 0; l < P->d && P->box; ++l) {
+      g.box[l][0] = P->box[2 * l];
+      g.box[l][1] = P->box[2 * l + 1];
+    }
+  }
+  *out = g;
+  return FK_OK;
+}
+
+// ---- regularisation path (many lambda, one pass over the data) -------------
+// M(lambda) = M0 + lambda Dg with Dg = P^* R P diagonal (R_k on the centre, 2 R_k on a_k, b_k).
+// With Dg^{-1/2} M0 Dg^{-1/2} = V diag(ev) V^T (one dsyevd): z(lambda) = Dg^{-1/2} V (V^T
+// Dg^{-1/2} c) / (ev + lambda), i.e. one GEMV and one D x L GEMM for all lambdas.
+__global__ void k_path_diag(SysArgs g, double* __restrict__ dg) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= g.D) return;
+  const PCol p = pcol(g, u);
+  // R at mode i: the diagonal of A(lambda = 1) minus A(lambda = 0), via entry()
+  SysArgs g1 = g, g0 = g;
+  g1.lambda = 1.0;
+  g0.lambda = 0.0;
+  const double r = entry(g1, p.i[0], p.i[0]).x - entry(g0, p.i[0], p.i[0]).x;
+  dg[u] = p.cnt * r;
+}
+
+__global__ void k_path_scale(double* __restrict__ M, int64_t ld, int D, const double* __restrict__ dg) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)D * D; t += (int64_t)gridDim.x * blockDim.x) {
+    const int v = (int)(t / D), u = (int)(t % D);
+    if (u < v) continue;
+    M[u + v * ld] *= rsqrt(dg[u]) * rsqrt(dg[v]);
+  }
+}
+
+__global__ void k_path_rhs(const double* __restrict__ M, int64_t ld, int D, const double* __restrict__ dg, double* __restrict__ c) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u < D) c[u] = M[D + u * ld] * rsqrt(dg[u]);  // c lives in the augmented row D
+}
+
+__global__ void k_path_weights(const double* __restrict__ w, const double* __restrict__ ev, const double* __restrict__ lams, int D,
+                               int nl, double* __restrict__ S) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)D * nl; t += (int64_t)gridDim.x * blockDim.x) {
+    const int u = (int)(t % D), l = (int)(t / D);
+    S[t] = w[u] / (ev[u] + lams[l]);
+  }
+}
+
+__global__ void k_path_theta(SysArgs g, const double* __restrict__ Z, const double* __restrict__ dg, int nl, double2* __restrict__ theta) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)g.D * nl; t += (int64_t)gridDim.x * blockDim.x) {
+    const int u = (int)(t % g.D), l = (int)(t / g.D);
+    const int v = g.kind == FK_ADDITIVE ? u % (2 * g.m + 1) : u;
+    const double* z = Z + (int64_t)l * g.D;
+    double2* th = theta + (int64_t)l * g.D;
+    if (v == 0) {
+      const int c0 = g.kind == FK_ADDITIVE ? u - v + g.m : (g.D - 1) / 2;
+      th[c0] = make_double2(z[u] * rsqrt(dg[u]), 0.0);
+    } else if (v & 1) {
+      const PCol p = pcol(g, u);
+      const double a = z[u] * rsqrt(dg[u]), b = z[u + 1] * rsqrt(dg[u + 1]);
+      th[p.i[0]] = make_double2(a, b);
+      th[p.i[1]] = make_double2(a, -b);
+    }
+  }
+}
+
+static fk_status syevd_lwork(int D, int ld, int* lwork) {
+  std::lock_guard<std::mutex> lk(g_sol_mu);
+  cusolverDnHandle_t h;
+  FK_TRY(handle_for_device(&h));
+  if (cusolverDnDsyevd_bufferSize(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, D, nullptr, ld, nullptr, lwork) !=
+      CUSOLVER_STATUS_SUCCESS)
+    return fail(FK_E_CUDA, "cusolverDnDsyevd_bufferSize failed");
+  return FK_OK;
+}
+
+struct PathWs {
+  double *M, *work, *dg, *ev, *wv, *lam, *S, *Z;
+  int* info;
+  double2 *dsym, *boxt;
+};
+// one layout for the size query and the run
+static void path_layout(Bump& b, int d, int m, int kind, int D, int lwork, int nlam, PathWs* w) {
+  const int N = D + 1;
+  w->M = (double*)b.take((size_t)N * N * 8);
+  w->work = (double*)b.take((size_t)lwork * 8);
+  w->dg = (double*)b.take((size_t)D * 8);
+  w->ev = (double*)b.take((size_t)D * 8);
+  w->wv = (double*)b.take((size_t)D * 8);
+  w->lam = (double*)b.take((size_t)nlam * 8);
+  w->S = (double*)b.take((size_t)D * nlam * 8);
+  w->Z = (double*)b.take((size_t)D * nlam * 8);
+  w->info = (int*)b.take(16);
+  w->dsym = w->boxt = nullptr;
+  if (kind == FK_PIK_BOX || kind == FK_PIK_COLLOC) {
+    w->dsym = (double2*)b.take((size_t)D * 16);
+    w->boxt = (double2*)b.take((size_t)d * (4 * m + 1) * 16);
+  }
+}
+
+size_t solve_path_ws_bytes(int d, int m, int kind, int nlam) {
+  const int D = unknowns(d, m, kind);
+  int lwork = 0;
+  if (syevd_lwork(D, D + 1, &lwork) != FK_OK) return 0;
+  Bump b(nullptr, 0);
+  PathWs w;
+  path_layout(b, d, m, kind, D, lwork, std::max(nlam, 1), &w);
+  return b.used;
+}
+
+fk_status solve_path_run(const fk_problem* P, const double* lambdas, int nlam, double* theta, int* info_out, void* ws, size_t ws_bytes,
+                         cudaStream_t s) {
+  SysArgs g;
+  FK_TRY(fill_sysargs(P, &g));
+  g.lambda = 0.0;  // M0: the data (and PDE) part only
+  const int D = g.D, N = D + 1;
+  int lwork = 0;
+  FK_TRY(syevd_lwork(D, N, &lwork));
+  Bump b(ws, ws_bytes);
+  PathWs w;
+  path_layout(b, P->d, P->m, P->kind, D, lwork, nlam, &w);
+  double *M = w.M, *work = w.work, *dg = w.dg, *ev = w.ev, *wv = w.wv, *lam_d = w.lam, *S = w.S, *Z = w.Z;
+  int* info = w.info;
+  double2 *dsym = w.dsym, *boxt = w.boxt;
+  if (!b.ok()) return fail(FK_E_WORKSPACE, "fk_solve_path: workspace too small");
+  const int sms = device_sm_count();
+  FK_CUDA_TRY(cudaMemcpyAsync(lam_d, lambdas, (size_t)nlam * 8, cudaMemcpyHostToDevice, s));
+  if (dsym) {
+    const int nt = std::max(D, P->d * (4 * P->m + 1));
+    k_pi_tables<<<(nt + 255) / 256, 256, 0, s>>>(g, dsym, boxt);
+    g.dsym = dsym;
+    g.boxt = boxt;
+    count_launch();
+  }
+  k_assemble_real<<<sms * 8, 256, 0, s>>>(g, M);
+  k_rhs_real<<<(N + 255) / 256, 256, 0, s>>>(g, (const double2*)P->rhs, M);
+  k_path_diag<<<(D + 255) / 256, 256, 0, s>>>(g, dg);
+  k_path_scale<<<sms * 8, 256, 0, s>>>(M, N, D, dg);
+  k_path_rhs<<<(D + 255) / 256, 256, 0, s>>>(M, N, D, dg, Z);  // scaled c into Z[:,0] (scratch)
+  FK_CUDA_TRY(cudaGetLastError());
+  count_launch(5);
+  {
+    std::lock_guard<std::mutex> lk(g_sol_mu);
+    cusolverDnHandle_t h;
+    FK_TRY(handle_for_device(&h));
+    if (cusolverDnSetStream(h, s) != CUSOLVER_STATUS_SUCCESS) return fail(FK_E_CUDA, "cusolverDnSetStream failed");
+    if (cusolverDnDsyevd(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, D, M, N, ev, work, lwork, info) !=
+        CUSOLVER_STATUS_SUCCESS)
+      return fail(FK_E_CUDA, "cusolverDnDsyevd failed");
+    cublasHandle_t bh;
+    FK_TRY(blas_for_device(&bh));
+    if (cublasSetStream(bh, s) != CUBLAS_STATUS_SUCCESS) return fail(FK_E_CUDA, "cublasSetStream failed");
+    const double one = 1.0, zero = 0.0;
+    // w = V^T (Dg^{-1/2} c)
+    if (cublasDgemv(bh, CUBLAS_OP_T, D, D, &one, M, N, Z, 1, &zero, wv, 1) != CUBLAS_STATUS_SUCCESS)
+      return fail(FK_E_CUDA, "cublasDgemv failed");
+    k_path_weights<<<sms * 4, 256, 0, s>>>(wv, ev, lam_d, D, nlam, S);
+    count_launch();
+    // Z = V S  (D x nlam)
+    if (cublasDgemm(bh, CUBLAS_OP_N, CUBLAS_OP_N, D, nlam, D, &one, M, N, S, D, &zero, Z, D) != CUBLAS_STATUS_SUCCESS)
+      return fail(FK_E_CUDA, "cublasDgemm failed");
+  }
+  k_path_theta<<<sms * 4, 256, 0, s>>>(g, Z, dg, nlam, (double2*)theta);
+  FK_CUDA_TRY(cudaGetLastError());
+  count_launch();
+  if (info_out) {
+    int hinfo = 0;
+    FK_CUDA_TRY(cudaMemcpyAsync(&hinfo, info, 4, cudaMemcpyDeviceToHost, s));
+    FK_CUDA_TRY(cudaStreamSynchronize(s));
+    *info_out = hinfo;
+    if (hinfo != 0) return fail(FK_E_SOLVE, "fk_solve_path: eigensolver failed, info = " + std::to_string(hinfo));
+  }
+  return FK_OK;
+}
+
+// ---- held-out risk along the path (grid search; reading R11) -----------------
+// For real Y and Hermitian theta, f(x) = sum_k theta_k e^{i k t} is real and, with the validation
+// set's moments mu^v, rhs r^v (n_v samples):  sum_j (Y_j - f(x_j))^2 / n_v
+//   = sum_y2 / n_v - 2 Re(theta^* r^v) / n_v + theta^* T(mu^v) theta / n_v
+//   = sum_y2 / n_v - 2 z^T c_v + z^T M_v z      (z = real coordinates of theta, theta = P z)
+// with M_v, c_v the real-reduced data system of the validation moments (k_assemble_real, lambda = 0).
+__global__ void k_z_from_theta(SysArgs g, const double2* __restrict__ theta, int nl, double* __restrict__ Z) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)g.D * nl; t += (int64_t)gridDim.x * blockDim.x) {
+    const int u = (int)(t % g.D), l = (int)(t / g.D);
+    const double2* th = theta + (int64_t)l * g.D;
+    const int v = g.kind == FK_ADDITIVE ? u % (2 * g.m + 1) : u;
+    double z;
+    if (v == 0) {
+      z = th[g.kind == FK_ADDITIVE ? u - v + g.m : (g.D - 1) / 2].x;
+    } else {
+      const PCol p = pcol(g, u);
+      z = (v & 1) ? th[p.i[0]].x : th[p.i[0]].y;
+    }
+    Z[t] = z;
+  }
+}
+
+__global__ void k_val_risk(const double* __restrict__ Z, const double* __restrict__ W, const double* __restrict__ M, int64_t ld, int D,
+                           double base, double* __restrict__ out) {
+  const int l = blockIdx.x;
+  const double* z = Z + (int64_t)l * D;
+  const double* w = W + (int64_t)l * D;
+  double acc = 0.0;
+  for (int u = threadIdx.x; u < D; u += blockDim.x) acc += z[u] * (w[u] - 2.0 * M[D + u * ld]);
+  __shared__ double red[32];
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    acc = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (threadIdx.x == 0) out[l] = base + acc;
+  }
+}
+
+size_t path_validate_ws_bytes(int d, int m, int kind, int nlam) {
+  const int D = unknowns(d, m, kind), N = D + 1;
+  Bump b(nullptr, 0);
+  b.take((size_t)N * N * 8);
+  b.take((size_t)D * std::max(nlam, 1) * 8);
+  b.take((size_t)D * std::max(nlam, 1) * 8);
+  return b.used;
+}
+
+fk_status path_validate_run(const fk_problem* Pv, const double* theta, int nlam, double sum_y2, double* risk_out, void* ws,
+                            size_t ws_bytes, cudaStream_t s) {
+  SysArgs g;
+  FK_TRY(fill_sysargs(Pv, &g));
+  g.lambda = 0.0;
+  g.mu_pde = 0.0;
+  if (g.kind == FK_PIK_BOX || g.kind == FK_PIK_COLLOC) g.kind = FK_SOBOLEV;  // data part only
+  const int D = g.D, N = D + 1;
+  Bump b(ws, ws_bytes);
+  double* M = (double*)b.take((size_t)N * N * 8);
+  double* Z = (double*)b.take((size_t)D * nlam * 8);
+  double* W = (double*)b.take((size_t)D * nlam * 8);
+  if (!b.ok()) return fail(FK_E_WORKSPACE, "fk_path_validate: workspace too small");
+  const int sms = device_sm_count();
+  k_assemble_real<<<sms * 8, 256, 0, s>>>(g, M);
+  k_rhs_real<<<(N + 255) / 256, 256, 0, s>>>(g, (const double2*)Pv->rhs, M);
+  k_z_from_theta<<<sms * 4, 256, 0, s>>>(g, (const double2*)theta, nlam, Z);
+  FK_CUDA_TRY(cudaGetLastError());
+  count_launch(3);
+  {
+    std::lock_guard<std::mutex> lk(g_sol_mu);
+    cublasHandle_t bh;
+    FK_TRY(blas_for_device(&bh));
+    if (cublasSetStream(bh, s) != CUBLAS_STATUS_SUCCESS) return fail(FK_E_CUDA, "cublasSetStream failed");
+    const double one = 1.0, zero = 0.0;
+    if (cublasDsymm(bh, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, D, nlam, &one, M, N, Z, D, &zero, W, D) != CUBLAS_STATUS_SUCCESS)
+      return fail(FK_E_CUDA, "cublasDsymm failed");
+  }
+  k_val_risk<<<nlam, 256, 0, s>>>(Z, W, M, N, D, sum_y2 * g.inv_n, risk_out);
+  FK_CUDA_TRY(cudaGetLastError());
+  count_launch();
+  return FK_OK;
 }
 
 fk_status solve_run(const fk_problem* P, double* theta, fk_solve_report* rep, void* ws, size_t ws_bytes, cudaStream_t s) {

@@ -4,6 +4,10 @@
   fit_distributed(...)        one process per GPU: each rank passes its sample shard, the small
                               unnormalised [mu | r] vector is all-reduced (sum) over NCCL, rank 0
                               solves and broadcasts theta (shard additivity R5)
+  grid_search(...)            regularisation path: type-1 passes over the training and
+                              validation sets, ONE eigendecomposition for every lambda
+                              (fk_solve_path), held-out risk of every lambda from the validation
+                              moments (fk_path_validate) -- no per-lambda prediction pass
   fit_host(X_host, Y_host)    host (pinned) inputs streamed to the device in chunks on a copy
                               stream, overlapped with the spreading of the previous chunk; the
                               per-chunk outputs accumulate (FK_ACCUMULATE)
@@ -116,6 +120,45 @@ def fit_additive_distributed(X_shard: torch.Tensor, Y_shard: torch.Tensor, n_tot
         _, rep = fk.fk_solve(mus, rs, n_total, d, m, L, lam, "additive", cross=G, theta_out=theta_out, report=report)
     broadcast_theta(theta_out, group)
     return FitResult(theta_out, mus, rs, n_total, rep)
+
+
+@dataclass
+class GridResult:
+    lambdas: list
+    risk: torch.Tensor        # float64 (nlam,), held-out mean squared error of each lambda
+    thetas: torch.Tensor      # complex128 (nlam, D)
+    best: int                 # argmin of risk
+    theta: torch.Tensor       # thetas[best]
+
+
+def _passes(X, Y, L, m, eps, additive):
+    """One type-1 pass over (X, Y): (mu, r, cross) in the layout fk_solve expects."""
+    if additive:
+        d = X.shape[1]
+        _, mus, rs, G = additive_buffers(d, m, X.device)
+        for l in range(d):
+            fk.fk_rhs_type1(X[:, l], Y, L, m, eps, r_out=rs[l], mu_out=mus[l], check=False)
+        fk.fk_additive_cross_moments(X, L, m, eps, G_out=G, check=False)
+        return mus, rs, G
+    d = 1 if X.dim() == 1 else X.shape[1]
+    _, mu, r = _moment_buffers(d, m, X.device)
+    fk.fk_rhs_type1(X, Y, L, m, eps, r_out=r, mu_out=mu, check=False)
+    return mu.reshape(-1), r.reshape(-1), None
+
+
+def grid_search(X: torch.Tensor, Y: torch.Tensor, X_val: torch.Tensor, Y_val: torch.Tensor, L: float, m: int, lambdas,
+                kind: str = "sobolev", s: float = 1.0, eps: float = 1e-6, **pi) -> GridResult:
+    """Choose lambda on a held-out split (P:542-548 grid search over 300 values; R11)."""
+    additive = kind == "additive"
+    d = X.shape[1] if X.dim() == 2 else 1
+    mu, r, G = _passes(X, Y, L, m, eps, additive)
+    mu_v, r_v, G_v = _passes(X_val, Y_val, L, m, eps, additive)
+    thetas = fk.fk_solve_path(mu, r, X.shape[0], d, m, L, list(lambdas), kind, s, cross=G, **pi)
+    # sum Y_v^2 only shifts every risk by the same constant (reported MSE, not the argmin)
+    sum_y2 = float(torch.dot(Y_val.double(), Y_val.double()))
+    risk = fk.fk_path_validate(thetas, mu_v, r_v, X_val.shape[0], d, m, L, kind, sum_y2, cross_v=G_v)
+    best = int(torch.argmin(risk))
+    return GridResult(list(lambdas), risk, thetas, best, thetas[best])
 
 
 class HostStreamer:

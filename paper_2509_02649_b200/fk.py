@@ -22,7 +22,8 @@ FK_F32, FK_F64 = 0, 1
 FK_ACCUMULATE = 1
 FK_SOBOLEV, FK_LOWBIAS, FK_PIK_BOX, FK_ADDITIVE, FK_PIK_COLLOC = 0, 1, 2, 3, 4
 KINDS = {"sobolev": FK_SOBOLEV, "lowbias": FK_LOWBIAS, "pik_box": FK_PIK_BOX, "additive": FK_ADDITIVE, "pik_colloc": FK_PIK_COLLOC}
-FK_ENTRY_MOMENTS, FK_ENTRY_RHS, FK_ENTRY_CROSS, FK_ENTRY_SOLVE, FK_ENTRY_PREDICT = range(5)
+(FK_ENTRY_MOMENTS, FK_ENTRY_RHS, FK_ENTRY_CROSS, FK_ENTRY_SOLVE, FK_ENTRY_PREDICT, FK_ENTRY_SOLVE_PATH,
+ FK_ENTRY_PATH_VALIDATE) = range(7)
 _STATUS = {1: "FK_E_ARG", 2: "FK_E_RANGE", 3: "FK_E_EPS", 4: "FK_E_CUDA", 5: "FK_E_WORKSPACE", 6: "FK_E_SOLVE", 7: "FK_E_UNSUPPORTED"}
 
 
@@ -64,12 +65,15 @@ def lib():
         L.fk_rhs_type1.argtypes = [fk_points, vp, dp, ip, dp, vp, vp, ip, vp, sz, vp, vp]
         L.fk_additive_cross_moments.argtypes = [fk_points, dp, ip, dp, vp, ip, vp, sz, vp, vp]
         L.fk_solve.argtypes = [ctypes.POINTER(fk_problem), vp, ctypes.POINTER(fk_solve_report), vp, sz, vp]
+        L.fk_solve_path.argtypes = [ctypes.POINTER(fk_problem), vp, ip, vp, vp, vp, sz, vp]
+        L.fk_path_validate.argtypes = [ctypes.POINTER(fk_problem), vp, ip, dp, vp, vp, sz, vp]
         L.fk_predict_type2.argtypes = [vp, ip, ip, dp, ip, fk_points, dp, vp, vp, sz, vp, vp]
         L.fk_workspace_bytes.argtypes = [ip, ip, ip, dp, ip, ctypes.c_int64, ip]
         L.fk_workspace_bytes.restype = ctypes.c_size_t
         L.fk_last_error.restype = ctypes.c_char_p
         L.fk_version.restype = ctypes.c_char_p
-        for f in ("fk_moments_type1", "fk_rhs_type1", "fk_additive_cross_moments", "fk_solve", "fk_predict_type2"):
+        for f in ("fk_moments_type1", "fk_rhs_type1", "fk_additive_cross_moments", "fk_solve", "fk_solve_path", "fk_path_validate",
+                  "fk_predict_type2"):
             getattr(L, f).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -195,6 +199,62 @@ def fk_solve(mu: torch.Tensor, r: torch.Tensor, n_total: float, d: int, m: int, 
     D = d * (2 * m + 1) if k == FK_ADDITIVE else (2 * m + 1) ** d
     if theta_out is None:
         theta_out = torch.empty(D, dtype=torch.complex128, device=mu.device)
+    prob, keep = _problem(mu, r, n_total, d, m, L, lam, k, s, mu_pde, alpha, a_alpha, box, cross, colloc_moments, n_colloc)
+    nb = fk_workspace_bytes(FK_ENTRY_SOLVE, d, m, 1e-6, FK_F64, 0, k)
+    ws = _workspace(nb, mu.device)
+    rep = fk_solve_report()
+    _check(lib().fk_solve(ctypes.byref(prob), theta_out.data_ptr(), ctypes.byref(rep) if report else None, ws.data_ptr(), ws.numel(),
+                          _stream(stream)))
+    del keep
+    out = None
+    if report:
+        out = {"backward_err": rep.backward_err, "ms": rep.ms, "info": rep.info, "n_unknowns": rep.n_unknowns}
+    return theta_out, out
+
+
+def fk_solve_path(mu: torch.Tensor, r: torch.Tensor, n_total: float, d: int, m: int, L: float, lambdas: Sequence[float],
+                  kind: str = "sobolev", s: float = 1.0, mu_pde: float = 0.0, alpha: Optional[Sequence] = None,
+                  a_alpha: Optional[Sequence[float]] = None, box: Optional[Sequence] = None, cross: Optional[torch.Tensor] = None,
+                  theta_out: Optional[torch.Tensor] = None, check: bool = True, stream=None,
+                  colloc_moments: Optional[torch.Tensor] = None, n_colloc: float = 0.0) -> torch.Tensor:
+    """theta(lambda_l) for every lambda in `lambdas` from ONE eigendecomposition (regularisation path,
+    P:542-548).  Returns a (nlam, D) complex128 tensor."""
+    k = KINDS[kind] if isinstance(kind, str) else int(kind)
+    D = d * (2 * m + 1) if k == FK_ADDITIVE else (2 * m + 1) ** d
+    lams = (ctypes.c_double * len(lambdas))(*[float(v) for v in lambdas])
+    if theta_out is None:
+        theta_out = torch.empty(len(lambdas), D, dtype=torch.complex128, device=mu.device)
+    prob, keep = _problem(mu, r, n_total, d, m, L, 0.0, k, s, mu_pde, alpha, a_alpha, box, cross, colloc_moments, n_colloc)
+    nb = fk_workspace_bytes(FK_ENTRY_SOLVE_PATH, d, m, 1e-6, FK_F64, len(lambdas), k)
+    ws = _workspace(nb, mu.device)
+    info = ctypes.c_int(0)
+    _check(lib().fk_solve_path(ctypes.byref(prob), lams, len(lambdas), theta_out.data_ptr(), ctypes.byref(info) if check else None,
+                               ws.data_ptr(), ws.numel(), _stream(stream)))
+    del keep
+    return theta_out
+
+
+def fk_path_validate(theta: torch.Tensor, mu_v: torch.Tensor, r_v: torch.Tensor, n_v: float, d: int, m: int, L: float,
+                     kind: str = "sobolev", sum_y2: float = 0.0, cross_v: Optional[torch.Tensor] = None,
+                     risk_out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """Held-out mean squared error of each row of theta (nlam x D) on a validation set given by its
+    type-1 moments mu_v / rhs r_v (and cross moments for the additive model), n_v samples and
+    sum_y2 = sum Y_v^2 (P:542-548 grid search; R11).  Returns nlam float64 (device)."""
+    k = KINDS[kind] if isinstance(kind, str) else int(kind)
+    theta = theta.contiguous()
+    nlam = theta.shape[0] if theta.dim() == 2 else 1
+    if risk_out is None:
+        risk_out = torch.empty(nlam, dtype=torch.float64, device=theta.device)
+    prob, keep = _problem(mu_v, r_v, n_v, d, m, L, 0.0, k, 1.0, 0.0, None, None, None, cross_v, None, 0.0)
+    nb = fk_workspace_bytes(FK_ENTRY_PATH_VALIDATE, d, m, 1e-6, FK_F64, nlam, k)
+    ws = _workspace(nb, theta.device)
+    _check(lib().fk_path_validate(ctypes.byref(prob), theta.data_ptr(), nlam, float(sum_y2), risk_out.data_ptr(), ws.data_ptr(),
+                                  ws.numel(), _stream(stream)))
+    del keep
+    return risk_out
+
+
+def _problem(mu, r, n_total, d, m, L, lam, k, s, mu_pde, alpha, a_alpha, box, cross, colloc_moments, n_colloc):
     prob = fk_problem()
     prob.d, prob.m, prob.kind = d, m, k
     prob.n_total, prob.L, prob.s, prob.lam, prob.mu_pde = float(n_total), float(L), float(s), float(lam), float(mu_pde)
@@ -219,17 +279,12 @@ def fk_solve(mu: torch.Tensor, r: torch.Tensor, n_total: float, d: int, m: int, 
     r = r.contiguous()
     prob.mu_moments = mu.data_ptr()
     prob.rhs = r.data_ptr()
-    prob.cross = cross.contiguous().data_ptr() if cross is not None else None
-    nb = fk_workspace_bytes(FK_ENTRY_SOLVE, d, m, 1e-6, FK_F64, 0, k)
-    ws = _workspace(nb, mu.device)
-    rep = fk_solve_report()
-    _check(lib().fk_solve(ctypes.byref(prob), theta_out.data_ptr(), ctypes.byref(rep) if report else None, ws.data_ptr(), ws.numel(),
-                          _stream(stream)))
-    del keep
-    out = None
-    if report:
-        out = {"backward_err": rep.backward_err, "ms": rep.ms, "info": rep.info, "n_unknowns": rep.n_unknowns}
-    return theta_out, out
+    if cross is not None:
+        cross = cross.contiguous()
+        keep.append(cross)
+        prob.cross = cross.data_ptr()
+    keep += [mu, r]
+    return prob, keep
 
 
 def fk_predict_type2(theta: torch.Tensor, d: int, m: int, L: float, Xq: torch.Tensor, eps: float = 1e-6, additive: bool = False,
