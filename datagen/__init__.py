@@ -10,6 +10,7 @@ Recipe (DESIGN.md "Input recipe"):
   z(i, stream)   = splitmix64((seed << 48) ^ (stream << 40) ^ i)
   u24            = z >> 40  (and (z >> 16) & 0xFFFFFF as a second draw)
   uniform X      = (2 u24 + 1 - 2^24) * 2^-24            in (-1, 1), exact in fp32
+  unit X         = u24 * 2^-24                           in [0, 1) (the rate experiment)
   gaussian X     = clip(IH4 * 0.6928203f, -1, 1): Irwin-Hall of 4 draws (sd 0.577) rescaled
                    to sd 0.4 and truncated to the box
   noise          = (sum of 12 draws - 6 * 2^24) * 2^-24   (Irwin-Hall approx. of N(0,1))
@@ -23,8 +24,8 @@ from __future__ import annotations
 import numpy as np
 
 M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
-XKIND = {"uniform": 0, "gaussian": 1, "equispaced": 2}
-YKIND = {"sin": 0, "expcos": 1, "additive": 2, "pattern01": 3, "zero": 4}
+XKIND = {"uniform": 0, "gaussian": 1, "equispaced": 2, "unit": 3}
+YKIND = {"sin": 0, "expcos": 1, "additive": 2, "pattern01": 3, "zero": 4, "exp": 5}
 EQ_N = 1 << 24
 
 
@@ -50,6 +51,11 @@ def _u24pair(idx, stream, seed):
 def _uniform(idx, stream, seed) -> np.ndarray:
     u, _ = _u24pair(idx, stream, seed)
     return ((2 * u + 1 - (1 << 24)).astype(np.float32) * np.float32(2.0 ** -24)).astype(np.float32)
+
+
+def _unit(idx, stream, seed) -> np.ndarray:
+    u, _ = _u24pair(idx, stream, seed)
+    return (u.astype(np.float32) * np.float32(2.0 ** -24)).astype(np.float32)
 
 
 def _gaussian(idx, stream, seed) -> np.ndarray:
@@ -107,10 +113,11 @@ def dataset(n: int, d: int = 1, i0: int = 0, xkind: str = "uniform", ykind: str 
     idx = np.arange(i0, i0 + n, dtype=np.int64)
     X = np.empty((n, d), dtype=np.float32)
     f = np.float32
-    if xkind not in ("uniform", "gaussian"):
-        raise ValueError("xkind must be 'uniform' or 'gaussian' (use equispaced() for the pin data)")
+    gen = {"uniform": _uniform, "gaussian": _gaussian, "unit": _unit}
+    if xkind not in gen:
+        raise ValueError("xkind must be 'uniform', 'gaussian' or 'unit' (use equispaced() for the pin data)")
     for l in range(d):
-        X[:, l] = _uniform(idx, l, seed) if xkind == "uniform" else _gaussian(idx, l, seed)
+        X[:, l] = gen[xkind](idx, l, seed)
     Y = _response(X, idx, d, ykind, seed, noise)
     if L != 1.0:
         X = (X * f(L)).astype(np.float32)
@@ -128,6 +135,8 @@ def _response(Xu, idx, d, ykind, seed, noise):
         Y = np.zeros(n, dtype=np.float32)
         for l in range(d):
             Y = f(Y + _expm1_poly(f(Xu[:, l] * f(1.0 / (l + 1)))))
+    elif ykind == "exp":  # e^x, as the 4-term polynomial + 1
+        Y = f(_expm1_poly(Xu[:, 0]) + f(1.0))
     elif ykind == "zero":
         Y = np.zeros(n, dtype=np.float32)
     else:

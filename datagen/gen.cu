@@ -31,6 +31,12 @@ __device__ __forceinline__ float uniform_x(uint64_t i, int stream, uint32_t seed
   return __fmul_rn((float)(2 * u + 1 - (1LL << 24)), 5.9604644775390625e-08f);
 }
 
+__device__ __forceinline__ float unit_x(uint64_t i, int stream, uint32_t seed) {  // [0, 1), exact in fp32
+  int64_t u, v;
+  u24pair(i, stream, seed, u, v);
+  return __fmul_rn((float)u, 5.9604644775390625e-08f);
+}
+
 __device__ __forceinline__ float gaussian_x(uint64_t i, int stream, uint32_t seed) {
   int64_t a, b, c, e;
   u24pair(i, stream, seed, a, b);
@@ -72,7 +78,7 @@ __device__ __forceinline__ float fstar_expcos(float x1, float x2) {
   return __fmul_rn(e, c);
 }
 
-// xkind: 0 uniform, 1 gaussian.  ykind: 0 sin, 1 expcos, 2 additive, 4 zero.  X written at
+// xkind: 0 uniform, 1 gaussian, 3 unit (U[0,1)).  ykind: 0 sin, 1 expcos, 2 additive, 4 zero, 5 exp.  X written at
 // X[j*stride_n + l*stride_d] (element strides), Y[j] contiguous; sample ids i0 + j.
 __global__ void gen_dataset(float* __restrict__ X, float* __restrict__ Y, int64_t n, int d, int64_t stride_n,
                             int64_t stride_d, int64_t i0, int xkind, int ykind, uint32_t seed, float L, int with_noise) {
@@ -80,7 +86,7 @@ __global__ void gen_dataset(float* __restrict__ X, float* __restrict__ Y, int64_
     const uint64_t i = (uint64_t)(i0 + j);
     float x0 = 0.f, x1 = 0.f, yacc = 0.f;
     for (int l = 0; l < d; ++l) {
-      const float xu = xkind == 0 ? uniform_x(i, l, seed) : gaussian_x(i, l, seed);
+      const float xu = xkind == 0 ? uniform_x(i, l, seed) : (xkind == 3 ? unit_x(i, l, seed) : gaussian_x(i, l, seed));
       if (l == 0) x0 = xu;
       if (l == 1) x1 = xu;
       if (ykind == 2) yacc = __fadd_rn(yacc, expm1_poly(__fmul_rn(xu, (float)(1.0 / (double)(l + 1)))));
@@ -91,6 +97,7 @@ __global__ void gen_dataset(float* __restrict__ X, float* __restrict__ Y, int64_
       if (ykind == 0) y = fstar_sin(x0);
       else if (ykind == 1) y = fstar_expcos(x0, x1);
       else if (ykind == 2) y = yacc;
+      else if (ykind == 5) y = __fadd_rn(expm1_poly(x0), 1.0f);
       if (with_noise) y = __fadd_rn(y, noise(i, seed));
       Y[j] = y;
     }

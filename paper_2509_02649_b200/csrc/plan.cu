@@ -124,7 +124,7 @@ fk_status make_plan1(int d, int m, double eps, bool need_mu, bool need_r, Plan1*
     w = std::min(16, std::max(4, w));
     q.es.w = w;
     q.es.beta = 2.30 * w;  // ES shape for sigma = 2
-    q.nf_mu = fft_friendly(2 * modes_mu);
+    q.nf_mu = fft_friendly(std::max(2 * modes_mu, 4 * w + 16));  // nf_r >= 2w + 8: tiles never wrap (small m)
     q.nf_r = q.nf_mu / 2;
     q.gA = {q.nf_mu, q.nf_mu / 4 - w / 2 - 2, q.nf_mu / 2 + w + 4};
     q.gB = {q.nf_r, q.nf_r / 4 - w / 2 - 2, q.nf_r / 2 + w + 4};

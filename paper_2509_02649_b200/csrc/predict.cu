@@ -46,7 +46,7 @@ static fk_status make_pred_plan(int d, int m, double eps, int additive, PredPlan
     w = std::min(16, std::max(4, w));
     q.es.w = w;
     q.es.beta = 2.30 * w;
-    q.nf = fft_friendly(2 * (2 * m + 1));
+    q.nf = fft_friendly(std::max(2 * (2 * m + 1), 2 * w + 8));  // grid must not wrap (small m)
     q.g = {q.nf, q.nf / 4 - w / 2 - 2, q.nf / 2 + w + 4};
     q.smem = (size_t)q.g.G * q.g.G * (q.fp64 ? 8 : 4);
   } else if (!q.fp64) {
@@ -60,7 +60,7 @@ static fk_status make_pred_plan(int d, int m, double eps, int additive, PredPlan
     w = std::min(16, std::max(4, w));
     q.es.w = w;
     q.es.beta = 2.30 * w;
-    q.nf = fft_friendly(2 * (2 * m + 1));
+    q.nf = fft_friendly(std::max(2 * (2 * m + 1), 2 * w + 8));  // grid must not wrap (small m)
     q.g = {q.nf, q.nf / 4 - w / 2 - 2, q.nf / 2 + w + 4};
     q.smem = (size_t)q.nfeat * q.g.G * 8;
   }

@@ -603,7 +603,8 @@ static fk_status make_plan2(int m, double eps, bool mu, bool r, int dtype, Plan2
   q.fp64 = eps < 1e-7 || dtype == FK_F64;
   q.w = es_width(eps, q.fp64);
   q.beta = 2.30 * q.w;
-  q.nfA = fft_friendly(2 * (4 * m + 1));
+  // tiles (nf/2 + w + 4 cells from nf/4 - w/2 - 2) must not wrap: nfB = nfA/2 >= 2w + 8
+  q.nfA = fft_friendly(std::max(2 * (4 * m + 1), 4 * q.w + 16));
   q.nfB = q.nfA / 2;
   int GA, GB;
   es_geo(q.nfA, q.w, &q.offA, &q.KA, &GA);
@@ -813,7 +814,7 @@ static fk_status make_planx(int d, int m, double eps, int dtype, PlanX* p) {
   q.fp64 = eps < 1e-7 || dtype == FK_F64;
   q.w = es_width(eps, q.fp64);
   q.beta = 2.30 * q.w;
-  q.nf = fft_friendly(2 * (2 * m + 1));
+  q.nf = fft_friendly(std::max(2 * (2 * m + 1), 2 * q.w + 8));  // tile must not wrap (small m)
   es_geo(q.nf, q.w, &q.off, &q.K, &q.G);
   q.npairs = d * (d - 1) / 2;
   const size_t esz = q.fp64 ? 8 : 4;

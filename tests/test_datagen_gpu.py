@@ -9,7 +9,8 @@ pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
 
-@pytest.mark.parametrize("d,xkind,ykind", [(1, "uniform", "sin"), (1, "gaussian", "sin"), (2, "uniform", "expcos"), (10, "uniform", "additive")])
+@pytest.mark.parametrize("d,xkind,ykind", [(1, "uniform", "sin"), (1, "gaussian", "sin"), (2, "uniform", "expcos"), (10, "uniform", "additive"),
+                                            (1, "unit", "exp")])
 def test_generator_bit_identical(d, xkind, ykind):
     n, i0 = 50_000, 123_456_789
     X = torch.empty((n, d), dtype=torch.float32, device="cuda")
