@@ -25,6 +25,7 @@ namespace fk {
 namespace {
 
 constexpr int kMaxTerms = 8, kMaxD = 4;
+constexpr unsigned long long kZSentinel = 0x7ff4dead5eed1e55ULL;  // 'not yet published' (k_trsv_lt)
 
 struct SysArgs {
   int d, m, kind, D;
@@ -293,28 +294,35 @@ __device__ __forceinline__ PCol pcol(const SysArgs& g, int u) {
 
 // M is the (D+1) x (D+1) column-major augmented matrix [[P*AP, c], [c^T, huge]] (lower triangle):
 // its Cholesky factor's last row is y = L^{-1} c, so only the backward solve L^T z = y remains.
+// lower triangle of P^*AP (column v = blockIdx.y, rows u >= v), ld = D + 1
 __global__ void k_assemble_real(SysArgs g, double* __restrict__ M) {
-  const int64_t D = g.D, N = g.D + 1;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < D * D; t += (int64_t)gridDim.x * blockDim.x) {
-    const int v = (int)(t / D), u = (int)(t % D);
-    if (u < v) continue;
-    const PCol pu = pcol(g, u), pv = pcol(g, v);
-    double s = 0.0;
-    for (int x = 0; x < pu.cnt; ++x)
-      for (int y = 0; y < pv.cnt; ++y) {
-        const double2 a = entry(g, pu.i[x], pv.i[y]);
-        const double2 c = cmul(cmul(cconj(pu.a[x]), a), pv.a[y]);
-        s += c.x;
-      }
-    M[u + v * N] = s;
-  }
+  const int64_t N = g.D + 1;
+  const int v = blockIdx.y;
+  const int u = v + blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= g.D) return;
+  const PCol pu = pcol(g, u), pv = pcol(g, v);
+  double s = 0.0;
+  for (int x = 0; x < pu.cnt; ++x)
+    for (int y = 0; y < pv.cnt; ++y) {
+      const double2 a = entry(g, pu.i[x], pv.i[y]);
+      const double2 c = cmul(cmul(cconj(pu.a[x]), a), pv.a[y]);
+      s += c.x;
+    }
+  M[u + v * N] = s;
 }
 
-__global__ void k_rhs_real(SysArgs g, const double2* __restrict__ r, double* __restrict__ M) {  // last row of M
+void launch_assemble(const SysArgs& g, double* M, cudaStream_t s) {
+  k_assemble_real<<<dim3((g.D + 255) / 256, g.D), 256, 0, s>>>(g, M);
+}
+
+__global__ void k_rhs_real(SysArgs g, const double2* __restrict__ r, double* __restrict__ M, double* __restrict__ zbuf,
+                           int* __restrict__ ticket) {  // last row of M (+ reset of k_trsv_lt's sentinels / ticket)
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t N = g.D + 1;
   if (u == g.D) M[g.D + g.D * N] = 1e200;  // any value above c^T (P*AP)^{-1} c keeps it SPD
+  if (u == 0 && ticket) *ticket = 0;
   if (u >= g.D) return;
+  if (zbuf) zbuf[u] = __longlong_as_double((long long)kZSentinel);
   const PCol p = pcol(g, u);
   double s = 0.0;
   for (int x = 0; x < p.cnt; ++x) {
@@ -341,6 +349,110 @@ __global__ void k_theta_from_real(SysArgs g, const double* __restrict__ zs, int6
   }
 }
 
+
+// ---- back substitution L^T z = y on many SMs (replaces the single-SM cublasDtrsv) ------------
+// Block I (32 rows of z) is owned by one 64-thread CTA.  It inverts its diagonal block W = L_II^{-1}
+// and prefetches its off-diagonal blocks while z is not yet known, then accumulates
+// sum_{J>I} L_JI^T z_J as the blocks z_J appear (J descending) and finishes with z_I = W^T (y_I - acc).
+// z_J is published element by element: zbuf is pre-filled with a sentinel NaN pattern (k_rhs_real)
+// that no computed value has, so a reader spins on the value itself (one L2 round trip per block
+// on the critical path, no separate flag).  Blocks are taken in ticket order (an atomic counter,
+// highest block first), so a CTA only ever waits on CTAs that started before it: no co-residency
+// requirement, no deadlock at any D.
+__device__ __forceinline__ double ld_volatile(const double* p) {
+  double v;
+  asm volatile("ld.volatile.global.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
+__global__ void __launch_bounds__(64) k_trsv_lt(const double* __restrict__ M, int64_t ld, int D, const double* __restrict__ y,
+                                                 int64_t ystride, double* zbuf, int* ticket) {
+  __shared__ double W[32][33];
+  __shared__ double Ls[32][33];
+  __shared__ double red[2][32][17];
+  __shared__ double rv[32];
+  __shared__ double zv[32];
+  __shared__ int tk;
+  const int nb = (D + 31) / 32;
+  if (threadIdx.x == 0) tk = atomicAdd(ticket, 1);
+  __syncthreads();
+  const int I = nb - 1 - tk;
+  const int lane = threadIdx.x & 31, h = threadIdx.x >> 5;  // warp h holds columns 16h .. 16h+15 of block I
+  const int r0 = I * 32;
+  // stage L_II (identity on padded rows) in shared memory, then W = L_II^{-1}: lane j solves L w = e_j
+  for (int c = h; c < 32; c += 2) {
+    const int gr = r0 + lane, gc = r0 + c;
+    const double l = (gr < D && gc < D) ? M[gr + (int64_t)gc * ld] : (lane == c ? 1.0 : 0.0);
+    W[lane][c] = l;
+    Ls[lane][c] = l;
+  }
+  __syncthreads();
+  double w[32];  // column `lane` of W, built top-down in registers
+  if (h == 0) {
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      double a = (r == lane) ? 1.0 : 0.0;
+#pragma unroll
+      for (int c = 0; c < r; ++c) a -= W[r][c] * w[c];
+      w[r] = (r >= lane) ? a / W[r][r] : 0.0;
+    }
+  }
+  __syncthreads();
+  if (h == 0) {
+#pragma unroll
+    for (int r = 0; r < 32; ++r) W[r][lane] = w[r];
+  }
+  double acc[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) acc[q] = 0.0;
+  const int cbase = r0 + 16 * h;
+  double Lb[16];
+  auto load_block = [&](int J) {
+    const int row = J * 32 + lane;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) Lb[q] = (row < D && cbase + q < D) ? M[row + (int64_t)(cbase + q) * ld] : 0.0;
+  };
+  if (I + 1 < nb) load_block(nb - 1);
+  for (int J = nb - 1; J > I; --J) {
+    const int row = J * 32 + lane;
+    double zc = 0.0;
+    if (row < D) {
+      do {
+        zc = ld_volatile(zbuf + row);
+      } while (__double_as_longlong(zc) == (long long)kZSentinel);
+    }
+    double Lc[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) Lc[q] = Lb[q];
+    if (J - 1 > I) load_block(J - 1);  // prefetch the next block while this one is consumed
+#pragma unroll
+    for (int q = 0; q < 16; ++q) acc[q] = fma(Lc[q], zc, acc[q]);
+  }
+  // reduce over lanes: red[h][lane][q] -> column 16h + q
+#pragma unroll
+  for (int q = 0; q < 16; ++q) red[h][lane][q] = acc[q];
+  __syncthreads();
+  if (h == 0) {
+    const int col = lane, hh = col >> 4, q = col & 15;
+    double t = 0.0;
+    for (int l = 0; l < 32; ++l) t += red[hh][l][q];
+    const int gr = r0 + col;
+    rv[col] = (gr < D) ? y[(int64_t)gr * ystride] - t : 0.0;
+    __syncwarp();
+    double z = 0.0;
+    for (int c = 0; c < 32; ++c) z = fma(W[c][col], rv[c], z);
+    // one step of refinement with L_II itself keeps the block solve backward stable
+    zv[col] = z;
+    __syncwarp();
+    double res = rv[col];
+    for (int r = col; r < 32; ++r) res = fma(-Ls[r][col], zv[r], res);
+    __syncwarp();
+    rv[col] = res;
+    __syncwarp();
+    for (int c = 0; c < 32; ++c) z = fma(W[c][col], rv[c], z);
+    if (gr < D) asm volatile("st.volatile.global.f64 [%0], %1;" ::"l"(zbuf + gr), "d"(z) : "memory");
+  }
+}
 
 fk_status lwork_for(int D, int* lwork) {
   std::lock_guard<std::mutex> lk(g_sol_mu);
@@ -524,8 +636,8 @@ fk_status solve_path_run(const fk_problem* P, const double* lambdas, int nlam, d
     g.boxt = boxt;
     count_launch();
   }
-  k_assemble_real<<<sms * 8, 256, 0, s>>>(g, M);
-  k_rhs_real<<<(N + 255) / 256, 256, 0, s>>>(g, (const double2*)P->rhs, M);
+  launch_assemble(g, M, s);
+  k_rhs_real<<<(N + 255) / 256, 256, 0, s>>>(g, (const double2*)P->rhs, M, nullptr, nullptr);
   k_path_diag<<<(D + 255) / 256, 256, 0, s>>>(g, dg);
   k_path_scale<<<sms * 8, 256, 0, s>>>(M, N, D, dg);
   k_path_rhs<<<(D + 255) / 256, 256, 0, s>>>(M, N, D, dg, Z);  // scaled c into Z[:,0] (scratch)
@@ -628,8 +740,8 @@ fk_status path_validate_run(const fk_problem* Pv, const double* theta, int nlam,
   double* W = (double*)b.take((size_t)D * nlam * 8);
   if (!b.ok()) return fail(FK_E_WORKSPACE, "fk_path_validate: workspace too small");
   const int sms = device_sm_count();
-  k_assemble_real<<<sms * 8, 256, 0, s>>>(g, M);
-  k_rhs_real<<<(N + 255) / 256, 256, 0, s>>>(g, (const double2*)Pv->rhs, M);
+  launch_assemble(g, M, s);
+  k_rhs_real<<<(N + 255) / 256, 256, 0, s>>>(g, (const double2*)Pv->rhs, M, nullptr, nullptr);
   k_z_from_theta<<<sms * 4, 256, 0, s>>>(g, (const double2*)theta, nlam, Z);
   FK_CUDA_TRY(cudaGetLastError());
   count_launch(3);
@@ -649,33 +761,8 @@ fk_status path_validate_run(const fk_problem* Pv, const double* theta, int nlam,
 }
 
 fk_status solve_run(const fk_problem* P, double* theta, fk_solve_report* rep, void* ws, size_t ws_bytes, cudaStream_t s) {
-  SysArgs g{};
-  g.d = P->d;
-  g.m = P->m;
-  g.kind = P->kind;
-  g.D = unknowns(P->d, P->m, P->kind);
-  g.inv_n = 1.0 / P->n_total;
-  g.lambda = P->lambda;
-  g.s = P->s;
-  g.mu_pde = P->mu_pde;
-  g.c = 3.14159265358979323846 / (2.0 * P->L);
-  g.inv4L = 1.0 / (4.0 * P->L);
-  g.mu = (const double2*)P->mu_moments;
-  g.cross = (const double2*)P->cross;
-  g.mur = (const double2*)P->colloc_moments;
-  g.inv_nr = P->n_colloc > 0 ? 1.0 / P->n_colloc : 0.0;
-  if (P->kind == FK_PIK_BOX || P->kind == FK_PIK_COLLOC) {
-    if (P->n_terms < 0 || P->n_terms > kMaxTerms || P->d > kMaxD) return fail(FK_E_ARG, "fk_solve: at most 8 PDE terms, d <= 4");
-    g.n_terms = P->n_terms;
-    for (int t = 0; t < P->n_terms; ++t) {
-      g.a_alpha[t] = P->a_alpha[t];
-      for (int l = 0; l < P->d; ++l) g.alpha[t][l] = P->alpha[t * P->d + l];
-    }
-    for (int l = 0; l < P->d && P->box; ++l) {
-      g.box[l][0] = P->box[2 * l];
-      g.box[l][1] = P->box[2 * l + 1];
-    }
-  }
+  SysArgs g;
+  FK_TRY(fill_sysargs(P, &g));
   const int D = g.D;
   int lwork = 0;
   const int N = D + 1;
@@ -683,7 +770,8 @@ fk_status solve_run(const fk_problem* P, double* theta, fk_solve_report* rep, vo
   Bump b(ws, ws_bytes);
   double* M = (double*)b.take((size_t)N * N * 8);
   double* work = (double*)b.take((size_t)lwork * 8);
-  int* info = (int*)b.take(16);
+  double* zbuf = (double*)b.take((size_t)D * 8);
+  int* info = (int*)b.take(64);
   double* res = (double*)(info + 4);
   double2* dsym = nullptr;
   double2* boxt = nullptr;
@@ -699,7 +787,6 @@ fk_status solve_run(const fk_problem* P, double* theta, fk_solve_report* rep, vo
     cudaEventCreate(&e1);
     cudaEventRecord(e0, s);
   }
-  const int sms = device_sm_count();
   if (P->kind == FK_PIK_BOX || P->kind == FK_PIK_COLLOC) {
     const int nt = std::max(D, P->d * (4 * P->m + 1));
     k_pi_tables<<<(nt + 255) / 256, 256, 0, s>>>(g, dsym, boxt);
@@ -708,8 +795,10 @@ fk_status solve_run(const fk_problem* P, double* theta, fk_solve_report* rep, vo
     g.dsym = dsym;
     g.boxt = boxt;
   }
-  k_assemble_real<<<sms * 8, 256, 0, s>>>(g, M);
-  k_rhs_real<<<(N + 255) / 256, 256, 0, s>>>(g, (const double2*)P->rhs, M);
+  const bool own_trsv = true;
+  int* ticket = info + 12;
+  launch_assemble(g, M, s);
+  k_rhs_real<<<(N + 255) / 256, 256, 0, s>>>(g, (const double2*)P->rhs, M, zbuf, ticket);
   FK_CUDA_TRY(cudaGetLastError());
   count_launch(2);
   {
@@ -722,11 +811,16 @@ fk_status solve_run(const fk_problem* P, double* theta, fk_solve_report* rep, vo
     cublasHandle_t bh;
     FK_TRY(blas_for_device(&bh));
     if (cublasSetStream(bh, s) != CUBLAS_STATUS_SUCCESS) return fail(FK_E_CUDA, "cublasSetStream failed");
-    // y = L^{-1} c is the factor's last row (stride N); solve L^T z = y in place
-    if (cublasDtrsv(bh, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, D, M, N, M + D, N) != CUBLAS_STATUS_SUCCESS)
+    // y = L^{-1} c is the factor's last row (stride N); solve L^T z = y
+    if (!own_trsv &&
+        cublasDtrsv(bh, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, D, M, N, M + D, N) != CUBLAS_STATUS_SUCCESS)
       return fail(FK_E_CUDA, "cublasDtrsv failed");
   }
-  k_theta_from_real<<<(D + 255) / 256, 256, 0, s>>>(g, M + D, N, (double2*)theta);
+  if (own_trsv) {
+    k_trsv_lt<<<(D + 31) / 32, 64, 0, s>>>(M, N, D, M + D, N, zbuf, ticket);
+    count_launch();
+  }
+  k_theta_from_real<<<(D + 255) / 256, 256, 0, s>>>(g, own_trsv ? zbuf : M + D, own_trsv ? 1 : N, (double2*)theta);
   FK_CUDA_TRY(cudaGetLastError());
   count_launch();
   if (rep) {

@@ -33,6 +33,11 @@ int main() {
       cudaMemcpy(A, A0, (size_t)D * D * 8, cudaMemcpyDeviceToDevice);
       cudaEventRecord(e0); cusolverDnDpotrf(h, CUBLAS_FILL_MODE_LOWER, D, A, D, work, lwork, info); cudaEventRecord(e1); cudaEventSynchronize(e1);
       cudaEventElapsedTime(&ms, e0, e1); printf("D=%d Dpotrf %.3f ms\n", D, ms);
+      cudaMemcpy(A, A0, (size_t)D * D * 8, cudaMemcpyDeviceToDevice);
+      cudaEventRecord(e0); cusolverDnDpotrf(h, CUBLAS_FILL_MODE_UPPER, D, A, D, work, lwork, info); cudaEventRecord(e1); cudaEventSynchronize(e1);
+      cudaEventElapsedTime(&ms, e0, e1); printf("D=%d Dpotrf UPPER %.3f ms\n", D, ms);
+      cudaEventRecord(e0); cublasDtrsv(cb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, D, A, D, b, 1); cudaEventRecord(e1); cudaEventSynchronize(e1);
+      cudaEventElapsedTime(&ms, e0, e1); printf("D=%d Dtrsv T %.3f ms\n", D, ms);
       cudaEventRecord(e0); cusolverDnDpotrs(h, CUBLAS_FILL_MODE_LOWER, D, 1, A, D, b, D, info); cudaEventRecord(e1); cudaEventSynchronize(e1);
       cudaEventElapsedTime(&ms, e0, e1); printf("D=%d Dpotrs %.3f ms\n", D, ms);
       cudaEventRecord(e0); cublasDtrsv(cb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, D, A, D, b, 1); cudaEventRecord(e1); cudaEventSynchronize(e1);
