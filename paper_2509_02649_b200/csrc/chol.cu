@@ -1,0 +1,352 @@
+// chol.cu -- dense fp64 Cholesky of the (augmented) real fit system, A = L L^T, in ONE persistent
+// dataflow kernel (the factorisation step of A11; DESIGN.md §5 "Solve").
+//
+// Why not cuSOLVER potrf at the fit sizes: for N ~ 2000-4000 its factorisation is latency bound
+// (~0.45 us per column, 0.88 ms at N = 2002, 3 TF/s).  Here the matrix is cut into 32 x 32 tiles and
+// every tile is owned by one 128-thread CTA, which
+//   1. loads its tile A_ij into fp64 tensor-core accumulators (mma.m8n8k4.f64, one 16 x 16 quadrant
+//      per warp),
+//   2. applies the updates A_ij -= L_ik L_jk^T for k = 0 .. j-1 as soon as the tiles L_ik, L_jk are
+//      published (their flags), staging both in shared memory,
+//   3. finishes with POTRF (diagonal tile, one warp, register resident, shuffles) or TRSM
+//      (X L_jj^T = A_ij, one warp, row per lane) and publishes L_ij (tile + flag).
+// Tiles are handed out by an atomic ticket counter in column-major order, so a CTA only ever waits
+// on tiles whose tickets are smaller -- held by CTAs that are already running and never wait on
+// larger tickets: deadlock free for any grid size, no co-residency assumption.  Tiles are read
+// with ld.global.cg (L2) because the same addresses held A before they hold L.
+// Padding rows/columns beyond N behave as the identity.  info: first failing pivot + 1 (0 = SPD).
+#include <cstdint>
+#include <cstdlib>
+
+#include "fk_internal.cuh"
+
+namespace fk {
+namespace {
+
+constexpr int TS = 32;    // tile size
+constexpr int LDS = 36;   // smem leading dimension of staged tiles [p][r]: conflict-free stores and fragment loads
+constexpr int CT = 128;   // threads per CTA
+
+// Flags are polled with relaxed loads: ld.acquire would invalidate the whole L1 (CCTL.IVALL) on every
+// poll; the tile data is read with ld.global.cg (L2, coherent), so no L1 invalidation is needed.
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release(int* p, int v) { asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory"); }
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ double elem(const double* __restrict__ M, int64_t ld, int N, int r, int c) {
+  if (r < N && c < N) return __ldcg(M + r + (int64_t)c * ld);
+  return r == c ? 1.0 : 0.0;
+}
+
+// tile (ti, tj) into smem T[p][r] = tile(r, p) (column p of the tile is row p of T)
+__device__ __forceinline__ void stage(double (*T)[LDS], const double* __restrict__ M, int64_t ld, int N, int ti, int tj) {
+  const int r = threadIdx.x & 31;
+#pragma unroll
+  for (int q = 0; q < TS * TS / CT; ++q) {
+    const int p = (threadIdx.x >> 5) + 4 * q;
+    T[p][r] = elem(M, ld, N, ti * TS + r, tj * TS + p);
+  }
+}
+
+// wait until both flags are set (thread 0 polls fa, thread 32 polls fb; fb may be null)
+__device__ __forceinline__ void wait_flags(const int* fa, const int* fb) {
+  if (threadIdx.x == 0)
+    while (ld_relaxed(fa) == 0) {
+    }
+  if (threadIdx.x == 32 && fb)
+    while (ld_relaxed(fb) == 0) {
+    }
+  __syncthreads();
+}
+
+__device__ __forceinline__ int tile_id(int i, int j, int nt) { return j * nt - j * (j - 1) / 2 + (i - j); }
+
+// Tasks in ticket order, column by column: column j holds first the DIAGONAL task D_j (which owns
+// the sub-diagonal tile (j, j-1) and the diagonal tile (j, j)), then the tiles (i, j), i >= j + 2
+// (tile (j+1, j) belongs to D_{j+1}).  Every dependency of a task has a smaller ticket.
+// ticket -> (i, j); i == j marks D_j.
+__device__ __forceinline__ void task_of(int t, int nt, int* i, int* j) {
+  int c = 0, start = 0;
+  for (;;) {
+    const int cnt = 1 + max(0, nt - c - 2);
+    if (t < start + cnt) break;
+    start += cnt;
+    ++c;
+  }
+  *j = c;
+  *i = (t == start) ? c : c + 1 + (t - start);
+}
+
+// 32 x 32 POTRF step J on a register-resident row (lane r holds row r, one warp), fully unrolled
+// by recursion.  dj = pivot J, inv = rsqrt(dj) (MUFU + Newton, no IEEE sqrt/div).  Lane J+1 forms
+// the next pivot from its own l_{J+1,J} and publishes it through shared memory before the general
+// update, so the dependency chain per column is mul -> fma -> sts/lds -> rsqrt.  The general update
+// reads column J of L from shared memory (broadcast loads) instead of 31 shuffles.  1/L_JJ goes to
+// my_dinv (lane J), bad = first non-positive pivot (or -1).
+template <int J>
+__device__ __forceinline__ void potrf_step(double (&x)[TS], double (*colL)[LDS], double* piv, int lane, double& my_dinv, int& bad,
+                                           double dj, double inv) {
+  if (!(dj > 0.0) && bad < 0) bad = J;
+  const double lj = x[J] * inv;
+  x[J] = (lane == J) ? dj * inv : lj;
+  if (lane == J) my_dinv = inv;
+  colL[J][lane] = lj;
+  if constexpr (J + 1 < TS) {
+    if (lane == J + 1) piv[J + 1] = fma(-lj, lj, x[J + 1]);
+  }
+  __syncwarp();
+  double dn = 0.0, invn = 0.0;
+  if constexpr (J + 1 < TS) {
+    dn = piv[J + 1];
+    invn = rsqrt(dn);
+  }
+  // lanes r < c update their (unused, later zeroed) upper entries too: no select on the chain
+#pragma unroll
+  for (int c = J + 1; c < TS; ++c) x[c] = fma(-lj, colL[J][c], x[c]);
+  if constexpr (J + 1 < TS) potrf_step<J + 1>(x, colL, piv, lane, my_dinv, bad, dn, invn);
+}
+
+// row solve x L^T = a, L(c, p) = T[p][c], 1/L(c, c) = dv[c] (forward substitution, right-looking)
+template <int C>
+__device__ __forceinline__ void trsm_step(double (&x)[TS], const double (*T)[LDS], const double* dv) {
+  x[C] *= dv[C];
+#pragma unroll
+  for (int c2 = C + 1; c2 < TS; ++c2) x[c2] = fma(-x[C], T[C][c2], x[c2]);
+  if constexpr (C + 1 < TS) trsm_step<C + 1>(x, T, dv);
+}
+
+struct Acc {
+  double v[2][2][2];  // v[rb][cb][e] = tile(qr*16 + rb*8 + g, qc*16 + cb*8 + 2tq + e)
+};
+
+__device__ __forceinline__ void acc_load(Acc& a, const double* __restrict__ M, int64_t ld, int N, int ti, int tj, int qr, int qc, int g,
+                                         int tq) {
+#pragma unroll
+  for (int rb = 0; rb < 2; ++rb)
+#pragma unroll
+    for (int cb = 0; cb < 2; ++cb)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) a.v[rb][cb][e] = elem(M, ld, N, ti * TS + qr * 16 + rb * 8 + g, tj * TS + qc * 16 + cb * 8 + 2 * tq + e);
+}
+
+// a -= A B^T with A, B staged as T[p][r] = tile(r, p)
+__device__ __forceinline__ void acc_update(Acc& a, const double (*A)[LDS], const double (*B)[LDS], int qr, int qc, int g, int tq) {
+#pragma unroll
+  for (int p0 = 0; p0 < TS; p0 += 4) {
+    double fa[2], fb[2];
+#pragma unroll
+    for (int rb = 0; rb < 2; ++rb) fa[rb] = -A[p0 + tq][qr * 16 + rb * 8 + g];  // A frag: row g, k tq
+#pragma unroll
+    for (int cb = 0; cb < 2; ++cb) fb[cb] = B[p0 + tq][qc * 16 + cb * 8 + g];   // B frag: k tq, col g
+#pragma unroll
+    for (int rb = 0; rb < 2; ++rb)
+#pragma unroll
+      for (int cb = 0; cb < 2; ++cb) dmma(a.v[rb][cb][0], a.v[rb][cb][1], fa[rb], fb[cb]);
+  }
+}
+
+__device__ __forceinline__ void acc_gather(const Acc& a, double (*Ct)[TS + 1], int qr, int qc, int g, int tq) {
+#pragma unroll
+  for (int rb = 0; rb < 2; ++rb)
+#pragma unroll
+    for (int cb = 0; cb < 2; ++cb)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) Ct[qr * 16 + rb * 8 + g][qc * 16 + cb * 8 + 2 * tq + e] = a.v[rb][cb][e];
+}
+
+// write Ct as tile (ti, tj) of M, then release its flag
+__device__ __forceinline__ void publish(const double (*Ct)[TS + 1], double* __restrict__ M, int64_t ld, int N, int ti, int tj, int* flag) {
+  const int r = threadIdx.x & 31;
+#pragma unroll
+  for (int q = 0; q < TS * TS / CT; ++q) {
+    const int c = (threadIdx.x >> 5) + 4 * q;
+    const int gr = ti * TS + r, gc = tj * TS + c;
+    if (gr < N && gc < N) M[gr + (int64_t)gc * ld] = Ct[r][c];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    st_release(flag, 1);
+  }
+}
+
+// warp 0: Ct <- Ct L^{-T} (TRSM; L staged in Ta, 1/diag in dv)
+__device__ __forceinline__ void final_trsm(double (*Ct)[TS + 1], const double (*Ta)[LDS], const double* dv, int lane) {
+  double x[TS];
+#pragma unroll
+  for (int c = 0; c < TS; ++c) x[c] = Ct[lane][c];
+  trsm_step<0>(x, Ta, dv);
+#pragma unroll
+  for (int c = 0; c < TS; ++c) Ct[lane][c] = x[c];
+}
+
+// warp 0: Ct <- chol(Ct) (lower, zero upper), 1/diag to dinv_out, first failing pivot to info
+__device__ __forceinline__ void final_potrf(double (*Ct)[TS + 1], double (*colL)[LDS], double* piv, double* dinv_out, int col0, int N,
+                                            int* info, int lane) {
+  double x[TS];
+#pragma unroll
+  for (int c = 0; c < TS; ++c) x[c] = Ct[lane][c];
+  double my_dinv = 1.0;
+  int bad = -1;
+  if (lane == 0) piv[0] = x[0];
+  __syncwarp();
+  const double d0 = piv[0];
+  potrf_step<0>(x, colL, piv, lane, my_dinv, bad, d0, rsqrt(d0));
+  if (bad >= 0 && lane == 0 && col0 + bad < N) atomicCAS(info, 0, col0 + bad + 1);
+  dinv_out[lane] = my_dinv;
+#pragma unroll
+  for (int c = 0; c < TS; ++c) Ct[lane][c] = (c > lane) ? 0.0 : x[c];
+}
+
+__global__ void __launch_bounds__(CT) k_chol_tiles(double* __restrict__ M, int64_t ld, int N, int nt, int* __restrict__ flags,
+                                                   int* __restrict__ ticket, int* __restrict__ info, double* __restrict__ dinv,
+                                                   unsigned long long* __restrict__ trace) {
+  __shared__ double Ta[TS][LDS], Tb[TS][LDS];
+  __shared__ double Ct[TS][TS + 1];
+  __shared__ double dv[TS];
+  __shared__ int s_t;
+  const int ntasks = nt + (nt - 2) * (nt - 1) / 2;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int qr = w >> 1, qc = w & 1;  // quadrant of a tile held by this warp
+  const int g = lane >> 2, tq = lane & 3;
+  for (;;) {
+    if (threadIdx.x == 0) s_t = atomicAdd(ticket, 1);
+    __syncthreads();
+    const int t = s_t;
+    __syncthreads();
+    if (t >= ntasks) return;
+    int i, j;
+    task_of(t, nt, &i, &j);
+    unsigned long long t0 = 0, t1 = 0, t1b = 0, t1c = 0;
+    if (trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    if (i != j) {
+      // ---- off-diagonal tile (i, j), i >= j + 2: updates k < j, then TRSM with L_jj ----
+      Acc a;
+      acc_load(a, M, ld, N, i, j, qr, qc, g, tq);
+      for (int k = 0; k < j; ++k) {
+        wait_flags(flags + tile_id(i, k, nt), flags + tile_id(j, k, nt));
+        stage(Ta, M, ld, N, i, k);
+        stage(Tb, M, ld, N, j, k);
+        __syncthreads();
+        acc_update(a, Ta, Tb, qr, qc, g, tq);
+        __syncthreads();
+      }
+      if (trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+      acc_gather(a, Ct, qr, qc, g, tq);
+      wait_flags(flags + tile_id(j, j, nt), nullptr);
+      stage(Ta, M, ld, N, j, j);  // Ta[p][r] = L_jj(r, p)
+      if (threadIdx.x < TS) dv[threadIdx.x] = __ldcg(dinv + j * TS + threadIdx.x);
+      __syncthreads();
+      if (trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1b));
+      if (w == 0) final_trsm(Ct, Ta, dv, lane);
+      if (trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1c));
+      __syncthreads();
+      publish(Ct, M, ld, N, i, j, flags + tile_id(i, j, nt));
+    } else {
+      // ---- diagonal task D_j: sub-diagonal tile (j, j-1) and diagonal tile (j, j) ----
+      Acc d;  // A_jj
+      acc_load(d, M, ld, N, j, j, qr, qc, g, tq);
+      if (j > 0) {
+        Acc sb;  // A_{j, j-1}
+        acc_load(sb, M, ld, N, j, j - 1, qr, qc, g, tq);
+        for (int k = 0; k < j - 1; ++k) {
+          wait_flags(flags + tile_id(j, k, nt), flags + tile_id(j - 1, k, nt));
+          stage(Ta, M, ld, N, j, k);
+          stage(Tb, M, ld, N, j - 1, k);
+          __syncthreads();
+          acc_update(sb, Ta, Tb, qr, qc, g, tq);
+          acc_update(d, Ta, Ta, qr, qc, g, tq);
+          __syncthreads();
+        }
+        if (trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        // L_{j, j-1} = A_{j, j-1} L_{j-1, j-1}^{-T}
+        acc_gather(sb, Ct, qr, qc, g, tq);
+        wait_flags(flags + tile_id(j - 1, j - 1, nt), nullptr);
+        stage(Ta, M, ld, N, j - 1, j - 1);
+        if (threadIdx.x < TS) dv[threadIdx.x] = __ldcg(dinv + (j - 1) * TS + threadIdx.x);
+        __syncthreads();
+        if (trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1b));
+        if (w == 0) final_trsm(Ct, Ta, dv, lane);
+        __syncthreads();
+        publish(Ct, M, ld, N, j, j - 1, flags + tile_id(j, j - 1, nt));
+        // A_jj -= L_{j, j-1} L_{j, j-1}^T from the tile still in shared memory
+#pragma unroll
+        for (int q = 0; q < TS * TS / CT; ++q) {
+          const int p = (threadIdx.x >> 5) + 4 * q;
+          Ta[p][lane] = Ct[lane][p];
+        }
+        __syncthreads();
+        acc_update(d, Ta, Ta, qr, qc, g, tq);
+        __syncthreads();
+      } else if (trace && threadIdx.x == 0) {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        t1b = t1;
+      }
+      acc_gather(d, Ct, qr, qc, g, tq);
+      __syncthreads();
+      if (w == 0) final_potrf(Ct, Tb, dv, dinv + j * TS, j * TS, N, info, lane);
+      if (trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1c));
+      __syncthreads();
+      publish(Ct, M, ld, N, j, j, flags + tile_id(j, j, nt));
+    }
+    if (trace && threadIdx.x == 0) {
+      unsigned long long t2;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t2));
+      unsigned sm;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+      trace[6 * t] = t0;
+      trace[6 * t + 1] = t1;
+      trace[6 * t + 2] = t1b;
+      trace[6 * t + 3] = t1c;
+      trace[6 * t + 4] = t2;
+      trace[6 * t + 5] = sm;
+    }
+  }
+}
+
+}  // namespace
+
+static size_t flags_bytes(int nt) { return ((size_t)(nt * (nt + 1) / 2 + 8) * sizeof(int) + 255) & ~(size_t)255; }
+
+size_t chol_ws_bytes(int N) {
+  const int nt = (N + TS - 1) / TS;
+  return flags_bytes(nt) + (size_t)nt * TS * sizeof(double);
+}
+
+// Factor the N x N SPD matrix M (column-major, leading dimension ld, lower triangle read and
+// overwritten with L).  ws: chol_ws_bytes(N) bytes (flags + ticket); info: device int, set to 0 here.
+fk_status chol_tiles(double* M, int64_t ld, int N, int* info, void* ws, cudaStream_t s, unsigned long long* trace) {
+  const int nt = (N + TS - 1) / TS;
+  const int ntiles = nt * (nt + 1) / 2;
+  const int ntasks = nt + (nt - 2) * (nt - 1) / 2;
+  int* flags = (int*)ws;
+  int* ticket = flags + ntiles;
+  double* dinv = (double*)((char*)ws + flags_bytes(nt));
+  FK_CUDA_TRY(cudaMemsetAsync(flags, 0, (size_t)(ntiles + 8) * sizeof(int), s));
+  FK_CUDA_TRY(cudaMemsetAsync(info, 0, sizeof(int), s));
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_chol_tiles, CT, 0) != cudaSuccess || per_sm < 1) per_sm = 1;
+  }
+  // fewer co-resident CTAs shorten the latency-bound critical path at small N; the update throughput
+  // needs more at larger N (measured on B200: N = 2002 best at 2/SM, N >= 3000 at 8/SM)
+  int ps = std::min(per_sm, N <= 2500 ? 2 : 8);
+  if (const char* e = getenv("FK_CHOL_PER_SM")) ps = std::max(1, std::min(per_sm, atoi(e)));  // experiments
+  const int grid = std::min(ntasks, ps * device_sm_count());
+  k_chol_tiles<<<grid, CT, 0, s>>>(M, ld, N, nt, flags, ticket, info, dinv, trace);
+  FK_CUDA_TRY(cudaGetLastError());
+  count_launch();
+  return FK_OK;
+}
+
+}  // namespace fk

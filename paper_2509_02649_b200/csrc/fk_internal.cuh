@@ -120,6 +120,8 @@ fk_status type1_run(const Plan1& p, const fk_points& X, const void* Y, double L,
 // solve (solve.cu), predict (predict.cu), additive (additive.cu)
 // ------------------------------------------------------------------------------------------
 size_t solve_ws_bytes(int d, int m, int kind);
+size_t chol_ws_bytes(int N);
+fk_status chol_tiles(double* M, int64_t ld, int N, int* info, void* ws, cudaStream_t s, unsigned long long* trace = nullptr);
 size_t solve_path_ws_bytes(int d, int m, int kind, int nlam);
 fk_status solve_path_run(const fk_problem* P, const double* lambdas, int nlam, double* theta, int* info, void* ws, size_t ws_bytes,
                          cudaStream_t s);

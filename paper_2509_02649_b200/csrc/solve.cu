@@ -16,6 +16,7 @@
 #include <cusolverDn.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 
@@ -478,7 +479,20 @@ size_t solve_ws_bytes(int d, int m, int kind) {
     b.take((size_t)D * 16);
     b.take((size_t)d * (4 * m + 1) * 16);
   }
+  b.take(chol_ws_bytes(D + 1));
   return b.used + 256;
+}
+
+// factorisation path: the tile dataflow kernel (chol.cu) up to kTilesMaxN, cuSOLVER potrf above,
+// where the factorisation is throughput bound and cuSOLVER's larger blocking wins (measured on
+// B200: tiles 0.59 / cuSOLVER 0.85 ms at N = 2002, 1.00 / 1.29 at 3001, 1.95 / 1.78 at 4226).
+// FK_CHOL=cusolver|tiles overrides (tests, measurements).
+constexpr int kTilesMaxN = 3500;
+bool use_tiles(int N) {
+  const char* e = getenv("FK_CHOL");
+  if (e && e[0] == 'c') return false;
+  if (e && e[0] == 't') return true;
+  return N <= kTilesMaxN;
 }
 
 static fk_status fill_sysargs(const fk_problem* P, SysArgs* out) {
@@ -779,6 +793,7 @@ fk_status solve_run(const fk_problem* P, double* theta, fk_solve_report* rep, vo
     dsym = (double2*)b.take((size_t)D * 16);
     boxt = (double2*)b.take((size_t)P->d * (4 * P->m + 1) * 16);
   }
+  void* chol_ws = b.take(chol_ws_bytes(N));
   if (!b.ok()) return fail(FK_E_WORKSPACE, "fk_solve: workspace too small");
 
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -806,8 +821,11 @@ fk_status solve_run(const fk_problem* P, double* theta, fk_solve_report* rep, vo
     cusolverDnHandle_t h;
     FK_TRY(handle_for_device(&h));
     if (cusolverDnSetStream(h, s) != CUSOLVER_STATUS_SUCCESS) return fail(FK_E_CUDA, "cusolverDnSetStream failed");
-    if (cusolverDnDpotrf(h, CUBLAS_FILL_MODE_LOWER, N, M, N, work, lwork, info) != CUSOLVER_STATUS_SUCCESS)
+    if (use_tiles(N)) {
+      FK_TRY(chol_tiles(M, N, N, info, chol_ws, s));
+    } else if (cusolverDnDpotrf(h, CUBLAS_FILL_MODE_LOWER, N, M, N, work, lwork, info) != CUSOLVER_STATUS_SUCCESS) {
       return fail(FK_E_CUDA, "cusolverDnDpotrf failed");
+    }
     cublasHandle_t bh;
     FK_TRY(blas_for_device(&bh));
     if (cublasSetStream(bh, s) != CUBLAS_STATUS_SUCCESS) return fail(FK_E_CUDA, "cublasSetStream failed");
