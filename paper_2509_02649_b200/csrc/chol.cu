@@ -69,6 +69,47 @@ __device__ __forceinline__ void wait_flags(const int* fa, const int* fb) {
   __syncthreads();
 }
 
+// Diagonal factors are also published to a side buffer Ld[j] = {L_jj as [p][r], 1/diag} that is
+// pre-filled with all-ones bytes (a NaN pattern no arithmetic produces): consumers poll the data
+// itself (one L2 round trip) instead of a flag followed by the loads.
+constexpr int LDW = TS * TS + TS;  // doubles per side-buffer entry
+constexpr unsigned long long kUnset = ~0ULL;
+
+__device__ __forceinline__ double ld_cg_volatile(const double* p) {
+  double v;
+  asm volatile("ld.volatile.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Ta[p][r] = L_jj(r, p), dv[c] = 1 / L_jj(c, c) from the side buffer, waiting until published
+__device__ __forceinline__ void stage_diag(double (*T)[LDS], double* dv, const double* __restrict__ Ld) {
+  constexpr int PER = TS * TS / CT;
+  double v[PER];
+#pragma unroll
+  for (int q = 0; q < PER; ++q) v[q] = ld_cg_volatile(Ld + threadIdx.x + CT * q);
+  double d = (threadIdx.x < TS) ? ld_cg_volatile(Ld + TS * TS + threadIdx.x) : 0.0;
+  for (;;) {
+    bool ok = true;
+#pragma unroll
+    for (int q = 0; q < PER; ++q)
+      if (__double_as_longlong(v[q]) == (long long)kUnset) {
+        v[q] = ld_cg_volatile(Ld + threadIdx.x + CT * q);
+        ok = false;
+      }
+    if (threadIdx.x < TS && __double_as_longlong(d) == (long long)kUnset) {
+      d = ld_cg_volatile(Ld + TS * TS + threadIdx.x);
+      ok = false;
+    }
+    if (ok) break;
+  }
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int e = threadIdx.x + CT * q;
+    T[e / TS][e % TS] = v[q];
+  }
+  if (threadIdx.x < TS) dv[threadIdx.x] = d;
+}
+
 __device__ __forceinline__ int tile_id(int i, int j, int nt) { return j * nt - j * (j - 1) / 2 + (i - j); }
 
 // Tasks in ticket order, column by column: column j holds first the DIAGONAL task D_j (which owns
@@ -164,8 +205,8 @@ __device__ __forceinline__ void acc_gather(const Acc& a, double (*Ct)[TS + 1], i
       for (int e = 0; e < 2; ++e) Ct[qr * 16 + rb * 8 + g][qc * 16 + cb * 8 + 2 * tq + e] = a.v[rb][cb][e];
 }
 
-// write Ct as tile (ti, tj) of M, then release its flag
-__device__ __forceinline__ void publish(const double (*Ct)[TS + 1], double* __restrict__ M, int64_t ld, int N, int ti, int tj, int* flag) {
+// write Ct as tile (ti, tj) of M (ends with a CTA barrier)
+__device__ __forceinline__ void store_tile(const double (*Ct)[TS + 1], double* __restrict__ M, int64_t ld, int N, int ti, int tj) {
   const int r = threadIdx.x & 31;
 #pragma unroll
   for (int q = 0; q < TS * TS / CT; ++q) {
@@ -174,10 +215,18 @@ __device__ __forceinline__ void publish(const double (*Ct)[TS + 1], double* __re
     if (gr < N && gc < N) M[gr + (int64_t)gc * ld] = Ct[r][c];
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    st_release(flag, 1);
-  }
+}
+
+// release a tile stored before the last CTA barrier (called by one thread; the fence makes the
+// whole CTA's stores visible at GPU scope before the flag)
+__device__ __forceinline__ void release(int* flag) {
+  __threadfence();
+  st_release(flag, 1);
+}
+
+__device__ __forceinline__ void publish(const double (*Ct)[TS + 1], double* __restrict__ M, int64_t ld, int N, int ti, int tj, int* flag) {
+  store_tile(Ct, M, ld, N, ti, tj);
+  if (threadIdx.x == 0) release(flag);
 }
 
 // warp 0: Ct <- Ct L^{-T} (TRSM; L staged in Ta, 1/diag in dv)
@@ -190,8 +239,9 @@ __device__ __forceinline__ void final_trsm(double (*Ct)[TS + 1], const double (*
   for (int c = 0; c < TS; ++c) Ct[lane][c] = x[c];
 }
 
-// warp 0: Ct <- chol(Ct) (lower, zero upper), 1/diag to dinv_out, first failing pivot to info
-__device__ __forceinline__ void final_potrf(double (*Ct)[TS + 1], double (*colL)[LDS], double* piv, double* dinv_out, int col0, int N,
+// warp 0: Ct <- chol(Ct) (lower, zero upper), also written with 1/diag to the side buffer entry
+// Ld_out; first failing pivot to info
+__device__ __forceinline__ void final_potrf(double (*Ct)[TS + 1], double (*colL)[LDS], double* piv, double* Ld_out, int col0, int N,
                                             int* info, int lane) {
   double x[TS];
 #pragma unroll
@@ -203,13 +253,17 @@ __device__ __forceinline__ void final_potrf(double (*Ct)[TS + 1], double (*colL)
   const double d0 = piv[0];
   potrf_step<0>(x, colL, piv, lane, my_dinv, bad, d0, rsqrt(d0));
   if (bad >= 0 && lane == 0 && col0 + bad < N) atomicCAS(info, 0, col0 + bad + 1);
-  dinv_out[lane] = my_dinv;
 #pragma unroll
-  for (int c = 0; c < TS; ++c) Ct[lane][c] = (c > lane) ? 0.0 : x[c];
+  for (int c = 0; c < TS; ++c) {
+    x[c] = (c > lane) ? 0.0 : x[c];
+    Ct[lane][c] = x[c];
+    Ld_out[c * TS + lane] = x[c];  // [p][r] order, coalesced
+  }
+  Ld_out[TS * TS + lane] = my_dinv;
 }
 
 __global__ void __launch_bounds__(CT) k_chol_tiles(double* __restrict__ M, int64_t ld, int N, int nt, int* __restrict__ flags,
-                                                   int* __restrict__ ticket, int* __restrict__ info, double* __restrict__ dinv,
+                                                   int* __restrict__ ticket, int* __restrict__ info, double* __restrict__ Ld,
                                                    unsigned long long* __restrict__ trace) {
   __shared__ double Ta[TS][LDS], Tb[TS][LDS];
   __shared__ double Ct[TS][TS + 1];
@@ -243,9 +297,7 @@ __global__ void __launch_bounds__(CT) k_chol_tiles(double* __restrict__ M, int64
       }
       if (trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
       acc_gather(a, Ct, qr, qc, g, tq);
-      wait_flags(flags + tile_id(j, j, nt), nullptr);
-      stage(Ta, M, ld, N, j, j);  // Ta[p][r] = L_jj(r, p)
-      if (threadIdx.x < TS) dv[threadIdx.x] = __ldcg(dinv + j * TS + threadIdx.x);
+      stage_diag(Ta, dv, Ld + (int64_t)j * LDW);  // Ta[p][r] = L_jj(r, p)
       __syncthreads();
       if (trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1b));
       if (w == 0) final_trsm(Ct, Ta, dv, lane);
@@ -271,14 +323,12 @@ __global__ void __launch_bounds__(CT) k_chol_tiles(double* __restrict__ M, int64
         if (trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
         // L_{j, j-1} = A_{j, j-1} L_{j-1, j-1}^{-T}
         acc_gather(sb, Ct, qr, qc, g, tq);
-        wait_flags(flags + tile_id(j - 1, j - 1, nt), nullptr);
-        stage(Ta, M, ld, N, j - 1, j - 1);
-        if (threadIdx.x < TS) dv[threadIdx.x] = __ldcg(dinv + (j - 1) * TS + threadIdx.x);
+        stage_diag(Ta, dv, Ld + (int64_t)(j - 1) * LDW);
         __syncthreads();
         if (trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1b));
         if (w == 0) final_trsm(Ct, Ta, dv, lane);
         __syncthreads();
-        publish(Ct, M, ld, N, j, j - 1, flags + tile_id(j, j - 1, nt));
+        store_tile(Ct, M, ld, N, j, j - 1);  // released below by warp 1, off the POTRF path
         // A_jj -= L_{j, j-1} L_{j, j-1}^T from the tile still in shared memory
 #pragma unroll
         for (int q = 0; q < TS * TS / CT; ++q) {
@@ -294,7 +344,8 @@ __global__ void __launch_bounds__(CT) k_chol_tiles(double* __restrict__ M, int64
       }
       acc_gather(d, Ct, qr, qc, g, tq);
       __syncthreads();
-      if (w == 0) final_potrf(Ct, Tb, dv, dinv + j * TS, j * TS, N, info, lane);
+      if (j > 0 && threadIdx.x == 32) release(flags + tile_id(j, j - 1, nt));
+      if (w == 0) final_potrf(Ct, Tb, dv, Ld + (int64_t)j * LDW, j * TS, N, info, lane);
       if (trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1c));
       __syncthreads();
       publish(Ct, M, ld, N, j, j, flags + tile_id(j, j, nt));
@@ -320,7 +371,7 @@ static size_t flags_bytes(int nt) { return ((size_t)(nt * (nt + 1) / 2 + 8) * si
 
 size_t chol_ws_bytes(int N) {
   const int nt = (N + TS - 1) / TS;
-  return flags_bytes(nt) + (size_t)nt * TS * sizeof(double);
+  return flags_bytes(nt) + (size_t)nt * LDW * sizeof(double);
 }
 
 // Factor the N x N SPD matrix M (column-major, leading dimension ld, lower triangle read and
@@ -331,7 +382,8 @@ fk_status chol_tiles(double* M, int64_t ld, int N, int* info, void* ws, cudaStre
   const int ntasks = nt + (nt - 2) * (nt - 1) / 2;
   int* flags = (int*)ws;
   int* ticket = flags + ntiles;
-  double* dinv = (double*)((char*)ws + flags_bytes(nt));
+  double* Ld = (double*)((char*)ws + flags_bytes(nt));
+  FK_CUDA_TRY(cudaMemsetAsync(Ld, 0xff, (size_t)nt * LDW * sizeof(double), s));
   FK_CUDA_TRY(cudaMemsetAsync(flags, 0, (size_t)(ntiles + 8) * sizeof(int), s));
   FK_CUDA_TRY(cudaMemsetAsync(info, 0, sizeof(int), s));
   static int per_sm = 0;
@@ -343,7 +395,7 @@ fk_status chol_tiles(double* M, int64_t ld, int N, int* info, void* ws, cudaStre
   int ps = std::min(per_sm, N <= 2500 ? 2 : 8);
   if (const char* e = getenv("FK_CHOL_PER_SM")) ps = std::max(1, std::min(per_sm, atoi(e)));  // experiments
   const int grid = std::min(ntasks, ps * device_sm_count());
-  k_chol_tiles<<<grid, CT, 0, s>>>(M, ld, N, nt, flags, ticket, info, dinv, trace);
+  k_chol_tiles<<<grid, CT, 0, s>>>(M, ld, N, nt, flags, ticket, info, Ld, trace);
   FK_CUDA_TRY(cudaGetLastError());
   count_launch();
   return FK_OK;

@@ -312,8 +312,43 @@ __global__ void k_assemble_real(SysArgs g, double* __restrict__ M) {
   M[u + v * N] = s;
 }
 
+// d = 1 without a PDE term: closed forms of (P^*AP)_{uv} in the moments (checked against the generic
+// kernel by tests/test_gpu_chol.py and the oracle's dense solve).  With M_q = mu_q / n, basis order
+// u = 0 centre, u = 2t-1 a_t = e_t + e_{-t}, u = 2t b_t = i e_t - i e_{-t}:
+//   (c,c) Re M_0            (c,a_t) 2 Re M_t         (c,b_t) 2 Im M_t     [rows u > v only]
+//   (a_s,a_t) 2 Re(M_{s-t} + M_{s+t})   (a_s,b_t) 2 Im(M_{s+t} - M_{s-t})
+//   (b_s,a_t) 2 Im(M_{s-t} + M_{s+t})   (b_s,b_t) 2 Re(M_{s-t} - M_{s+t})
+// plus lambda cnt R_t on the diagonal (R_t = 1 + t^{2s}, or 1 for the low-bias space).
+__global__ void k_assemble_real_d1(SysArgs g, double* __restrict__ M) {
+  const int64_t N = g.D + 1;
+  const int v = blockIdx.y;
+  const int u = v + blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= g.D) return;
+  const double2* mu = g.mu + 2 * g.m;  // mu[q], q in [-2m, 2m]
+  auto Mq = [&](int q) { return mu[q]; };
+  const int s = (u + 1) >> 1, t = (v + 1) >> 1;
+  const bool ua = u & 1, va = v & 1;
+  double e;
+  if (v == 0) {
+    e = (u == 0) ? Mq(0).x : (ua ? 2.0 * Mq(s).x : 2.0 * Mq(s).y);
+  } else {
+    const double2 dm = Mq(s - t), sm = Mq(s + t);
+    if (ua) e = va ? 2.0 * (dm.x + sm.x) : 2.0 * (sm.y - dm.y);
+    else e = va ? 2.0 * (dm.y + sm.y) : 2.0 * (dm.x - sm.x);
+  }
+  e *= g.inv_n;
+  if (u == v) {
+    const double R = (g.kind == FK_LOWBIAS) ? 1.0 : 1.0 + pow((double)s * s, g.s);
+    e += g.lambda * (u == 0 ? 1.0 : 2.0) * R;
+  }
+  M[u + v * N] = e;
+}
+
 void launch_assemble(const SysArgs& g, double* M, cudaStream_t s) {
-  k_assemble_real<<<dim3((g.D + 255) / 256, g.D), 256, 0, s>>>(g, M);
+  if (g.d == 1 && (g.kind == FK_SOBOLEV || g.kind == FK_LOWBIAS))
+    k_assemble_real_d1<<<dim3((g.D + 255) / 256, g.D), 256, 0, s>>>(g, M);
+  else
+    k_assemble_real<<<dim3((g.D + 255) / 256, g.D), 256, 0, s>>>(g, M);
 }
 
 __global__ void k_rhs_real(SysArgs g, const double2* __restrict__ r, double* __restrict__ M, double* __restrict__ zbuf,
