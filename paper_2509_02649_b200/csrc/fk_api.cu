@@ -44,6 +44,9 @@ fk_status type1_entry(const fk_points& X, const void* Y, double L, int m, double
   if (X.d == 2) return type1_2d_run(m, eps, X, Y, L, mu_out, r_out, (flags & FK_ACCUMULATE) != 0, ws, ws_bytes, d_status, s);
   Plan1 p;
   FK_TRY(make_plan1(X.d, m, eps, mu_out != nullptr, r_out != nullptr, &p));
+  // small n: no more CTAs than ~8 samples per thread need (fewer partial grids to reduce); the
+  // workspace query sized the full count, of which this layout is a prefix
+  if (p.smem) p.ctas = (int)std::min<int64_t>(p.ctas, std::max<int64_t>(1, (X.n + 8 * p.threads - 1) / (8 * p.threads)));
   Type1Out out{mu_out, r_out, (flags & FK_ACCUMULATE) != 0};
   return type1_run(p, X, Y, L, out, ws, ws_bytes, d_status, s);
 }

@@ -8,8 +8,10 @@
 //     nf_mu ~ sigma (4m+1) with sigma ~ 16, rhs grid nf_r = nf_mu / 2; both grids' occupied
 //     halves live in ONE CTA's shared memory as int32 fixed point (native ATOMS.ADD; fp32 smem
 //     atomics are CAS loops on sm_100a).  Partition of unity is exact in fixed point.  A cell
-//     that reaches 2^30 is drained into an fp64 global carry grid (atomicExch), so no periodic
-//     flush is needed and no overflow is possible.  The rhs channel uses a per-CTA power-of-two
+//     that reaches 2^29 in magnitude is drained into an fp64 global carry grid (atomicExch), so no
+//     periodic flush is needed.  No overflow: after a cell crosses 2^29 each of the CTA's 1024
+//     threads can add at most once more (<= 2/3 x 2^21 each) before it drains, 2^29 + 1024 x 1.4e6
+//     < 2^31 (tests/test_gpu_d1.py: 10^4 identical samples in one CTA).  The rhs channel uses a per-CTA power-of-two
 //     scale from the CTA's first 4096 |Y|; |Y| outliers (and NaN) take an exact fp64 slow path.
 //   fp64 path: exponential-of-semicircle window (sigma = 2, w ~ log10(1/eps) + 2) accumulated in
 //     fp64 (shared memory when it fits, else global).
@@ -70,7 +72,7 @@ __device__ __forceinline__ void bs3_sample(int* __restrict__ A, int* __restrict_
     bs3_fixed(fA, kSA * (1.0f / 6.0f), (int)kSA, i0, i1, i2, i3);
     int* c = A + tA;
     const int o0 = atomicAdd(c, i0), o1 = atomicAdd(c + 1, i1), o2 = atomicAdd(c + 2, i2), o3 = atomicAdd(c + 3, i3);
-    if ((o0 | o1 | o2 | o3) & 0x40000000) drain_cells(A, tA, g.carryA, kInvSA);
+    if ((o0 | o1 | o2 | o3) & 0x60000000) drain_cells(A, tA, g.carryA, kInvSA);  // some cell >= 2^29
   }
   if (R) {
     const float ys = y * SY;
@@ -81,8 +83,8 @@ __device__ __forceinline__ void bs3_sample(int* __restrict__ A, int* __restrict_
       int* c = B + tB;
       const unsigned p0 = (unsigned)atomicAdd(c, j0), p1 = (unsigned)atomicAdd(c + 1, j1);
       const unsigned p2 = (unsigned)atomicAdd(c + 2, j2), p3 = (unsigned)atomicAdd(c + 3, j3);
-      const unsigned T = 1u << 30;
-      if (((p0 + T) | (p1 + T) | (p2 + T) | (p3 + T)) & 0x80000000u) drain_cells(B, tB, g.carryB, invSY);
+      const unsigned T = 1u << 29;  // |cell| >= 2^29  <=>  cell + 2^29 outside [0, 2^30)
+      if (((p0 + T) | (p1 + T) | (p2 + T) | (p3 + T)) & 0xC0000000u) drain_cells(B, tB, g.carryB, invSY);
     } else {
       rhs_slow(y, fB, g.carryB, tB);
     }

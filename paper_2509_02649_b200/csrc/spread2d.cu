@@ -8,7 +8,7 @@
 // the samples whose first tap row lies in its row range and keeps those rows plus a (w-1)-row
 // halo in shared memory; CTA (chunk, t) streams its chunk of samples and spreads the ones it
 // owns.  Accumulation: int32 fixed point (weights x 2^21, rhs with a per-CTA power-of-two scale,
-// native ATOMS.ADD, drain-at-2^30 into fp64 carry grids) on the fp32 path; fp64 smem atomics on
+// native ATOMS.ADD, drain-at-2^29 into fp64 carry grids) on the fp32 path; fp64 smem atomics on
 // the fp64 path.  Partials are reduced per fine-grid cell in a fixed CTA order, FFT'd (cuFFT 2-D
 // D2Z, batched over pairs) and deconvolved by psi-hat(q0) psi-hat(q1).
 #include <cmath>
@@ -20,8 +20,10 @@ namespace fk {
 namespace {
 
 constexpr int kW = 16;  // max taps per dimension
-constexpr float kS2 = 2097152.0f;  // 2^21
-constexpr double kInvS2 = 1.0 / 2097152.0;
+// 2^20: a tap weight is <= 1, so after a cell crosses the drain threshold 2^29 the CTA's 1024
+// threads add at most 1024 x 2^20 more before one of them drains it: < 2^31, no overflow
+constexpr float kS2 = 1048576.0f;
+constexpr double kInvS2 = 1.0 / 1048576.0;
 
 // Exact position of a coordinate on a grid: p = x * a (compensated when a is not a power of
 // two), P = floor(p), f = p - P in [0,1).  The first tap of a w-tap ES window centred at the
@@ -133,10 +135,10 @@ __device__ __forceinline__ void spread_fixed(int* T, const Tile& g, int lr /*loc
     for (int b = 0; b < W; ++b) {
       const int v = __float_as_int(fmaf(wy, px[b], FK_MAGIC)) - FK_MAGIC_BITS;
       const unsigned o = (unsigned)atomicAdd(row + a * g.G + b, v);
-      orr |= SIGNED ? (o + (1u << 30)) : o;
+      orr |= SIGNED ? (o + (1u << 29)) : o;
     }
   }
-  if (SIGNED ? (orr & 0x80000000u) : (orr & 0x40000000u))
+  if (SIGNED ? (orr & 0xC0000000u) : (orr & 0x60000000u))  // some cell >= 2^29 in magnitude
     for (int a = 0; a < W; ++a) drain_row(row + a * g.G, W, carry + (int64_t)(lr + a) * g.G + lc, inv_scale);
 }
 

@@ -128,3 +128,27 @@ def test_additive_fit_end_to_end(F, oracle):
     # additive prediction alone
     f2 = host(F.fk_predict_type2(dev(th_o), d, m, 1.0, dev(Xq), 1e-6, additive=True))
     assert rel(f2, f_o) <= 1e-5
+
+
+@pytest.mark.parametrize("x0", [(0.3141, -0.777), (1.0, -1.0)])
+def test_identical_samples_drain_2d(F, x0):
+    """2^20 identical samples: every CTA's 1024 threads hammer the same w^2 cells, so the int32
+    cells cross the drain threshold many times concurrently (overflow regression).  Closed form:
+    mu_q = n e^{-i pi <q, x0>/2}, r_k = (sum Y) e^{-i pi <k, x0>/2}; cross moments of the pair
+    (x0_0, x0_1): n e^{-i pi (a x0_0 - b x0_1)/2}."""
+    n, m = 1 << 20, 24
+    X = torch.tensor(x0, dtype=torch.float32, device="cuda").repeat(n, 1)
+    Y = torch.linspace(-1.0, 2.0, n, dtype=torch.float32, device="cuda")
+    r, mu = F.fk_rhs_type1(X, Y, 1.0, m, 1e-6)
+    q = np.arange(-2 * m, 2 * m + 1)
+    ph = lambda k: np.exp(-1j * np.pi * k * np.float64(np.float32(x0[0])) / 2)[:, None] * \
+        np.exp(-1j * np.pi * k * np.float64(np.float32(x0[1])) / 2)[None, :]
+    mu_cf = n * ph(q)
+    k = np.arange(-m, m + 1)
+    r_cf = float(Y.double().sum()) * ph(k)
+    assert rel(host(mu), mu_cf) <= 1e-5
+    assert rel(host(r), r_cf) <= 1e-5
+    G = host(F.fk_additive_cross_moments(X, 1.0, m, 1e-6))
+    a = np.exp(-1j * np.pi * k * np.float64(np.float32(x0[0])) / 2)[:, None]
+    b = np.exp(+1j * np.pi * k * np.float64(np.float32(x0[1])) / 2)[None, :]
+    assert rel(G[0], n * a * b) <= 1e-5
