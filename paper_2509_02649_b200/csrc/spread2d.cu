@@ -12,6 +12,7 @@
 // the fp64 path.  Partials are reduced per fine-grid cell in a fixed CTA order, FFT'd (cuFFT 2-D
 // D2Z, batched over pairs) and deconvolved by psi-hat(q0) psi-hat(q1).
 #include <cmath>
+#include <cstdlib>
 #include <type_traits>
 
 #include "fk_internal.cuh"
@@ -816,7 +817,22 @@ static fk_status make_planx(int d, int m, double eps, int dtype, PlanX* p) {
   q.fp64 = eps < 1e-7 || dtype == FK_F64;
   q.w = es_width(eps, q.fp64);
   q.beta = 2.30 * q.w;
-  q.nf = fft_friendly(std::max(2 * (2 * m + 1), 2 * q.w + 8));  // tile must not wrap (small m)
+  // fp32 path: sigma = 4 with one tap fewer per dimension (w = 6 at eps = 1e-6, 2.2e-7 in SURVEY
+  // V3) when one pair grid still fits a CTA: 36 instead of 49 atomics per sample and pair
+  // (C5: 1040 -> 820 ms per fit); sigma = 2 otherwise.  FK_CROSS_SIGMA=2|4 overrides (experiments).
+  int sigma = 2;
+  if (!q.fp64) {
+    const int w4 = std::max(5, q.w - 1);
+    const int nf4 = fft_friendly(std::max(4 * (2 * m + 1), 2 * w4 + 8));
+    const size_t g4 = (size_t)(nf4 / 2 + w4 + 4);
+    if (g4 * g4 * 4 <= (size_t)max_optin() - 2048) sigma = 4;
+  }
+  if (const char* e = getenv("FK_CROSS_SIGMA")) sigma = atoi(e) == 4 ? 4 : 2;
+  if (sigma == 4 && !q.fp64) {
+    q.w = std::max(5, q.w - 1);
+    q.beta = 0.97 * 3.14159265358979 * (1.0 - 1.0 / (2.0 * sigma)) * q.w;
+  }
+  q.nf = fft_friendly(std::max(sigma * (2 * m + 1), 2 * q.w + 8));  // tile must not wrap (small m)
   es_geo(q.nf, q.w, &q.off, &q.K, &q.G);
   q.npairs = d * (d - 1) / 2;
   const size_t esz = q.fp64 ? 8 : 4;
@@ -829,7 +845,9 @@ static fk_status make_planx(int d, int m, double eps, int dtype, PlanX* p) {
   q.threads = q.fp64 ? 256 : 1024;
   const int sms = device_sm_count();
   const int per_sm = std::max(1, std::min(4, (int)(cap / (q.smem + 1024))));
-  q.chunks = std::max(1, (sms * per_sm + q.ngroups - 1) / q.ngroups);
+  // one wave: chunks x groups <= resident CTAs (rounding up left a second wave of a few CTAs
+  // that doubled the kernel time)
+  q.chunks = std::max(1, (sms * per_sm) / q.ngroups);
   *p = q;
   return FK_OK;
 }
