@@ -217,9 +217,28 @@ def ncu_traffic(config: str):
 
 
 def es_width(eps):
+    """Taps per dimension of the fp32 d = 2 spreading window (csrc/spread2d.cu es_width, sigma = 2)."""
     import math
 
-    return min(16, max(4, int(math.ceil(math.log10(1.0 / eps))) + 1))
+    return min(8, max(5, int(math.ceil(math.log10(1.0 / eps))) + 1))
+
+
+def cross_width(eps, m):
+    """Taps per dimension of the cross-moment window: sigma = 4 with one tap fewer when one pair
+    grid fits a CTA (csrc/spread2d.cu make_planx), else the sigma = 2 width."""
+    w = es_width(eps)
+    w4 = max(5, w - 1)
+    nf4 = 4 * (2 * m + 1)
+    nf4 = next(v for v in range(nf4, 8 * nf4 + 64) if v % 8 == 0 and _smooth(v))
+    g4 = nf4 // 2 + w4 + 4
+    return w4 if g4 * g4 * 4 <= 232448 - 2048 else w
+
+
+def _smooth(v):
+    for p in (2, 3, 5):
+        while v % p == 0:
+            v //= p
+    return v == 1
 
 
 # ---------------------------------------------------------------------------------------------
@@ -347,7 +366,8 @@ def main():
         # npairs w^2 + 2 d x 4 per sample for the additive model); peak = the measured random ATOMS rate
         w = es_width(eps)
         if additive:
-            atoms = n_loc * (d * (d - 1) // 2 * w * w + d * 8)
+            wc = cross_width(eps, m)
+            atoms = n_loc * (d * (d - 1) // 2 * wc * wc + d * 8)
         else:
             atoms = n_loc * 2 * w * w
         achieved = atoms / (spread_per_step_ms * 1e-3) / 1e9

@@ -123,10 +123,13 @@ typedef struct fk_solve_report {
   int32_t n_unknowns;  /* D */
 } fk_solve_report;
 
-/* theta = A^{-1} r / n by dense Hermitian Cholesky in fp64 (P:513 for the additive block
- * system; reading R9 for why not CG).  theta_out: D complex128, D = (2m+1)^d (d(2m+1) for
- * ADDITIVE).  rep may be NULL (no synchronisation); otherwise the call synchronises `stream`
- * and fills *rep.  Returns FK_E_SOLVE if A is not numerically positive definite. */
+/* theta = A^{-1} r / n by dense Cholesky in fp64 (P:513 for the additive block system;
+ * reading R9 for why not CG).  For real Y theta is Hermitian, so the real-symmetric form
+ * P^*AP z = P^*r/n (D unknowns) is factorised: by a tile dataflow kernel up to D = 3500, by
+ * cuSOLVER potrf above.  theta_out: D complex128, D = (2m+1)^d (d(2m+1) for
+ * ADDITIVE).  rep may be NULL (no synchronisation, CUDA-graph capturable); otherwise the call
+ * synchronises `stream` and fills *rep.  Returns FK_E_SOLVE if A is not numerically positive
+ * definite (only detected when rep != NULL). */
 fk_status fk_solve(const fk_problem* P, double* theta_out, fk_solve_report* rep, void* ws, size_t ws_bytes,
                    fk_stream_t stream);
 

@@ -223,3 +223,24 @@ def test_full_size_equispaced_closed_form(F):
     print(f"full size n={n}: mu {e_mu:.2e} r {e_r:.2e}")
     assert mu[2 * m] == n and r[m] == n / 2  # exact totals
     assert e_mu <= 1e-5 and e_r <= 1e-5
+
+
+def test_fit_graph_replay_matches_eager(F):
+    """fit.FitGraph (type-1 pass + solve captured as one CUDA graph) reproduces the eager fit
+    bit for bit (the fixed-point path is deterministic), and refits when the inputs change."""
+    from datagen.device import gen_dataset
+    from paper_2509_02649_b200 import fit
+
+    n, m, lam = 100_000, 50, 1e-4
+    X = torch.empty(n, device="cuda")
+    Y = torch.empty(n, device="cuda")
+    gen_dataset(X, Y, n, 1, seed=91)
+    g = fit.FitGraph(X, Y, 1.0, m, lam, "sobolev", 2.0)
+    th_g = g.replay().clone()
+    th_e = fit.fit(X, Y, 1.0, m, lam, "sobolev", 2.0).theta
+    assert torch.equal(th_g, th_e)
+    gen_dataset(X, Y, n, 1, seed=92)  # new data in the same buffers
+    th_g2 = g.replay().clone()
+    assert torch.equal(th_g2, fit.fit(X, Y, 1.0, m, lam, "sobolev", 2.0).theta)
+    assert not torch.equal(th_g2, th_g)
+    assert g.launches > 0
