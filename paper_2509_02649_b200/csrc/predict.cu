@@ -9,6 +9,8 @@
 #include <cmath>
 #include <type_traits>
 
+#include <cstdlib>
+
 #include "fk_internal.cuh"
 #include "window.cuh"
 
@@ -174,6 +176,49 @@ __global__ void __launch_bounds__(512) k_gather_bs3_vec(const float4* __restrict
       r[q] = ok ? (w[0] * c[0] + w[1] * c[1] + w[2] * c[2] + w[3] * c[3]) : NAN;
     }
     __stcs(out4 + j, make_float4(r[0], r[1], r[2], r[3]));
+  }
+  if (bad && d_status) atomicOr(d_status, (int)FK_E_RANGE);
+}
+
+// Same with the grid held as overlapping pairs P[i] = (g[i], g[i+1]) (8 B per cell): the 4 taps
+// of a query are 2 LDS.64 instead of 4 LDS.32, half the shared-memory wavefronts per query
+// under random addresses (the gather is bound by them, not by HBM, with the 4-byte layout).
+template <bool EXACT>
+__global__ void __launch_bounds__(1024) k_gather_bs3_pair(const float4* __restrict__ Xq4, int64_t n4, const double* __restrict__ grid,
+                                                        int nf, int off, int G, float a_hi, float a_lo, float4* __restrict__ out4,
+                                                        int* __restrict__ d_status) {
+  extern __shared__ float2 sgp[];
+  for (int i = threadIdx.x; i < G; i += blockDim.x)
+    sgp[i] = make_float2((float)grid[off + i], i + 1 < G ? (float)grid[off + i + 1] : 0.0f);
+  __syncthreads();
+  const int nq = nf / 4;
+  bool bad = false;
+  auto one = [&](float x) {
+    int t;
+    float fr;
+    pos1_f32<EXACT>(x, a_hi, a_lo, nq, t, fr);
+    const bool ok = (unsigned)t <= (unsigned)(G - 4);
+    bad |= !ok;
+    t = ok ? t : 0;
+    float w[4];
+    bs3_float(fr, w);
+    const float2 lo = sgp[t], hi = sgp[t + 2];
+    return ok ? (w[0] * lo.x + w[1] * lo.y + w[2] * hi.x + w[3] * hi.y) : NAN;
+  };
+  // U float4 per thread per step (4U queries in flight)
+  constexpr int U = 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (; j + (U - 1) * stride < n4; j += U * stride) {
+    float4 xv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) xv[u] = __ldcs(Xq4 + j + u * stride);
+#pragma unroll
+    for (int u = 0; u < U; ++u) __stcs(out4 + j + u * stride, make_float4(one(xv[u].x), one(xv[u].y), one(xv[u].z), one(xv[u].w)));
+  }
+  for (; j < n4; j += stride) {
+    const float4 xa = __ldcs(Xq4 + j);
+    __stcs(out4 + j, make_float4(one(xa.x), one(xa.y), one(xa.z), one(xa.w)));
   }
   if (bad && d_status) atomicOr(d_status, (int)FK_E_RANGE);
 }
@@ -382,9 +427,26 @@ static fk_status gather(const PredPlan& p, const fk_points& Xq, double L, const 
                      ((uintptr_t)out % 16 == 0) && Xq.n >= 4;
     if (vec) {
       const int64_t n4 = Xq.n / 4;
-      auto kv = exact ? k_gather_bs3_vec<true> : k_gather_bs3_vec<false>;
-      cudaFuncSetAttribute(kv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
-      kv<<<sms * per_sm, 512, p.smem, s>>>((const float4*)Xq.ptr, n4, w.grid, p.nf, p.g.off, p.g.G, a_hi, a_lo, (float4*)out, d_status);
+      const size_t pair_smem = (size_t)p.g.G * 8;
+      int optin = 0, dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+      // pair layout + 16 queries in flight per thread: 5.08e11 -> 6.06e11 queries/s at m = 1000
+      // (0.62 -> 0.74 of the measured copy bandwidth, bench_rows predict)
+      bool pair = pair_smem <= (size_t)optin;
+      if (const char* e = getenv("FK_PRED_PAIR")) pair = pair && e[0] == '1';  // experiments
+      if (pair) {
+        auto kv = exact ? k_gather_bs3_pair<true> : k_gather_bs3_pair<false>;
+        cudaFuncSetAttribute(kv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pair_smem);
+        const int ps = std::max(1, std::min(2, (int)(optin / (pair_smem + 1024))));
+        kv<<<sms * ps, 1024, pair_smem, s>>>((const float4*)Xq.ptr, n4, w.grid, p.nf, p.g.off, p.g.G, a_hi, a_lo, (float4*)out,
+                                             d_status);
+      } else {
+        auto kv = exact ? k_gather_bs3_vec<true> : k_gather_bs3_vec<false>;
+        cudaFuncSetAttribute(kv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+        kv<<<sms * per_sm, 512, p.smem, s>>>((const float4*)Xq.ptr, n4, w.grid, p.nf, p.g.off, p.g.G, a_hi, a_lo, (float4*)out,
+                                             d_status);
+      }
       FK_CUDA_TRY(cudaGetLastError());
       count_launch();
       if (n4 * 4 == Xq.n) return FK_OK;
