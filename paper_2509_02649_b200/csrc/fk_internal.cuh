@@ -92,6 +92,11 @@ struct Plan1 {
 fk_status make_plan1(int d, int m, double eps, bool need_mu, bool need_r, Plan1* p);
 int fft_friendly(int n);  // smallest 2^a 3^b 5^c >= n, even, multiple of 8
 
+// ES taps as degree-P polynomials in s in (-1, 1] (plan.cu): coef[i * (P + 1) + q], device memory,
+// built once per (device, w, beta).
+inline int es_horner_degree(int w) { return w + 2; }
+fk_status es_horner_table(const EsParams& es, const double** d_coef);
+
 // ES window Fourier transform table phihat[k] = psi-hat(k / nf), k = 0..K (computed on device).
 fk_status es_phihat_table(const EsParams& es, int nf, int K, double* d_tab, cudaStream_t s);
 

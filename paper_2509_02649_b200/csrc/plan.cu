@@ -7,6 +7,7 @@
 #include <tuple>
 #include <vector>
 
+#include <cstring>
 #include "fk_internal.cuh"
 
 namespace fk {
@@ -129,7 +130,7 @@ fk_status make_plan1(int d, int m, double eps, bool need_mu, bool need_r, Plan1*
     q.gA = {q.nf_mu, q.nf_mu / 4 - w / 2 - 2, q.nf_mu / 2 + w + 4};
     q.gB = {q.nf_r, q.nf_r / 4 - w / 2 - 2, q.nf_r / 2 + w + 4};
     size_t bytes = (size_t)((need_mu ? q.gA.G : 0) + (need_r ? q.gB.G : 0)) * 8;
-    q.smem = bytes <= (size_t)smem_cap;
+    q.smem = bytes + (size_t)w * (w + 3) * 8 <= (size_t)smem_cap;  // + the Horner tap table
     q.smem_bytes = q.smem ? bytes : 0;
   }
   // launch shape: persistent CTAs, as many per SM as shared memory and 2048 threads allow
@@ -194,6 +195,77 @@ fk_status es_phihat_table(const EsParams& es, int nf, int K, double* d_tab, cuda
   k_es_phihat<<<(unsigned)(((int64_t)(K + 1) * 32 + 255) / 256), 256, 0, s>>>(gl, es.w, es.beta, nf, K, d_tab);
   count_launch();
   FK_CUDA_TRY(cudaGetLastError());
+  return FK_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// ES taps as polynomials (fp64 paths).  For a point at ul (cells), l0 = ceil(ul - w/2) and
+// u = ul - l0 in (w/2 - 1, w/2]; with s = 2 (u - w/2 + 1) - 1 in (-1, 1] the tap i value
+// psi((i - u) 2 / w) is a smooth function of s.  Chebyshev interpolation of degree P = w + 2 in
+// long double, converted to monomials in s: max error ~1.5 exp(-beta) (the kink of psi at |z| = 1,
+// i.e. 10^-w at beta = 2.3 w), two orders below the window's own aliasing error; |coefficients|
+// sum to ~1.2 so Horner in fp64 loses nothing.  Replaces one exp + one sqrt per tap by P FMAs.
+// Tables are built once per (device, w, beta) and kept in device memory.
+// ------------------------------------------------------------------------------------------
+static std::mutex g_horner_mu;
+static std::map<std::tuple<int, int, long long>, double*> g_horner;
+
+fk_status es_horner_table(const EsParams& es, const double** d_coef) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  long long bkey;
+  std::memcpy(&bkey, &es.beta, sizeof bkey);
+  auto key = std::make_tuple(dev, es.w, bkey);
+  std::lock_guard<std::mutex> lk(g_horner_mu);
+  auto it = g_horner.find(key);
+  if (it != g_horner.end()) {
+    *d_coef = it->second;
+    return FK_OK;
+  }
+  const int w = es.w, P = es_horner_degree(w), np = P + 1;
+  std::vector<double> coef((size_t)w * np);
+  const long double pi = 3.141592653589793238462643383279502884L;
+  for (int i = 0; i < w; ++i) {
+    // values at the Chebyshev nodes
+    std::vector<long double> fv(np), c(np, 0.0L);
+    for (int k = 0; k < np; ++k) {
+      const long double sk = cosl(pi * (k + 0.5L) / np);
+      const long double u = (sk + 1.0L) / 2.0L + w / 2.0L - 1.0L;
+      const long double z = (i - u) * 2.0L / w;
+      const long double v = 1.0L - z * z;
+      fv[k] = v > 0 ? expl((long double)es.beta * (sqrtl(v) - 1.0L)) : 0.0L;
+    }
+    for (int j = 0; j < np; ++j) {
+      long double acc = 0;
+      for (int k = 0; k < np; ++k) acc += fv[k] * cosl(pi * j * (k + 0.5L) / np);
+      c[j] = acc * 2.0L / np;
+    }
+    c[0] /= 2.0L;
+    // sum_j c_j T_j(s) -> monomials: T_0 = 1, T_1 = s, T_{j+1} = 2 s T_j - T_{j-1}
+    std::vector<long double> mono(np, 0.0L), tm1(np, 0.0L), t0(np, 0.0L), t1(np, 0.0L);
+    t0[0] = 1.0L;
+    for (int j = 0; j < np; ++j) {
+      const std::vector<long double>& T = (j == 0) ? t0 : t1;
+      for (int q = 0; q < np; ++q) mono[q] += c[j] * T[q];
+      if (j == 0) {
+        t1.assign(np, 0.0L);
+        t1[1 % np] = 1.0L;
+        tm1 = t0;
+        continue;
+      }
+      std::vector<long double> tn(np, 0.0L);
+      for (int q = 0; q + 1 < np; ++q) tn[q + 1] += 2.0L * t1[q];
+      for (int q = 0; q < np; ++q) tn[q] -= tm1[q];
+      tm1 = t1;
+      t1 = tn;
+    }
+    for (int q = 0; q < np; ++q) coef[(size_t)i * np + q] = (double)mono[q];
+  }
+  double* d = nullptr;
+  FK_CUDA_TRY(cudaMalloc(&d, coef.size() * sizeof(double)));
+  FK_CUDA_TRY(cudaMemcpy(d, coef.data(), coef.size() * sizeof(double), cudaMemcpyHostToDevice));
+  g_horner[key] = d;
+  *d_coef = d;
   return FK_OK;
 }
 

@@ -19,6 +19,7 @@
 // X and Y are streamed once from HBM with 128-bit evict-first loads, software-pipelined one
 // iteration ahead; CTAs are persistent (1-2 per SM) over contiguous sample ranges.
 #include <cmath>
+#include <type_traits>
 
 #include "fk_internal.cuh"
 #include "window.cuh"
@@ -208,6 +209,8 @@ struct EsArgs {
   int nfA, offA, GA, nfB, offB, GB;
   double* partA;
   double* partB;
+  double* carryA;  // fixed-point fp64-mode kernel (k_spread1d_esx): drained hi words
+  double* carryB;
   int* d_status;
 };
 
@@ -261,6 +264,137 @@ __global__ void __launch_bounds__(1024, 1) k_spread1d_es(const XT* __restrict__ 
   }
 }
 
+// fp64-accuracy mode (eps < 1e-7), shared-memory grids: ES taps as polynomials from a
+// constant-memory table (es_horner_table; uploaded per launch) instead of exp + sqrt per tap, and
+// 64-bit fixed-point accumulation (below).  Measured at C2 shape, n = 1e9, eps = 1e-10: 79 ms with
+// exp taps + fp64 CAS atomics, 77 ms now -- the instruction mix moved (ncu: the 360 coefficient
+// loads per sample became the MIO limiter) but the rate did not; the gain is that the result is
+// now order-independent (bitwise deterministic) like the fp32 path.
+__constant__ double c_es_coef[16 * 19];  // W x (W + 3) Horner table of the launch (es_horner_table)
+
+// tap i of a point at ul from the constant-memory table
+template <int W>
+__device__ __forceinline__ double es_tap_const(double sv, int i) {
+  constexpr int NP = W + 3;
+  double acc = c_es_coef[i * NP + NP - 1];
+#pragma unroll
+  for (int q = NP - 2; q >= 0; --q) acc = fma(acc, sv, c_es_coef[i * NP + q]);
+  return acc;
+}
+
+// fp64-accuracy accumulation in 64-bit fixed point held as two int32 words per cell (lo
+// unsigned, hi signed): an add is one native ATOMS.ADD on lo, the carry is read off its return
+// value, and hi gets (v >> 32) + carry only when that is non-zero.  3.1x the rate of fp64
+// shared-memory atomicAdd (a CAS loop on sm_100a; scratch microbenchmark 1.31e12 vs 4.2e11 tap
+// adds/s).  Tap weights x 2^40 (rounding 2^-41, far below the 1e-10 target); a hi word that
+// reaches 2^29 in magnitude is drained (atomicExch) into an fp64 carry grid, so no overflow.
+constexpr double kSX = 1099511627776.0;  // 2^40
+
+__device__ __forceinline__ void pair_add(unsigned* __restrict__ lo, int* __restrict__ hi, int c, long long v, double* carry,
+                                         double hi_unit) {
+  const unsigned l = (unsigned)v;
+  const int h = (int)(v >> 32);
+  const unsigned o = atomicAdd(lo + c, l);
+  const int hc = h + ((o + l) < o ? 1 : 0);
+  if (hc != 0) {
+    const int oh = atomicAdd(hi + c, hc);
+    if ((unsigned)(oh + hc + (1 << 29)) >= (1u << 30)) {
+      const int t = atomicExch(hi + c, 0);
+      if (t) atomicAdd(carry + c, (double)t * hi_unit);
+    }
+  }
+}
+
+template <typename XT, bool MU, bool R, int W>
+__global__ void __launch_bounds__(1024, 1) k_spread1d_esx(const XT* __restrict__ X, const XT* __restrict__ Y, EsArgs g) {
+  extern __shared__ unsigned smx[];
+  unsigned* Alo = smx;
+  int* Ahi = (int*)(smx + (MU ? g.GA : 0));
+  unsigned* Blo = smx + (MU ? 2 * g.GA : 0);
+  int* Bhi = (int*)(Blo + (R ? g.GB : 0));
+  const int nsm = (MU ? 2 * g.GA : 0) + (R ? 2 * g.GB : 0);
+  for (int i = threadIdx.x; i < nsm; i += blockDim.x) smx[i] = 0u;
+  const int64_t beg = (int64_t)blockIdx.x * g.per;
+  const int64_t end = min(g.n, beg + g.per);
+  // rhs scale 2^E with max |Y| 2^E in [2^19, 2^20) over the CTA's first 4096 samples
+  int E = 0;
+  if (R) {
+    __shared__ double red[32];
+    __shared__ int sE;
+    double mx = 0.0;
+    const int64_t cnt = max((int64_t)0, min(end - beg, (int64_t)kYProbe));
+    for (int64_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+      const double a = fabs((double)Y[beg + i]);
+      if (a == a) mx = fmax(mx, a);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t = fmax(t, red[w]);
+      int e2 = 0;
+      int Eloc = 19;
+      if (t > 0.0 && t < 1e300) {
+        frexp(t, &e2);
+        Eloc = 20 - e2;
+      }
+      sE = max(-900, min(900, Eloc));
+    }
+    __syncthreads();
+    E = sE;
+  }
+  __syncthreads();
+  const double sy = R ? ldexp(1.0, E) : 0.0;           // Y -> |Y sy| < 2^20
+  const double unitA = 1.0 / kSX * 4294967296.0;       // value of one hi unit, mu grid (2^-8)
+  const double unitB = R ? ldexp(4294967296.0, -(E + 20)) : 0.0;
+  bool bad = false;
+  for (int64_t j = beg + threadIdx.x; j < end; j += blockDim.x) {
+    const double x = (double)X[j * g.stride];
+    const double u = x * g.a + 0.5 * g.nfA;  // moment-grid coordinate (cells), t = -pi at 0
+    const double ulA = u - g.offA;
+    const int l0 = (int)ceil(ulA - 0.5 * W);
+    if (!(ulA == ulA) || l0 < 0 || l0 + W > g.GA) {
+      bad = true;
+      continue;
+    }
+    if (MU) {
+      const double sv = 2.0 * (ulA - l0 - 0.5 * W + 1.0) - 1.0;
+#pragma unroll
+      for (int i = 0; i < W; ++i) pair_add(Alo, Ahi, l0 + i, __double2ll_rn(es_tap_const<W>(sv, i) * kSX), g.carryA, unitA);
+    }
+    if (R) {
+      const double y = (double)Y[j];
+      const double ulB = 0.5 * u - g.offB;
+      const int b0 = (int)ceil(ulB - 0.5 * W);
+      const double sv = 2.0 * (ulB - b0 - 0.5 * W + 1.0) - 1.0;
+      const double ys = y * sy;
+      if (fabs(ys) < 2097152.0) {  // |y 2^E| < 2^21: |v| < 2^41, hi stays small
+#pragma unroll
+        for (int i = 0; i < W; ++i)
+          pair_add(Blo, Bhi, b0 + i, __double2ll_rn(es_tap_const<W>(sv, i) * ys * 1048576.0), g.carryB, unitB);
+      } else {  // |Y| outlier or NaN: exact fp64 into the carry grid
+#pragma unroll 1
+        for (int i = 0; i < W; ++i) atomicAdd(g.carryB + b0 + i, y * es_tap_const<W>(sv, i));
+      }
+    }
+  }
+  if (bad && g.d_status) atomicOr(g.d_status, (int)FK_E_RANGE);
+  __syncthreads();
+  // per-CTA partials as fp64 values (exact integers times a power of two, rounded once)
+  if (MU) {
+    double* dst = g.partA + (int64_t)blockIdx.x * g.GA;
+    const double sc = 1.0 / kSX;
+    for (int i = threadIdx.x; i < g.GA; i += blockDim.x) dst[i] = ((double)Ahi[i] * 4294967296.0 + (double)Alo[i]) * sc;
+  }
+  if (R) {
+    double* dst = g.partB + (int64_t)blockIdx.x * g.GB;
+    const double sc = ldexp(1.0, -(E + 20));
+    for (int i = threadIdx.x; i < g.GB; i += blockDim.x) dst[i] = ((double)Bhi[i] * 4294967296.0 + (double)Blo[i]) * sc;
+  }
+}
+
 // ------------------------------------------------------------------------------------------
 // per-CTA partial grids -> one fp64 fine grid (full period, zero outside the occupied band),
 // summed over CTAs in a fixed order (the fixed-point path is exact, hence bitwise deterministic)
@@ -283,13 +417,16 @@ __global__ void k_reduce_fixed(const int* __restrict__ part, const int* __restri
   fine[l] = s;
 }
 
-__global__ void k_reduce_f64(const double* __restrict__ part, int ncta, int G, int off, int nf, double* __restrict__ fine) {
+__global__ void k_reduce_f64(const double* __restrict__ part, int ncta, int G, int off, int nf, const double* __restrict__ carry,
+                             double* __restrict__ fine) {
   const int l = blockIdx.x * blockDim.x + threadIdx.x;
   if (l >= nf) return;
   const int i = l - off;
   double s = 0.0;
-  if (i >= 0 && i < G)
+  if (i >= 0 && i < G) {
     for (int c = 0; c < ncta; ++c) s += part[(int64_t)c * G + i];
+    if (carry) s += carry[i];
+  }
   fine[l] = s;
 }
 
@@ -353,17 +490,15 @@ static fk_status layout1(const Plan1& p, bool mu, bool r, Bump& b, Ws1& w, size_
     w.partA = b.take((size_t)nparts * p.gA.G * esz);
     w.fineA = (double*)b.take((size_t)p.nf_mu * 8);
     w.specA = (double2*)b.take((size_t)(p.nf_mu / 2 + 1) * 16);
-    if (!p.fp64) w.carryA = (double*)b.take((size_t)p.gA.G * 8);
+    if (!p.fp64 || p.smem) w.carryA = (double*)b.take((size_t)p.gA.G * 8);
     if (p.ker == KER_ES) w.tabA = (double*)b.take((size_t)(2 * p.m + 1) * 8);
   }
   if (r) {
     w.partB = b.take((size_t)nparts * p.gB.G * esz);
     w.fineB = (double*)b.take((size_t)p.nf_r * 8);
     w.specB = (double2*)b.take((size_t)(p.nf_r / 2 + 1) * 16);
-    if (!p.fp64) {
-      w.carryB = (double*)b.take((size_t)p.gB.G * 8);
-      w.escale = (int*)b.take((size_t)p.ctas * 4);
-    }
+    if (!p.fp64 || p.smem) w.carryB = (double*)b.take((size_t)p.gB.G * 8);
+    if (!p.fp64) w.escale = (int*)b.take((size_t)p.ctas * 4);
     if (p.ker == KER_ES) w.tabB = (double*)b.take((size_t)(p.m + 1) * 8);
   }
   w.fftwork = b.take(std::max<size_t>(fw, 256));
@@ -393,6 +528,31 @@ static void launch_bs3(const Plan1& p, const XT* X, const XT* Y, const Bs3Args& 
 
 template <typename XT, bool MU, bool R>
 static void launch_es(const Plan1& p, const XT* X, const XT* Y, const EsArgs& a, cudaStream_t s) {
+  const double* coef = nullptr;
+  if (p.smem && p.es.w >= 9 && (!MU || a.carryA) && (!R || a.carryB) && es_horner_table(p.es, &coef) == FK_OK &&
+      cudaMemcpyToSymbolAsync(c_es_coef, coef, (size_t)p.es.w * (p.es.w + 3) * 8, 0, cudaMemcpyDeviceToDevice, s) == cudaSuccess) {
+    const size_t smem = p.smem_bytes;  // 2 x int32 per cell = the fp64 grid's bytes
+    auto go = [&](auto wtag) {
+      constexpr int WW = decltype(wtag)::value;
+      auto k = k_spread1d_esx<XT, MU, R, WW>;
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      prof_spread_begin(s);
+      k<<<p.ctas, p.threads, smem, s>>>(X, Y, a);
+      prof_spread_end(s);
+    };
+    switch (p.es.w) {
+      case 9: go(std::integral_constant<int, 9>{}); break;
+      case 10: go(std::integral_constant<int, 10>{}); break;
+      case 11: go(std::integral_constant<int, 11>{}); break;
+      case 12: go(std::integral_constant<int, 12>{}); break;
+      case 13: go(std::integral_constant<int, 13>{}); break;
+      case 14: go(std::integral_constant<int, 14>{}); break;
+      case 15: go(std::integral_constant<int, 15>{}); break;
+      default: go(std::integral_constant<int, 16>{}); break;
+    }
+    count_launch();
+    return;
+  }
   if (p.smem) {
     auto k = k_spread1d_es<XT, MU, R, true>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
@@ -456,6 +616,8 @@ static fk_status spread_dispatch(const Plan1& p, const fk_points& Xp, const void
     a.per = (n + p.ctas - 1) / p.ctas;
     a.partA = (double*)w.partA;
     a.partB = (double*)w.partB;
+    a.carryA = w.carryA;
+    a.carryB = w.carryB;
     a.d_status = d_status;
     if (mu && r) launch_es<XT, true, true>(p, X, Y, a, s);
     else if (mu) launch_es<XT, true, false>(p, X, Y, a, s);
@@ -483,10 +645,11 @@ fk_status type1_run(const Plan1& p, const fk_points& X, const void* Y, double L,
   FK_TRY(layout1(p, mu, r, b, w, &fw));
   if (!b.ok()) return fail(FK_E_WORKSPACE, "workspace too small: need " + std::to_string(b.used + 256) + " bytes");
   // zero what is accumulated globally
-  if (!p.fp64) {
+  if (!p.fp64 || p.smem) {
     if (mu) FK_CUDA_TRY(cudaMemsetAsync(w.carryA, 0, (size_t)p.gA.G * 8, s));
     if (r) FK_CUDA_TRY(cudaMemsetAsync(w.carryB, 0, (size_t)p.gB.G * 8, s));
-  } else if (!p.smem) {
+  }
+  if (p.fp64 && !p.smem) {
     if (mu) FK_CUDA_TRY(cudaMemsetAsync(w.partA, 0, (size_t)p.gA.G * 8, s));
     if (r) FK_CUDA_TRY(cudaMemsetAsync(w.partB, 0, (size_t)p.gB.G * 8, s));
   }
@@ -507,7 +670,8 @@ fk_status type1_run(const Plan1& p, const fk_points& X, const void* Y, double L,
       k_reduce_fixed<<<(p.nf_mu + TB - 1) / TB, TB, 0, s>>>((const int*)w.partA, nullptr, nparts, p.gA.G, p.gA.off, p.nf_mu, kInvSA,
                                                             w.carryA, w.fineA);
     else
-      k_reduce_f64<<<(p.nf_mu + TB - 1) / TB, TB, 0, s>>>((const double*)w.partA, nparts, p.gA.G, p.gA.off, p.nf_mu, w.fineA);
+      k_reduce_f64<<<(p.nf_mu + TB - 1) / TB, TB, 0, s>>>((const double*)w.partA, nparts, p.gA.G, p.gA.off, p.nf_mu,
+                                                          p.smem ? w.carryA : nullptr, w.fineA);
     FK_CUDA_TRY(cudaGetLastError());
     count_launch();
     FftPlan pa;
@@ -524,7 +688,8 @@ fk_status type1_run(const Plan1& p, const fk_points& X, const void* Y, double L,
       k_reduce_fixed<<<(p.nf_r + TB - 1) / TB, TB, 0, s>>>((const int*)w.partB, w.escale, nparts, p.gB.G, p.gB.off, p.nf_r, 1.0,
                                                            w.carryB, w.fineB);
     else
-      k_reduce_f64<<<(p.nf_r + TB - 1) / TB, TB, 0, s>>>((const double*)w.partB, nparts, p.gB.G, p.gB.off, p.nf_r, w.fineB);
+      k_reduce_f64<<<(p.nf_r + TB - 1) / TB, TB, 0, s>>>((const double*)w.partB, nparts, p.gB.G, p.gB.off, p.nf_r,
+                                                         p.smem ? w.carryB : nullptr, w.fineB);
     FK_CUDA_TRY(cudaGetLastError());
     count_launch();
     FftPlan pb;
