@@ -244,3 +244,17 @@ def test_fit_graph_replay_matches_eager(F):
     assert torch.equal(th_g2, fit.fit(X, Y, 1.0, m, lam, "sobolev", 2.0).theta)
     assert not torch.equal(th_g2, th_g)
     assert g.launches > 0
+
+
+@pytest.mark.parametrize("eps,dt", [(1e-6, torch.float32), (1e-10, torch.float64)])
+def test_type1_bitwise_deterministic(F, eps, dt):
+    """Fixed-point accumulation + fixed-order reduction: repeated passes agree bit for bit (fp32
+    mode and the fp64 mode's 64-bit fixed point)."""
+    n, m = 3_000_000, 300
+    X = torch.empty(n, device="cuda")
+    Y = torch.empty(n, device="cuda")
+    gen_dataset(X, Y, n, 1, seed=93)
+    X, Y = X.to(dt), Y.to(dt)
+    r1, mu1 = F.fk_rhs_type1(X, Y, 1.0, m, eps)
+    r2, mu2 = F.fk_rhs_type1(X, Y, 1.0, m, eps)
+    assert torch.equal(r1, r2) and torch.equal(mu1, mu2)
