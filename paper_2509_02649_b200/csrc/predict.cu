@@ -297,7 +297,7 @@ __device__ __forceinline__ void es_place(double x, double a, int K, int w, int& 
 }
 
 template <typename XT, typename GT, int W>
-__global__ void __launch_bounds__(256) k_gather2d(const XT* __restrict__ Xq, int64_t n, int64_t sn, int64_t sd,
+__global__ void __launch_bounds__(1024) k_gather2d(const XT* __restrict__ Xq, int64_t n, int64_t sn, int64_t sd,
                                                  const double* __restrict__ grid, int nf, int off, int G, int K, double a, int w_unused,
                                                  double beta, int in_smem, XT* __restrict__ out, int* __restrict__ d_status) {
   constexpr int w = W;
@@ -383,11 +383,17 @@ static fk_status gather2d(const PredPlan& p, const fk_points& Xq, double L, cons
   const int sms = device_sm_count();
   const double a = (double)p.nf / (4.0 * L);
   const int K = p.nf / 2 - p.g.off;
-  const int per_sm = p.smem ? std::max(1, std::min(4, (int)(200000 / (p.smem + 1024)))) : 4;
+  // 1024-thread CTAs, as many per SM as the grid copy allows (2 at m = 64): the gather is bound by
+  // the latency of its w^2 random shared-memory loads, so occupancy is what matters (256-thread
+  // CTAs left 16 warps per SM: 3.4e10 queries/s at C3's m)
+  int optin = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+  const int per_sm = p.smem ? std::max(1, std::min(2, (int)(optin / (p.smem + 1024)))) : 2;
   auto go = [&](auto k) {
     if (p.smem) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
-    k<<<sms * per_sm, 256, p.smem, s>>>((const XT*)Xq.ptr, Xq.n, Xq.stride_n, Xq.stride_d, w.grid, p.nf, p.g.off, p.g.G, K, a, p.es.w,
-                                        p.es.beta, p.in_smem ? 1 : 0, (XT*)out, d_status);
+    k<<<sms * per_sm, 1024, p.smem, s>>>((const XT*)Xq.ptr, Xq.n, Xq.stride_n, Xq.stride_d, w.grid, p.nf, p.g.off, p.g.G, K, a,
+                                         p.es.w, p.es.beta, p.in_smem ? 1 : 0, (XT*)out, d_status);
   };
   auto byw = [&](auto wtag) {
     constexpr int WW = decltype(wtag)::value;
