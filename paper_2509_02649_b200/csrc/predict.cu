@@ -223,6 +223,48 @@ __global__ void __launch_bounds__(1024) k_gather_bs3_pair(const float4* __restri
   if (bad && d_status) atomicOr(d_status, (int)FK_E_RANGE);
 }
 
+// fp64 gather, d = 1 or additive, grid in shared memory: compile-time width, taps as polynomials
+// from a constant-memory table (es_horner_table) instead of exp + sqrt per tap
+__constant__ double c_pred_coef[16 * 19];
+
+template <typename XT, int W>
+__global__ void __launch_bounds__(512) k_gather_es_h(const XT* __restrict__ Xq, int64_t n, int nfeat, int64_t sn, int64_t sd,
+                                                    const double* __restrict__ grid, int nf, int off, int G, double a,
+                                                    XT* __restrict__ out, int* __restrict__ d_status) {
+  constexpr int NP = W + 3;
+  extern __shared__ double sgh[];
+  for (int64_t i = threadIdx.x; i < (int64_t)nfeat * G; i += blockDim.x) {
+    const int f = (int)(i / G), c = (int)(i % G);
+    sgh[i] = grid[(int64_t)f * nf + off + c];
+  }
+  __syncthreads();
+  bool bad = false;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    bool ok = true;
+    for (int f = 0; f < nfeat; ++f) {
+      const double ul = (double)Xq[j * sn + f * sd] * a + 0.5 * nf - off;
+      const int l0 = (int)ceil(ul - 0.5 * W);
+      if (!(ul == ul) || l0 < 0 || l0 + W > G) {
+        ok = false;
+        continue;
+      }
+      const double sv = 2.0 * (ul - l0 - 0.5 * W + 1.0) - 1.0;
+      const double* c = sgh + (int64_t)f * G + l0;
+#pragma unroll
+      for (int i = 0; i < W; ++i) {
+        double psi = c_pred_coef[i * NP + NP - 1];
+#pragma unroll
+        for (int q = NP - 2; q >= 0; --q) psi = fma(psi, sv, c_pred_coef[i * NP + q]);
+        acc = fma(psi, c[i], acc);
+      }
+    }
+    bad |= !ok;
+    out[j] = ok ? (XT)acc : (XT)NAN;
+  }
+  if (bad && d_status) atomicOr(d_status, (int)FK_E_RANGE);
+}
+
 template <typename XT>
 __global__ void __launch_bounds__(512) k_gather_es(const XT* __restrict__ Xq, int64_t n, int nfeat, int64_t sn, int64_t sd,
                                                   const double* __restrict__ grid, int nf, int off, int G, double a, int w,
@@ -473,6 +515,31 @@ static fk_status gather(const PredPlan& p, const fk_points& Xq, double L, const 
     k<<<sms * per_sm, 512, p.smem, s>>>((const XT*)Xq.ptr, Xq.n, p.nfeat, Xq.stride_n, Xq.stride_d, w.grid, p.nf, p.g.off, p.g.G,
                                         a_hi, a_lo, a, p.in_smem ? 1 : 0, (XT*)out, d_status);
   } else {
+    const double* coef = nullptr;
+    if (p.in_smem && p.es.w >= 9 && es_horner_table(p.es, &coef) == FK_OK &&
+        cudaMemcpyToSymbolAsync(c_pred_coef, coef, (size_t)p.es.w * (p.es.w + 3) * 8, 0, cudaMemcpyDeviceToDevice, s) == cudaSuccess) {
+      const int per_sm = std::max(1, std::min(4, (int)(200000 / (p.smem + 1024))));
+      auto go = [&](auto wtag) {
+        constexpr int WW = decltype(wtag)::value;
+        auto k = k_gather_es_h<XT, WW>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+        k<<<sms * per_sm, 512, p.smem, s>>>((const XT*)Xq.ptr, Xq.n, p.nfeat, Xq.stride_n, Xq.stride_d, w.grid, p.nf, p.g.off, p.g.G, a,
+                                            (XT*)out, d_status);
+      };
+      switch (p.es.w) {
+        case 9: go(std::integral_constant<int, 9>{}); break;
+        case 10: go(std::integral_constant<int, 10>{}); break;
+        case 11: go(std::integral_constant<int, 11>{}); break;
+        case 12: go(std::integral_constant<int, 12>{}); break;
+        case 13: go(std::integral_constant<int, 13>{}); break;
+        case 14: go(std::integral_constant<int, 14>{}); break;
+        case 15: go(std::integral_constant<int, 15>{}); break;
+        default: go(std::integral_constant<int, 16>{}); break;
+      }
+      FK_CUDA_TRY(cudaGetLastError());
+      count_launch();
+      return FK_OK;
+    }
     auto k = k_gather_es<XT>;
     if (p.smem) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
     const int per_sm = p.smem ? std::max(1, std::min(4, (int)(200000 / (p.smem + 1024)))) : 4;
