@@ -147,6 +147,44 @@ __global__ void __launch_bounds__(512) k_gather_bs3(const XT* __restrict__ Xq, i
   if (bad && d_status) atomicOr(d_status, (int)FK_E_RANGE);
 }
 
+// fp32, any layout (additive: nfeat grids), grids in shared memory as overlapping float2 pairs
+// (2 LDS.64 per feature instead of 4 LDS.32), 1024-thread CTAs
+template <bool EXACT>
+__global__ void __launch_bounds__(1024) k_gather_bs3_pairs(const float* __restrict__ Xq, int64_t n, int nfeat, int64_t sn, int64_t sd,
+                                                         const double* __restrict__ grid, int nf, int off, int G, float a_hi,
+                                                         float a_lo, float* __restrict__ out, int* __restrict__ d_status) {
+  extern __shared__ float2 sgq[];
+  for (int64_t i = threadIdx.x; i < (int64_t)nfeat * G; i += blockDim.x) {
+    const int f = (int)(i / G), c = (int)(i % G);
+    const double* gf = grid + (int64_t)f * nf + off;
+    sgq[i] = make_float2((float)gf[c], c + 1 < G ? (float)gf[c + 1] : 0.0f);
+  }
+  __syncthreads();
+  const int nq = nf / 4;
+  bool bad = false;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    float acc = 0.0f;
+    bool ok = true;
+    for (int f = 0; f < nfeat; ++f) {
+      int t;
+      float fr;
+      pos1_f32<EXACT>(Xq[j * sn + f * sd], a_hi, a_lo, nq, t, fr);
+      if ((unsigned)t > (unsigned)(G - 4)) {
+        ok = false;
+        continue;
+      }
+      float w[4];
+      bs3_float(fr, w);
+      const float2* c = sgq + (int64_t)f * G + t;
+      const float2 lo = c[0], hi = c[2];
+      acc += w[0] * lo.x + w[1] * lo.y + w[2] * hi.x + w[3] * hi.y;
+    }
+    if (!ok) bad = true;
+    out[j] = ok ? acc : NAN;
+  }
+  if (bad && d_status) atomicOr(d_status, (int)FK_E_RANGE);
+}
+
 // d = 1, fp32, contiguous 16-byte-aligned Xq / out, grid in smem: 4 queries per thread per step,
 // 128-bit streaming loads and stores (the scalar kernel above handles every other case)
 template <bool EXACT>
@@ -509,6 +547,22 @@ static fk_status gather(const PredPlan& p, const fk_points& Xq, double L, const 
       FK_CUDA_TRY(cudaGetLastError());
       count_launch();
       return FK_OK;
+    }
+    if (sizeof(XT) == 4 && p.in_smem) {
+      const size_t pair_smem = (size_t)p.nfeat * p.g.G * 8;
+      int optin = 0, dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+      if (pair_smem <= (size_t)optin) {
+        auto kp = exact ? k_gather_bs3_pairs<true> : k_gather_bs3_pairs<false>;
+        cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pair_smem);
+        const int ps = std::max(1, std::min(2, (int)(optin / (pair_smem + 1024))));
+        kp<<<sms * ps, 1024, pair_smem, s>>>((const float*)Xq.ptr, Xq.n, p.nfeat, Xq.stride_n, Xq.stride_d, w.grid, p.nf, p.g.off,
+                                             p.g.G, a_hi, a_lo, (float*)out, d_status);
+        FK_CUDA_TRY(cudaGetLastError());
+        count_launch();
+        return FK_OK;
+      }
     }
     auto k = exact ? k_gather_bs3<XT, true> : k_gather_bs3<XT, false>;
     if (p.smem) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
