@@ -152,3 +152,27 @@ def test_identical_samples_drain_2d(F, x0):
     a = np.exp(-1j * np.pi * k * np.float64(np.float32(x0[0])) / 2)[:, None]
     b = np.exp(+1j * np.pi * k * np.float64(np.float32(x0[1])) / 2)[None, :]
     assert rel(G[0], n * a * b) <= 1e-5
+
+
+@pytest.mark.parametrize("d,m,eps", [(1, 200, 1e-6), (1, 60, 1e-12), (2, 24, 1e-6), (2, 12, 1e-11)])
+def test_type1_type2_adjoint(F, d, m, eps):
+    """SURVEY P9 across the two GPU transforms: for Hermitian theta, <theta, r> = sum_k conj(theta_k)
+    r_k = sum_j Y_j conj(f_theta(X_j)) = sum_j Y_j f_theta(X_j) (f real), with r from fk_rhs_type1
+    and f from fk_predict_type2 at the same points."""
+    n = 200_000
+    X, Y = datagen.dataset(n, d=d, ykind="expcos" if d == 2 else "sin", seed=95)
+    X = X.reshape(-1) if d == 1 else X
+    t = torch.float32 if eps >= 1e-7 else torch.float64
+    Xd, Yd = dev(X, t), dev(Y, t)
+    rng = np.random.default_rng(7)
+    D = (2 * m + 1) ** d
+    th = rng.normal(size=D) + 1j * rng.normal(size=D)
+    th = (th + np.conj(th[::-1])) / 2  # Hermitian: theta_{-k} = conj theta_k (lexicographic reversal)
+    r, _ = F.fk_rhs_type1(Xd, Yd, 1.0, m, eps)
+    f = F.fk_predict_type2(dev(th), d, m, 1.0, Xd, eps)
+    lhs = np.sum(np.conj(th) * host(r).reshape(-1))
+    rhs = float(torch.dot(Yd.double(), f.double()))
+    scale = np.sum(np.abs(th)) * float(Yd.abs().sum())
+    print(f"adjoint d={d} m={m} eps={eps}: |lhs-rhs|/scale {abs(lhs - rhs) / scale:.2e}, imag {abs(lhs.imag) / scale:.1e}")
+    tol = 1e-6 if eps >= 1e-7 else 1e-11
+    assert abs(lhs - rhs) <= tol * scale
