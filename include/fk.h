@@ -32,7 +32,8 @@
  *   - Accuracy: eps is the requested relative l2 accuracy of each output vector against the
  *     exact sums (reading R7); valid range [1e-14, 1e-1].  eps >= 1e-7 selects the fp32
  *     spreading path (cubic B-spline window, fixed-point shared-memory accumulation); smaller eps
- *     selects the fp64 path (exponential-of-semicircle window, fp64 accumulation).
+ *     selects the fp64 mode (d = 1: septic B-spline window, 64-bit fixed-point accumulation;
+ *     d = 2 / cross moments: exponential-of-semicircle window, fp64 accumulation).
  */
 #ifndef FK_H
 #define FK_H

@@ -59,7 +59,7 @@ struct Bump {
 // ------------------------------------------------------------------------------------------
 // spreading plans
 // ------------------------------------------------------------------------------------------
-enum KerKind { KER_BS3 = 0, KER_ES = 1 };
+enum KerKind { KER_BS3 = 0, KER_ES = 1, KER_BS7 = 2 };  // BS7: septic B-spline, fp64 mode (spread1d.cu)
 
 // One fine grid of one channel along one dimension: period nf, cells [off, off + G) held locally.
 struct Geo {

@@ -119,6 +119,30 @@ fk_status make_plan1(int d, int m, double eps, bool need_mu, bool need_r, Plan1*
     }
   }
   if (!fp32) {
+    // fp64 mode, first choice: septic B-spline (8 taps, weights by the Cox-de Boor recursion: no
+    // transcendentals, no coefficient tables) at sigma with 2 (2 sigma - 1)^-8 ~ eps / 2, one
+    // channel per pass so each grid may use all of a CTA's shared memory (64-bit fixed point,
+    // 8 B per cell).  Falls back to the ES window when a grid does not fit (very small eps / large m).
+    const double s7 = std::max(4.0, 0.5 * (std::pow(4.0 / std::max(eps, 1e-300), 0.125) + 1.0));
+    const int nf7 = fft_friendly((int)std::ceil(s7 * modes_mu));
+    const size_t bA = (size_t)(nf7 / 2 + 8) * 8, bB = (size_t)(nf7 / 4 + 8) * 8;
+    const size_t need = std::max(need_mu ? bA : 0, need_r ? bB : 0);
+    if (eps >= 1e-13 && need + 1024 <= (size_t)smem_cap) {
+      q.ker = KER_BS7;
+      q.fp64 = true;
+      q.nf_mu = nf7;
+      q.nf_r = nf7 / 2;
+      q.gA = {q.nf_mu, q.nf_mu / 4 - 3, q.nf_mu / 2 + 8};
+      q.gB = {q.nf_r, q.nf_r / 4 - 3, q.nf_r / 2 + 8};
+      q.smem = true;
+      q.smem_bytes = need;
+      q.threads = 1024;
+      q.ctas = sms * std::max(1, std::min(2, (int)((smem_cap + 1024) / (need + 1024))));
+      *p = q;
+      return FK_OK;
+    }
+  }
+  if (!fp32) {
     q.ker = KER_ES;
     q.fp64 = true;
     int w = (int)std::ceil(std::log10(1.0 / eps)) + 2;

@@ -396,6 +396,117 @@ __global__ void __launch_bounds__(1024, 1) k_spread1d_esx(const XT* __restrict__
 }
 
 // ------------------------------------------------------------------------------------------
+// fp64 mode, septic B-spline (plan KER_BS7): one channel per pass (CH = 0 moments, 1 rhs), the
+// channel's occupied grid in shared memory as 64-bit fixed point (int32 pairs, pair_add), tap
+// weights by the uniform Cox-de Boor recursion in fp64 (28 steps, constants 1/j only).  Taps at
+// cells floor(p) - 3 .. floor(p) + 4 relative to the grid centre; transform sinc^8 (k_deconv1d).
+// Moments: the 8 integer weights are closed to 2^40 exactly (partition of unity: mu_0 = n).
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ void bs7_weights(double f, double* N) {
+  N[0] = 1.0;
+#pragma unroll
+  for (int j = 1; j <= 7; ++j) {
+    const double invj = 1.0 / j;  // folded at compile time
+    double saved = 0.0;
+#pragma unroll
+    for (int r = 0; r < j; ++r) {
+      const double temp = N[r] * invj;
+      N[r] = fma((double)(r + 1) - f, temp, saved);  // right[r+1] = r + 1 - f
+      saved = ((double)(j - r - 1) + f) * temp;      // left[j-r]  = f + j - r - 1
+    }
+    N[j] = saved;
+  }
+}
+
+struct Bs7Args {
+  int64_t n, stride, per;
+  double a;  // nf / (4L) of the channel's grid (moment grid: nf_mu; rhs grid: nf_r)
+  int nq, G;
+  double* part;
+  double* carry;
+  int* d_status;
+};
+
+template <typename XT, int CH>
+__global__ void __launch_bounds__(1024, 1) k_spread1d_bs7(const XT* __restrict__ X, const XT* __restrict__ Y, Bs7Args g) {
+  extern __shared__ unsigned sm7[];
+  unsigned* lo = sm7;
+  int* hi = (int*)(sm7 + g.G);
+  for (int i = threadIdx.x; i < 2 * g.G; i += blockDim.x) sm7[i] = 0u;
+  const int64_t beg = (int64_t)blockIdx.x * g.per;
+  const int64_t end = min(g.n, beg + g.per);
+  int E = 0;
+  if (CH == 1) {  // rhs scale 2^E with max |Y| 2^E in [2^19, 2^20) over the CTA's first samples
+    __shared__ double red[32];
+    __shared__ int sE;
+    double mx = 0.0;
+    const int64_t cnt = max((int64_t)0, min(end - beg, (int64_t)kYProbe));
+    for (int64_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+      const double a = fabs((double)Y[beg + i]);
+      if (a == a) mx = fmax(mx, a);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t = fmax(t, red[w]);
+      int e2 = 0, Eloc = 19;
+      if (t > 0.0 && t < 1e300) {
+        frexp(t, &e2);
+        Eloc = 20 - e2;
+      }
+      sE = max(-900, min(900, Eloc));
+    }
+    __syncthreads();
+    E = sE;
+  }
+  __syncthreads();
+  const double sy = CH == 1 ? ldexp(1.0, E) : 0.0;
+  const double unit = CH == 0 ? 4294967296.0 / kSX : ldexp(4294967296.0, -(E + 20));
+  bool bad = false;
+  for (int64_t j = beg + threadIdx.x; j < end; j += blockDim.x) {
+    const double p = (double)X[j * g.stride] * g.a;
+    const double fl = floor(p);
+    const double f = p - fl;
+    const int t0 = (p == p && fabs(p) < 1e9) ? (int)fl + g.nq : -1;
+    if ((unsigned)t0 > (unsigned)(g.G - 8)) {
+      bad = true;
+      continue;
+    }
+    double wv[8];
+    bs7_weights(f, wv);
+    if (CH == 0) {
+      long long q[8], sum = 0;
+#pragma unroll
+      for (int i = 0; i < 7; ++i) {
+        q[i] = __double2ll_rn(wv[i] * kSX);
+        sum += q[i];
+      }
+      q[7] = (long long)kSX - sum;  // partition of unity closed in integers
+#pragma unroll
+      for (int i = 0; i < 8; ++i) pair_add(lo, hi, t0 + i, q[i], g.carry, unit);
+    } else {
+      const double y = (double)Y[j];
+      const double ys = y * sy;
+      if (fabs(ys) < 2097152.0) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) pair_add(lo, hi, t0 + i, __double2ll_rn(wv[i] * ys * 1048576.0), g.carry, unit);
+      } else {  // |Y| outlier or NaN: exact fp64 into the carry grid
+#pragma unroll 1
+        for (int i = 0; i < 8; ++i) atomicAdd(g.carry + t0 + i, y * wv[i]);
+      }
+    }
+  }
+  if (bad && g.d_status) atomicOr(g.d_status, (int)FK_E_RANGE);
+  __syncthreads();
+  double* dst = g.part + (int64_t)blockIdx.x * g.G;
+  const double sc = CH == 0 ? 1.0 / kSX : ldexp(1.0, -(E + 20));
+  for (int i = threadIdx.x; i < g.G; i += blockDim.x) dst[i] = ((double)hi[i] * 4294967296.0 + (double)lo[i]) * sc;
+}
+
+// ------------------------------------------------------------------------------------------
 // per-CTA partial grids -> one fp64 fine grid (full period, zero outside the occupied band),
 // summed over CTAs in a fixed order (the fixed-point path is exact, hence bitwise deterministic)
 // ------------------------------------------------------------------------------------------
@@ -444,6 +555,10 @@ __global__ void k_deconv1d(const double2* __restrict__ F, int nf, int K, int ker
   if (ker == KER_BS3) {
     const double s = sinc_pi((double)aq / nf);
     ph = (s * s) * (s * s);
+  } else if (ker == KER_BS7) {
+    const double s = sinc_pi((double)aq / nf);
+    const double s2 = s * s, s4 = s2 * s2;
+    ph = s4 * s4;
   } else {
     ph = tab[aq];
   }
@@ -573,6 +688,31 @@ static fk_status spread_dispatch(const Plan1& p, const fk_points& Xp, const void
   const XT* X = (const XT*)Xp.ptr;
   const XT* Y = (const XT*)Yv;
   const int64_t n = Xp.n;
+  if (p.ker == KER_BS7) {  // one pass per channel
+    for (int ch = 0; ch < 2; ++ch) {
+      if ((ch == 0 && !mu) || (ch == 1 && !r)) continue;
+      Bs7Args a{};
+      a.n = n;
+      a.stride = Xp.stride_n;
+      a.per = (n + p.ctas - 1) / p.ctas;
+      const Geo& gg = ch == 0 ? p.gA : p.gB;
+      a.a = (double)gg.nf / (4.0 * L);
+      a.nq = gg.nf / 4;
+      a.G = gg.G;
+      a.part = (double*)(ch == 0 ? w.partA : w.partB);
+      a.carry = ch == 0 ? w.carryA : w.carryB;
+      a.d_status = d_status;
+      const size_t smem = (size_t)gg.G * 8;
+      auto k = ch == 0 ? k_spread1d_bs7<XT, 0> : k_spread1d_bs7<XT, 1>;
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      prof_spread_begin(s);
+      k<<<p.ctas, p.threads, smem, s>>>(X, Y, a);
+      prof_spread_end(s);
+      count_launch();
+    }
+    FK_CUDA_TRY(cudaGetLastError());
+    return FK_OK;
+  }
   if (!p.fp64) {
     Bs3Args a{};
     a.n = n;

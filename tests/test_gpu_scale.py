@@ -127,3 +127,25 @@ def test_workspace_too_small_is_reported(F):
                                   ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
     assert st == F.FK_E_WORKSPACE
     assert b"workspace" in F.lib().fk_last_error()
+
+
+@pytest.mark.parametrize("eps", [1e-6, 1e-10])
+def test_identical_samples_many_drains(F, eps):
+    """2^29 identical samples: in every CTA each touched cell overflows its fixed-point range many
+    times over (int32 cells at eps = 1e-6; the high words of the 64-bit fixed point at eps = 1e-10),
+    so the drains into the fp64 carry grids carry the result.  Closed form mu_q = n e^{-i q t0},
+    r_k = 1.5 n e^{-i k t0}."""
+    n, m, x0 = 1 << 29, 300, 0.3
+    X = torch.full((n,), x0, dtype=torch.float32, device="cuda")
+    Y = torch.full((n,), 1.5, dtype=torch.float32, device="cuda")
+    r, mu = F.fk_rhs_type1(X, Y, 1.0, m, eps)
+    t0 = np.pi * np.float64(np.float32(x0)) / 2
+    q = np.arange(-2 * m, 2 * m + 1)
+    k = np.arange(-m, m + 1)
+    mu_cf = n * np.exp(-1j * q * t0)
+    r_cf = 1.5 * n * np.exp(-1j * k * t0)
+    tol = 1e-5 if eps >= 1e-7 else 1e-10
+    e_mu, e_r = rel(host(mu), mu_cf), rel(host(r), r_cf)
+    print(f"identical n=2^29 eps={eps}: mu {e_mu:.2e} r {e_r:.2e}")
+    assert e_mu <= tol and e_r <= tol
+    del X, Y
