@@ -57,14 +57,26 @@ static fk_status make_pred_plan(int d, int m, double eps, int additive, PredPlan
     q.g = {q.nf, q.nf / 4 - 1, q.nf / 2 + 4};
     q.smem = (size_t)q.nfeat * q.g.G * 4;
   } else {
-    q.ker = KER_ES;
-    int w = (int)std::ceil(std::log10(1.0 / eps)) + 2;
-    w = std::min(16, std::max(4, w));
-    q.es.w = w;
-    q.es.beta = 2.30 * w;
-    q.nf = fft_friendly(std::max(2 * (2 * m + 1), 2 * w + 8));  // grid must not wrap (small m)
-    q.g = {q.nf, q.nf / 4 - w / 2 - 2, q.nf / 2 + w + 4};
-    q.smem = (size_t)q.nfeat * q.g.G * 8;
+    // fp64: septic B-spline (8 taps, Cox-de Boor weights, sinc^8 transform) when its grids fit in
+    // shared memory, as in the type-1 fp64 mode; else the ES window
+    const double s7 = std::max(4.0, 0.5 * (std::pow(4.0 / std::max(eps, 1e-300), 0.125) + 1.0));
+    const int nf7 = fft_friendly((int)std::ceil(s7 * (2 * m + 1)));
+    const size_t b7 = (size_t)q.nfeat * (nf7 / 2 + 8) * 8;
+    if (eps >= 1e-13 && b7 <= (size_t)smem_cap) {
+      q.ker = KER_BS7;
+      q.nf = nf7;
+      q.g = {q.nf, q.nf / 4 - 3, q.nf / 2 + 8};
+      q.smem = b7;
+    } else {
+      q.ker = KER_ES;
+      int w = (int)std::ceil(std::log10(1.0 / eps)) + 2;
+      w = std::min(16, std::max(4, w));
+      q.es.w = w;
+      q.es.beta = 2.30 * w;
+      q.nf = fft_friendly(std::max(2 * (2 * m + 1), 2 * w + 8));  // grid must not wrap (small m)
+      q.g = {q.nf, q.nf / 4 - w / 2 - 2, q.nf / 2 + w + 4};
+      q.smem = (size_t)q.nfeat * q.g.G * 8;
+    }
   }
   q.in_smem = q.smem <= (size_t)smem_cap;
   if (!q.in_smem) q.smem = 0;
@@ -83,9 +95,10 @@ __global__ void k_pred_prep(const double2* __restrict__ theta, int nfeat, int m,
     const double2 a = theta[(int64_t)f * (2 * m + 1) + m + k];
     const double2 b = theta[(int64_t)f * (2 * m + 1) + m - k];
     double ph;
-    if (ker == KER_BS3) {
+    if (ker == KER_BS3 || ker == KER_BS7) {
       const double s = sinc_pi((double)k / nf);
       ph = (s * s) * (s * s);
+      if (ker == KER_BS7) ph *= ph;
     } else {
       ph = tab[k];
     }
@@ -257,6 +270,58 @@ __global__ void __launch_bounds__(1024) k_gather_bs3_pair(const float4* __restri
   for (; j < n4; j += stride) {
     const float4 xa = __ldcs(Xq4 + j);
     __stcs(out4 + j, make_float4(one(xa.x), one(xa.y), one(xa.z), one(xa.w)));
+  }
+  if (bad && d_status) atomicOr(d_status, (int)FK_E_RANGE);
+}
+
+// fp64 gather with the septic B-spline (d = 1 or additive, grids in shared memory)
+__device__ __forceinline__ void bs7_w(double f, double* N) {
+  N[0] = 1.0;
+#pragma unroll
+  for (int j = 1; j <= 7; ++j) {
+    const double invj = 1.0 / j;
+    double saved = 0.0;
+#pragma unroll
+    for (int r = 0; r < j; ++r) {
+      const double temp = N[r] * invj;
+      N[r] = fma((double)(r + 1) - f, temp, saved);
+      saved = ((double)(j - r - 1) + f) * temp;
+    }
+    N[j] = saved;
+  }
+}
+
+template <typename XT>
+__global__ void __launch_bounds__(512) k_gather_bs7(const XT* __restrict__ Xq, int64_t n, int nfeat, int64_t sn, int64_t sd,
+                                                   const double* __restrict__ grid, int nf, int off, int G, double a,
+                                                   XT* __restrict__ out, int* __restrict__ d_status) {
+  extern __shared__ double sg7[];
+  for (int64_t i = threadIdx.x; i < (int64_t)nfeat * G; i += blockDim.x) {
+    const int f = (int)(i / G), c = (int)(i % G);
+    sg7[i] = grid[(int64_t)f * nf + off + c];
+  }
+  __syncthreads();
+  const int nq = nf / 4;
+  bool bad = false;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    bool ok = true;
+    for (int f = 0; f < nfeat; ++f) {
+      const double p = (double)Xq[j * sn + f * sd] * a;
+      const double fl = floor(p);
+      const int t0 = (p == p && fabs(p) < 1e9) ? (int)fl + nq : -1;
+      if ((unsigned)t0 > (unsigned)(G - 8)) {
+        ok = false;
+        continue;
+      }
+      double w[8];
+      bs7_w(p - fl, w);
+      const double* c = sg7 + (int64_t)f * G + t0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc = fma(w[i], c[i], acc);
+    }
+    bad |= !ok;
+    out[j] = ok ? (XT)acc : (XT)NAN;
   }
   if (bad && d_status) atomicOr(d_status, (int)FK_E_RANGE);
 }
@@ -568,6 +633,12 @@ static fk_status gather(const PredPlan& p, const fk_points& Xq, double L, const 
     if (p.smem) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
     k<<<sms * per_sm, 512, p.smem, s>>>((const XT*)Xq.ptr, Xq.n, p.nfeat, Xq.stride_n, Xq.stride_d, w.grid, p.nf, p.g.off, p.g.G,
                                         a_hi, a_lo, a, p.in_smem ? 1 : 0, (XT*)out, d_status);
+  } else if (p.ker == KER_BS7) {
+    auto k = k_gather_bs7<XT>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+    const int per_sm = std::max(1, std::min(4, (int)(200000 / (p.smem + 1024))));
+    k<<<sms * per_sm, 512, p.smem, s>>>((const XT*)Xq.ptr, Xq.n, p.nfeat, Xq.stride_n, Xq.stride_d, w.grid, p.nf, p.g.off, p.g.G, a,
+                                        (XT*)out, d_status);
   } else {
     const double* coef = nullptr;
     if (p.in_smem && p.es.w >= 9 && es_horner_table(p.es, &coef) == FK_OK &&
