@@ -459,7 +459,7 @@ def run_e2e(args, cfg, dev, eps):
     ms = e0.elapsed_time(e1) / steps
     return {"value": n / (ms * 1e-3), "unit": "samples/s", "h2d_bytes_per_step": n * (d + 1) * 4, "d2h_bytes_per_step": D * 16,
             "n": n, "ms_per_step": ms,
-            "path": "fit.HostStreamer + fk_solve: pinned host X,Y -> chunked H2D on a copy stream overlapped with fk_rhs_type1; theta D2H"}
+            "path": "fit.HostStreamer + fk_solve: pinned host X,Y -> chunked H2D (X and Y on two copy streams) overlapped with fk_rhs_type1; theta D2H; bound by the PCIe link (~55 GB/s)"}
 
 
 if __name__ == "__main__":

@@ -164,8 +164,9 @@ def grid_search(X: torch.Tensor, Y: torch.Tensor, X_val: torch.Tensor, Y_val: to
 
 
 class HostStreamer:
-    """Streams pinned host (X, Y) to the device in fixed-size chunks, double-buffered on a copy
-    stream, and runs the one-pass moments + rhs on each chunk as it lands."""
+    """Streams pinned host (X, Y) to the device in fixed-size chunks, double-buffered, X and Y on
+    two copy streams (both DMA engines), and runs the one-pass moments + rhs on each chunk as it
+    lands (FK_ACCUMULATE across chunks)."""
 
     def __init__(self, chunk: int, d: int, dtype, device):
         self.chunk = chunk
@@ -173,8 +174,8 @@ class HostStreamer:
         shape = (chunk,) if d == 1 else (chunk, d)
         self.xb = [torch.empty(shape, dtype=dtype, device=device) for _ in range(2)]
         self.yb = [torch.empty(chunk, dtype=dtype, device=device) for _ in range(2)]
-        self.copy_stream = torch.cuda.Stream(device)
-        self.copied = [torch.cuda.Event() for _ in range(2)]
+        self.copy_streams = [torch.cuda.Stream(device), torch.cuda.Stream(device)]
+        self.copied = [[torch.cuda.Event() for _ in range(2)] for _ in range(2)]
         self.consumed = [torch.cuda.Event() for _ in range(2)]
 
     def moments(self, Xh: torch.Tensor, Yh: torch.Tensor, L: float, m: int, eps: float, mu, r):
@@ -184,13 +185,14 @@ class HostStreamer:
         for i in range(nchunks):
             b = i & 1
             lo, hi = i * self.chunk, min(n, (i + 1) * self.chunk)
-            with torch.cuda.stream(self.copy_stream):
-                if i >= 2:
-                    self.copy_stream.wait_event(self.consumed[b])
-                self.xb[b][: hi - lo].copy_(Xh[lo:hi], non_blocking=True)
-                self.yb[b][: hi - lo].copy_(Yh[lo:hi], non_blocking=True)
-                self.copied[b].record(self.copy_stream)
-            comp.wait_event(self.copied[b])
+            for c, (dst, src) in enumerate(((self.xb[b], Xh), (self.yb[b], Yh))):
+                cs = self.copy_streams[c]
+                with torch.cuda.stream(cs):
+                    if i >= 2:
+                        cs.wait_event(self.consumed[b])
+                    dst[: hi - lo].copy_(src[lo:hi], non_blocking=True)
+                    self.copied[c][b].record(cs)
+                comp.wait_event(self.copied[c][b])
             fk.fk_rhs_type1(self.xb[b][: hi - lo], self.yb[b][: hi - lo], L, m, eps, r_out=r, mu_out=mu, accumulate=i > 0,
                             check=False)
             self.consumed[b].record(comp)
