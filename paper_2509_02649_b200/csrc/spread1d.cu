@@ -288,23 +288,6 @@ __device__ __forceinline__ double es_tap_const(double sv, int i) {
 // shared-memory atomicAdd (a CAS loop on sm_100a; scratch microbenchmark 1.31e12 vs 4.2e11 tap
 // adds/s).  Tap weights x 2^40 (rounding 2^-41, far below the 1e-10 target); a hi word that
 // reaches 2^29 in magnitude is drained (atomicExch) into an fp64 carry grid, so no overflow.
-constexpr double kSX = 1099511627776.0;  // 2^40
-
-__device__ __forceinline__ void pair_add(unsigned* __restrict__ lo, int* __restrict__ hi, int c, long long v, double* carry,
-                                         double hi_unit) {
-  const unsigned l = (unsigned)v;
-  const int h = (int)(v >> 32);
-  const unsigned o = atomicAdd(lo + c, l);
-  const int hc = h + ((o + l) < o ? 1 : 0);
-  if (hc != 0) {
-    const int oh = atomicAdd(hi + c, hc);
-    if ((unsigned)(oh + hc + (1 << 29)) >= (1u << 30)) {
-      const int t = atomicExch(hi + c, 0);
-      if (t) atomicAdd(carry + c, (double)t * hi_unit);
-    }
-  }
-}
-
 template <typename XT, bool MU, bool R, int W>
 __global__ void __launch_bounds__(1024, 1) k_spread1d_esx(const XT* __restrict__ X, const XT* __restrict__ Y, EsArgs g) {
   extern __shared__ unsigned smx[];

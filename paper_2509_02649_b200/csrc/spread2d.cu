@@ -440,20 +440,22 @@ __global__ void __launch_bounds__(1024) k_cross2d_fixed(const float* __restrict_
   for (int i = threadIdx.x; i < np * cells; i += blockDim.x) dst[i] = smx[i];
 }
 
+// fp64-accuracy cross moments: unit weights, 64-bit fixed point (pair_add) in shared memory,
+// 1024-thread CTAs (a pair grid of 124^2 cells x 8 B leaves room for one CTA per SM)
 template <int W, typename XT>
-__global__ void __launch_bounds__(256) k_cross2d_f64(const XT* __restrict__ X, const ArgsX* __restrict__ gp) {
-  extern __shared__ double smxd[];
+__global__ void __launch_bounds__(1024, 1) k_cross2d_f64(const XT* __restrict__ X, const ArgsX* __restrict__ gp) {
+  extern __shared__ unsigned smxp[];
   const ArgsX& g = *gp;
   const int grp = blockIdx.x % g.ngroups;
   const int chunk = blockIdx.x / g.ngroups;
   const int p0 = grp * g.per_cta;
   const int np = min(g.per_cta, g.npairs - p0);
   const int cells = g.G * g.G;
-  for (int i = threadIdx.x; i < np * cells; i += blockDim.x) smxd[i] = 0.0;
+  for (int i = threadIdx.x; i < 2 * np * cells; i += blockDim.x) smxp[i] = 0u;
   __syncthreads();
   const int64_t beg = (int64_t)chunk * g.per;
   const int64_t end = min(g.n, beg + g.per);
-  Tile t{g.G, g.K, g.G, g.G};
+  const double unit = 4294967296.0 / kSX;
   bool bad = false;
   double px[W], py[W];
   for (int64_t j = beg + threadIdx.x; j < end; j += blockDim.x) {
@@ -474,13 +476,27 @@ __global__ void __launch_bounds__(256) k_cross2d_f64(const XT* __restrict__ X, c
       }
       es_taps_f64<W>(fa, d00, g.beta_d, py);
       es_taps_f64<W>(fb, d01, g.beta_d, px);
-      spread_f64<W>(smxd + q * cells, t, lr, lc, py, px, 1.0, 0);
+      unsigned* lo = smxp + 2 * q * cells;
+      int* hi = (int*)(lo + cells);
+      double* carry = g.carry + (int64_t)(p0 + q) * cells;
+#pragma unroll
+      for (int a = 0; a < W; ++a) {
+        const double wy = py[a] * kSX;
+        const int rowc = (lr + a) * g.G + lc;
+#pragma unroll
+        for (int b = 0; b < W; ++b) pair_add(lo, hi, rowc + b, __double2ll_rn(wy * px[b]), carry, unit);
+      }
     }
   }
   if (bad && g.d_status) atomicOr(g.d_status, (int)FK_E_RANGE);
   __syncthreads();
   double* dst = (double*)g.part + ((int64_t)chunk * g.npairs + p0) * cells;
-  for (int i = threadIdx.x; i < np * cells; i += blockDim.x) dst[i] = smxd[i];
+  for (int i = threadIdx.x; i < np * cells; i += blockDim.x) {
+    const int q = i / cells, c = i % cells;
+    const unsigned* lo = smxp + 2 * q * cells;
+    const int* hi = (const int*)(lo + cells);
+    dst[i] = ((double)hi[c] * 4294967296.0 + (double)lo[c]) / kSX;
+  }
 }
 
 // ------------------------------------------------------------------------------------------
@@ -951,8 +967,8 @@ fk_status cross_run(const fk_points& X, double L, int m, double eps, double* G, 
     } else {
       auto byw = [&](auto wtag) {
         constexpr int WW = decltype(wtag)::value;
-        if (X.dtype == FK_F32) go(k_cross2d_f64<WW, float>, (const float*)X.ptr, 256);  // fp32 points, fp64 accuracy
-        else go(k_cross2d_f64<WW, double>, (const double*)X.ptr, 256);
+        if (X.dtype == FK_F32) go(k_cross2d_f64<WW, float>, (const float*)X.ptr, 1024);  // fp32 points, fp64 accuracy
+        else go(k_cross2d_f64<WW, double>, (const double*)X.ptr, 1024);
       };
       dispatch_w64(p.w, byw);
     }
@@ -965,7 +981,7 @@ fk_status cross_run(const fk_points& X, double L, int m, double eps, double* G, 
   const int64_t tot = (int64_t)p.npairs * p.nf * p.nf;
   // part layout: [chunk][pair][G][G] -> batch stride G*G, "cta" stride npairs*G*G, T = 1
   k_reduce2d<<<(unsigned)((tot + TB - 1) / TB), TB, 0, s>>>(part, fixed ? 1 : 0, nullptr, p.chunks, 1, p.G, p.G, p.G, p.off, p.nf,
-                                                           kInvS2, fixed ? carry : nullptr, fine, p.npairs, (int64_t)p.G * p.G,
+                                                           kInvS2, carry, fine, p.npairs, (int64_t)p.G * p.G,
                                                            (int64_t)p.npairs * p.G * p.G);
   FK_CUDA_TRY(cudaGetLastError());
   FftPlan fp;
