@@ -320,20 +320,54 @@ __global__ void __launch_bounds__(1024) k_spread2d_fixed(const float* __restrict
   }
 }
 
-// fp64 path (any input dtype): fp64 window, fp64 smem atomics
+// fp64 path (any input dtype): fp64 window, 64-bit fixed point (pair_add; weights x 2^40, rhs with
+// a per-CTA power-of-two scale of Y, |Y| outliers exact in fp64 into the carry grid), 1024 threads
 template <int W, typename XT>
-__global__ void __launch_bounds__(256) k_spread2d_f64(const XT* __restrict__ X, const XT* __restrict__ Y, Args2 g, bool MU, bool R) {
-  extern __shared__ double smd2[];
-  double* A = smd2;
-  double* B = smd2 + (MU ? g.gA.rows * g.gA.G : 0);
+__global__ void __launch_bounds__(1024, 1) k_spread2d_f64(const XT* __restrict__ X, const XT* __restrict__ Y, Args2 g, bool MU, bool R) {
+  extern __shared__ unsigned smp2[];
+  const int cellsA = MU ? g.gA.rows * g.gA.G : 0, cellsB = R ? g.gB.rows * g.gB.G : 0;
+  unsigned* Alo = smp2;
+  int* Ahi = (int*)(Alo + cellsA);
+  unsigned* Blo = smp2 + 2 * cellsA;
+  int* Bhi = (int*)(Blo + cellsB);
   const int tile = blockIdx.x % g.T;
   const int chunk = blockIdx.x / g.T;
-  const int nsm = (MU ? g.gA.rows * g.gA.G : 0) + (R ? g.gB.rows * g.gB.G : 0);
-  for (int i = threadIdx.x; i < nsm; i += blockDim.x) smd2[i] = 0.0;
-  __syncthreads();
+  for (int i = threadIdx.x; i < 2 * (cellsA + cellsB); i += blockDim.x) smp2[i] = 0u;
   const int64_t beg = (int64_t)chunk * g.per;
   const int64_t end = min(g.n, beg + g.per);
+  int E = 0;
+  if (R) {  // rhs scale 2^E with max |Y| 2^E in [2^19, 2^20) over the chunk's first samples
+    __shared__ double red[32];
+    __shared__ int sE;
+    double mx = 0.0;
+    const int64_t cnt = max((int64_t)0, min(end - beg, (int64_t)4096));
+    for (int64_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+      const double v = fabs((double)Y[beg + i]);
+      if (v == v) mx = fmax(mx, v);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t = fmax(t, red[w]);
+      int e2 = 0, Eloc = 19;
+      if (t > 0.0 && t < 1e300) {
+        frexp(t, &e2);
+        Eloc = 20 - e2;
+      }
+      sE = max(-900, min(900, Eloc));
+    }
+    __syncthreads();
+    E = sE;
+  }
+  __syncthreads();
+  const double sy = R ? ldexp(1.0, E) : 0.0;
+  const double unitA = 4294967296.0 / kSX, unitB = R ? ldexp(4294967296.0, -(E + 20)) : 0.0;
   const int rA0 = tile * g.gA.R, rB0 = tile * g.gB.R;
+  double* carA = g.carryA ? g.carryA + (int64_t)rA0 * g.gA.G : nullptr;  // local cell index -> global carry
+  double* carB = g.carryB ? g.carryB + (int64_t)rB0 * g.gB.G : nullptr;
   bool bad = false;
   double px[W], py[W];
   for (int64_t j = beg + threadIdx.x; j < end; j += blockDim.x) {
@@ -355,7 +389,13 @@ __global__ void __launch_bounds__(256) k_spread2d_f64(const XT* __restrict__ X, 
     if (MU && lrA >= rA0 && lrA < rA0 + g.gA.R) {
       es_taps_f64<W>(f0, d00, g.beta_d, py);
       es_taps_f64<W>(f1, d01, g.beta_d, px);
-      spread_f64<W>(A, g.gA, lrA, lcA, py, px, 1.0, rA0);
+#pragma unroll
+      for (int a = 0; a < W; ++a) {
+        const double wy = py[a] * kSX;
+        const int rowc = (lrA - rA0 + a) * g.gA.G + lcA;
+#pragma unroll
+        for (int b = 0; b < W; ++b) pair_add(Alo, Ahi, rowc + b, __double2ll_rn(wy * px[b]), carA, unitA);
+      }
     }
     if (R) {
       const double h0 = 0.5 * p0, h1 = 0.5 * p1;
@@ -367,19 +407,33 @@ __global__ void __launch_bounds__(256) k_spread2d_f64(const XT* __restrict__ X, 
       if (lrB >= rB0 && lrB < rB0 + g.gB.R) {
         es_taps_f64<W>(g0, e0, g.beta_d, py);
         es_taps_f64<W>(g1, e1, g.beta_d, px);
-        spread_f64<W>(B, g.gB, lrB, lcB, py, px, (double)Y[j], rB0);
+        const double y = (double)Y[j];
+        const double ys = y * sy;
+        if (fabs(ys) < 2097152.0) {
+#pragma unroll
+          for (int a = 0; a < W; ++a) {
+            const double wy = py[a] * ys * 1048576.0;
+            const int rowc = (lrB - rB0 + a) * g.gB.G + lcB;
+#pragma unroll
+            for (int b = 0; b < W; ++b) pair_add(Blo, Bhi, rowc + b, __double2ll_rn(wy * px[b]), carB, unitB);
+          }
+        } else {  // |Y| outlier or NaN: exact fp64 into the carry grid
+          for (int a = 0; a < W; ++a)
+            for (int b = 0; b < W; ++b) atomicAdd(carB + (lrB - rB0 + a) * g.gB.G + lcB + b, y * py[a] * px[b]);
+        }
       }
     }
   }
   if (bad && g.d_status) atomicOr(g.d_status, (int)FK_E_RANGE);
   __syncthreads();
   if (MU) {
-    double* dst = (double*)g.partA + (int64_t)blockIdx.x * g.gA.rows * g.gA.G;
-    for (int i = threadIdx.x; i < g.gA.rows * g.gA.G; i += blockDim.x) dst[i] = A[i];
+    double* dst = (double*)g.partA + (int64_t)blockIdx.x * cellsA;
+    for (int i = threadIdx.x; i < cellsA; i += blockDim.x) dst[i] = ((double)Ahi[i] * 4294967296.0 + (double)Alo[i]) / kSX;
   }
   if (R) {
-    double* dst = (double*)g.partB + (int64_t)blockIdx.x * g.gB.rows * g.gB.G;
-    for (int i = threadIdx.x; i < g.gB.rows * g.gB.G; i += blockDim.x) dst[i] = B[i];
+    double* dst = (double*)g.partB + (int64_t)blockIdx.x * cellsB;
+    const double sc = ldexp(1.0, -(E + 20));
+    for (int i = threadIdx.x; i < cellsB; i += blockDim.x) dst[i] = ((double)Bhi[i] * 4294967296.0 + (double)Blo[i]) * sc;
   }
 }
 
@@ -645,7 +699,7 @@ static fk_status make_plan2(int m, double eps, bool mu, bool r, int dtype, Plan2
     }
   }
   if (q.T == 0) return fail(FK_E_UNSUPPORTED, "d=2 grid too large for 64 row tiles");
-  q.threads = q.fp64 ? 256 : 1024;
+  q.threads = 1024;
   const int sms = device_sm_count();
   const int per_sm = std::max(1, std::min(4, (int)(cap / (q.smem + 1024))));
   q.chunks = std::max(1, (sms * per_sm) / q.T);
@@ -681,7 +735,7 @@ static fk_status layout2(const Plan2& p, bool mu, bool r, Bump& b, Ws2& w) {
     w.fineA = (double*)b.take((size_t)p.nfA * p.nfA * 8);
     w.specA = (double2*)b.take((size_t)p.nfA * (p.nfA / 2 + 1) * 16);
     w.tabA = (double*)b.take((size_t)(2 * p.m + 1) * 8);
-    if (!p.fp64) w.carryA = (double*)b.take((size_t)p.gA.G * p.gA.G * 8);
+    w.carryA = (double*)b.take((size_t)p.gA.G * p.gA.G * 8);  // fixed point: drained cells (both paths)
   }
   if (r) {
     FK_TRY(fft_plan(2, dB, 1, CUFFT_D2Z, &pb));
@@ -690,10 +744,8 @@ static fk_status layout2(const Plan2& p, bool mu, bool r, Bump& b, Ws2& w) {
     w.fineB = (double*)b.take((size_t)p.nfB * p.nfB * 8);
     w.specB = (double2*)b.take((size_t)p.nfB * (p.nfB / 2 + 1) * 16);
     w.tabB = (double*)b.take((size_t)(p.m + 1) * 8);
-    if (!p.fp64) {
-      w.carryB = (double*)b.take((size_t)p.gB.G * p.gB.G * 8);
-      w.escale = (int*)b.take((size_t)ctas * 4);
-    }
+    w.carryB = (double*)b.take((size_t)p.gB.G * p.gB.G * 8);
+    if (!p.fp64) w.escale = (int*)b.take((size_t)ctas * 4);
   }
   w.work = b.take(std::max<size_t>(fw, 256));
   return FK_OK;
@@ -798,7 +850,7 @@ fk_status type1_2d_run(int m, double eps, const fk_points& X, const void* Y, dou
                     int K, double* out) -> fk_status {
     const int64_t tot = (int64_t)nf * nf;
     k_reduce2d<<<(unsigned)((tot + TB - 1) / TB), TB, 0, s>>>(part, fixed ? 1 : 0, esc, p.chunks, p.T, g.R, g.rows, g.G, off, nf,
-                                                             kInvS2, fixed ? carry : nullptr, fine, 1, 0,
+                                                             kInvS2, carry, fine, 1, 0,
                                                              (int64_t)g.rows * g.G);
     FK_CUDA_TRY(cudaGetLastError());
     FftPlan fp;
