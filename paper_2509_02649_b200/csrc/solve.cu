@@ -344,11 +344,81 @@ __global__ void k_assemble_real_d1(SysArgs g, double* __restrict__ M) {
   M[u + v * N] = e;
 }
 
+// d = 2, non-additive kinds: the complex entry with the mode decode done by one fp32 reciprocal
+// multiply + fix-up (no integer division) and the PI terms from the tabulated symbols / box
+// integrals.  The generic path spent ~500 us on D = 4225 (C4) in 16 integer divisions and the
+// general PDE branches per real entry.
+struct K2 {
+  int a, b;
+};
+__device__ __forceinline__ K2 decode2(int i, int side, float inv_side, int m) {
+  int q = __float2int_rz((float)i * inv_side);
+  int r = i - q * side;
+  if (r < 0) {
+    --q;
+    r += side;
+  } else if (r >= side) {
+    ++q;
+    r -= side;
+  }
+  return K2{q - m, r - m};
+}
+
+__device__ __forceinline__ double2 entry_d2(const SysArgs& g, int i, int j, int side, float inv_side) {
+  const K2 k1 = decode2(i, side, inv_side, g.m), k2 = decode2(j, side, inv_side, g.m);
+  const int qside = 4 * g.m + 1;
+  const int qi = (k1.a - k2.a + 2 * g.m) * qside + (k1.b - k2.b + 2 * g.m);
+  double2 v = g.mu[qi];
+  v.x *= g.inv_n;
+  v.y *= g.inv_n;
+  if (i == j) {
+    double R = 1.0;
+    if (g.kind != FK_LOWBIAS) R = 1.0 + pow((double)(k1.a * k1.a + k1.b * k1.b), g.s);
+    v.x += g.lambda * R;
+  }
+  if (g.mu_pde != 0.0 && (g.kind == FK_PIK_BOX || g.kind == FK_PIK_COLLOC)) {
+    double2 t;
+    if (g.kind == FK_PIK_BOX) {
+      const double2 b = cmul(g.boxt[k2.a - k1.a + 2 * g.m], g.boxt[qside + (k2.b - k1.b + 2 * g.m)]);
+      t = cmul(cmul(cconj(g.dsym[i]), b), g.dsym[j]);
+    } else {
+      double2 tr = g.mur[qi];
+      tr.x *= g.inv_nr;
+      tr.y *= g.inv_nr;
+      t = cmul(cmul(cconj(g.dsym[i]), tr), g.dsym[j]);
+    }
+    v.x += g.mu_pde * t.x;
+    v.y += g.mu_pde * t.y;
+  }
+  return v;
+}
+
+__global__ void k_assemble_real_d2(SysArgs g, double* __restrict__ M) {
+  const int64_t N = g.D + 1;
+  const int v = blockIdx.y;
+  const int u = v + blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= g.D) return;
+  const int side = 2 * g.m + 1;
+  const float inv_side = 1.0f / (float)side;
+  const PCol pu = pcol(g, u), pv = pcol(g, v);
+  double s = 0.0;
+  for (int x = 0; x < pu.cnt; ++x)
+    for (int y = 0; y < pv.cnt; ++y) {
+      const double2 a = entry_d2(g, pu.i[x], pv.i[y], side, inv_side);
+      const double2 c = cmul(cmul(cconj(pu.a[x]), a), pv.a[y]);
+      s += c.x;
+    }
+  M[u + v * N] = s;
+}
+
 void launch_assemble(const SysArgs& g, double* M, cudaStream_t s) {
+  const dim3 grid((g.D + 255) / 256, g.D);
   if (g.d == 1 && (g.kind == FK_SOBOLEV || g.kind == FK_LOWBIAS))
-    k_assemble_real_d1<<<dim3((g.D + 255) / 256, g.D), 256, 0, s>>>(g, M);
+    k_assemble_real_d1<<<grid, 256, 0, s>>>(g, M);
+  else if (g.d == 2 && g.kind != FK_ADDITIVE && (g.kind == FK_SOBOLEV || g.kind == FK_LOWBIAS || g.dsym))
+    k_assemble_real_d2<<<grid, 256, 0, s>>>(g, M);
   else
-    k_assemble_real<<<dim3((g.D + 255) / 256, g.D), 256, 0, s>>>(g, M);
+    k_assemble_real<<<grid, 256, 0, s>>>(g, M);
 }
 
 __global__ void k_rhs_real(SysArgs g, const double2* __restrict__ r, double* __restrict__ M, double* __restrict__ zbuf,
