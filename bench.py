@@ -379,8 +379,8 @@ def main():
                 "spread_share_of_step": spread_per_step_ms / ms_step, "atomics_per_step": atoms}
 
     e2e = None
-    if not args.no_e2e and rank == 0 and not additive:
-        e2e = run_e2e(args, cfg, dev, eps)
+    if not args.no_e2e and rank == 0:
+        e2e = run_e2e_additive(args, cfg, dev, eps) if additive else run_e2e(args, cfg, dev, eps)
     cpu = None
     if not args.no_cpu and rank == 0 and world == 1:
         rate, n_s, t_s, cores, note = oracle_fit_rate(cfg, args.cpu_seconds)
@@ -411,6 +411,55 @@ def main():
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def run_e2e_additive(args, cfg, dev, eps):
+    """Additive model end to end: pinned host X (SoA columns) and Y -> chunked H2D on two copy
+    streams overlapped with the per-feature passes and the cross moments -> block solve -> theta D2H."""
+    import torch
+
+    from datagen.device import gen_dataset
+    from paper_2509_02649_b200 import fk
+    from paper_2509_02649_b200.fit import HostStreamerAdditive, additive_buffers
+
+    d, m = cfg["d"], cfg["m"]
+    n = int(min(args.e2e_n / 4, cfg["n"]))  # 44 B per sample: a quarter of the d = 1 sample count
+    chunk = 1 << 24
+    Xh = torch.empty((d, n), dtype=torch.float32, pin_memory=True)
+    Yh = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    tx = torch.empty((d, chunk), dtype=torch.float32, device=dev)
+    ty = torch.empty(chunk, dtype=torch.float32, device=dev)
+    for lo in range(0, n, chunk):
+        c = min(chunk, n - lo)
+        gen_dataset(tx[:, :c].t(), ty[:c], c, d, i0=lo, xkind=cfg["xkind"], ykind=cfg["ykind"], seed=0, stride_n=1, stride_d=chunk)
+        Xh[:, lo:lo + c].copy_(tx[:, :c])
+        Yh[lo:lo + c].copy_(ty[:c])
+    del tx, ty
+    st = HostStreamerAdditive(chunk, d, dev)
+    _, mus, rs, G = additive_buffers(d, m, dev)
+    D = d * (2 * m + 1)
+    theta_h = torch.empty(D, dtype=torch.complex128, pin_memory=True)
+
+    def step():
+        st.moments(Xh, Yh, 1.0, m, eps, mus, rs, G)
+        th, _ = fk.fk_solve(mus, rs, n, d, m, 1.0, cfg["lam"], "additive", report=False, cross=G)
+        theta_h.copy_(th, non_blocking=True)
+
+    step()
+    torch.cuda.synchronize()
+    steps = max(2, min(3, args.steps))
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(steps):
+        step()
+    e1.record(s)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    return {"value": n / (ms * 1e-3), "unit": "samples/s", "h2d_bytes_per_step": n * (d + 1) * 4, "d2h_bytes_per_step": D * 16,
+            "n": n, "ms_per_step": ms,
+            "path": "fit.HostStreamerAdditive + fk_solve: pinned host SoA X and Y -> chunked H2D on two copy streams overlapped with "
+                    "the per-feature passes and the cross moments; theta D2H"}
 
 
 def run_e2e(args, cfg, dev, eps):

@@ -201,6 +201,46 @@ class HostStreamer:
             r.zero_()
 
 
+class HostStreamerAdditive:
+    """Additive model from pinned HOST buffers: X as SoA columns (d, n), Y (n).  Chunks of every
+    column and of Y go to the device on two copy streams, double-buffered; each landed chunk gets
+    the per-feature one-pass moments + rhs and all pairwise cross moments (FK_ACCUMULATE)."""
+
+    def __init__(self, chunk: int, d: int, device):
+        self.chunk, self.d, self.dev = chunk, d, device
+        self.xb = [torch.empty((d, chunk), dtype=torch.float32, device=device) for _ in range(2)]
+        self.yb = [torch.empty(chunk, dtype=torch.float32, device=device) for _ in range(2)]
+        self.copy_streams = [torch.cuda.Stream(device), torch.cuda.Stream(device)]
+        self.copied = [[torch.cuda.Event() for _ in range(2)] for _ in range(2)]
+        self.consumed = [torch.cuda.Event() for _ in range(2)]
+
+    def moments(self, Xh_soa: torch.Tensor, Yh: torch.Tensor, L: float, m: int, eps: float, mus, rs, G):
+        d, n = Xh_soa.shape
+        comp = torch.cuda.current_stream(self.dev)
+        nchunks = (n + self.chunk - 1) // self.chunk
+        for i in range(nchunks):
+            b = i & 1
+            lo, hi = i * self.chunk, min(n, (i + 1) * self.chunk)
+            k = hi - lo
+            for c in range(2):
+                cs = self.copy_streams[c]
+                with torch.cuda.stream(cs):
+                    if i >= 2:
+                        cs.wait_event(self.consumed[b])
+                    if c == 0:
+                        for l in range(d):  # contiguous 1-D copies (a 2-D strided slice is not a plain DMA)
+                            self.xb[b][l, :k].copy_(Xh_soa[l, lo:hi], non_blocking=True)
+                    else:
+                        self.yb[b][:k].copy_(Yh[lo:hi], non_blocking=True)
+                    self.copied[c][b].record(cs)
+                comp.wait_event(self.copied[c][b])
+            Xk = self.xb[b][:, :k].t()  # (k, d) view of SoA columns
+            for l in range(d):
+                fk.fk_rhs_type1(Xk[:, l], self.yb[b][:k], L, m, eps, r_out=rs[l], mu_out=mus[l], accumulate=i > 0, check=False)
+            fk.fk_additive_cross_moments(Xk, L, m, eps, G_out=G, accumulate=i > 0, check=False)
+            self.consumed[b].record(comp)
+
+
 def fit_host(Xh: torch.Tensor, Yh: torch.Tensor, L: float, m: int, lam: float, kind: str = "sobolev", s: float = 1.0,
              eps: float = 1e-6, chunk: int = 1 << 26, streamer: Optional[HostStreamer] = None, device=None):
     """Fit from host (ideally pinned) buffers; returns theta on the HOST (complex128 numpy array)."""
