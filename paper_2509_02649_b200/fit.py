@@ -282,6 +282,9 @@ class FitGraph:
         with torch.cuda.graph(self.graph):
             run()
         self.launches = fk.profile_read()[2]
+        # the captured kernels hold raw pointers into the cached workspace: keep that buffer alive
+        # even if a later call with a larger workspace replaces the cache entry
+        self._ws = fk._workspace(0, X.device)
 
     def replay(self) -> torch.Tensor:
         self.graph.replay()
