@@ -163,6 +163,68 @@ def grid_search(X: torch.Tensor, Y: torch.Tensor, X_val: torch.Tensor, Y_val: to
     return GridResult(list(lambdas), risk, thetas, best, thetas[best])
 
 
+def reduce_grid_inputs(buf: torch.Tensor, buf_v: torch.Tensor, sum_y2: torch.Tensor, group=None) -> None:
+    """Data-parallel grid search, the exchange step: sum the ranks' unnormalised training and
+    validation moment buffers and the validation sum of Y^2 (one all-reduce each; exact by shard
+    additivity, R5).  No-op on one rank."""
+    import torch.distributed as dist
+
+    reduce_moments(buf, group)
+    reduce_moments(buf_v, group)
+    if _world(group) > 1:
+        dist.all_reduce(sum_y2, op=dist.ReduceOp.SUM, group=group)
+
+
+def broadcast_best(theta: torch.Tensor, best: torch.Tensor, group=None, src: int = 0) -> None:
+    """Send rank src's chosen lambda index and its theta to every rank.  No-op on one rank."""
+    import torch.distributed as dist
+
+    if _world(group) > 1:
+        dist.broadcast(best, src=src, group=group)
+        broadcast_theta(theta, group, src)
+
+
+def grid_search_distributed(X_shard: torch.Tensor, Y_shard: torch.Tensor, n_total: int, Xv_shard: torch.Tensor,
+                            Yv_shard: torch.Tensor, nv_total: int, L: float, m: int, lambdas, kind: str = "sobolev",
+                            s: float = 1.0, eps: float = 1e-6, group=None, **pi) -> GridResult:
+    """grid_search with the training and validation samples sharded over the ranks (one process
+    per GPU): every rank runs the type-1 passes on its shards, the moment buffers are all-reduced,
+    rank 0 runs the lambda path and the held-out risks, and broadcasts the chosen theta."""
+    import torch.distributed as dist
+
+    additive = kind == "additive"
+    d = X_shard.shape[1] if X_shard.dim() == 2 else 1
+    dev = X_shard.device
+    if additive:
+        buf, mus, rs, G = additive_buffers(d, m, dev)
+        buf_v, mus_v, rs_v, G_v = additive_buffers(d, m, dev)
+        for bb, Xs, Ys, a, b_, c in ((buf, X_shard, Y_shard, mus, rs, G), (buf_v, Xv_shard, Yv_shard, mus_v, rs_v, G_v)):
+            for l in range(d):
+                fk.fk_rhs_type1(Xs[:, l], Ys, L, m, eps, r_out=b_[l], mu_out=a[l], check=False)
+            fk.fk_additive_cross_moments(Xs, L, m, eps, G_out=c, check=False)
+        mu, r, mu_v, r_v = mus, rs, mus_v, rs_v
+        D = d * (2 * m + 1)
+    else:
+        buf, mu3, r3 = _moment_buffers(d, m, dev)
+        buf_v, mu3v, r3v = _moment_buffers(d, m, dev)
+        fk.fk_rhs_type1(X_shard, Y_shard, L, m, eps, r_out=r3, mu_out=mu3, check=False)
+        fk.fk_rhs_type1(Xv_shard, Yv_shard, L, m, eps, r_out=r3v, mu_out=mu3v, check=False)
+        mu, r, mu_v, r_v, G, G_v = mu3.reshape(-1), r3.reshape(-1), mu3v.reshape(-1), r3v.reshape(-1), None, None
+        D = (2 * m + 1) ** d
+    sum_y2 = torch.dot(Yv_shard.double(), Yv_shard.double()).reshape(1)  # validation constant (reporting only)
+    reduce_grid_inputs(buf, buf_v, sum_y2, group)
+    best = torch.zeros(1, dtype=torch.int64, device=dev)
+    theta = torch.empty(D, dtype=torch.complex128, device=dev)
+    thetas, risk = None, None
+    if _world(group) == 1 or dist.get_rank(group) == 0:
+        thetas = fk.fk_solve_path(mu, r, n_total, d, m, L, list(lambdas), kind, s, cross=G, **pi)
+        risk = fk.fk_path_validate(thetas, mu_v, r_v, nv_total, d, m, L, kind, float(sum_y2), cross_v=G_v)
+        best[0] = int(torch.argmin(risk))
+        theta.copy_(thetas[int(best[0])])
+    broadcast_best(theta, best, group)
+    return GridResult(list(lambdas), risk, thetas, int(best[0]), theta)
+
+
 class HostStreamer:
     """Streams pinned host (X, Y) to the device in fixed-size chunks, double-buffered, X and Y on
     two copy streams (both DMA engines), and runs the one-pass moments + rhs on each chunk as it

@@ -110,3 +110,21 @@ def test_grid_search_end_to_end(F, oracle):
     # fp32 type-1 moments (eps 1e-6): the chosen lambda is optimal up to that accuracy
     assert direct[g.best] <= min(direct) * (1 + 1e-4)
     assert abs(float(g.risk[g.best]) - direct[g.best]) / direct[g.best] < 1e-3
+
+
+@pytest.mark.parametrize("kind,d", [("sobolev", 1), ("additive", 3)])
+def test_grid_search_distributed_single_rank(F, kind, d):
+    """fit.grid_search_distributed on one rank (no process group) = fit.grid_search."""
+    from paper_2509_02649_b200 import fit
+
+    yk = "additive" if kind == "additive" else "sin"
+    X, Y = datagen.dataset(30_000, d=d, ykind=yk, seed=97)
+    Xv, Yv = datagen.dataset(8_000, d=d, ykind=yk, seed=98)
+    Xd = dev(X.reshape(-1) if d == 1 else X)
+    Xvd = dev(Xv.reshape(-1) if d == 1 else Xv)
+    lams = list(np.logspace(-8, -1, 12))
+    g1 = fit.grid_search(Xd, dev(Y), Xvd, dev(Yv), 1.0, 12, lams, kind, 2.0)
+    g2 = fit.grid_search_distributed(Xd, dev(Y), 30_000, Xvd, dev(Yv), 8_000, 1.0, 12, lams, kind, 2.0)
+    assert g1.best == g2.best
+    assert torch.allclose(g1.theta, g2.theta, rtol=0, atol=1e-12 * float(g1.theta.abs().max()))
+    assert torch.allclose(g1.risk, g2.risk, rtol=1e-12, atol=0)
