@@ -1,19 +1,22 @@
 // chol.cu -- dense fp64 Cholesky of the (augmented) real fit system, A = L L^T, in ONE persistent
 // dataflow kernel (the factorisation step of A11; DESIGN.md §5 "Solve").
 //
-// Why not cuSOLVER potrf at the fit sizes: for N ~ 2000-4000 its factorisation is latency bound
-// (~0.45 us per column, 0.88 ms at N = 2002, 3 TF/s).  Here the matrix is cut into 32 x 32 tiles and
-// every tile is owned by one 128-thread CTA, which
-//   1. loads its tile A_ij into fp64 tensor-core accumulators (mma.m8n8k4.f64, one 16 x 16 quadrant
-//      per warp),
-//   2. applies the updates A_ij -= L_ik L_jk^T for k = 0 .. j-1 as soon as the tiles L_ik, L_jk are
-//      published (their flags), staging both in shared memory,
-//   3. finishes with POTRF (diagonal tile, one warp, register resident, shuffles) or TRSM
-//      (X L_jj^T = A_ij, one warp, row per lane) and publishes L_ij (tile + flag).
-// Tiles are handed out by an atomic ticket counter in column-major order, so a CTA only ever waits
-// on tiles whose tickets are smaller -- held by CTAs that are already running and never wait on
-// larger tickets: deadlock free for any grid size, no co-residency assumption.  Tiles are read
-// with ld.global.cg (L2) because the same addresses held A before they hold L.
+// Why not cuSOLVER potrf at the fit sizes: for N ~ 2000-3500 its factorisation is latency bound
+// (~0.45 us per column, 0.83 ms at N = 2002).  Here the matrix is cut into 32 x 32 tiles and every
+// task is owned by one 128-thread CTA:
+//   * an off-diagonal tile (i, j), i >= j + 2, loads A_ij into fp64 tensor-core accumulators
+//     (mma.m8n8k4.f64, a 16 x 16 quadrant per warp), applies A_ij -= L_ik L_jk^T for k < j as soon
+//     as both operand tiles are published (flags), then solves X L_jj^T = A_ij (TRSM, a row per
+//     lane, 1/L_cc from the diagonal task);
+//   * the diagonal task D_j owns the sub-diagonal tile (j, j-1) AND the diagonal tile (j, j): it
+//     accumulates both, TRSMs the former, applies its rank-32 update to the latter straight from
+//     shared memory (no round trip through L2 on the critical path), then runs the 32 x 32 POTRF
+//     (one warp, a row per lane, rsqrt per pivot, column broadcast through shared memory) and
+//     publishes L_jj and 1/diag(L_jj) into a sentinel-filled side buffer that consumers poll as data.
+// Tasks are handed out by an atomic ticket counter in dependency order, so a CTA only ever waits
+// on tasks with smaller tickets -- held by CTAs that are already running and never wait on larger
+// tickets: deadlock free for any grid size, no co-residency assumption.  Tiles are read with
+// ld.global.cg (L2) because the same addresses held A before they hold L.
 // Padding rows/columns beyond N behave as the identity.  info: first failing pivot + 1 (0 = SPD).
 #include <cstdint>
 #include <cstdlib>
