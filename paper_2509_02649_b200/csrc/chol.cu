@@ -20,6 +20,10 @@
 // Padding rows/columns beyond N behave as the identity.  info: first failing pivot + 1 (0 = SPD).
 #include <cstdint>
 #include <cstdlib>
+#include <utility>
+#include <vector>
+#include <mutex>
+#include <map>
 
 #include "fk_internal.cuh"
 
@@ -113,13 +117,9 @@ __device__ __forceinline__ void stage_diag(double (*T)[LDS], double* dv, const d
   if (threadIdx.x < TS) dv[threadIdx.x] = d;
 }
 
-__device__ __forceinline__ int tile_id(int i, int j, int nt) { return j * nt - j * (j - 1) / 2 + (i - j); }
-
-// Tasks in ticket order, column by column: column j holds first the DIAGONAL task D_j (which owns
-// the sub-diagonal tile (j, j-1) and the diagonal tile (j, j)), then the tiles (i, j), i >= j + 2
-// (tile (j+1, j) belongs to D_{j+1}).  Every dependency of a task has a smaller ticket.
-// ticket -> (i, j); i == j marks D_j.
-__device__ __forceinline__ void task_of(int t, int nt, int* i, int* j) {
+// ticket -> task when there are no U tasks (computed: no table load on the chain): column j holds
+// D_j, then the tiles (i, j), i >= j + 2.  Returns (type, i, j, 0).
+__device__ __forceinline__ int4 task_of(int t, int nt) {
   int c = 0, start = 0;
   for (;;) {
     const int cnt = 1 + max(0, nt - c - 2);
@@ -127,9 +127,10 @@ __device__ __forceinline__ void task_of(int t, int nt, int* i, int* j) {
     start += cnt;
     ++c;
   }
-  *j = c;
-  *i = (t == start) ? c : c + 1 + (t - start);
+  return t == start ? make_int4(0, c, c, 0) : make_int4(1, c + 1 + (t - start), c, 0);
 }
+
+__device__ __forceinline__ int tile_id(int i, int j, int nt) { return j * nt - j * (j - 1) / 2 + (i - j); }
 
 // 32 x 32 POTRF step J on a register-resident row (lane r holds row r, one warp), fully unrolled
 // by recursion.  dj = pivot J, inv = rsqrt(dj) (MUFU + Newton, no IEEE sqrt/div).  Lane J+1 forms
@@ -265,14 +266,20 @@ __device__ __forceinline__ void final_potrf(double (*Ct)[TS + 1], double (*colL)
   Ld_out[TS * TS + lane] = my_dinv;
 }
 
+// Partial accumulation tasks U(j, c): the updates k in [cB, cB + B) of D_j's two tiles, summed into
+// a scratch buffer (fragment layout) that D_j adds in fixed order c = 0, 1, ... -- so the diagonal
+// task, which starts late in ticket order, only has the last < B + 2 updates left on the chain.
+constexpr int UB = 8;
+
+template <bool USE_U>
 __global__ void __launch_bounds__(CT) k_chol_tiles(double* __restrict__ M, int64_t ld, int N, int nt, int* __restrict__ flags,
                                                    int* __restrict__ ticket, int* __restrict__ info, double* __restrict__ Ld,
-                                                   unsigned long long* __restrict__ trace) {
+                                                   const int4* __restrict__ tasks, int ntasks, double* __restrict__ part,
+                                                   int* __restrict__ uflags, int maxc, unsigned long long* __restrict__ trace) {
   __shared__ double Ta[TS][LDS], Tb[TS][LDS];
   __shared__ double Ct[TS][TS + 1];
   __shared__ double dv[TS];
   __shared__ int s_t;
-  const int ntasks = nt + (nt - 2) * (nt - 1) / 2;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int qr = w >> 1, qc = w & 1;  // quadrant of a tile held by this warp
   const int g = lane >> 2, tq = lane & 3;
@@ -282,11 +289,37 @@ __global__ void __launch_bounds__(CT) k_chol_tiles(double* __restrict__ M, int64
     const int t = s_t;
     __syncthreads();
     if (t >= ntasks) return;
-    int i, j;
-    task_of(t, nt, &i, &j);
+    const int4 tk = USE_U ? tasks[t] : task_of(t, nt);
+    const int i = tk.y, j = tk.z;
     unsigned long long t0 = 0, t1 = 0, t1b = 0, t1c = 0;
     if (trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    if (i != j) {
+    if (USE_U && tk.x == 2) {
+      // ---- U(j, c): partial sums of D_j's updates over k in [cB, cB + B) ----
+      const int c = tk.w;
+      Acc ps, pd;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        (&ps.v[0][0][0])[e] = 0.0;
+        (&pd.v[0][0][0])[e] = 0.0;
+      }
+      for (int k = c * UB; k < (c + 1) * UB; ++k) {
+        wait_flags(flags + tile_id(j, k, nt), flags + tile_id(j - 1, k, nt));
+        stage(Ta, M, ld, N, j, k);
+        stage(Tb, M, ld, N, j - 1, k);
+        __syncthreads();
+        acc_update(ps, Ta, Tb, qr, qc, g, tq);
+        acc_update(pd, Ta, Ta, qr, qc, g, tq);
+        __syncthreads();
+      }
+      double* base = part + ((int64_t)j * maxc + c) * 2 * TS * TS;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        base[e * CT + threadIdx.x] = (&ps.v[0][0][0])[e];
+        base[TS * TS + e * CT + threadIdx.x] = (&pd.v[0][0][0])[e];
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) release(uflags + j * maxc + c);
+    } else if (i != j) {
       // ---- off-diagonal tile (i, j), i >= j + 2: updates k < j, then TRSM with L_jj ----
       Acc a;
       acc_load(a, M, ld, N, i, j, qr, qc, g, tq);
@@ -314,7 +347,17 @@ __global__ void __launch_bounds__(CT) k_chol_tiles(double* __restrict__ M, int64
       if (j > 0) {
         Acc sb;  // A_{j, j-1}
         acc_load(sb, M, ld, N, j, j - 1, qr, qc, g, tq);
-        for (int k = 0; k < j - 1; ++k) {
+        const int nc = USE_U ? max(0, (j - 2) / UB) : 0;  // chunks summed by the U tasks (they end before k = j - 2)
+        for (int c = 0; c < nc; ++c) {
+          wait_flags(uflags + j * maxc + c, nullptr);
+          const double* base = part + ((int64_t)j * maxc + c) * 2 * TS * TS;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            (&sb.v[0][0][0])[e] += __ldcg(base + e * CT + threadIdx.x);
+            (&d.v[0][0][0])[e] += __ldcg(base + TS * TS + e * CT + threadIdx.x);
+          }
+        }
+        for (int k = nc * UB; k < j - 1; ++k) {
           wait_flags(flags + tile_id(j, k, nt), flags + tile_id(j - 1, k, nt));
           stage(Ta, M, ld, N, j, k);
           stage(Tb, M, ld, N, j - 1, k);
@@ -371,34 +414,81 @@ __global__ void __launch_bounds__(CT) k_chol_tiles(double* __restrict__ M, int64
 }  // namespace
 
 static size_t flags_bytes(int nt) { return ((size_t)(nt * (nt + 1) / 2 + 8) * sizeof(int) + 255) & ~(size_t)255; }
+static int max_chunks(int nt) { return nt / UB + 1; }
+static size_t uflags_bytes(int nt) { return ((size_t)nt * max_chunks(nt) * sizeof(int) + 255) & ~(size_t)255; }
+static size_t part_bytes(int nt) { return (size_t)nt * max_chunks(nt) * 2 * TS * TS * sizeof(double); }
 
 size_t chol_ws_bytes(int N) {
   const int nt = (N + TS - 1) / TS;
-  return flags_bytes(nt) + (size_t)nt * LDW * sizeof(double);
+  return flags_bytes(nt) + (size_t)nt * LDW * sizeof(double) + uflags_bytes(nt) + part_bytes(nt);
+}
+
+// Task table in ticket order (built once per tile count, device memory): per column col,
+// D_col, the off-diagonal tiles (i >= col + 2, col), and after every B-th column the U(j, c) tasks
+// whose chunk it completes.  Every task only depends on tasks listed before it.
+static std::mutex g_task_mu;
+static std::map<std::pair<int, int>, std::pair<int4*, int>> g_tasks;
+
+// U tasks pay off once the diagonal tasks' own update chains dominate (measured: N = 4226 1.95 ->
+// 1.62 ms; at N <= 3001 they cost 10-20 %), so they are generated for nt >= kUMinTiles only.
+constexpr int kUMinTiles = 100;
+
+static fk_status task_table(int nt, int4** d_tasks, int* ntasks) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_task_mu);
+  auto key = std::make_pair(dev, nt);
+  const bool use_u = nt >= kUMinTiles;
+  auto it = g_tasks.find(key);
+  if (it == g_tasks.end()) {
+    std::vector<int4> t;
+    for (int col = 0; col < nt; ++col) {
+      t.push_back(make_int4(0, col, col, 0));
+      for (int i = col + 2; i < nt; ++i) t.push_back(make_int4(1, i, col, 0));
+      if (use_u && (col + 1) % UB == 0) {
+        const int c = (col + 1) / UB - 1;
+        for (int j = (c + 1) * UB + 2; j < nt; ++j) t.push_back(make_int4(2, j, j, c));
+      }
+    }
+    int4* d = nullptr;
+    FK_CUDA_TRY(cudaMalloc(&d, t.size() * sizeof(int4)));
+    FK_CUDA_TRY(cudaMemcpy(d, t.data(), t.size() * sizeof(int4), cudaMemcpyHostToDevice));
+    it = g_tasks.emplace(key, std::make_pair(d, (int)t.size())).first;
+  }
+  *d_tasks = it->second.first;
+  *ntasks = it->second.second;
+  return FK_OK;
 }
 
 // Factor the N x N SPD matrix M (column-major, leading dimension ld, lower triangle read and
-// overwritten with L).  ws: chol_ws_bytes(N) bytes (flags + ticket); info: device int, set to 0 here.
+// overwritten with L).  ws: chol_ws_bytes(N) bytes; info: device int, set to 0 here.
 fk_status chol_tiles(double* M, int64_t ld, int N, int* info, void* ws, cudaStream_t s, unsigned long long* trace) {
   const int nt = (N + TS - 1) / TS;
   const int ntiles = nt * (nt + 1) / 2;
-  const int ntasks = nt + (nt - 2) * (nt - 1) / 2;
+  int4* tasks = nullptr;
+  int ntasks = 0;
+  FK_TRY(task_table(nt, &tasks, &ntasks));
   int* flags = (int*)ws;
   int* ticket = flags + ntiles;
   double* Ld = (double*)((char*)ws + flags_bytes(nt));
+  int* uflags = (int*)((char*)Ld + (size_t)nt * LDW * sizeof(double));
+  double* part = (double*)((char*)uflags + uflags_bytes(nt));
   FK_CUDA_TRY(cudaMemsetAsync(Ld, 0xff, (size_t)nt * LDW * sizeof(double), s));
   FK_CUDA_TRY(cudaMemsetAsync(flags, 0, (size_t)(ntiles + 8) * sizeof(int), s));
+  if (nt >= kUMinTiles) FK_CUDA_TRY(cudaMemsetAsync(uflags, 0, uflags_bytes(nt), s));
   FK_CUDA_TRY(cudaMemsetAsync(info, 0, sizeof(int), s));
+  const bool use_u = nt >= kUMinTiles;
+  auto kern = use_u ? k_chol_tiles<true> : k_chol_tiles<false>;
   static int per_sm = 0;
   if (per_sm == 0) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_chol_tiles, CT, 0) != cudaSuccess || per_sm < 1) per_sm = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_chol_tiles<true>, CT, 0) != cudaSuccess || per_sm < 1) per_sm = 1;
   }
   // fewer co-resident CTAs shorten the latency-bound critical path at small N; the update throughput
   // needs more at larger N (measured on B200: N = 2002 best at 2/SM, N >= 3000 at 8/SM)
   int ps = std::min(per_sm, N <= 2500 ? 2 : 8);
   if (const char* e = getenv("FK_CHOL_PER_SM")) ps = std::max(1, std::min(per_sm, atoi(e)));  // experiments
   const int grid = std::min(ntasks, ps * device_sm_count());
-  k_chol_tiles<<<grid, CT, 0, s>>>(M, ld, N, nt, flags, ticket, info, Ld, trace);
+  kern<<<grid, CT, 0, s>>>(M, ld, N, nt, flags, ticket, info, Ld, tasks, ntasks, part, uflags, max_chunks(nt), trace);
   FK_CUDA_TRY(cudaGetLastError());
   count_launch();
   return FK_OK;
