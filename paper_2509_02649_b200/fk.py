@@ -241,6 +241,8 @@ def fk_path_validate(theta: torch.Tensor, mu_v: torch.Tensor, r_v: torch.Tensor,
     type-1 moments mu_v / rhs r_v (and cross moments for the additive model), n_v samples and
     sum_y2 = sum Y_v^2 (P:542-548 grid search; R11).  Returns nlam float64 (device)."""
     k = KINDS[kind] if isinstance(kind, str) else int(kind)
+    if k in (FK_PIK_BOX, FK_PIK_COLLOC):  # the risk needs only the data part of the system
+        k = FK_SOBOLEV
     theta = theta.contiguous()
     nlam = theta.shape[0] if theta.dim() == 2 else 1
     if risk_out is None:

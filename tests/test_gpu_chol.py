@@ -76,3 +76,17 @@ def test_tiles_report_not_spd(F):
             F.fk_solve(mu, r, 1000, 1, m, 1.0, 1e-6, "sobolev", 1.0)
     finally:
         del os.environ["FK_CHOL"]
+
+
+def test_tiles_report_not_spd_with_partial_tasks(F):
+    """N >= 3200 runs the partial-accumulation (U) tasks; an indefinite system still reports."""
+    m = 1700  # D = 3401, N = 3402: 107 tile columns
+    mu = torch.zeros(4 * m + 1, dtype=torch.complex128, device="cuda")
+    mu[2 * m] = -1000.0
+    r = torch.ones(2 * m + 1, dtype=torch.complex128, device="cuda")
+    os.environ["FK_CHOL"] = "tiles"
+    try:
+        with pytest.raises(F.FkError):
+            F.fk_solve(mu, r, 1000, 1, m, 1.0, 1e-9, "sobolev", 1.0)
+    finally:
+        del os.environ["FK_CHOL"]

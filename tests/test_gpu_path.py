@@ -70,7 +70,7 @@ def test_path_rejects_bad_lambda(F):
         F.fk_solve_path(mu, r, 10, 1, 3, 1.0, [1e-3, 0.0])
 
 
-@pytest.mark.parametrize("d,m,kind", [(1, 30, "sobolev"), (2, 6, "sobolev"), (4, 8, "additive")])
+@pytest.mark.parametrize("d,m,kind", [(1, 30, "sobolev"), (2, 6, "sobolev"), (4, 8, "additive"), (2, 6, "pik_box")])
 def test_path_validate_matches_direct_prediction(F, oracle, d, m, kind):
     """Held-out risk from validation moments == mean (Y - f(x))^2 by direct prediction (oracle)."""
     n, nv = 10_000, 3_000
@@ -87,7 +87,8 @@ def test_path_validate_matches_direct_prediction(F, oracle, d, m, kind):
         kv = dict(cross_v=dev(oracle.cross_moments(Xv, 1.0, m)))
     else:
         args = [dev(oracle.moments(X, 1.0, m).reshape(-1)), dev(oracle.rhs(X, Y, 1.0, m).reshape(-1))]
-        kw, kv = {}, {}
+        kw = dict(mu_pde=1.0, box=[[-1.0, 0.5], [-0.5, 1.0]], **HEAT) if kind == "pik_box" else {}
+        kv = {}
         mu_v, r_v = dev(oracle.moments(Xv, 1.0, m).reshape(-1)), dev(oracle.rhs(Xv, Yv, 1.0, m).reshape(-1))
     th = F.fk_solve_path(*args, n, d, m, 1.0, lams, kind, 2.0, **kw)
     yy = float(np.dot(Yv.astype(np.float64), Yv.astype(np.float64)))
