@@ -371,8 +371,9 @@ def main():
         else:
             atoms = n_loc * 2 * w * w
         achieved = atoms / (spread_per_step_ms * 1e-3) / 1e9
+        tr = ncu_traffic(args.config)
         roof = {"bound": "alu", "achieved": achieved, "peak": ATOMS_RANDOM_PEAK / 1e9, "unit": "Gatomic/s",
-                "frac": achieved * 1e9 / ATOMS_RANDOM_PEAK, "traffic": None,
+                "frac": achieved * 1e9 / ATOMS_RANDOM_PEAK, "traffic": None if tr is None else tr["dram_bytes_per_sample"] * n_loc,
                 "kernel": "spreading kernels (shared-memory int32 atomics)",
                 "peak_source": "measured random-address ATOMS.ADD rate, profiles/r01_microbench_spread.log",
                 "hbm_gbs": bytes_step / (spread_per_step_ms * 1e-3) / 1e9, "spread_ms_per_step": spread_per_step_ms,
