@@ -65,14 +65,28 @@ __device__ __forceinline__ void stage(double (*T)[LDS], const double* __restrict
   }
 }
 
+// Watchdog for every spin-wait: a dependency that is not published within 5 s (it never happens
+// in a correct schedule -- the longest legitimate wait is a few ms) ends the wait, so a scheduling
+// bug yields a wrong factor (caught by the backward error) instead of a hung GPU.
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+constexpr unsigned long long kSpinLimitNs = 5000000000ULL;
+
 // wait until both flags are set (thread 0 polls fa, thread 32 polls fb; fb may be null)
 __device__ __forceinline__ void wait_flags(const int* fa, const int* fb) {
-  if (threadIdx.x == 0)
-    while (ld_relaxed(fa) == 0) {
+  if (threadIdx.x == 0) {
+    const unsigned long long t0 = gtime();
+    while (ld_relaxed(fa) == 0 && gtime() - t0 < kSpinLimitNs) {
     }
-  if (threadIdx.x == 32 && fb)
-    while (ld_relaxed(fb) == 0) {
+  }
+  if (threadIdx.x == 32 && fb) {
+    const unsigned long long t0 = gtime();
+    while (ld_relaxed(fb) == 0 && gtime() - t0 < kSpinLimitNs) {
     }
+  }
   __syncthreads();
 }
 
@@ -95,6 +109,7 @@ __device__ __forceinline__ void stage_diag(double (*T)[LDS], double* dv, const d
 #pragma unroll
   for (int q = 0; q < PER; ++q) v[q] = ld_cg_volatile(Ld + threadIdx.x + CT * q);
   double d = (threadIdx.x < TS) ? ld_cg_volatile(Ld + TS * TS + threadIdx.x) : 0.0;
+  const unsigned long long t0 = gtime();
   for (;;) {
     bool ok = true;
 #pragma unroll
@@ -107,7 +122,7 @@ __device__ __forceinline__ void stage_diag(double (*T)[LDS], double* dv, const d
       d = ld_cg_volatile(Ld + TS * TS + threadIdx.x);
       ok = false;
     }
-    if (ok) break;
+    if (ok || gtime() - t0 > kSpinLimitNs) break;
   }
 #pragma unroll
   for (int q = 0; q < PER; ++q) {

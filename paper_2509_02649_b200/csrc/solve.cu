@@ -523,9 +523,12 @@ __global__ void __launch_bounds__(64) k_trsv_lt(const double* __restrict__ M, in
     const int row = J * 32 + lane;
     double zc = 0.0;
     if (row < D) {
-      do {
+      unsigned long long t0, t1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+      do {  // watchdog: a block never published within 5 s ends the wait (wrong z, no hung GPU)
         zc = ld_volatile(zbuf + row);
-      } while (__double_as_longlong(zc) == (long long)kZSentinel);
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+      } while (__double_as_longlong(zc) == (long long)kZSentinel && t1 - t0 < 5000000000ULL);
     }
     double Lc[16];
 #pragma unroll
