@@ -284,7 +284,7 @@ __device__ __forceinline__ void final_potrf(double (*Ct)[TS + 1], double (*colL)
 // Partial accumulation tasks U(j, c): the updates k in [cB, cB + B) of D_j's two tiles, summed into
 // a scratch buffer (fragment layout) that D_j adds in fixed order c = 0, 1, ... -- so the diagonal
 // task, which starts late in ticket order, only has the last < B + 2 updates left on the chain.
-constexpr int UB = 8;
+constexpr int UB = 16;
 
 template <bool USE_U>
 __global__ void __launch_bounds__(CT) k_chol_tiles(double* __restrict__ M, int64_t ld, int N, int nt, int* __restrict__ flags,
@@ -444,9 +444,10 @@ size_t chol_ws_bytes(int N) {
 static std::mutex g_task_mu;
 static std::map<std::pair<int, int>, std::pair<int4*, int>> g_tasks;
 
-// U tasks pay off once the diagonal tasks' own update chains dominate (measured: N = 4226 1.95 ->
-// 1.62 ms; at N <= 3001 they cost 10-20 %), so they are generated for nt >= kUMinTiles only.
-constexpr int kUMinTiles = 100;
+// U tasks pay off once the diagonal tasks' own update chains dominate (measured with chunks of 16:
+// N = 4226 1.83 -> 1.53 ms, 3201 1.03 -> 0.92; at 63 tile columns they cost 5 %), so they are
+// generated for nt >= kUMinTiles only.
+constexpr int kUMinTiles = 80;
 
 static fk_status task_table(int nt, int4** d_tasks, int* ntasks) {
   int dev = 0;

@@ -593,8 +593,8 @@ size_t solve_ws_bytes(int d, int m, int kind) {
 
 // factorisation path: the tile dataflow kernel (chol.cu) up to kTilesMaxN, cuSOLVER potrf above,
 // where the factorisation is throughput bound and cuSOLVER's larger blocking wins (measured on
-// B200, potrf alone: tiles 0.44 / cuSOLVER 0.83 ms at N = 2002, 0.85 / 1.30 at 3001, 1.62 / 1.79
-// at 4226, 2.53 / 2.35 at 5000).  FK_CHOL=cusolver|tiles overrides (tests, measurements).
+// B200, potrf alone: tiles 0.45 / cuSOLVER 0.83 ms at N = 2002, 0.92 / 1.41 at 3201, 1.53 / 1.79
+// at 4226, 1.84 / 1.97 at 4600, 2.40 / 2.34 at 5000).  FK_CHOL=cusolver|tiles overrides (tests, measurements).
 constexpr int kTilesMaxN = 4600;
 bool use_tiles(int N) {
   const char* e = getenv("FK_CHOL");
