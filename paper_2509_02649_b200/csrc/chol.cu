@@ -147,6 +147,25 @@ __device__ __forceinline__ int4 task_of(int t, int nt) {
 
 __device__ __forceinline__ int tile_id(int i, int j, int nt) { return j * nt - j * (j - 1) / 2 + (i - j); }
 
+// Operand readiness for a run of updates k = k0 .. kend-1 that need tiles (ia, k) and (ib, k):
+// one parallel scan of both flag columns finds the first k not yet published (smem min), so the
+// ready prefix is consumed without a flag round trip per update; at a not-ready k the CTA waits on
+// that k alone and scans again afterwards.  Returns the first k that is NOT known ready (> k0).
+__device__ __forceinline__ int ready_prefix(const int* __restrict__ flags, int nt, int ia, int ib, int k0, int kend, int* s_min) {
+  if (threadIdx.x == 0) *s_min = kend;
+  __syncthreads();
+  for (int k = k0 + threadIdx.x; k < kend; k += blockDim.x)
+    if (!ld_relaxed(flags + tile_id(ia, k, nt)) || !ld_relaxed(flags + tile_id(ib, k, nt))) atomicMin(s_min, k);
+  __syncthreads();
+  int first = *s_min;
+  __syncthreads();
+  if (first == k0) {  // nothing ready yet: wait for k0 itself
+    wait_flags(flags + tile_id(ia, k0, nt), flags + tile_id(ib, k0, nt));
+    first = k0 + 1;
+  }
+  return first;
+}
+
 // 32 x 32 POTRF step J on a register-resident row (lane r holds row r, one warp), fully unrolled
 // by recursion.  dj = pivot J, inv = rsqrt(dj) (MUFU + Newton, no IEEE sqrt/div).  Lane J+1 forms
 // the next pivot from its own l_{J+1,J} and publishes it through shared memory before the general
@@ -295,6 +314,7 @@ __global__ void __launch_bounds__(CT) k_chol_tiles(double* __restrict__ M, int64
   __shared__ double Ct[TS][TS + 1];
   __shared__ double dv[TS];
   __shared__ int s_t;
+  __shared__ int s_min;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int qr = w >> 1, qc = w & 1;  // quadrant of a tile held by this warp
   const int g = lane >> 2, tq = lane & 3;
@@ -317,8 +337,9 @@ __global__ void __launch_bounds__(CT) k_chol_tiles(double* __restrict__ M, int64
         (&ps.v[0][0][0])[e] = 0.0;
         (&pd.v[0][0][0])[e] = 0.0;
       }
+      int rdy = c * UB;
       for (int k = c * UB; k < (c + 1) * UB; ++k) {
-        wait_flags(flags + tile_id(j, k, nt), flags + tile_id(j - 1, k, nt));
+        if (k >= rdy) rdy = ready_prefix(flags, nt, j, j - 1, k, (c + 1) * UB, &s_min);
         stage(Ta, M, ld, N, j, k);
         stage(Tb, M, ld, N, j - 1, k);
         __syncthreads();
@@ -338,8 +359,9 @@ __global__ void __launch_bounds__(CT) k_chol_tiles(double* __restrict__ M, int64
       // ---- off-diagonal tile (i, j), i >= j + 2: updates k < j, then TRSM with L_jj ----
       Acc a;
       acc_load(a, M, ld, N, i, j, qr, qc, g, tq);
+      int rdy = 0;
       for (int k = 0; k < j; ++k) {
-        wait_flags(flags + tile_id(i, k, nt), flags + tile_id(j, k, nt));
+        if (k >= rdy) rdy = ready_prefix(flags, nt, i, j, k, j, &s_min);
         stage(Ta, M, ld, N, i, k);
         stage(Tb, M, ld, N, j, k);
         __syncthreads();
@@ -372,8 +394,9 @@ __global__ void __launch_bounds__(CT) k_chol_tiles(double* __restrict__ M, int64
             (&d.v[0][0][0])[e] += __ldcg(base + TS * TS + e * CT + threadIdx.x);
           }
         }
+        int rdy = nc * UB;
         for (int k = nc * UB; k < j - 1; ++k) {
-          wait_flags(flags + tile_id(j, k, nt), flags + tile_id(j - 1, k, nt));
+          if (k >= rdy) rdy = ready_prefix(flags, nt, j, j - 1, k, j - 1, &s_min);
           stage(Ta, M, ld, N, j, k);
           stage(Tb, M, ld, N, j - 1, k);
           __syncthreads();
