@@ -876,6 +876,7 @@ struct PlanX {
   int m, w, nf, off, K, G, npairs, per_cta, ngroups, chunks, threads;
   double beta;
   bool fp64;
+  bool by_pair;  // one pair grid does not fit a CTA: per-pair 2-D moment passes (cross_by_pair)
   size_t smem;
 };
 
@@ -906,7 +907,11 @@ static fk_status make_planx(int d, int m, double eps, int dtype, PlanX* p) {
   const size_t esz = q.fp64 ? 8 : 4;
   const size_t cap = (size_t)max_optin() - 2048;
   const size_t per = (size_t)q.G * q.G * esz;
-  if (per > cap) return fail(FK_E_UNSUPPORTED, "fk_additive_cross_moments: m too large for one pair grid per CTA");
+  if (per > cap) {  // large m: the tiled 2-D moment pass, one pair at a time
+    q.by_pair = true;
+    *p = q;
+    return FK_OK;
+  }
   q.per_cta = (int)std::min<size_t>(q.npairs, cap / per);
   q.ngroups = (q.npairs + q.per_cta - 1) / q.per_cta;
   q.smem = (size_t)q.per_cta * per;
@@ -936,11 +941,65 @@ static fk_status layoutx(const PlanX& p, Bump& b, void** part, double** carry, d
   return FK_OK;
 }
 
+// Large-m cross moments (a pair grid exceeds one CTA's shared memory).  The pair (l1, l2) moments
+// are the 2-D unit-weight moments of the points (X_l1, X_l2) read at q = (a, -b):
+//   G_{a,b} = sum_j exp(-i (a t_{j,l1} - b t_{j,l2})) = mu_{(a,-b)},  |a|, |b| <= m,
+// so each pair is one tiled type-1 pass (type1_2d_run, moments only) at m2 = ceil(m/2), whose
+// mode box {-2 m2..2 m2}^2 covers {-m..m}^2, followed by a crop/reflect into G[p].
+__global__ void k_cross_from_mu(const double2* __restrict__ mu2, int m2, int m, double2* __restrict__ Gp, int acc) {
+  const int K2 = 4 * m2 + 1, D = 2 * m + 1;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)D * D) return;
+  const int a = (int)(t / D) - m, b = (int)(t % D) - m;
+  const double2 v = mu2[(int64_t)(a + 2 * m2) * K2 + (-b + 2 * m2)];
+  if (acc) {
+    Gp[t].x += v.x;
+    Gp[t].y += v.y;
+  } else {
+    Gp[t] = v;
+  }
+}
+
+static size_t cross_by_pair_ws(int m, double eps, int dtype) {
+  const int m2 = (m + 1) / 2;
+  const size_t inner = type1_2d_ws_bytes(m2, eps, true, false, dtype);
+  if (inner == 0) return 0;
+  return (((size_t)(4 * m2 + 1) * (4 * m2 + 1) * 16 + 255) & ~(size_t)255) + inner;
+}
+
+static fk_status cross_by_pair(const fk_points& X, double L, int m, double eps, double* G, bool accumulate, void* ws, size_t ws_bytes,
+                               int* d_status, cudaStream_t s) {
+  const int m2 = (m + 1) / 2;
+  const size_t need = cross_by_pair_ws(m, eps, X.dtype);
+  if (need == 0) return fail(FK_E_UNSUPPORTED, "fk_additive_cross_moments: no 2-D plan for this m");
+  if (ws_bytes < need) return fail(FK_E_WORKSPACE, "workspace too small");
+  const size_t mub = ((size_t)(4 * m2 + 1) * (4 * m2 + 1) * 16 + 255) & ~(size_t)255;
+  double* mu2 = (double*)ws;
+  void* inner = (char*)ws + mub;
+  const size_t esz = X.dtype == FK_F64 ? 8 : 4;
+  const int D = 2 * m + 1;
+  int p = 0;
+  for (int l1 = 0; l1 < X.d; ++l1)
+    for (int l2 = l1 + 1; l2 < X.d; ++l2, ++p) {
+      fk_points Xp = X;
+      Xp.ptr = (const char*)X.ptr + (size_t)l1 * X.stride_d * esz;
+      Xp.d = 2;
+      Xp.stride_d = (int64_t)(l2 - l1) * X.stride_d;
+      FK_TRY(type1_2d_run(m2, eps, Xp, nullptr, L, mu2, nullptr, false, inner, ws_bytes - mub, d_status, s));
+      k_cross_from_mu<<<(D * D + 255) / 256, 256, 0, s>>>((const double2*)mu2, m2, m, (double2*)G + (int64_t)p * D * D,
+                                                          accumulate ? 1 : 0);
+      FK_CUDA_TRY(cudaGetLastError());
+      count_launch();
+    }
+  return FK_OK;
+}
+
 size_t cross_ws_bytes(int d, int m, double eps, int64_t n, int dtype) {
   (void)n;
   if (d < 2) return 0;
   PlanX p;
   if (make_planx(d, m, eps, dtype, &p) != FK_OK) return 0;
+  if (p.by_pair) return cross_by_pair_ws(m, eps, dtype);
   Bump b(nullptr, 0);
   void *part, *work;
   double *carry, *fine, *tab;
@@ -954,6 +1013,7 @@ fk_status cross_run(const fk_points& X, double L, int m, double eps, double* G, 
                     int* d_status, cudaStream_t s) {
   PlanX p;
   FK_TRY(make_planx(X.d, m, eps, X.dtype, &p));
+  if (p.by_pair) return cross_by_pair(X, L, m, eps, G, accumulate, ws, ws_bytes, d_status, s);
   if (p.npairs > 528) return fail(FK_E_UNSUPPORTED, "fk_additive_cross_moments: at most 528 pairs");
   Bump b(ws, ws_bytes);
   void *part, *work;

@@ -258,3 +258,24 @@ def test_type1_bitwise_deterministic(F, eps, dt):
     r1, mu1 = F.fk_rhs_type1(X, Y, 1.0, m, eps)
     r2, mu2 = F.fk_rhs_type1(X, Y, 1.0, m, eps)
     assert torch.equal(r1, r2) and torch.equal(mu1, mu2)
+
+
+@pytest.mark.parametrize("m,eps", [(8000, 1e-6), (3000, 1e-10), (6000, 1e-12)])
+def test_large_m_beyond_shared_memory(F, oracle, m, eps):
+    """m too large for a CTA-resident grid (fp32: sigma (4m+1) cells > 227 KB; fp64: the septic
+    grid too): the type-1 pass falls back to the ES window accumulated in global fp64 grids, and
+    predict to its global-grid gather.  Same gates as the shared-memory paths."""
+    n = 12_001
+    dt = torch.float32 if eps >= 1e-7 else torch.float64
+    X, Y = datagen.dataset(n, seed=19)
+    X, Y = X.reshape(-1).astype(np.float32 if dt == torch.float32 else np.float64), Y.astype(np.float32 if dt == torch.float32 else np.float64)
+    mu, r = _run(F, X, Y, m, eps, dt)
+    tol = 1e-5 if eps >= 1e-7 else 1e-10
+    assert rel(mu, oracle.moments(X, 1.0, m)) <= tol
+    assert rel(r, oracle.rhs(X, Y, 1.0, m)) <= tol
+    rng = np.random.default_rng(5)
+    k = np.arange(-m, m + 1)
+    th = (rng.normal(size=2 * m + 1) + 1j * rng.normal(size=2 * m + 1)) / (1.0 + np.abs(k))
+    Xq = datagen.dataset(4_001, seed=20)[0].reshape(-1).astype(X.dtype)
+    out = host(F.fk_predict_type2(dev(th), 1, m, 1.0, dev(Xq, dt), eps))
+    assert rel(out, oracle.predict(th, Xq, 1.0, m)) <= tol

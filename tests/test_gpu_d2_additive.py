@@ -90,7 +90,8 @@ def test_pi_fit_end_to_end(F, oracle):
     assert rel(f, f_o) <= 1e-4
 
 
-@pytest.mark.parametrize("d,m,n,eps", [(3, 10, 20_000, 1e-6), (10, 50, 2_000, 1e-6), (4, 8, 5_000, 1e-10)])
+@pytest.mark.parametrize("d,m,n,eps", [(3, 10, 20_000, 1e-6), (10, 50, 2_000, 1e-6), (4, 8, 5_000, 1e-10),
+                                        (3, 131, 3_001, 1e-6), (3, 90, 2_001, 1e-10)])  # last two: a pair grid exceeds a CTA (per-pair 2-D passes)
 def test_cross_moments_match_oracle(F, oracle, d, m, n, eps):
     X, _ = datagen.dataset(n, d=d, ykind="additive", seed=27)
     t = torch.float32 if eps >= 1e-7 else torch.float64
