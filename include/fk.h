@@ -122,14 +122,20 @@ typedef struct fk_solve_report {
   double ms;           /* device time of the solve (assembly + factorisation + solves) */
   int32_t info;        /* Cholesky info (0 = success) */
   int32_t n_unknowns;  /* D */
+  int32_t iters;       /* conjugate-gradient iterations (0: dense Cholesky) */
+  int32_t reserved;
 } fk_solve_report;
 
-/* theta = A^{-1} r / n by dense Cholesky in fp64 (P:513 for the additive block system;
- * reading R9 for why not CG).  For real Y theta is Hermitian, so the real-symmetric form
- * P^*AP z = P^*r/n (D unknowns) is factorised: by a tile dataflow kernel up to D = 3500, by
- * cuSOLVER potrf above.  theta_out: D complex128, D = (2m+1)^d (d(2m+1) for
- * ADDITIVE).  rep may be NULL (no synchronisation, CUDA-graph capturable); otherwise the call
- * synchronises `stream` and fills *rep.  Returns FK_E_SOLVE if A is not numerically positive
+/* theta = A^{-1} r / n in fp64 (P:513 for the additive block system).  For real Y theta
+ * is Hermitian, so the real-symmetric form P^*AP z = P^*r/n (D unknowns) is solved: by dense
+ * Cholesky (reading R9) -- a tile dataflow kernel up to D = 4599, cuSOLVER potrf above -- except
+ * for the Sobolev estimator with D >= 4600, d <= 2, where the paper's conjugate gradients
+ * run with FFT-Toeplitz products and a block preconditioner (reading R13) to a
+ * relative residual of 1e-13 when a cost model predicts it faster; that path reads
+ * a convergence flag back every 10 iterations (the stream is synchronised even with rep == NULL)
+ * and is skipped while the stream is being captured into a CUDA graph.  theta_out: D complex128,
+ * D = (2m+1)^d (d(2m+1) for ADDITIVE).  rep may be NULL (dense path: no synchronisation,
+ * CUDA-graph capturable); otherwise the call synchronises `stream` and fills *rep.  Returns FK_E_SOLVE if A is not numerically positive
  * definite (only detected when rep != NULL). */
 fk_status fk_solve(const fk_problem* P, double* theta_out, fk_solve_report* rep, void* ws, size_t ws_bytes,
                    fk_stream_t stream);

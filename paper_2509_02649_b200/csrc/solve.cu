@@ -18,6 +18,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <map>
+#include <vector>
 #include <mutex>
 
 #include "fk_internal.cuh"
@@ -882,6 +883,384 @@ fk_status path_validate_run(const fk_problem* Pv, const double* theta, int nlam,
   return FK_OK;
 }
 
+// ------------------------------------------------------------------------------------------
+// Preconditioned conjugate gradients for the Sobolev system at large D (NEXT-3; the paper's own
+// solver, with FFT-Toeplitz products).  Real form P^*AP z = P^*r/n as in the dense path.
+//   matvec: theta = P z -> Hermitian half spectrum -> cuFFT Z2D -> x (DFT of mu)/(n L^d) -> D2Z
+//           -> (T theta)_k / n, + lambda R_k theta_k, -> P^* (a_k: 2 Re, b_k: 2 Im, centre: Re);
+//           circular length L >= 4m+1 per dimension keeps k1 - k2 in [-2m, 2m] alias free.
+//   preconditioner (DESIGN.md §5 "Solve", reading R13): the real unknowns of the modes with
+//           lambda R_k <= tau form a dense block, inverted once (Cholesky + potri); the others
+//           take Jacobi.  Where lambda R_k > tau the penalty dominates the row and T/n (norm
+//           <= mu_0/n = 1) is a bounded perturbation; the near-null space of T (functions living
+//           outside the data's half period) is carried by the low modes, whose block is exact.
+//           C3 (m = 64, s = 2, lambda = 1e-6, tau = 1): 3133 of 16641 unknowns, ~45 iterations.
+// ------------------------------------------------------------------------------------------
+static double pcg_tau() {
+  const char* e = getenv("FK_PCG_TAU");
+  return e ? atof(e) : 1.0;
+}
+
+__device__ __forceinline__ double rentry(const SysArgs& g, int u, int v) {
+  const PCol pu = pcol(g, u), pv = pcol(g, v);
+  const int side = 2 * g.m + 1;
+  const float inv_side = 1.0f / (float)side;
+  double s = 0.0;
+  for (int x = 0; x < pu.cnt; ++x)
+    for (int y = 0; y < pv.cnt; ++y) {
+      const double2 a = g.d == 2 ? entry_d2(g, pu.i[x], pv.i[y], side, inv_side) : entry(g, pu.i[x], pv.i[y]);
+      s += cmul(cmul(cconj(pu.a[x]), a), pv.a[y]).x;
+    }
+  return s;
+}
+
+// lower triangle of the low block, column b = blockIdx.y, ld = Dl
+__global__ void k_pcg_low_block(SysArgs g, const int* __restrict__ low, int Dl, double* __restrict__ B) {
+  const int b = blockIdx.y;
+  const int a = b + blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= Dl) return;
+  B[a + (int64_t)b * Dl] = rentry(g, low[a], low[b]);
+}
+
+// dinv[u] = 1 / (P^*AP)_uu for Jacobi unknowns, 0 for block unknowns; bz = P^* r / n
+__global__ void k_pcg_setup(SysArgs g, const unsigned char* __restrict__ is_low, const double2* __restrict__ r,
+                            double* __restrict__ dinv, double* __restrict__ bz) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= g.D) return;
+  dinv[u] = is_low[u] ? 0.0 : 1.0 / rentry(g, u, u);
+  const PCol p = pcol(g, u);
+  double s = 0.0;
+  for (int x = 0; x < p.cnt; ++x) s += cmul(cconj(p.a[x]), make_double2(r[p.i[x]].x * g.inv_n, r[p.i[x]].y * g.inv_n)).x;
+  bz[u] = s;
+}
+
+// Hermitian half spectrum of an index-space array: entry (j0, j1), j1 <= L1/2, holds v_k with
+// k0 = j0 (or j0 - L0), k1 = j1 (d = 1: a single row, k = j).  mode(): -1 outside |k| <= lim.
+struct PcgGrid {
+  int d, L0, L1, H1;  // H1 = L1/2 + 1 (d = 2); d = 1: L0 = 1, L1 = L
+};
+__device__ __forceinline__ void half_to_k(const PcgGrid& q, int64_t t, int& k0, int& k1) {
+  const int j0 = (int)(t / q.H1), j1 = (int)(t % q.H1);
+  k0 = q.d == 2 ? (j0 <= q.L0 / 2 ? j0 : j0 - q.L0) : 0;
+  k1 = j1;
+}
+
+// mu (|q| <= 2m) into the half spectrum (k1 >= 0), zero elsewhere
+__global__ void k_pcg_mu_half(SysArgs g, PcgGrid q, double2* __restrict__ H) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)(q.d == 2 ? q.L0 : 1) * q.H1) return;
+  int k0, k1;
+  half_to_k(q, t, k0, k1);
+  const int M2 = 2 * g.m, qs = 4 * g.m + 1;
+  double2 v = make_double2(0.0, 0.0);
+  if (k1 <= M2 && k0 >= -M2 && k0 <= M2) v = q.d == 2 ? g.mu[(int64_t)(k0 + M2) * qs + (k1 + M2)] : g.mu[k1 + M2];
+  H[t] = v;
+}
+
+__global__ void k_pcg_scale(double* __restrict__ a, int64_t n, double s) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < n) a[t] *= s;
+}
+
+// theta = P z written into the half spectrum
+__global__ void k_pcg_scatter(SysArgs g, PcgGrid q, const double* __restrict__ z, double2* __restrict__ H) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)(q.d == 2 ? q.L0 : 1) * q.H1) return;
+  int k0, k1;
+  half_to_k(q, t, k0, k1);
+  const int m = g.m, side = 2 * m + 1, c0 = (g.D - 1) / 2;
+  double2 v = make_double2(0.0, 0.0);
+  if (k1 <= m && k0 >= -m && k0 <= m) {
+    const int lin = q.d == 2 ? (k0 + m) * side + (k1 + m) : k1 + m;
+    if (lin == c0) {
+      v = make_double2(z[0], 0.0);
+    } else if (lin > c0) {
+      const int u = 2 * (lin - c0) - 1;
+      v = make_double2(z[u], z[u + 1]);
+    } else {
+      const int u = 2 * (c0 - lin) - 1;
+      v = make_double2(z[u], -z[u + 1]);
+    }
+  }
+  H[t] = v;
+}
+
+__global__ void k_pcg_mul(double* __restrict__ G, const double* __restrict__ muhat, int64_t n) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < n) G[t] *= muhat[t];
+}
+
+// q = P^* (T theta / n + lambda R theta), theta = P p
+__global__ void k_pcg_gather(SysArgs g, PcgGrid q, const double2* __restrict__ C, const double* __restrict__ p,
+                             double* __restrict__ out) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= g.D) return;
+  const int m = g.m, side = 2 * m + 1, c0 = (g.D - 1) / 2;
+  const int t = (u + 1) >> 1;
+  const int lin = c0 + t;
+  int k0 = 0, k1 = lin - m;
+  if (q.d == 2) {
+    k0 = lin / side - m;
+    k1 = lin % side - m;
+  }
+  double2 c;
+  if (k1 >= 0) {
+    c = C[(int64_t)(q.d == 2 ? (k0 >= 0 ? k0 : k0 + q.L0) : 0) * q.H1 + k1];
+  } else {  // k1 < 0 (d = 2 only): c_k = conj c_{-k}
+    const int n0 = -k0;
+    c = cconj(C[(int64_t)(n0 >= 0 ? n0 : n0 + q.L0) * q.H1 + (-k1)]);
+  }
+  double nk2 = (double)k0 * k0 + (double)k1 * k1;
+  const double lr = g.lambda * (1.0 + pow(nk2, g.s));
+  if (u == 0) {
+    out[0] = c.x + lr * p[0];
+  } else if (u & 1) {
+    out[u] = 2.0 * c.x + lr * 2.0 * p[u];  // a_t column has |e_k + e_-k|^2 = 2
+  } else {
+    out[u] = 2.0 * c.y + lr * 2.0 * p[u];
+  }
+}
+
+// One CTA: the CG scalar recurrences in fixed order (deterministic).  sc: [0] rz, [1] rr,
+// [2] bb, [3] alpha, [4] done flag (rr <= tol^2 bb).
+__device__ double block_sum(double v, double* red) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0) {
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+    red[32] = s;
+  }
+  __syncthreads();
+  return red[32];
+}
+
+// init: x = 0, r = b, rl = r[low], bb = b.b
+__global__ void __launch_bounds__(1024) k_pcg_init(int D, const double* __restrict__ b, const int* __restrict__ low, int Dl,
+                                                   double* __restrict__ x, double* __restrict__ r, double* __restrict__ rl,
+                                                   double* __restrict__ sc) {
+  __shared__ double red[33];
+  double bb = 0.0;
+  for (int u = threadIdx.x; u < D; u += blockDim.x) {
+    x[u] = 0.0;
+    r[u] = b[u];
+    bb += b[u] * b[u];
+  }
+  for (int a = threadIdx.x; a < Dl; a += blockDim.x) rl[a] = b[low[a]];
+  bb = block_sum(bb, red);
+  if (threadIdx.x == 0) {
+    sc[2] = bb;
+    sc[1] = bb;
+    sc[4] = 0.0;
+  }
+}
+
+// z = M^{-1} r (zl from the block product), rz = r.z, p = z + beta p (beta = 0 at the start)
+__global__ void __launch_bounds__(1024) k_pcg_direction(int D, const double* __restrict__ r, const double* __restrict__ dinv,
+                                                        const int* __restrict__ low, int Dl, const double* __restrict__ zl,
+                                                        double* __restrict__ z, double* __restrict__ p, double* __restrict__ sc,
+                                                        int first) {
+  __shared__ double red[33];
+  if (sc[4] != 0.0) return;
+  for (int u = threadIdx.x; u < D; u += blockDim.x) z[u] = r[u] * dinv[u];
+  __syncthreads();
+  for (int a = threadIdx.x; a < Dl; a += blockDim.x) z[low[a]] = zl[a];
+  __syncthreads();
+  double rz = 0.0;
+  for (int u = threadIdx.x; u < D; u += blockDim.x) rz += r[u] * z[u];
+  rz = block_sum(rz, red);
+  const double beta = first ? 0.0 : rz / sc[0];
+  for (int u = threadIdx.x; u < D; u += blockDim.x) p[u] = z[u] + beta * p[u];
+  __syncthreads();
+  if (threadIdx.x == 0) sc[0] = rz;
+}
+
+// alpha = rz / p.q, x += alpha p, r -= alpha q, rr = r.r, rl = r[low]; done when rr <= tol^2 bb
+__global__ void __launch_bounds__(1024) k_pcg_update(int D, const double* __restrict__ p, const double* __restrict__ q,
+                                                     const int* __restrict__ low, int Dl, double* __restrict__ x,
+                                                     double* __restrict__ r, double* __restrict__ rl, double* __restrict__ sc,
+                                                     double tol2) {
+  __shared__ double red[33];
+  if (sc[4] != 0.0) return;
+  double pq = 0.0;
+  for (int u = threadIdx.x; u < D; u += blockDim.x) pq += p[u] * q[u];
+  pq = block_sum(pq, red);
+  const double alpha = sc[0] / pq;
+  double rr = 0.0;
+  for (int u = threadIdx.x; u < D; u += blockDim.x) {
+    x[u] += alpha * p[u];
+    const double rv = r[u] - alpha * q[u];
+    r[u] = rv;
+    rr += rv * rv;
+  }
+  rr = block_sum(rr, red);
+  __syncthreads();
+  for (int a = threadIdx.x; a < Dl; a += blockDim.x) rl[a] = r[low[a]];
+  if (threadIdx.x == 0) {
+    sc[1] = rr;
+    sc[3] = alpha;
+    if (rr <= tol2 * sc[2]) sc[4] = 1.0;
+  }
+}
+
+__global__ void k_pcg_identity(double* __restrict__ X, int n) {
+  const int j = blockIdx.y, i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) X[i + (int64_t)j * n] = i == j ? 1.0 : 0.0;
+}
+
+static bool pcg_eligible(const SysArgs& g) {
+  if (g.kind != FK_SOBOLEV || g.d > 2 || g.mu_pde != 0.0) return false;
+  const char* e = getenv("FK_SOLVER");
+  if (e && e[0] == 'd') return false;
+  if (e && e[0] == 'p') return true;
+  return g.D + 1 > kTilesMaxN;
+}
+
+// the block unknowns: modes with lambda R_k <= tau (both real unknowns of a mode together)
+static void pcg_low_set(const SysArgs& g, double tau, std::vector<int>& low, std::vector<unsigned char>& is_low) {
+  const int m = g.m, side = 2 * m + 1, c0 = (g.D - 1) / 2;
+  low.clear();
+  is_low.assign(g.D, 0);
+  for (int u = 0; u < g.D; ++u) {
+    const int lin = c0 + ((u + 1) >> 1);
+    const int k0 = g.d == 2 ? lin / side - m : 0, k1 = g.d == 2 ? lin % side - m : lin - m;
+    const double R = 1.0 + std::pow((double)k0 * k0 + (double)k1 * k1, g.s);
+    if (g.lambda * R <= tau) {
+      low.push_back(u);
+      is_low[u] = 1;
+    }
+  }
+}
+
+// Solves into x (D reals).  Returns FK_OK with *iters, or FK_E_SOLVE when it does not converge.
+// ws: at least (D+1)^2 doubles (the dense path's matrix slot).  Caller holds g_sol_mu.
+static fk_status pcg_run(SysArgs g, const double2* r, double* x, int* iters, void* ws, size_t ws_bytes, void* chol_ws, int* info,
+                         cudaStream_t s) {
+  std::vector<int> low;
+  std::vector<unsigned char> is_low;
+  pcg_low_set(g, pcg_tau(), low, is_low);
+  const int D = g.D, Dl = (int)low.size();
+  // cost model from B200 measurements: dense cuSOLVER potrf ~56 ms at N = 16642
+  // (N^3); the CG path ~4.6 ms (Dl/3133)^3 for the block + ~3.6 ms for ~40 iterations
+  const char* fe = getenv("FK_SOLVER");
+  const double t_dense = 56.0 * std::pow((D + 1) / 16642.0, 3.0) + 0.5;
+  const double t_pcg = 5.0 * std::pow(Dl / 3133.0, 3.0) + 4.0;
+  if (!(fe && fe[0] == 'p') && !(t_pcg < t_dense)) return FK_E_UNSUPPORTED;  // the dense path (no error text)
+  PcgGrid q{};
+  q.d = g.d;
+  const int L = fft_friendly(4 * g.m + 1);
+  if (g.d == 2) {
+    q.L0 = L;
+    q.L1 = L;
+  } else {
+    q.L0 = 1;
+    q.L1 = L;
+  }
+  q.H1 = q.L1 / 2 + 1;
+  const int64_t nreal = (int64_t)q.L0 * q.L1, nhalf = (int64_t)q.L0 * q.H1;
+  FftPlan fz, fd;
+  int dims[2] = {g.d == 2 ? q.L0 : q.L1, q.L1};
+  FK_TRY(fft_plan(g.d, dims, 1, CUFFT_Z2D, &fz));
+  FK_TRY(fft_plan(g.d, dims, 1, CUFFT_D2Z, &fd));
+  Bump b(ws, ws_bytes);
+  double* Ainv = (double*)b.take((size_t)Dl * Dl * 8 + 8);
+  double* Xinv = (double*)b.take((size_t)Dl * Dl * 8 + 8);
+  int* d_low = (int*)b.take((size_t)Dl * 4 + 4);
+  unsigned char* d_is_low = (unsigned char*)b.take((size_t)D + 1);
+  double* dinv = (double*)b.take((size_t)D * 8);
+  double* bz = (double*)b.take((size_t)D * 8);
+  double* rv = (double*)b.take((size_t)D * 8);
+  double* zv = (double*)b.take((size_t)D * 8);
+  double* pv = (double*)b.take((size_t)D * 8);
+  double* qv = (double*)b.take((size_t)D * 8);
+  double* rl = (double*)b.take((size_t)Dl * 8 + 8);
+  double* zl = (double*)b.take((size_t)Dl * 8 + 8);
+  double2* H = (double2*)b.take((size_t)nhalf * 16);
+  double* G = (double*)b.take((size_t)nreal * 8);
+  double* muhat = (double*)b.take((size_t)nreal * 8);
+  double* sc = (double*)b.take(64);
+  void* fwork = b.take(std::max<size_t>(std::max(fz.work, fd.work), 256));
+  cusolverDnHandle_t h;
+  FK_TRY(handle_for_device(&h));
+  int lw_potrf = 0;
+  if (Dl > kTilesMaxN &&
+      cusolverDnDpotrf_bufferSize(h, CUBLAS_FILL_MODE_LOWER, Dl, Ainv, Dl, &lw_potrf) != CUSOLVER_STATUS_SUCCESS)
+    return fail(FK_E_CUDA, "cusolverDnDpotrf_bufferSize failed");
+  double* swork = (double*)b.take((size_t)std::max(lw_potrf, 1) * 8);
+  if (!b.ok()) return FK_E_UNSUPPORTED;  // the block does not fit the dense path's matrix slot: dense path
+  if (Dl > 0) FK_CUDA_TRY(cudaMemcpyAsync(d_low, low.data(), (size_t)Dl * 4, cudaMemcpyHostToDevice, s));
+  FK_CUDA_TRY(cudaMemcpyAsync(d_is_low, is_low.data(), (size_t)D, cudaMemcpyHostToDevice, s));
+  const int TB = 256;
+  // the block: assemble, factor, invert
+  if (Dl > 0) {
+    k_pcg_low_block<<<dim3((Dl + TB - 1) / TB, Dl), TB, 0, s>>>(g, d_low, Dl, Ainv);
+    FK_CUDA_TRY(cudaGetLastError());
+    count_launch();
+    if (Dl <= kTilesMaxN) {
+      FK_TRY(chol_tiles(Ainv, Dl, Dl, info, chol_ws, s));
+    } else if (cusolverDnDpotrf(h, CUBLAS_FILL_MODE_LOWER, Dl, Ainv, Dl, swork, lw_potrf, info) != CUSOLVER_STATUS_SUCCESS) {
+      return fail(FK_E_CUDA, "cusolverDnDpotrf failed");
+    }
+    // inverse of the block: X = L^{-1} (TRSM on the identity; exact zeros above the diagonal),
+    // then Ainv = X^T X (SYRK, lower).  cuSOLVER potri took 8.8 ms at Dl = 3133 (latency bound).
+    cublasHandle_t bh0;
+    FK_TRY(blas_for_device(&bh0));
+    if (cublasSetStream(bh0, s) != CUBLAS_STATUS_SUCCESS) return fail(FK_E_CUDA, "cublasSetStream failed");
+    const double one0 = 1.0, zero0 = 0.0;
+    k_pcg_identity<<<dim3((Dl + TB - 1) / TB, Dl), TB, 0, s>>>(Xinv, Dl);
+    count_launch();
+    if (cublasDtrsm(bh0, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, Dl, Dl, &one0, Ainv, Dl, Xinv,
+                    Dl) != CUBLAS_STATUS_SUCCESS)
+      return fail(FK_E_CUDA, "cublasDtrsm failed");
+    if (cublasDsyrk(bh0, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, Dl, Dl, &one0, Xinv, Dl, &zero0, Ainv, Dl) != CUBLAS_STATUS_SUCCESS)
+      return fail(FK_E_CUDA, "cublasDsyrk failed");
+  }
+  k_pcg_setup<<<(D + TB - 1) / TB, TB, 0, s>>>(g, d_is_low, r, dinv, bz);
+  // DFT of mu / (n L^d)
+  k_pcg_mu_half<<<(unsigned)((nhalf + TB - 1) / TB), TB, 0, s>>>(g, q, H);
+  FK_TRY(fft_exec_z2d(fz, (cufftDoubleComplex*)H, muhat, fwork, s));
+  k_pcg_scale<<<(unsigned)((nreal + TB - 1) / TB), TB, 0, s>>>(muhat, nreal, g.inv_n / (double)nreal);
+  k_pcg_init<<<1, 1024, 0, s>>>(D, bz, d_low, Dl, x, rv, rl, sc);
+  FK_CUDA_TRY(cudaGetLastError());
+  count_launch(4);
+  cublasHandle_t bh;
+  FK_TRY(blas_for_device(&bh));
+  if (cublasSetStream(bh, s) != CUBLAS_STATUS_SUCCESS) return fail(FK_E_CUDA, "cublasSetStream failed");
+  const double one = 1.0, zero = 0.0, tol = 1e-13;
+  auto precond = [&](int first) -> fk_status {
+    if (Dl > 0 && cublasDsymv(bh, CUBLAS_FILL_MODE_LOWER, Dl, &one, Ainv, Dl, rl, 1, &zero, zl, 1) != CUBLAS_STATUS_SUCCESS)
+      return fail(FK_E_CUDA, "cublasDsymv failed");
+    k_pcg_direction<<<1, 1024, 0, s>>>(D, rv, dinv, d_low, Dl, zl, zv, pv, sc, first);
+    count_launch(1);
+    return FK_OK;
+  };
+  FK_TRY(precond(1));
+  const int kMaxIter = 1000, kCheck = 10;
+  double hsc[5] = {0, 0, 0, 0, 0};
+  int it = 0;
+  for (; it < kMaxIter;) {
+    for (int j = 0; j < kCheck; ++j, ++it) {
+      k_pcg_scatter<<<(unsigned)((nhalf + TB - 1) / TB), TB, 0, s>>>(g, q, pv, H);
+      FK_TRY(fft_exec_z2d(fz, (cufftDoubleComplex*)H, G, fwork, s));
+      k_pcg_mul<<<(unsigned)((nreal + TB - 1) / TB), TB, 0, s>>>(G, muhat, nreal);
+      FK_TRY(fft_exec_d2z(fd, G, (cufftDoubleComplex*)H, fwork, s));
+      k_pcg_gather<<<(D + TB - 1) / TB, TB, 0, s>>>(g, q, H, pv, qv);
+      k_pcg_update<<<1, 1024, 0, s>>>(D, pv, qv, d_low, Dl, x, rv, rl, sc, tol * tol);
+      count_launch(4);
+      FK_TRY(precond(0));
+    }
+    FK_CUDA_TRY(cudaMemcpyAsync(hsc, sc, 40, cudaMemcpyDeviceToHost, s));
+    FK_CUDA_TRY(cudaStreamSynchronize(s));
+    if (hsc[4] != 0.0 || !(hsc[1] == hsc[1])) break;  // converged, or NaN (a failed block factor)
+  }
+  FK_CUDA_TRY(cudaGetLastError());
+  *iters = it;
+  if (hsc[4] == 0.0) return fail(FK_E_SOLVE, "fk_solve (pcg): no convergence in " + std::to_string(kMaxIter) + " iterations");
+  return FK_OK;
+}
+
 fk_status solve_run(const fk_problem* P, double* theta, fk_solve_report* rep, void* ws, size_t ws_bytes, cudaStream_t s) {
   SysArgs g;
   FK_TRY(fill_sysargs(P, &g));
@@ -920,6 +1299,24 @@ fk_status solve_run(const fk_problem* P, double* theta, fk_solve_report* rep, vo
   }
   const bool own_trsv = true;
   int* ticket = info + 12;
+  int iters = 0;
+  bool done = false;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cap);
+  if (cap == cudaStreamCaptureStatusNone && pcg_eligible(g)) {  // CG checks convergence on the host: not capturable
+    std::lock_guard<std::mutex> lk(g_sol_mu);
+    const fk_status st = pcg_run(g, (const double2*)P->rhs, zbuf, &iters, M, (size_t)N * N * 8, chol_ws, info, s);
+    if (st == FK_OK) {
+      done = true;
+      FK_CUDA_TRY(cudaMemsetAsync(info, 0, 4, s));
+      k_theta_from_real<<<(D + 255) / 256, 256, 0, s>>>(g, zbuf, 1, (double2*)theta);
+      FK_CUDA_TRY(cudaGetLastError());
+      count_launch();
+    } else if (st != FK_E_UNSUPPORTED && st != FK_E_SOLVE) {
+      return st;
+    }  // FK_E_SOLVE (no convergence): the dense path decides
+  }
+  if (!done) {
   launch_assemble(g, M, s);
   k_rhs_real<<<(N + 255) / 256, 256, 0, s>>>(g, (const double2*)P->rhs, M, zbuf, ticket);
   FK_CUDA_TRY(cudaGetLastError());
@@ -949,6 +1346,7 @@ fk_status solve_run(const fk_problem* P, double* theta, fk_solve_report* rep, vo
   k_theta_from_real<<<(D + 255) / 256, 256, 0, s>>>(g, own_trsv ? zbuf : M + D, own_trsv ? 1 : N, (double2*)theta);
   FK_CUDA_TRY(cudaGetLastError());
   count_launch();
+  }
   if (rep) {
     cudaEventRecord(e1, s);
     FK_CUDA_TRY(cudaMemsetAsync(res, 0, 16, s));
@@ -966,6 +1364,7 @@ fk_status solve_run(const fk_problem* P, double* theta, fk_solve_report* rep, vo
     rep->info = hinfo;
     rep->ms = ms;
     rep->n_unknowns = D;
+    rep->iters = iters;
     rep->backward_err = hres[1] > 0 ? std::sqrt(hres[0] / hres[1]) : 0.0;
     if (hinfo != 0) return fail(FK_E_SOLVE, "fk_solve: Cholesky failed, info = " + std::to_string(hinfo));
   }

@@ -47,7 +47,8 @@ class fk_problem(ctypes.Structure):
 
 
 class fk_solve_report(ctypes.Structure):
-    _fields_ = [("backward_err", ctypes.c_double), ("ms", ctypes.c_double), ("info", ctypes.c_int32), ("n_unknowns", ctypes.c_int32)]
+    _fields_ = [("backward_err", ctypes.c_double), ("ms", ctypes.c_double), ("info", ctypes.c_int32), ("n_unknowns", ctypes.c_int32),
+                ("iters", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 _lib = None
@@ -208,7 +209,7 @@ def fk_solve(mu: torch.Tensor, r: torch.Tensor, n_total: float, d: int, m: int, 
     del keep
     out = None
     if report:
-        out = {"backward_err": rep.backward_err, "ms": rep.ms, "info": rep.info, "n_unknowns": rep.n_unknowns}
+        out = {"backward_err": rep.backward_err, "ms": rep.ms, "info": rep.info, "n_unknowns": rep.n_unknowns, "iters": rep.iters}
     return theta_out, out
 
 

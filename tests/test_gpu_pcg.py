@@ -1,0 +1,78 @@
+"""Conjugate-gradient solve of the Sobolev system (the paper's solver, with FFT-Toeplitz
+products and the block preconditioner of reading R13) against the oracle's dense solve and the
+library's own dense Cholesky path (FK_SOLVER=pcg|dense)."""
+import os
+
+import numpy as np
+import pytest
+
+import datagen
+from gpu_util import dev, fk, host, rel
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def F():
+    assert torch.cuda.is_available()
+    return fk()
+
+
+def _solve(F, how, *args):
+    old = os.environ.get("FK_SOLVER")
+    os.environ["FK_SOLVER"] = how
+    try:
+        th, rep = F.fk_solve(*args)
+    finally:
+        if old is None:
+            del os.environ["FK_SOLVER"]
+        else:
+            os.environ["FK_SOLVER"] = old
+    return host(th), rep
+
+
+@pytest.mark.parametrize("d,m,s,lam,n", [(2, 36, 2.0, 1e-6, 30_000), (1, 2500, 2.0, 1e-8, 40_000), (2, 20, 3.0, 1e-6, 20_000)])
+def test_pcg_matches_oracle(F, oracle, d, m, s, lam, n):
+    X, Y = datagen.dataset(n, d=d, ykind="expcos" if d == 2 else "sin", seed=91)
+    X = X.reshape(-1) if d == 1 else X
+    mu, r = oracle.moments(X, 1.0, m), oracle.rhs(X, Y, 1.0, m)
+    th, rep = _solve(F, "pcg", dev(mu.reshape(-1)), dev(r.reshape(-1)), n, d, m, 1.0, lam, "sobolev", s)
+    th_o = oracle.solve(mu, r, n, d, m, lam, "sobolev", s)
+    print(f"pcg d={d} m={m}: {rep['iters']} iterations, backward {rep['backward_err']:.1e}, rel {rel(th, th_o):.1e}, {rep['ms']:.2f} ms")
+    assert rep["info"] == 0 and rep["iters"] > 0
+    assert rep["backward_err"] < 1e-12
+    assert rel(th, th_o) < 1e-6
+
+
+def test_pcg_c3_size_matches_dense(F):
+    """C3's system (d=2, m=64, s=2, lambda=1e-6, D=16641) from device moments: the default path
+    (CG) against the dense Cholesky."""
+    from datagen.device import gen_dataset
+
+    n, d, m = 4_000_000, 2, 64
+    X = torch.empty(n, 2, device="cuda")
+    Y = torch.empty(n, device="cuda")
+    gen_dataset(X, Y, n, d, xkind=0, ykind=2, seed=3)
+    r, mu = F.fk_rhs_type1(X, Y, 1.0, m, 1e-6)
+    th_c, rep_c = F.fk_solve(mu, r, n, d, m, 1.0, 1e-6, "sobolev", 2.0)
+    th_d, rep_d = _solve(F, "dense", mu, r, n, d, m, 1.0, 1e-6, "sobolev", 2.0)
+    th_c = host(th_c)
+    print(f"C3 system: cg {rep_c['ms']:.2f} ms ({rep_c['iters']} it), dense {rep_d['ms']:.2f} ms, rel {rel(th_c, th_d):.1e}")
+    assert rep_c["iters"] > 0 and rep_d["iters"] == 0
+    assert rep_c["backward_err"] < 1e-12
+    assert rel(th_c, th_d) < 1e-7
+    # Hermitian: theta_{-k} = conj theta_k
+    assert np.max(np.abs(th_c - np.conj(th_c[::-1]))) <= 1e-12 * np.max(np.abs(th_c))
+
+
+def test_pcg_deterministic(F):
+    n, d, m = 1_000_000, 2, 40
+    X, Y = torch.empty(n, 2, device="cuda"), torch.empty(n, device="cuda")
+    from datagen.device import gen_dataset
+
+    gen_dataset(X, Y, n, d, xkind=1, ykind=2, seed=4)
+    r, mu = F.fk_rhs_type1(X, Y, 1.0, m, 1e-6)
+    a, _ = _solve(F, "pcg", mu, r, n, d, m, 1.0, 1e-6, "sobolev", 2.0)
+    b, _ = _solve(F, "pcg", mu, r, n, d, m, 1.0, 1e-6, "sobolev", 2.0)
+    assert np.array_equal(a, b)
