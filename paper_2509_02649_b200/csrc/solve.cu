@@ -896,9 +896,11 @@ fk_status path_validate_run(const fk_problem* Pv, const double* theta, int nlam,
 //           outside the data's half period) is carried by the low modes, whose block is exact.
 //           C3 (m = 64, s = 2, lambda = 1e-6, tau = 1): 3133 of 16641 unknowns, ~45 iterations.
 // ------------------------------------------------------------------------------------------
+// block threshold tau: lambda R_k <= tau.  C3 (B200): tau = 0.25 / 0.5 / 1 / 2 -> 65 / 47 / 34 / 25
+// iterations, 5.82 / 5.81 / 6.70 / 10.2 ms per solve
 static double pcg_tau() {
   const char* e = getenv("FK_PCG_TAU");
-  return e ? atof(e) : 1.0;
+  return e ? atof(e) : 0.5;
 }
 
 __device__ __forceinline__ double rentry(const SysArgs& g, int u, int v) {
@@ -914,20 +916,20 @@ __device__ __forceinline__ double rentry(const SysArgs& g, int u, int v) {
   return s;
 }
 
-// lower triangle of the low block, column b = blockIdx.y, ld = Dl
-__global__ void k_pcg_low_block(SysArgs g, const int* __restrict__ low, int Dl, double* __restrict__ B) {
+// lower triangle of the low block, column b = blockIdx.y
+__global__ void k_pcg_low_block(SysArgs g, const int* __restrict__ low, int Dl, double* __restrict__ B, int64_t ld) {
   const int b = blockIdx.y;
   const int a = b + blockIdx.x * blockDim.x + threadIdx.x;
   if (a >= Dl) return;
-  B[a + (int64_t)b * Dl] = rentry(g, low[a], low[b]);
+  B[a + b * ld] = rentry(g, low[a], low[b]);
 }
 
 // dinv[u] = 1 / (P^*AP)_uu for Jacobi unknowns, 0 for block unknowns; bz = P^* r / n
-__global__ void k_pcg_setup(SysArgs g, const unsigned char* __restrict__ is_low, const double2* __restrict__ r,
-                            double* __restrict__ dinv, double* __restrict__ bz) {
+__global__ void k_pcg_setup(SysArgs g, const int* __restrict__ lowpos, const double2* __restrict__ r, double* __restrict__ dinv,
+                            double* __restrict__ bz) {
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
   if (u >= g.D) return;
-  dinv[u] = is_low[u] ? 0.0 : 1.0 / rentry(g, u, u);
+  dinv[u] = lowpos[u] >= 0 ? 0.0 : 1.0 / rentry(g, u, u);
   const PCol p = pcol(g, u);
   double s = 0.0;
   for (int x = 0; x < p.cnt; ++x) s += cmul(cconj(p.a[x]), make_double2(r[p.i[x]].x * g.inv_n, r[p.i[x]].y * g.inv_n)).x;
@@ -962,10 +964,44 @@ __global__ void k_pcg_scale(double* __restrict__ a, int64_t n, double s) {
   if (t < n) a[t] *= s;
 }
 
-// theta = P z written into the half spectrum
-__global__ void k_pcg_scatter(SysArgs g, PcgGrid q, const double* __restrict__ z, double2* __restrict__ H) {
+// Deterministic grid-wide sum: every CTA writes its partial, the last CTA to arrive (atomic
+// ticket) adds the partials in CTA order (lane-strided, then a fixed xor tree) and runs fin(sum)
+// on thread 0.  sc scalars: [0] rz, [1] rr, [2] bb, [3] alpha, [4] done, [5] beta.
+template <class Fin>
+__device__ __forceinline__ void grid_sum(double v, double* __restrict__ part, unsigned* __restrict__ ticket, Fin fin) {
+  __shared__ double red[32];
+  __shared__ int last;
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+    part[blockIdx.x] = s;
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x < 32) {
+    __threadfence();
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += 32) acc += __ldcg(part + i);
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (threadIdx.x == 0) {
+      *ticket = 0;
+      fin(acc);
+    }
+  }
+}
+
+// p_new = z + beta p_old (beta = sc[5]) for every unknown, theta = P p_new into the half spectrum.
+// Each half-spectrum entry with |k| <= m carries one mode pair (its own or its mirror's); entries
+// on the k1 = 0 column carry a pair twice and write identical values.
+__global__ void k_pcg_scatter(SysArgs g, PcgGrid q, const double* __restrict__ z, const double* __restrict__ p_old,
+                              double* __restrict__ p_new, double2* __restrict__ H, const double* __restrict__ sc) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= (int64_t)(q.d == 2 ? q.L0 : 1) * q.H1) return;
+  if (t >= (int64_t)(q.d == 2 ? q.L0 : 1) * q.H1 || sc[4] != 0.0) return;
+  const double beta = sc[5];
   int k0, k1;
   half_to_k(q, t, k0, k1);
   const int m = g.m, side = 2 * m + 1, c0 = (g.D - 1) / 2;
@@ -973,141 +1009,198 @@ __global__ void k_pcg_scatter(SysArgs g, PcgGrid q, const double* __restrict__ z
   if (k1 <= m && k0 >= -m && k0 <= m) {
     const int lin = q.d == 2 ? (k0 + m) * side + (k1 + m) : k1 + m;
     if (lin == c0) {
-      v = make_double2(z[0], 0.0);
-    } else if (lin > c0) {
-      const int u = 2 * (lin - c0) - 1;
-      v = make_double2(z[u], z[u + 1]);
+      const double a = z[0] + beta * p_old[0];
+      p_new[0] = a;
+      v = make_double2(a, 0.0);
     } else {
-      const int u = 2 * (c0 - lin) - 1;
-      v = make_double2(z[u], -z[u + 1]);
+      const int u = 2 * (lin > c0 ? lin - c0 : c0 - lin) - 1;
+      const double a = z[u] + beta * p_old[u], b = z[u + 1] + beta * p_old[u + 1];
+      p_new[u] = a;
+      p_new[u + 1] = b;
+      v = make_double2(a, lin > c0 ? b : -b);
     }
   }
   H[t] = v;
 }
 
-__global__ void k_pcg_mul(double* __restrict__ G, const double* __restrict__ muhat, int64_t n) {
+__global__ void k_pcg_mul(double* __restrict__ G, const double* __restrict__ muhat, int64_t n, const double* __restrict__ sc) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t < n) G[t] *= muhat[t];
+  if (t < n && sc[4] == 0.0) G[t] *= muhat[t];
 }
 
-// q = P^* (T theta / n + lambda R theta), theta = P p
-__global__ void k_pcg_gather(SysArgs g, PcgGrid q, const double2* __restrict__ C, const double* __restrict__ p,
-                             double* __restrict__ out) {
+// q = P^* (T theta / n + lambda R theta), theta = P p; alpha = rz / p.q
+__global__ void __launch_bounds__(256) k_pcg_gather(SysArgs g, PcgGrid q, const double2* __restrict__ C, const double* __restrict__ p,
+                                                    double* __restrict__ out, double* __restrict__ sc, double* __restrict__ part,
+                                                    unsigned* __restrict__ ticket) {
+  if (sc[4] != 0.0) return;
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
-  if (u >= g.D) return;
-  const int m = g.m, side = 2 * m + 1, c0 = (g.D - 1) / 2;
-  const int t = (u + 1) >> 1;
-  const int lin = c0 + t;
-  int k0 = 0, k1 = lin - m;
-  if (q.d == 2) {
-    k0 = lin / side - m;
-    k1 = lin % side - m;
+  double pq = 0.0;
+  if (u < g.D) {
+    const int m = g.m, side = 2 * m + 1, c0 = (g.D - 1) / 2;
+    const int t = (u + 1) >> 1;
+    const int lin = c0 + t;
+    int k0 = 0, k1 = lin - m;
+    if (q.d == 2) {
+      k0 = lin / side - m;
+      k1 = lin % side - m;
+    }
+    double2 c;
+    if (k1 >= 0) {
+      c = C[(int64_t)(q.d == 2 ? (k0 >= 0 ? k0 : k0 + q.L0) : 0) * q.H1 + k1];
+    } else {  // k1 < 0 (d = 2 only): c_k = conj c_{-k}
+      const int n0 = -k0;
+      c = cconj(C[(int64_t)(n0 >= 0 ? n0 : n0 + q.L0) * q.H1 + (-k1)]);
+    }
+    const double nk2 = (double)k0 * k0 + (double)k1 * k1;
+    const double lr = g.lambda * (1.0 + pow(nk2, g.s));
+    double o;
+    if (u == 0) o = c.x + lr * p[0];
+    else if (u & 1) o = 2.0 * (c.x + lr * p[u]);  // a_t column: |e_k + e_-k|^2 = 2
+    else o = 2.0 * (c.y + lr * p[u]);
+    out[u] = o;
+    pq = p[u] * o;
   }
-  double2 c;
-  if (k1 >= 0) {
-    c = C[(int64_t)(q.d == 2 ? (k0 >= 0 ? k0 : k0 + q.L0) : 0) * q.H1 + k1];
-  } else {  // k1 < 0 (d = 2 only): c_k = conj c_{-k}
-    const int n0 = -k0;
-    c = cconj(C[(int64_t)(n0 >= 0 ? n0 : n0 + q.L0) * q.H1 + (-k1)]);
+  grid_sum(pq, part, ticket, [&](double s) { sc[3] = sc[0] / s; });
+}
+
+// x += alpha p, r -= alpha q, rl = r[low], rr = r.r; done when rr <= tol^2 bb
+__global__ void __launch_bounds__(256) k_pcg_update(int D, const double* __restrict__ p, const double* __restrict__ qv,
+                                                    const int* __restrict__ lowpos, double* __restrict__ x,
+                                                    double* __restrict__ r, double* __restrict__ rl, double* __restrict__ sc,
+                                                    double tol2, double* __restrict__ part, unsigned* __restrict__ ticket) {
+  if (sc[4] != 0.0) return;
+  const double alpha = sc[3];
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  double rr = 0.0;
+  if (u < D) {
+    x[u] += alpha * p[u];
+    const double v = r[u] - alpha * qv[u];
+    r[u] = v;
+    rr = v * v;
+    const int a = lowpos[u];  // position in the block, -1 for Jacobi unknowns
+    if (a >= 0) rl[a] = v;
   }
-  double nk2 = (double)k0 * k0 + (double)k1 * k1;
-  const double lr = g.lambda * (1.0 + pow(nk2, g.s));
-  if (u == 0) {
-    out[0] = c.x + lr * p[0];
-  } else if (u & 1) {
-    out[u] = 2.0 * c.x + lr * 2.0 * p[u];  // a_t column has |e_k + e_-k|^2 = 2
+  grid_sum(rr, part, ticket, [&](double s) {
+    sc[1] = s;
+    sc[6] += 1.0;  // iterations
+    if (s <= tol2 * sc[2]) sc[4] = 1.0;
+  });
+}
+
+// z = M^{-1} r: block rows z[low[a]] = (Ainv rl)_a, one warp per row reading column a of the
+// symmetric Ainv (contiguous); Jacobi rows z = dinv r.  rz = r.z; beta = rz / rz_old (0 first).
+__global__ void __launch_bounds__(256) k_pcg_precond(int D, const double* __restrict__ r, const double* __restrict__ dinv,
+                                                     const int* __restrict__ lowpos, const int* __restrict__ low, int Dl,
+                                                     const double* __restrict__ Ainv, int64_t lda, const double* __restrict__ rl,
+                                                     double* __restrict__ z, double* __restrict__ sc, int first, int nlow_ctas,
+                                                     double* __restrict__ part, unsigned* __restrict__ ticket) {
+  if (sc[4] != 0.0) return;
+  double rz = 0.0;
+  if ((int)blockIdx.x < nlow_ctas) {
+    const int a = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (a < Dl) {
+      const double* col = Ainv + (int64_t)a * lda;
+      double acc = 0.0;
+      const int D2 = Dl & ~1;
+      for (int b = 2 * lane; b < D2; b += 64) {
+        const double2 av = __ldg(reinterpret_cast<const double2*>(col + b));
+        const double2 rv = __ldg(reinterpret_cast<const double2*>(rl + b));
+        acc = fma(av.x, rv.x, acc);
+        acc = fma(av.y, rv.y, acc);
+      }
+      if ((Dl & 1) && lane == 0) acc = fma(col[Dl - 1], rl[Dl - 1], acc);
+      for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) {
+        z[low[a]] = acc;
+        rz = rl[a] * acc;
+      }
+    }
   } else {
-    out[u] = 2.0 * c.y + lr * 2.0 * p[u];
+    const int u = (blockIdx.x - nlow_ctas) * blockDim.x + threadIdx.x;
+    if (u < D && lowpos[u] < 0) {
+      const double v = r[u] * dinv[u];
+      z[u] = v;
+      rz = r[u] * v;
+    }
   }
+  grid_sum(rz, part, ticket, [&](double s) {
+    sc[5] = first ? 0.0 : s / sc[0];
+    sc[0] = s;
+  });
 }
 
-// One CTA: the CG scalar recurrences in fixed order (deterministic).  sc: [0] rz, [1] rr,
-// [2] bb, [3] alpha, [4] done flag (rr <= tol^2 bb).
-__device__ double block_sum(double v, double* red) {
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-  __syncthreads();
-  double s = 0.0;
-  if (threadIdx.x == 0) {
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
-    red[32] = s;
-  }
-  __syncthreads();
-  return red[32];
-}
-
-// init: x = 0, r = b, rl = r[low], bb = b.b
-__global__ void __launch_bounds__(1024) k_pcg_init(int D, const double* __restrict__ b, const int* __restrict__ low, int Dl,
-                                                   double* __restrict__ x, double* __restrict__ r, double* __restrict__ rl,
-                                                   double* __restrict__ sc) {
-  __shared__ double red[33];
+// x = 0, r = b, rl = b[low], bb = b.b
+__global__ void __launch_bounds__(256) k_pcg_init(int D, const double* __restrict__ b, const int* __restrict__ low, int Dl,
+                                                  double* __restrict__ x, double* __restrict__ r, double* __restrict__ rl,
+                                                  double* __restrict__ sc, double* __restrict__ part, unsigned* __restrict__ ticket) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
   double bb = 0.0;
-  for (int u = threadIdx.x; u < D; u += blockDim.x) {
+  if (u < D) {
     x[u] = 0.0;
     r[u] = b[u];
-    bb += b[u] * b[u];
+    bb = b[u] * b[u];
   }
-  for (int a = threadIdx.x; a < Dl; a += blockDim.x) rl[a] = b[low[a]];
-  bb = block_sum(bb, red);
-  if (threadIdx.x == 0) {
-    sc[2] = bb;
-    sc[1] = bb;
+  if (u < Dl) rl[u] = b[low[u]];
+  grid_sum(bb, part, ticket, [&](double s) {
+    sc[2] = s;
+    sc[1] = s;
     sc[4] = 0.0;
-  }
+  });
 }
 
-// z = M^{-1} r (zl from the block product), rz = r.z, p = z + beta p (beta = 0 at the start)
-__global__ void __launch_bounds__(1024) k_pcg_direction(int D, const double* __restrict__ r, const double* __restrict__ dinv,
-                                                        const int* __restrict__ low, int Dl, const double* __restrict__ zl,
-                                                        double* __restrict__ z, double* __restrict__ p, double* __restrict__ sc,
-                                                        int first) {
-  __shared__ double red[33];
-  if (sc[4] != 0.0) return;
-  for (int u = threadIdx.x; u < D; u += blockDim.x) z[u] = r[u] * dinv[u];
-  __syncthreads();
-  for (int a = threadIdx.x; a < Dl; a += blockDim.x) z[low[a]] = zl[a];
-  __syncthreads();
-  double rz = 0.0;
-  for (int u = threadIdx.x; u < D; u += blockDim.x) rz += r[u] * z[u];
-  rz = block_sum(rz, red);
-  const double beta = first ? 0.0 : rz / sc[0];
-  for (int u = threadIdx.x; u < D; u += blockDim.x) p[u] = z[u] + beta * p[u];
-  __syncthreads();
-  if (threadIdx.x == 0) sc[0] = rz;
+__global__ void k_pcg_unit_diag(double* __restrict__ X, int64_t ld, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) X[i + i * ld] = 1.0;
 }
 
-// alpha = rz / p.q, x += alpha p, r -= alpha q, rr = r.r, rl = r[low]; done when rr <= tol^2 bb
-__global__ void __launch_bounds__(1024) k_pcg_update(int D, const double* __restrict__ p, const double* __restrict__ q,
-                                                     const int* __restrict__ low, int Dl, double* __restrict__ x,
-                                                     double* __restrict__ r, double* __restrict__ rl, double* __restrict__ sc,
-                                                     double tol2) {
-  __shared__ double red[33];
-  if (sc[4] != 0.0) return;
-  double pq = 0.0;
-  for (int u = threadIdx.x; u < D; u += blockDim.x) pq += p[u] * q[u];
-  pq = block_sum(pq, red);
-  const double alpha = sc[0] / pq;
-  double rr = 0.0;
-  for (int u = threadIdx.x; u < D; u += blockDim.x) {
-    x[u] += alpha * p[u];
-    const double rv = r[u] - alpha * q[u];
-    r[u] = rv;
-    rr += rv * rv;
-  }
-  rr = block_sum(rr, red);
-  __syncthreads();
-  for (int a = threadIdx.x; a < Dl; a += blockDim.x) rl[a] = r[low[a]];
-  if (threadIdx.x == 0) {
-    sc[1] = rr;
-    sc[3] = alpha;
-    if (rr <= tol2 * sc[2]) sc[4] = 1.0;
-  }
-}
-
-__global__ void k_pcg_identity(double* __restrict__ X, int n) {
+// lower -> upper (column-major, ld): the block inverse is read by columns as rows
+__global__ void k_pcg_symmetrize(double* __restrict__ A, int64_t ld, int n) {
   const int j = blockIdx.y, i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) X[i + (int64_t)j * n] = i == j ? 1.0 : 0.0;
+  if (i < n && i > j) A[j + i * ld] = A[i + j * ld];
+}
+
+// X = L^{-1} (lower, n x n) by recursive halving: X21 = -X22 L21 X11 (two TRMMs, n^3/3 flops at
+// GEMM-like rates); leaves of 256 columns by TRSM on the identity.  X is zero above the diagonal
+// and has a unit diagonal on entry; S: scratch of n^2/4 doubles.
+// leaves of the recursive inverse: cuBLAS TRSM / SYRK below this size (256: 6.87, 512: 6.70 ms at C3)
+constexpr int kPcgLeaf = 512;
+
+static fk_status tri_inv(cublasHandle_t bh, const double* L, int64_t ld, double* X, int64_t ldx, int n, double* S) {
+  const double one = 1.0, mone = -1.0;
+  if (n <= kPcgLeaf) {
+    if (cublasDtrsm(bh, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, n, n, &one, L, (int)ld, X, (int)ldx) !=
+        CUBLAS_STATUS_SUCCESS)
+      return fail(FK_E_CUDA, "cublasDtrsm failed");
+    return FK_OK;
+  }
+  const int n1 = ((n / 2) + 31) / 32 * 32, n2 = n - n1;
+  FK_TRY(tri_inv(bh, L, ld, X, ldx, n1, S));
+  FK_TRY(tri_inv(bh, L + n1 + n1 * ld, ld, X + n1 + n1 * ldx, ldx, n2, S));
+  if (cublasDtrmm(bh, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, n2, n1, &one, X, (int)ldx, L + n1,
+                  (int)ld, S, n2) != CUBLAS_STATUS_SUCCESS ||
+      cublasDtrmm(bh, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, n2, n1, &mone, X + n1 + n1 * ldx,
+                  (int)ldx, S, n2, X + n1, (int)ldx) != CUBLAS_STATUS_SUCCESS)
+    return fail(FK_E_CUDA, "cublasDtrmm failed");
+  return FK_OK;
+}
+
+// lower(A) = X^T X for lower-triangular X (LAUUM by recursive halving, n^3/3 flops):
+// A11 = X11^T X11 + X21^T X21, A21 = X22^T X21, A22 = X22^T X22.
+static fk_status lauum(cublasHandle_t bh, const double* X, int64_t ldx, double* A, int64_t lda, int n) {
+  const double one = 1.0, zero = 0.0;
+  if (n <= kPcgLeaf) {
+    if (cublasDsyrk(bh, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, n, n, &one, X, (int)ldx, &zero, A, (int)lda) != CUBLAS_STATUS_SUCCESS)
+      return fail(FK_E_CUDA, "cublasDsyrk failed");
+    return FK_OK;
+  }
+  const int n1 = ((n / 2) + 31) / 32 * 32, n2 = n - n1;
+  FK_TRY(lauum(bh, X, ldx, A, lda, n1));
+  if (cublasDsyrk(bh, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, n1, n2, &one, X + n1, (int)ldx, &one, A, (int)lda) != CUBLAS_STATUS_SUCCESS)
+    return fail(FK_E_CUDA, "cublasDsyrk failed");
+  if (cublasDtrmm(bh, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, n2, n1, &one, X + n1 + n1 * ldx,
+                  (int)ldx, X + n1, (int)ldx, A + n1, (int)lda) != CUBLAS_STATUS_SUCCESS)
+    return fail(FK_E_CUDA, "cublasDtrmm failed");
+  return lauum(bh, X + n1 + n1 * ldx, ldx, A + n1 + n1 * lda, lda, n2);
 }
 
 static bool pcg_eligible(const SysArgs& g) {
@@ -1119,17 +1212,17 @@ static bool pcg_eligible(const SysArgs& g) {
 }
 
 // the block unknowns: modes with lambda R_k <= tau (both real unknowns of a mode together)
-static void pcg_low_set(const SysArgs& g, double tau, std::vector<int>& low, std::vector<unsigned char>& is_low) {
+static void pcg_low_set(const SysArgs& g, double tau, std::vector<int>& low, std::vector<int>& lowpos) {
   const int m = g.m, side = 2 * m + 1, c0 = (g.D - 1) / 2;
   low.clear();
-  is_low.assign(g.D, 0);
+  lowpos.assign(g.D, -1);
   for (int u = 0; u < g.D; ++u) {
     const int lin = c0 + ((u + 1) >> 1);
     const int k0 = g.d == 2 ? lin / side - m : 0, k1 = g.d == 2 ? lin % side - m : lin - m;
     const double R = 1.0 + std::pow((double)k0 * k0 + (double)k1 * k1, g.s);
     if (g.lambda * R <= tau) {
+      lowpos[u] = (int)low.size();
       low.push_back(u);
-      is_low[u] = 1;
     }
   }
 }
@@ -1138,125 +1231,116 @@ static void pcg_low_set(const SysArgs& g, double tau, std::vector<int>& low, std
 // ws: at least (D+1)^2 doubles (the dense path's matrix slot).  Caller holds g_sol_mu.
 static fk_status pcg_run(SysArgs g, const double2* r, double* x, int* iters, void* ws, size_t ws_bytes, void* chol_ws, int* info,
                          cudaStream_t s) {
-  std::vector<int> low;
-  std::vector<unsigned char> is_low;
-  pcg_low_set(g, pcg_tau(), low, is_low);
+  std::vector<int> low, lowpos;
+  pcg_low_set(g, pcg_tau(), low, lowpos);
   const int D = g.D, Dl = (int)low.size();
   // cost model from B200 measurements: dense cuSOLVER potrf ~56 ms at N = 16642
-  // (N^3); the CG path ~4.6 ms (Dl/3133)^3 for the block + ~3.6 ms for ~40 iterations
+  // (N^3); the CG path at C3 (Dl = 2221) ~3 ms for the block + ~2.8 ms for 47 iterations
   const char* fe = getenv("FK_SOLVER");
   const double t_dense = 56.0 * std::pow((D + 1) / 16642.0, 3.0) + 0.5;
-  const double t_pcg = 5.0 * std::pow(Dl / 3133.0, 3.0) + 4.0;
+  const double t_pcg = 3.0 * std::pow(Dl / 2221.0, 3.0) + 2.8;
   if (!(fe && fe[0] == 'p') && !(t_pcg < t_dense)) return FK_E_UNSUPPORTED;  // the dense path (no error text)
   PcgGrid q{};
   q.d = g.d;
   const int L = fft_friendly(4 * g.m + 1);
-  if (g.d == 2) {
-    q.L0 = L;
-    q.L1 = L;
-  } else {
-    q.L0 = 1;
-    q.L1 = L;
-  }
+  q.L0 = g.d == 2 ? L : 1;
+  q.L1 = L;
   q.H1 = q.L1 / 2 + 1;
   const int64_t nreal = (int64_t)q.L0 * q.L1, nhalf = (int64_t)q.L0 * q.H1;
   FftPlan fz, fd;
   int dims[2] = {g.d == 2 ? q.L0 : q.L1, q.L1};
   FK_TRY(fft_plan(g.d, dims, 1, CUFFT_Z2D, &fz));
   FK_TRY(fft_plan(g.d, dims, 1, CUFFT_D2Z, &fd));
+  const int64_t lda = (Dl + 1) & ~1;  // even: 16-byte aligned columns for the preconditioner's loads
+  const int TB = 256;
+  const int gD = (D + TB - 1) / TB, nlow_ctas = (Dl + 7) / 8, gP = nlow_ctas + gD;
   Bump b(ws, ws_bytes);
-  double* Ainv = (double*)b.take((size_t)Dl * Dl * 8 + 8);
-  double* Xinv = (double*)b.take((size_t)Dl * Dl * 8 + 8);
+  double* Ainv = (double*)b.take((size_t)lda * Dl * 8 + 16);
+  double* Xinv = (double*)b.take((size_t)lda * Dl * 8 + 16);
+  double* S = (double*)b.take((size_t)(Dl / 2 + 32) * (Dl / 2 + 32) * 8);  // n2 x n1 of tri_inv's top level
   int* d_low = (int*)b.take((size_t)Dl * 4 + 4);
-  unsigned char* d_is_low = (unsigned char*)b.take((size_t)D + 1);
+  int* d_lowpos = (int*)b.take((size_t)D * 4);
   double* dinv = (double*)b.take((size_t)D * 8);
   double* bz = (double*)b.take((size_t)D * 8);
   double* rv = (double*)b.take((size_t)D * 8);
   double* zv = (double*)b.take((size_t)D * 8);
-  double* pv = (double*)b.take((size_t)D * 8);
+  double* pv[2] = {(double*)b.take((size_t)D * 8), (double*)b.take((size_t)D * 8)};
   double* qv = (double*)b.take((size_t)D * 8);
-  double* rl = (double*)b.take((size_t)Dl * 8 + 8);
-  double* zl = (double*)b.take((size_t)Dl * 8 + 8);
+  double* rl = (double*)b.take((size_t)Dl * 8 + 16);
   double2* H = (double2*)b.take((size_t)nhalf * 16);
   double* G = (double*)b.take((size_t)nreal * 8);
   double* muhat = (double*)b.take((size_t)nreal * 8);
   double* sc = (double*)b.take(64);
+  double* part = (double*)b.take((size_t)(gP + 64) * 8);
+  unsigned* tickets = (unsigned*)b.take(64);
   void* fwork = b.take(std::max<size_t>(std::max(fz.work, fd.work), 256));
   cusolverDnHandle_t h;
   FK_TRY(handle_for_device(&h));
   int lw_potrf = 0;
   if (Dl > kTilesMaxN &&
-      cusolverDnDpotrf_bufferSize(h, CUBLAS_FILL_MODE_LOWER, Dl, Ainv, Dl, &lw_potrf) != CUSOLVER_STATUS_SUCCESS)
+      cusolverDnDpotrf_bufferSize(h, CUBLAS_FILL_MODE_LOWER, Dl, Ainv, (int)lda, &lw_potrf) != CUSOLVER_STATUS_SUCCESS)
     return fail(FK_E_CUDA, "cusolverDnDpotrf_bufferSize failed");
   double* swork = (double*)b.take((size_t)std::max(lw_potrf, 1) * 8);
   if (!b.ok()) return FK_E_UNSUPPORTED;  // the block does not fit the dense path's matrix slot: dense path
   if (Dl > 0) FK_CUDA_TRY(cudaMemcpyAsync(d_low, low.data(), (size_t)Dl * 4, cudaMemcpyHostToDevice, s));
-  FK_CUDA_TRY(cudaMemcpyAsync(d_is_low, is_low.data(), (size_t)D, cudaMemcpyHostToDevice, s));
-  const int TB = 256;
-  // the block: assemble, factor, invert
+  FK_CUDA_TRY(cudaMemcpyAsync(d_lowpos, lowpos.data(), (size_t)D * 4, cudaMemcpyHostToDevice, s));
+  FK_CUDA_TRY(cudaMemsetAsync(tickets, 0, 64, s));
+  FK_CUDA_TRY(cudaMemsetAsync(pv[0], 0, (size_t)D * 8, s));  // beta = 0 multiplies it in the first step
+  FK_CUDA_TRY(cudaMemsetAsync(sc, 0, 64, s));
+  cublasHandle_t bh;
+  FK_TRY(blas_for_device(&bh));
+  if (cublasSetStream(bh, s) != CUBLAS_STATUS_SUCCESS) return fail(FK_E_CUDA, "cublasSetStream failed");
+  // the block: assemble, factor (L in Ainv), invert (X = L^{-1}, then lower(Ainv) = X^T X), symmetrise.
+  // cuSOLVER potri took 8.8 ms at Dl = 3133 and TRSM on the identity + SYRK 3.75 ms.
   if (Dl > 0) {
-    k_pcg_low_block<<<dim3((Dl + TB - 1) / TB, Dl), TB, 0, s>>>(g, d_low, Dl, Ainv);
+    k_pcg_low_block<<<dim3((Dl + TB - 1) / TB, Dl), TB, 0, s>>>(g, d_low, Dl, Ainv, lda);
     FK_CUDA_TRY(cudaGetLastError());
     count_launch();
     if (Dl <= kTilesMaxN) {
-      FK_TRY(chol_tiles(Ainv, Dl, Dl, info, chol_ws, s));
-    } else if (cusolverDnDpotrf(h, CUBLAS_FILL_MODE_LOWER, Dl, Ainv, Dl, swork, lw_potrf, info) != CUSOLVER_STATUS_SUCCESS) {
+      FK_TRY(chol_tiles(Ainv, lda, Dl, info, chol_ws, s));
+    } else if (cusolverDnDpotrf(h, CUBLAS_FILL_MODE_LOWER, Dl, Ainv, (int)lda, swork, lw_potrf, info) != CUSOLVER_STATUS_SUCCESS) {
       return fail(FK_E_CUDA, "cusolverDnDpotrf failed");
     }
-    // inverse of the block: X = L^{-1} (TRSM on the identity; exact zeros above the diagonal),
-    // then Ainv = X^T X (SYRK, lower).  cuSOLVER potri took 8.8 ms at Dl = 3133 (latency bound).
-    cublasHandle_t bh0;
-    FK_TRY(blas_for_device(&bh0));
-    if (cublasSetStream(bh0, s) != CUBLAS_STATUS_SUCCESS) return fail(FK_E_CUDA, "cublasSetStream failed");
-    const double one0 = 1.0, zero0 = 0.0;
-    k_pcg_identity<<<dim3((Dl + TB - 1) / TB, Dl), TB, 0, s>>>(Xinv, Dl);
+    FK_CUDA_TRY(cudaMemsetAsync(Xinv, 0, (size_t)lda * Dl * 8, s));
+    k_pcg_unit_diag<<<(Dl + TB - 1) / TB, TB, 0, s>>>(Xinv, lda, Dl);
     count_launch();
-    if (cublasDtrsm(bh0, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, Dl, Dl, &one0, Ainv, Dl, Xinv,
-                    Dl) != CUBLAS_STATUS_SUCCESS)
-      return fail(FK_E_CUDA, "cublasDtrsm failed");
-    if (cublasDsyrk(bh0, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, Dl, Dl, &one0, Xinv, Dl, &zero0, Ainv, Dl) != CUBLAS_STATUS_SUCCESS)
-      return fail(FK_E_CUDA, "cublasDsyrk failed");
+    FK_TRY(tri_inv(bh, Ainv, lda, Xinv, lda, Dl, S));
+    FK_TRY(lauum(bh, Xinv, lda, Ainv, lda, Dl));
+    k_pcg_symmetrize<<<dim3((Dl + TB - 1) / TB, Dl), TB, 0, s>>>(Ainv, lda, Dl);
+    count_launch();
   }
-  k_pcg_setup<<<(D + TB - 1) / TB, TB, 0, s>>>(g, d_is_low, r, dinv, bz);
+  k_pcg_setup<<<gD, TB, 0, s>>>(g, d_lowpos, r, dinv, bz);
   // DFT of mu / (n L^d)
   k_pcg_mu_half<<<(unsigned)((nhalf + TB - 1) / TB), TB, 0, s>>>(g, q, H);
   FK_TRY(fft_exec_z2d(fz, (cufftDoubleComplex*)H, muhat, fwork, s));
   k_pcg_scale<<<(unsigned)((nreal + TB - 1) / TB), TB, 0, s>>>(muhat, nreal, g.inv_n / (double)nreal);
-  k_pcg_init<<<1, 1024, 0, s>>>(D, bz, d_low, Dl, x, rv, rl, sc);
+  k_pcg_init<<<gD, TB, 0, s>>>(D, bz, d_low, Dl, x, rv, rl, sc, part, tickets);
+  k_pcg_precond<<<gP, TB, 0, s>>>(D, rv, dinv, d_lowpos, d_low, Dl, Ainv, lda, rl, zv, sc, 1, nlow_ctas, part, tickets + 1);
   FK_CUDA_TRY(cudaGetLastError());
-  count_launch(4);
-  cublasHandle_t bh;
-  FK_TRY(blas_for_device(&bh));
-  if (cublasSetStream(bh, s) != CUBLAS_STATUS_SUCCESS) return fail(FK_E_CUDA, "cublasSetStream failed");
-  const double one = 1.0, zero = 0.0, tol = 1e-13;
-  auto precond = [&](int first) -> fk_status {
-    if (Dl > 0 && cublasDsymv(bh, CUBLAS_FILL_MODE_LOWER, Dl, &one, Ainv, Dl, rl, 1, &zero, zl, 1) != CUBLAS_STATUS_SUCCESS)
-      return fail(FK_E_CUDA, "cublasDsymv failed");
-    k_pcg_direction<<<1, 1024, 0, s>>>(D, rv, dinv, d_low, Dl, zl, zv, pv, sc, first);
-    count_launch(1);
-    return FK_OK;
-  };
-  FK_TRY(precond(1));
+  count_launch(5);
+  const double tol = 1e-13;
   const int kMaxIter = 1000, kCheck = 10;
-  double hsc[5] = {0, 0, 0, 0, 0};
+  double hsc[7] = {0, 0, 0, 0, 0, 0, 0};
   int it = 0;
   for (; it < kMaxIter;) {
     for (int j = 0; j < kCheck; ++j, ++it) {
-      k_pcg_scatter<<<(unsigned)((nhalf + TB - 1) / TB), TB, 0, s>>>(g, q, pv, H);
+      double* p_old = pv[it & 1];
+      double* p_new = pv[(it + 1) & 1];
+      k_pcg_scatter<<<(unsigned)((nhalf + TB - 1) / TB), TB, 0, s>>>(g, q, zv, p_old, p_new, H, sc);
       FK_TRY(fft_exec_z2d(fz, (cufftDoubleComplex*)H, G, fwork, s));
-      k_pcg_mul<<<(unsigned)((nreal + TB - 1) / TB), TB, 0, s>>>(G, muhat, nreal);
+      k_pcg_mul<<<(unsigned)((nreal + TB - 1) / TB), TB, 0, s>>>(G, muhat, nreal, sc);
       FK_TRY(fft_exec_d2z(fd, G, (cufftDoubleComplex*)H, fwork, s));
-      k_pcg_gather<<<(D + TB - 1) / TB, TB, 0, s>>>(g, q, H, pv, qv);
-      k_pcg_update<<<1, 1024, 0, s>>>(D, pv, qv, d_low, Dl, x, rv, rl, sc, tol * tol);
-      count_launch(4);
-      FK_TRY(precond(0));
+      k_pcg_gather<<<gD, TB, 0, s>>>(g, q, H, p_new, qv, sc, part, tickets + 2);
+      k_pcg_update<<<gD, TB, 0, s>>>(D, p_new, qv, d_lowpos, x, rv, rl, sc, tol * tol, part, tickets + 3);
+      k_pcg_precond<<<gP, TB, 0, s>>>(D, rv, dinv, d_lowpos, d_low, Dl, Ainv, lda, rl, zv, sc, 0, nlow_ctas, part, tickets + 1);
+      count_launch(5);
     }
-    FK_CUDA_TRY(cudaMemcpyAsync(hsc, sc, 40, cudaMemcpyDeviceToHost, s));
+    FK_CUDA_TRY(cudaMemcpyAsync(hsc, sc, 56, cudaMemcpyDeviceToHost, s));
     FK_CUDA_TRY(cudaStreamSynchronize(s));
     if (hsc[4] != 0.0 || !(hsc[1] == hsc[1])) break;  // converged, or NaN (a failed block factor)
   }
   FK_CUDA_TRY(cudaGetLastError());
-  *iters = it;
+  *iters = (int)hsc[6];
   if (hsc[4] == 0.0) return fail(FK_E_SOLVE, "fk_solve (pcg): no convergence in " + std::to_string(kMaxIter) + " iterations");
   return FK_OK;
 }
