@@ -76,3 +76,31 @@ def test_pcg_deterministic(F):
     a, _ = _solve(F, "pcg", mu, r, n, d, m, 1.0, 1e-6, "sobolev", 2.0)
     b, _ = _solve(F, "pcg", mu, r, n, d, m, 1.0, 1e-6, "sobolev", 2.0)
     assert np.array_equal(a, b)
+
+
+def test_pcg_jacobi_only_and_graph_capture(F, oracle):
+    """lambda large enough that no mode needs the dense block (Jacobi alone), and fk_solve under
+    CUDA-graph capture (the CG path reads a flag back, so capture takes the dense path)."""
+    n, d, m = 20_000, 2, 36
+    X, Y = datagen.dataset(n, d=d, ykind="expcos", seed=92)
+    mu, r = oracle.moments(X, 1.0, m), oracle.rhs(X, Y, 1.0, m)
+    th, rep = _solve(F, "pcg", dev(mu.reshape(-1)), dev(r.reshape(-1)), n, d, m, 1.0, 2.0, "sobolev", 2.0)
+    th_o = oracle.solve(mu, r, n, d, m, 2.0, "sobolev", 2.0)
+    assert rep["iters"] > 0 and rel(th, th_o) < 1e-10
+    mu_d, r_d = dev(mu.reshape(-1)), dev(r.reshape(-1))
+    th_g = torch.empty((2 * m + 1) ** 2, dtype=torch.complex128, device="cuda")
+    F.fk_solve(mu_d, r_d, n, d, m, 1.0, 1e-6, "sobolev", 2.0, theta_out=th_g, report=False)  # warm-up (plans, tables)
+    os.environ["FK_SOLVER"] = "pcg"
+    try:
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                F.fk_solve(mu_d, r_d, n, d, m, 1.0, 1e-6, "sobolev", 2.0, theta_out=th_g, report=False, stream=s)
+        th_g.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+    finally:
+        del os.environ["FK_SOLVER"]
+    th_c, _ = _solve(F, "pcg", mu_d, r_d, n, d, m, 1.0, 1e-6, "sobolev", 2.0)
+    assert rel(host(th_g), th_c) < 1e-8
