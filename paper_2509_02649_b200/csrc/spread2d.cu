@@ -438,6 +438,7 @@ __global__ void __launch_bounds__(1024, 1) k_spread2d_f64(const XT* __restrict__
 }
 
 // Cross moments: grid per pair, points (X_l1, -X_l2), unit weight; CTA = (chunk, pair group).
+constexpr int kMaxXCtas = 148 * 4;
 struct ArgsX {
   int64_t n, sn, sd, per;
   int w;
@@ -452,12 +453,65 @@ struct ArgsX {
   void* part;
   double* carry;  // npairs x G x G
   int* d_status;
+  // balanced split (one pair per CTA): CTA c spreads the sample-pair units [ubeg[c], ubeg[c+1]) of
+  // the npairs x n sequence -- at most a few pair segments -- into partial slots slot0[c], ...;
+  // pair p owns slots [pslot[p], pslot[p+1]) (consecutive, in CTA order)
+  int balanced, nctas;
+  int64_t ubeg[kMaxXCtas + 1];
+  int slot0[kMaxXCtas + 1];
+  int pslot[529];
 };
+
+// balanced split: CTA blockIdx.x walks its units pair segment by pair segment (one pair grid in
+// shared memory at a time), writing one partial slot per segment
+template <int W, bool EXACT>
+__device__ void cross_balanced(const float* __restrict__ X, const ArgsX& g, int* smx) {
+  const int cells = g.G * g.G;
+  const int64_t u0 = g.ubeg[blockIdx.x], u1 = g.ubeg[blockIdx.x + 1];
+  int slot = g.slot0[blockIdx.x];
+  Tile t{g.G, g.K, g.G, g.G};
+  bool bad = false;
+  float px[W], py[W];
+  for (int64_t u = u0; u < u1;) {
+    const int p = (int)(u / g.n);
+    const int64_t beg = u - (int64_t)p * g.n, end = min(g.n, u1 - (int64_t)p * g.n);
+    for (int i = threadIdx.x; i < cells; i += blockDim.x) smx[i] = 0;
+    __syncthreads();
+    const int l1 = g.pl1[p], l2 = g.pl2[p];
+    double* carry = g.carry + (int64_t)p * cells;
+    for (int64_t j = beg + threadIdx.x; j < end; j += blockDim.x) {
+      const float x0 = X[j * g.sn + l1 * g.sd];
+      const float x1 = -X[j * g.sn + l2 * g.sd];
+      const P1 q0 = place_f32<EXACT>(x0, g.a_hi, g.a_lo);
+      const P1 q1 = place_f32<EXACT>(x1, g.a_hi, g.a_lo);
+      const int d00 = first_tap(q0.f, W), d01 = first_tap(q1.f, W);
+      const int lr = q0.P + g.K + d00, lc = q1.P + g.K + d01;
+      if ((unsigned)lr > (unsigned)(g.G - W) || (unsigned)lc > (unsigned)(g.G - W) || x0 != x0 || x1 != x1) {
+        bad = true;
+        continue;
+      }
+      es_taps_f32<W>(q0.f, d00, g.beta_f, py);
+      es_taps_f32<W>(q1.f, d01, g.beta_f, px);
+      spread_fixed<false, W>(smx, t, lr, lc, py, px, kS2, carry, 0, kInvS2);
+    }
+    __syncthreads();
+    int* dst = (int*)g.part + (int64_t)slot * cells;
+    for (int i = threadIdx.x; i < cells; i += blockDim.x) dst[i] = smx[i];
+    ++slot;
+    u = (int64_t)(p + 1) * g.n;
+    __syncthreads();
+  }
+  if (bad && g.d_status) atomicOr(g.d_status, (int)FK_E_RANGE);
+}
 
 template <int W, bool EXACT>
 __global__ void __launch_bounds__(1024) k_cross2d_fixed(const float* __restrict__ X, const ArgsX* __restrict__ gp) {
   extern __shared__ int smx[];
   const ArgsX& g = *gp;
+  if (g.balanced) {
+    cross_balanced<W, EXACT>(X, g, smx);
+    return;
+  }
   const int grp = blockIdx.x % g.ngroups;
   const int chunk = blockIdx.x / g.ngroups;
   const int p0 = grp * g.per_cta;
@@ -583,6 +637,26 @@ __global__ void k_reduce2d(const void* __restrict__ part, int is_fixed, const in
       }
     }
     if (carry) s += carry[(int64_t)bi * G * G + (int64_t)r * G + col];
+  }
+  fine[t] = s;
+}
+
+// balanced cross moments: pair bi sums its slots [pslot[bi], pslot[bi+1]) in slot order
+__global__ void k_reduce_slots(const int* __restrict__ part, const ArgsX* __restrict__ gp, int off, int nf, double inv,
+                               const double* __restrict__ carry, double* __restrict__ fine) {
+  const ArgsX& g = *gp;
+  const int G = g.G;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t per = (int64_t)nf * nf;
+  if (t >= per * g.npairs) return;
+  const int bi = (int)(t / per);
+  const int64_t c = t % per;
+  const int r = (int)(c / nf) - off, col = (int)(c % nf) - off;
+  double s = 0.0;
+  if (r >= 0 && r < G && col >= 0 && col < G) {
+    const int64_t cell = (int64_t)r * G + col;
+    for (int sl = g.pslot[bi]; sl < g.pslot[bi + 1]; ++sl) s += (double)part[(int64_t)sl * G * G + cell] * inv;
+    s += carry[(int64_t)bi * G * G + cell];
   }
   fine[t] = s;
 }
@@ -876,7 +950,9 @@ struct PlanX {
   int m, w, nf, off, K, G, npairs, per_cta, ngroups, chunks, threads;
   double beta;
   bool fp64;
-  bool by_pair;  // one pair grid does not fit a CTA: per-pair 2-D moment passes (cross_by_pair)
+  bool by_pair;   // one pair grid does not fit a CTA: per-pair 2-D moment passes (cross_by_pair)
+  bool balanced;  // one pair per CTA: units split evenly over all resident CTAs (cross_balanced)
+  int nctas;
   size_t smem;
 };
 
@@ -921,6 +997,10 @@ static fk_status make_planx(int d, int m, double eps, int dtype, PlanX* p) {
   // one wave: chunks x groups <= resident CTAs (rounding up left a second wave of a few CTAs
   // that doubled the kernel time)
   q.chunks = std::max(1, (sms * per_sm) / q.ngroups);
+  // one pair per CTA (C5: 45 pairs, 1 CTA per SM): chunks x groups = 135 of 148 SMs; the balanced
+  // split gives every resident CTA the same number of sample-pair units instead
+  q.balanced = !q.fp64 && q.per_cta == 1 && !getenv("FK_CROSS_CHUNKED");
+  q.nctas = std::min(kMaxXCtas, sms * per_sm);
   *p = q;
   return FK_OK;
 }
@@ -931,7 +1011,7 @@ static fk_status layoutx(const PlanX& p, Bump& b, void** part, double** carry, d
   int dims[2] = {p.nf, p.nf};
   FK_TRY(fft_plan(2, dims, p.npairs, CUFFT_D2Z, &fp));
   const size_t esz = p.fp64 ? 8 : 4;
-  *part = b.take((size_t)p.chunks * p.npairs * p.G * p.G * esz);
+  *part = b.take((size_t)std::max(p.chunks * p.npairs, p.nctas + p.npairs) * p.G * p.G * esz);
   *carry = (double*)b.take((size_t)p.npairs * p.G * p.G * 8);
   *fine = (double*)b.take((size_t)p.npairs * p.nf * p.nf * 8);
   *spec = (double2*)b.take((size_t)p.npairs * p.nf * (p.nf / 2 + 1) * 16);
@@ -1053,9 +1133,27 @@ fk_status cross_run(const fk_points& X, double L, int m, double eps, double* G, 
   a.part = part;
   a.carry = carry;
   a.d_status = d_status;
+  a.balanced = p.balanced ? 1 : 0;
+  a.nctas = p.nctas;
+  if (p.balanced) {
+    const int64_t U = (int64_t)p.npairs * X.n;
+    int slot = 0, pnext = 0;
+    for (int c = 0; c < p.nctas; ++c) {
+      const int64_t u0 = (int64_t)((__int128)U * c / p.nctas), u1 = (int64_t)((__int128)U * (c + 1) / p.nctas);
+      a.ubeg[c] = u0;
+      a.slot0[c] = slot;
+      if (u1 > u0) {
+        for (int64_t pp = u0 / X.n; pp <= (u1 - 1) / X.n; ++pp, ++slot)
+          while (pnext <= pp) a.pslot[pnext++] = slot;  // first slot of pair pp
+      }
+    }
+    a.ubeg[p.nctas] = U;
+    a.slot0[p.nctas] = slot;
+    while (pnext <= p.npairs) a.pslot[pnext++] = slot;
+  }
   FK_CUDA_TRY(cudaMemsetAsync(carry, 0, (size_t)p.npairs * p.G * p.G * 8, s));
   FK_CUDA_TRY(cudaMemcpyAsync(dargs, &a, sizeof(ArgsX), cudaMemcpyHostToDevice, s));
-  const int ctas = p.chunks * p.ngroups;
+  const int ctas = p.balanced ? p.nctas : p.chunks * p.ngroups;
   const size_t esz = p.fp64 ? 8 : 4;
   if (X.n > 0) {
     auto go = [&](auto k, auto* Xp, int threads) {
@@ -1092,9 +1190,12 @@ fk_status cross_run(const fk_points& X, double L, int m, double eps, double* G, 
   const int TB = 256;
   const int64_t tot = (int64_t)p.npairs * p.nf * p.nf;
   // part layout: [chunk][pair][G][G] -> batch stride G*G, "cta" stride npairs*G*G, T = 1
-  k_reduce2d<<<(unsigned)((tot + TB - 1) / TB), TB, 0, s>>>(part, fixed ? 1 : 0, nullptr, p.chunks, 1, p.G, p.G, p.G, p.off, p.nf,
-                                                           kInvS2, carry, fine, p.npairs, (int64_t)p.G * p.G,
-                                                           (int64_t)p.npairs * p.G * p.G);
+  if (p.balanced && X.n > 0)
+    k_reduce_slots<<<(unsigned)((tot + TB - 1) / TB), TB, 0, s>>>((const int*)part, dargs, p.off, p.nf, kInvS2, carry, fine);
+  else
+    k_reduce2d<<<(unsigned)((tot + TB - 1) / TB), TB, 0, s>>>(part, fixed ? 1 : 0, nullptr, p.chunks, 1, p.G, p.G, p.G, p.off, p.nf,
+                                                             kInvS2, carry, fine, p.npairs, (int64_t)p.G * p.G,
+                                                             (int64_t)p.npairs * p.G * p.G);
   FK_CUDA_TRY(cudaGetLastError());
   FftPlan fp;
   int dims[2] = {p.nf, p.nf};

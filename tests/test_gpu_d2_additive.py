@@ -198,3 +198,18 @@ def test_host_streamed_additive_matches_device(F):
     for l in range(d):
         r2, mu2 = F.fk_rhs_type1(Xd[:, l], Yd, 1.0, m, 1e-6)
         assert rel(host(mus[l]), host(mu2)) < 1e-12 and rel(host(rs[l]), host(r2)) < 1e-6
+
+
+@pytest.mark.parametrize("n", [37, 149, 5_003])
+def test_cross_moments_balanced_split(F, oracle, n):
+    """One pair per CTA spreads an even share of the npairs x n sample-pair units (segments cross
+    pair boundaries; with npairs x n < resident CTAs some CTAs get nothing): oracle parity and
+    bitwise reproducibility."""
+    d, m = 4, 50
+    X, _ = datagen.dataset(n, d=d, ykind="additive", seed=29)
+    Xd = dev(np.ascontiguousarray(X.T)).t()  # SoA columns, as the bench lays them out
+    G1 = host(F.fk_additive_cross_moments(Xd, 1.0, m, 1e-6))
+    G2 = host(F.fk_additive_cross_moments(Xd, 1.0, m, 1e-6))
+    assert np.array_equal(G1, G2)
+    Go = oracle.cross_moments(X, 1.0, m)
+    assert max(rel(G1[p], Go[p]) for p in range(G1.shape[0])) <= 1e-5
