@@ -735,10 +735,42 @@ size_t solve_path_ws_bytes(int d, int m, int kind, int nlam) {
   return b.used;
 }
 
+static double solve_cost_ms(const SysArgs& g);
+size_t solve_ws_bytes(int d, int m, int kind);
+
 fk_status solve_path_run(const fk_problem* P, const double* lambdas, int nlam, double* theta, int* info_out, void* ws, size_t ws_bytes,
                          cudaStream_t s) {
   SysArgs g;
   FK_TRY(fill_sysargs(P, &g));
+  {
+    // Large Sobolev systems: one fk_solve per lambda (the CG path where it is cheaper) when that
+    // beats one eigendecomposition (~2.7 s at N = 16642 on the B200, tools/path_large.py).
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cap);
+    const double t_eig = 2700.0 * std::pow((g.D + 1) / 16642.0, 3.0);
+    double t_each = 0.0;
+    if (cap == cudaStreamCaptureStatusNone && g.kind == FK_SOBOLEV && g.d <= 2 && g.D + 1 > 9000 &&
+        solve_ws_bytes(P->d, P->m, P->kind) <= ws_bytes) {
+      for (int l = 0; l < nlam; ++l) {
+        SysArgs gl = g;
+        gl.lambda = lambdas[l];
+        t_each += solve_cost_ms(gl);
+      }
+    }
+    if (t_each > 0.0 && t_each < t_eig) {
+      for (int l = 0; l < nlam; ++l) {
+        if (!(lambdas[l] > 0.0)) return fail(FK_E_ARG, "fk_solve_path: lambda must be > 0");
+        fk_problem Pl = *P;
+        Pl.lambda = lambdas[l];
+        FK_TRY(solve_run(&Pl, theta + (int64_t)2 * g.D * l, nullptr, ws, ws_bytes, s));
+      }
+      if (info_out) {
+        FK_CUDA_TRY(cudaStreamSynchronize(s));
+        *info_out = 0;
+      }
+      return FK_OK;
+    }
+  }
   g.lambda = 0.0;  // M0: the data (and PDE) part only
   const int D = g.D, N = D + 1;
   int lwork = 0;
@@ -1229,16 +1261,25 @@ static void pcg_low_set(const SysArgs& g, double tau, std::vector<int>& low, std
 
 // Solves into x (D reals).  Returns FK_OK with *iters, or FK_E_SOLVE when it does not converge.
 // ws: at least (D+1)^2 doubles (the dense path's matrix slot).  Caller holds g_sol_mu.
+// predicted ms of fk_solve for g (the cheaper of the two paths; same model as pcg_run's choice)
+static double solve_cost_ms(const SysArgs& g) {
+  const double t_dense = 56.0 * std::pow((g.D + 1) / 16642.0, 3.0) + 0.5;
+  if (g.kind != FK_SOBOLEV || g.d > 2 || g.mu_pde != 0.0 || g.D + 1 <= kTilesMaxN) return t_dense;
+  std::vector<int> low, lowpos;
+  pcg_low_set(g, pcg_tau(), low, lowpos);
+  return std::min(t_dense, 3.0 * std::pow(low.size() / 2221.0, 1.8) + 2.8);
+}
+
 static fk_status pcg_run(SysArgs g, const double2* r, double* x, int* iters, void* ws, size_t ws_bytes, void* chol_ws, int* info,
                          cudaStream_t s) {
   std::vector<int> low, lowpos;
   pcg_low_set(g, pcg_tau(), low, lowpos);
   const int D = g.D, Dl = (int)low.size();
-  // cost model from B200 measurements: dense cuSOLVER potrf ~56 ms at N = 16642
-  // (N^3); the CG path at C3 (Dl = 2221) ~3 ms for the block + ~2.8 ms for 47 iterations
+  // cost model from B200 measurements (tools/pcg_lams.py): dense cuSOLVER potrf
+  // ~56 ms at N = 16642 (N^3); the CG path: the block + ~2.8 ms for ~47 iterations
   const char* fe = getenv("FK_SOLVER");
   const double t_dense = 56.0 * std::pow((D + 1) / 16642.0, 3.0) + 0.5;
-  const double t_pcg = 3.0 * std::pow(Dl / 2221.0, 3.0) + 2.8;
+  const double t_pcg = 3.0 * std::pow(Dl / 2221.0, 1.8) + 2.8;  // block: 3.0 / 7.5 / 22.8 ms at Dl = 2221 / 3930 / 7030
   if (!(fe && fe[0] == 'p') && !(t_pcg < t_dense)) return FK_E_UNSUPPORTED;  // the dense path (no error text)
   PcgGrid q{};
   q.d = g.d;

@@ -104,3 +104,19 @@ def test_pcg_jacobi_only_and_graph_capture(F, oracle):
         del os.environ["FK_SOLVER"]
     th_c, _ = _solve(F, "pcg", mu_d, r_d, n, d, m, 1.0, 1e-6, "sobolev", 2.0)
     assert rel(host(th_g), th_c) < 1e-8
+
+
+def test_path_large_sobolev_per_lambda(F):
+    """fk_solve_path at C3 size with a few lambdas takes one solve per lambda (CG where cheaper)
+    instead of the 16641-point eigendecomposition; each theta matches the dense solve."""
+    from datagen.device import gen_dataset
+
+    n, d, m = 2_000_000, 2, 64
+    X, Y = torch.empty(n, 2, device="cuda"), torch.empty(n, device="cuda")
+    gen_dataset(X, Y, n, d, xkind=0, ykind=2, seed=5)
+    r, mu = F.fk_rhs_type1(X, Y, 1.0, m, 1e-6)
+    lams = [3e-7, 1e-6, 1e-5]
+    th = host(F.fk_solve_path(mu, r, n, d, m, 1.0, lams, "sobolev", 2.0))
+    for i, lam in enumerate(lams):
+        th_d, _ = _solve(F, "dense", mu, r, n, d, m, 1.0, lam, "sobolev", 2.0)
+        assert rel(th[i], th_d) < 1e-7, (lam, rel(th[i], th_d))
