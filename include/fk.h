@@ -152,7 +152,10 @@ fk_status fk_predict_type2(const double* theta, int d, int m, double L, int addi
  * reduction of fk_solve; one eigendecomposition of Dg^{-1/2} A0 Dg^{-1/2} (Dg = the diagonal of
  * M^*M in the real basis) then costs O(D^2) per lambda.  theta_out: nlam x D complex128 (device,
  * row l = theta(lambda_l)).  If info != NULL the call synchronises `stream` and stores the
- * eigensolver's info (0 = success; FK_E_SOLVE otherwise). */
+ * eigensolver's info (0 = success; FK_E_SOLVE otherwise).  Sobolev systems with D >= 9000, d <= 2:
+ * when one fk_solve per lambda (CG where cheaper) is predicted faster than the eigendecomposition,
+ * the path runs those solves instead (same result to the solvers' accuracy; not-SPD systems are
+ * then not reported) and synchronises `stream` (CG convergence checks). */
 fk_status fk_solve_path(const fk_problem* P, const double* lambdas, int nlam, double* theta_out, int* info, void* ws,
                         size_t ws_bytes, fk_stream_t stream);
 
