@@ -89,7 +89,10 @@ fk_status fk_rhs_type1(fk_points X, const void* Y, double L, int m, double eps, 
 /* Additive-model cross moments for every feature pair l1 < l2 in lexicographic pair order
  * (P:505-512): G[p][a][b] = sum_j exp(-i pi (a X_{j,l1} - b X_{j,l2}) / 2L), a, b in {-m..m}:
  * the 2-D type-1 sum of unit weights at the points (X_{l1}, -X_{l2}).  G_out: d(d-1)/2 blocks of
- * (2m+1)^2 complex128, b fastest.  2 <= d <= 32. */
+ * (2m+1)^2 complex128, b fastest.  2 <= d <= 32.  A coordinate outside [-L, L] (or NaN) flags
+ * FK_E_RANGE and drops the sample from the pairs that use that coordinate only (as the per-feature
+ * 1-D passes drop it from that feature only).  Any m: when one pair grid exceeds a CTA's shared
+ * memory each pair is computed by a tiled 2-D moment pass (one read of its two columns per pair). */
 fk_status fk_additive_cross_moments(fk_points X, double L, int m, double eps, double* G_out, int flags, void* ws,
                                     size_t ws_bytes, int* d_status, fk_stream_t stream);
 

@@ -213,3 +213,41 @@ def test_cross_moments_balanced_split(F, oracle, n):
     assert np.array_equal(G1, G2)
     Go = oracle.cross_moments(X, 1.0, m)
     assert max(rel(G1[p], Go[p]) for p in range(G1.shape[0])) <= 1e-5
+
+
+@pytest.mark.parametrize("eps,dt", [(1e-6, "f32"), (1e-10, "f64")])
+@pytest.mark.parametrize("what", ["type1_2d", "cross", "cross_large_m"])
+def test_range_flag_2d_and_cross(F, oracle, what, eps, dt):
+    """A coordinate outside [-L, L] (or NaN) sets FK_E_RANGE in d_status; the sample is skipped
+    (d = 2: everywhere; cross moments: in the pairs that use that coordinate) and the other
+    samples' sums are unaffected."""
+    t = torch.float32 if dt == "f32" else torch.float64
+    X, Y = datagen.dataset(301, d=3, ykind="additive", seed=33)
+    X = X.astype(np.float64)
+    X[17, 1] = 1.5
+    X[200, 0] = np.nan
+    good = np.ones(301, bool)
+    good[[17, 200]] = False
+    ds = torch.zeros(1, dtype=torch.int32, device="cuda")
+    if what == "type1_2d":
+        m = 12
+        X2 = X[:, :2]
+        Xd = dev(X2, t)
+        r, mu = F.fk_rhs_type1(Xd, dev(Y, t), 1.0, m, eps, d_status=ds)
+        assert rel(host(mu), oracle.moments(X2[good], 1.0, m)) <= (1e-5 if dt == "f32" else 1e-10)
+        assert rel(host(r), oracle.rhs(X2[good], Y[good].astype(np.float64), 1.0, m)) <= (1e-5 if dt == "f32" else 1e-10)
+    else:
+        m = 10 if what == "cross" else 130
+        G = host(F.fk_additive_cross_moments(dev(X, t), 1.0, m, eps, d_status=ds))
+        # a bad coordinate removes the sample from the pairs that use that coordinate only
+        # (as the per-feature 1-D passes skip it only in their own column)
+        for p, (l1, l2) in enumerate([(0, 1), (0, 2), (1, 2)]):
+            ok = np.all(np.isfinite(X[:, [l1, l2]]) & (np.abs(X[:, [l1, l2]]) <= 1.0), axis=1)
+            Go = oracle.cross_moments(X[ok][:, [l1, l2]], 1.0, m)[0]
+            assert rel(G[p], Go) <= (1e-5 if dt == "f32" else 1e-10), (p, rel(G[p], Go))
+    assert int(ds.item()) & F.FK_E_RANGE
+    with pytest.raises(F.FkError):
+        if what == "type1_2d":
+            F.fk_moments_type1(dev(X[:, :2], t), 1.0, 12, eps)
+        else:
+            F.fk_additive_cross_moments(dev(X, t), 1.0, 10, eps)
