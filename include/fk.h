@@ -28,7 +28,10 @@
  *     enqueued); the message is available from fk_last_error() (thread-local).  Data errors found
  *     by a kernel (a coordinate outside [-L, L], NaN) are OR-ed into *d_status (device int, bit
  *     FK_E_RANGE) -- the caller zeroes it before and inspects it after synchronising.  Samples
- *     with such a coordinate are skipped.
+ *     with such a coordinate are skipped (predict: NaN at that query).  The check is made on the
+ *     fine grid: a coordinate within the window's halo beyond +-L (at most w/2 + 2 fine cells,
+ *     i.e. 4L (w/2 + 2) / nf) is still on the grid and is summed exactly (the sums are
+ *     4L-periodic), without a flag.
  *   - Accuracy: eps is the requested relative l2 accuracy of each output vector against the
  *     exact sums (reading R7); valid range [1e-14, 1e-1].  eps >= 1e-7 selects the fp32
  *     spreading path (cubic B-spline window, fixed-point shared-memory accumulation); smaller eps

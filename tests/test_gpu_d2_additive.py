@@ -251,3 +251,30 @@ def test_range_flag_2d_and_cross(F, oracle, what, eps, dt):
             F.fk_moments_type1(dev(X[:, :2], t), 1.0, 12, eps)
         else:
             F.fk_additive_cross_moments(dev(X, t), 1.0, 10, eps)
+
+
+@pytest.mark.parametrize("eps", [1e-6, 1e-10])
+@pytest.mark.parametrize("d,additive", [(1, False), (2, False), (3, True)])
+def test_predict_range_flag(F, oracle, d, additive, eps):
+    """A NaN query flags FK_E_RANGE and yields NaN at that query only.  A query outside [-L, L]
+    either does the same or -- when it still lies on the grid (within the window's halo; the
+    type-2 sum is 4L-periodic, so the value is exact there) -- equals the oracle's sum."""
+    m = 9
+    t = torch.float32 if eps >= 1e-7 else torch.float64
+    rng = np.random.default_rng(d)
+    D = d * (2 * m + 1) if additive else (2 * m + 1) ** d
+    th = rng.normal(size=D) + 1j * rng.normal(size=D)
+    Xq = datagen.dataset(257, d=d, seed=34)[0].astype(np.float64)
+    Xq[5, 0] = -1.25
+    Xq[100, d - 1] = np.nan
+    Xq = Xq.reshape(-1) if d == 1 else Xq
+    ds = torch.zeros(1, dtype=torch.int32, device="cuda")
+    f = host(F.fk_predict_type2(dev(th), d, m, 1.0, dev(Xq, t), eps, additive=additive, d_status=ds))
+    assert int(ds.item()) & F.FK_E_RANGE
+    assert np.isnan(f[100])
+    ok = np.ones(257, bool)
+    ok[100] = False
+    if np.isnan(f[5]):
+        ok[5] = False
+    fo = oracle.predict_additive(th, Xq[ok], 1.0, m) if additive else oracle.predict(th, Xq[ok], 1.0, m)
+    assert rel(f[ok], np.real(fo)) <= (1e-5 if eps >= 1e-7 else 1e-10)
