@@ -174,6 +174,41 @@ __device__ __forceinline__ void pair_add(unsigned* __restrict__ lo, int* __restr
   }
 }
 
+// pair_add over N consecutive cells c0 .. c0+N-1 with values vf(i), in groups of up to 8 whose
+// atomics are issued phase by phase (all low words, then the high words, then the rare drains):
+// one tap's high-word update needs its low word's old value, so tap-by-tap pair_add waits ~2
+// shared-atomic round trips per tap; grouped, 3 round trips per 8 taps.
+template <int N, class VF>
+__device__ __forceinline__ void pair_add_n(unsigned* __restrict__ lo, int* __restrict__ hi, int c0, VF vf, double* carry,
+                                           double hi_unit) {
+#pragma unroll
+  for (int g0 = 0; g0 < N; g0 += 8) {
+    constexpr int B = 8;
+    unsigned o[B], l[B];
+    int h[B];
+#pragma unroll
+    for (int i = 0; i < B; ++i)
+      if (g0 + i < N) {
+        const long long v = vf(g0 + i);
+        l[i] = (unsigned)v;
+        h[i] = (int)(v >> 32);
+        o[i] = atomicAdd(lo + c0 + g0 + i, l[i]);
+      }
+#pragma unroll
+    for (int i = 0; i < B; ++i)
+      if (g0 + i < N) {
+        h[i] += (o[i] + l[i]) < o[i] ? 1 : 0;  // carry out of the low word
+        o[i] = h[i] != 0 ? (unsigned)atomicAdd(hi + c0 + g0 + i, h[i]) : 0u;
+      }
+#pragma unroll
+    for (int i = 0; i < B; ++i)
+      if (g0 + i < N && h[i] != 0 && (unsigned)((int)o[i] + h[i] + (1 << 29)) >= (1u << 30)) {
+        const int t = atomicExch(hi + c0 + g0 + i, 0);
+        if (t) atomicAdd(carry + c0 + g0 + i, (double)t * hi_unit);
+      }
+  }
+}
+
 // exact 2^e for |e| < 1000 without the libm ldexp call
 __device__ inline double pow2(int e) { return __longlong_as_double((long long)(1023 + e) << 52); }
 

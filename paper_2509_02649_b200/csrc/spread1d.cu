@@ -468,14 +468,12 @@ __global__ void __launch_bounds__(1024, 1) k_spread1d_bs7(const XT* __restrict__
         sum += q[i];
       }
       q[7] = (long long)kSX - sum;  // partition of unity closed in integers
-#pragma unroll
-      for (int i = 0; i < 8; ++i) pair_add(lo, hi, t0 + i, q[i], g.carry, unit);
+      pair_add_n<8>(lo, hi, t0, [&](int i) { return q[i]; }, g.carry, unit);
     } else {
       const double y = (double)Y[j];
       const double ys = y * sy;
       if (fabs(ys) < 2097152.0) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) pair_add(lo, hi, t0 + i, __double2ll_rn(wv[i] * ys * 1048576.0), g.carry, unit);
+        pair_add_n<8>(lo, hi, t0, [&](int i) { return __double2ll_rn(wv[i] * ys * 1048576.0); }, g.carry, unit);
       } else {  // |Y| outlier or NaN: exact fp64 into the carry grid
 #pragma unroll 1
         for (int i = 0; i < 8; ++i) atomicAdd(g.carry + t0 + i, y * wv[i]);

@@ -60,7 +60,7 @@ def lib():
     if _lib is None:
         if not os.path.exists(LIB_PATH):
             raise ImportError(f"libfk.so not found at {LIB_PATH}; build it with `python -m paper_2509_02649_b200.build`")
-        L = ctypes.CDLL(LIB_PATH)
+        L = ctypes.CDLL(os.environ.get("FK_LIB_OVERRIDE", LIB_PATH))  # override: A/B measurements only
         vp, dp, ip, sz = ctypes.c_void_p, ctypes.c_double, ctypes.c_int, ctypes.c_size_t
         L.fk_moments_type1.argtypes = [fk_points, dp, ip, dp, vp, ip, vp, sz, vp, vp]
         L.fk_rhs_type1.argtypes = [fk_points, vp, dp, ip, dp, vp, vp, ip, vp, sz, vp, vp]
