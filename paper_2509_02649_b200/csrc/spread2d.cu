@@ -157,6 +157,7 @@ __device__ __forceinline__ void spread_f64(double* T, const Tile& g, int lr, int
 
 struct Args2 {
   int64_t n, sn, sd, per;
+  int aos2;  // sn == 2, sd == 1 and X 8-byte aligned (float2 loads)
   int w;
   float beta_f;
   double beta_d;
@@ -251,8 +252,14 @@ __global__ void __launch_bounds__(1024) k_spread2d_fixed(const float* __restrict
     bool ownA = false, ownB = false;
     float x0 = 0.f, x1 = 0.f, y = 0.f;
     if (j < end) {
-      x0 = X[j * g.sn];
-      x1 = X[j * g.sn + g.sd];
+      if (g.aos2) {  // interleaved (x0, x1) pairs, 8-byte aligned: one 64-bit load per sample
+        const float2 v = __ldcs(reinterpret_cast<const float2*>(X) + j);
+        x0 = v.x;
+        x1 = v.y;
+      } else {
+        x0 = X[j * g.sn];
+        x1 = X[j * g.sn + g.sd];
+      }
       const P1 q0 = place_f32<EXACT>(x0, g.a_hi, g.a_lo);
       const P1 q1 = place_f32<EXACT>(x1, g.a_hi, g.a_lo);
       // range check on the moment grid (both coordinates): |X| <= L
@@ -851,6 +858,7 @@ fk_status type1_2d_run(int m, double eps, const fk_points& X, const void* Y, dou
   a.n = X.n;
   a.sn = X.stride_n;
   a.sd = X.stride_d;
+  a.aos2 = X.dtype == FK_F32 && X.stride_n == 2 && X.stride_d == 1 && ((uintptr_t)X.ptr & 7) == 0;
   a.per = (X.n + p.chunks - 1) / p.chunks;
   a.w = p.w;
   a.beta_f = (float)(p.beta * 1.4426950408889634);  // beta log2(e) for the ex2-based taps
