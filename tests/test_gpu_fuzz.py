@@ -61,3 +61,25 @@ def test_predict_random_shapes(F, oracle, d, m, nq, eps, seed):
     f = host(F.fk_predict_type2(dev(th), d, m, 1.0, dev(Xq), eps, additive=additive))
     fo = oracle.predict_additive(th, Xq, 1.0, m) if additive else oracle.predict(th, Xq, 1.0, m)
     assert rel(f, np.real(fo)) <= _tol(eps)
+
+
+HEAT = dict(alpha=[[1, 0], [0, 2]], a_alpha=[1.0, -1.0], box=[[-1.0, 1.0], [-1.0, 1.0]])
+
+
+@settings(max_examples=40, deadline=None, derandomize=True)
+@given(d=st.sampled_from([1, 2]), m=st.integers(1, 24), n=st.integers(3, 3000), kind=st.sampled_from(["sobolev", "lowbias", "pik_box"]),
+       loglam=st.floats(-9, -1), s=st.sampled_from([1.0, 1.5, 2.0]), seed=st.integers(0, 10_000))
+def test_solve_random_systems(F, oracle, d, m, n, kind, loglam, s, seed):
+    """fk_solve on the oracle's moments at random shapes, penalties and lambdas: the backward error
+    in the oracle's own system (which tracks conditioning-independent accuracy, reading R8)."""
+    if kind == "pik_box" and d != 2:
+        kind = "sobolev"
+    lam = 10.0 ** loglam
+    X, Y = datagen.dataset(n, d=d, ykind="expcos" if d == 2 else "sin", seed=seed)
+    Xc = X.reshape(-1) if d == 1 else X
+    mu, r = oracle.moments(Xc, 1.0, m), oracle.rhs(Xc, Y, 1.0, m)
+    kw = dict(mu_pde=1.0, **HEAT) if kind == "pik_box" else {}
+    th, rep = F.fk_solve(dev(mu.reshape(-1)), dev(r.reshape(-1)), n, d, m, 1.0, lam, kind, s, **kw)
+    A = oracle.assemble(mu, n, d, m, lam, kind, s, **(dict(kw, L=1.0) if kw else {}))
+    assert rep["info"] == 0
+    assert oracle.backward_error(A, host(th), r.reshape(-1) / n) < 1e-11
