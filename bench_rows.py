@@ -127,12 +127,16 @@ def row_solve(out):
             t0 = time.perf_counter()
             np.linalg.solve(A, b)
             cpu = {"ms": 1e3 * (time.perf_counter() - t0), "what": "numpy.linalg.solve complex128 (the oracle's dense solve)"}
-        out.append({"row": "A10/A11 assemble + solve", "d": d, "m": m, "kind": kind, "D": D, "ms": ms,
-                    "backward_err": rep["backward_err"],
-                    "roofline": {"bound": "alu", "achieved": gflops / 1e3, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                                 "frac": gflops / 1e3 / FP64_PEAK_TFLOPS, "flops": (D + 1) ** 3 / 3.0,
-                                 "peak_source": "148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz"},
-                    "cpu_oracle": cpu})
+        if rep["iters"] > 0:  # the CG path: the N^3/3 Cholesky model does not describe it
+            roof = {"bound": "latency", "note": f"conjugate gradients, {rep['iters']} iterations of FFT-Toeplitz products "
+                    "(5 own kernels + cuFFT each) after a dense-block inverse; dense Cholesky of the same system: "
+                    f"(N^3/3 = {(D + 1) ** 3 / 3.0:.3g} flops) see profiles/r01_pcg_c3_launches.txt"}
+        else:
+            roof = {"bound": "alu", "achieved": gflops / 1e3, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                    "frac": gflops / 1e3 / FP64_PEAK_TFLOPS, "flops": (D + 1) ** 3 / 3.0,
+                    "peak_source": "148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz"}
+        out.append({"row": "A10/A11 assemble + solve", "d": d, "m": m, "kind": kind, "D": D, "ms": ms, "iters": rep["iters"],
+                    "backward_err": rep["backward_err"], "roofline": roof, "cpu_oracle": cpu})
 
 
 def row_post(out):

@@ -394,22 +394,37 @@ __device__ __forceinline__ double2 entry_d2(const SysArgs& g, int i, int j, int 
   return v;
 }
 
-__global__ void k_assemble_real_d2(SysArgs g, double* __restrict__ M) {
+// d = 2, one thread per pair of modes (t1 >= t2; t = 0 the centre, t >= 1 the positive-half mode
+// c0 + t and its mirror c0 - t): the 4 complex entries A(+-k1, +-k2) are evaluated once and give
+// the 2 x 2 real block (a1|b1) x (a2|b2) -- the per-entry kernel evaluated each complex entry 4 times.
+//   (a,a) Re(A++ + A+- + A-+ + A--)   (a,b) -Im(A++ - A+- + A-+ - A--)
+//   (b,a) Im(A++ + A+- - A-+ - A--)   (b,b) Re(A++ - A+- - A-+ + A--)
+__global__ void k_assemble_real_d2_blk(SysArgs g, double* __restrict__ M) {
   const int64_t N = g.D + 1;
-  const int v = blockIdx.y;
-  const int u = v + blockIdx.x * blockDim.x + threadIdx.x;
-  if (u >= g.D) return;
+  const int c0 = (g.D - 1) / 2;
+  const int t2 = blockIdx.y;
+  const int t1 = t2 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (t1 > c0) return;
   const int side = 2 * g.m + 1;
   const float inv_side = 1.0f / (float)side;
-  const PCol pu = pcol(g, u), pv = pcol(g, v);
-  double s = 0.0;
-  for (int x = 0; x < pu.cnt; ++x)
-    for (int y = 0; y < pv.cnt; ++y) {
-      const double2 a = entry_d2(g, pu.i[x], pv.i[y], side, inv_side);
-      const double2 c = cmul(cmul(cconj(pu.a[x]), a), pv.a[y]);
-      s += c.x;
+  if (t2 == 0) {
+    const double2 p = entry_d2(g, c0 + t1, c0, side, inv_side);
+    if (t1 == 0) {
+      M[0] = p.x;
+      return;
     }
-  M[u + v * N] = s;
+    const double2 q = entry_d2(g, c0 - t1, c0, side, inv_side);
+    M[(2 * t1 - 1)] = p.x + q.x;
+    M[(2 * t1)] = p.y - q.y;
+    return;
+  }
+  const double2 pp = entry_d2(g, c0 + t1, c0 + t2, side, inv_side), pm = entry_d2(g, c0 + t1, c0 - t2, side, inv_side);
+  const double2 mp = entry_d2(g, c0 - t1, c0 + t2, side, inv_side), mm = entry_d2(g, c0 - t1, c0 - t2, side, inv_side);
+  const int64_t ua = 2 * t1 - 1, ub = 2 * t1, va = 2 * t2 - 1, vb = 2 * t2;
+  M[ua + va * N] = pp.x + pm.x + mp.x + mm.x;
+  M[ub + va * N] = pp.y + pm.y - mp.y - mm.y;
+  M[ub + vb * N] = pp.x - pm.x - mp.x + mm.x;
+  if (t1 > t2) M[ua + vb * N] = -(pp.y - pm.y + mp.y - mm.y);
 }
 
 void launch_assemble(const SysArgs& g, double* M, cudaStream_t s) {
@@ -417,7 +432,7 @@ void launch_assemble(const SysArgs& g, double* M, cudaStream_t s) {
   if (g.d == 1 && (g.kind == FK_SOBOLEV || g.kind == FK_LOWBIAS))
     k_assemble_real_d1<<<grid, 256, 0, s>>>(g, M);
   else if (g.d == 2 && g.kind != FK_ADDITIVE && (g.kind == FK_SOBOLEV || g.kind == FK_LOWBIAS || g.dsym))
-    k_assemble_real_d2<<<grid, 256, 0, s>>>(g, M);
+    k_assemble_real_d2_blk<<<dim3(((g.D - 1) / 2 + 256) / 256, (g.D - 1) / 2 + 1), 256, 0, s>>>(g, M);
   else
     k_assemble_real<<<grid, 256, 0, s>>>(g, M);
 }
