@@ -392,7 +392,8 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64" if eps < 1e-7 else "f32",  # fp64 mode: fp64 taps, 64-bit fixed-point sums
             "data": "synthetic",
             "config": {"workload": cfg["desc"], "n": n, "d": d, "m": m, "s": cfg["s"], "lambda": cfg["lam"], "eps": eps, "L": L,
                        "kind": cfg["kind"], "xkind": "uniform" if cfg["xkind"] == 0 else "gaussian",

@@ -108,6 +108,40 @@ __device__ __forceinline__ void es_taps_f64(double f, int d0, double beta, doubl
   }
 }
 
+// fp64-accuracy taps of both dimensions by Horner's rule on the launch's Chebyshev-fitted table
+// (es_horner_table: W polynomials of degree W + 2 in s in [-1, 1], the same table the 1-D fp64
+// kernel uses) instead of 2W fp64 exp + sqrt; each coefficient serves both dimensions.  The
+// first tap d0 = first_tap_d(f, W) puts u = f - d0 in [W/2 - 1, W/2], the table's interval.
+__constant__ double c_es2_coef[16 * 19];
+
+template <int W>
+__device__ __forceinline__ void es_taps2_horner(double fy, int dy, double fx, int dx, double* py, double* px) {
+  constexpr int NP = W + 3;
+  const double sy = 2.0 * (fy - dy - 0.5 * W + 1.0) - 1.0;
+  const double sx = 2.0 * (fx - dx - 0.5 * W + 1.0) - 1.0;
+#pragma unroll
+  for (int i = 0; i < W; ++i) {
+    double ay = c_es2_coef[i * NP + NP - 1], ax = ay;
+#pragma unroll
+    for (int q = NP - 2; q >= 0; --q) {
+      const double c = c_es2_coef[i * NP + q];
+      ay = fma(ay, sy, c);
+      ax = fma(ax, sx, c);
+    }
+    py[i] = ay;
+    px[i] = ax;
+  }
+}
+
+static fk_status upload_es2_table(int w, double beta, cudaStream_t s) {
+  const double* coef = nullptr;
+  const fk_status st = es_horner_table(EsParams{w, beta}, &coef);
+  if (st != FK_OK) return st;
+  if (cudaMemcpyToSymbolAsync(c_es2_coef, coef, (size_t)w * (w + 3) * 8, 0, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+    return FK_E_CUDA;
+  return FK_OK;
+}
+
 __device__ __noinline__ void drain_row(int* row, int w, double* carry_row, double inv_scale) {
   for (int b = 0; b < w; ++b) {
     const int v = atomicExch(row + b, 0);
@@ -394,8 +428,7 @@ __global__ void __launch_bounds__(1024, 1) k_spread2d_f64(const XT* __restrict__
       continue;
     }
     if (MU && lrA >= rA0 && lrA < rA0 + g.gA.R) {
-      es_taps_f64<W>(f0, d00, g.beta_d, py);
-      es_taps_f64<W>(f1, d01, g.beta_d, px);
+      es_taps2_horner<W>(f0, d00, f1, d01, py, px);
 #pragma unroll
       for (int a = 0; a < W; ++a) {
         const double wy = py[a] * kSX;
@@ -412,8 +445,7 @@ __global__ void __launch_bounds__(1024, 1) k_spread2d_f64(const XT* __restrict__
       const int e1 = first_tap_d(g1, W);
       const int lrB = (int)H0 + g.KB + e0, lcB = (int)H1 + g.KB + e1;
       if (lrB >= rB0 && lrB < rB0 + g.gB.R) {
-        es_taps_f64<W>(g0, e0, g.beta_d, py);
-        es_taps_f64<W>(g1, e1, g.beta_d, px);
+        es_taps2_horner<W>(g0, e0, g1, e1, py, px);
         const double y = (double)Y[j];
         const double ys = y * sy;
         if (fabs(ys) < 2097152.0) {
@@ -589,8 +621,7 @@ __global__ void __launch_bounds__(1024, 1) k_cross2d_f64(const XT* __restrict__ 
         bad = true;
         continue;
       }
-      es_taps_f64<W>(fa, d00, g.beta_d, py);
-      es_taps_f64<W>(fb, d01, g.beta_d, px);
+      es_taps2_horner<W>(fa, d00, fb, d01, py, px);
       unsigned* lo = smxp + 2 * q * cells;
       int* hi = (int*)(lo + cells);
       double* carry = g.carry + (int64_t)(p0 + q) * cells;
@@ -704,6 +735,9 @@ __global__ void k_deconv2d(const double2* __restrict__ F, int nf, int K, const d
 // ------------------------------------------------------------------------------------------
 // host side
 // ------------------------------------------------------------------------------------------
+// the tap count dispatch_w64 instantiates for w (its Horner table must match)
+static int w64_of(int w) { return (w >= 9 && w <= 15) ? w : 16; }
+
 template <typename F>
 static void dispatch_w64(int w, F&& f) {
   switch (w) {
@@ -914,6 +948,7 @@ fk_status type1_2d_run(int m, double eps, const fk_points& X, const void* Y, dou
         if (X.dtype == FK_F32) go(k_spread2d_f64<WW, float>, (const float*)X.ptr, (const float*)Y);
         else go(k_spread2d_f64<WW, double>, (const double*)X.ptr, (const double*)Y);
       };
+      FK_TRY(upload_es2_table(w64_of(p.w), p.beta, s));
       dispatch_w64(p.w, byw);
     }
     FK_CUDA_TRY(cudaGetLastError());
@@ -1188,6 +1223,7 @@ fk_status cross_run(const fk_points& X, double L, int m, double eps, double* G, 
         if (X.dtype == FK_F32) go(k_cross2d_f64<WW, float>, (const float*)X.ptr, 1024);  // fp32 points, fp64 accuracy
         else go(k_cross2d_f64<WW, double>, (const double*)X.ptr, 1024);
       };
+      FK_TRY(upload_es2_table(w64_of(p.w), p.beta, s));
       dispatch_w64(p.w, byw);
     }
     FK_CUDA_TRY(cudaGetLastError());
