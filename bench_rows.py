@@ -55,7 +55,8 @@ def row_predict(out):
     from paper_2509_02649_b200 import fk
 
     for d, m, nq, eps, dt in [(1, 1000, 1 << 30, 1e-6, torch.float32), (1, 1000, 1 << 27, 1e-10, torch.float64),
-                              (2, 64, 1 << 28, 1e-6, torch.float32), (10, 50, 1 << 26, 1e-6, torch.float32)]:
+                              (2, 64, 1 << 28, 1e-6, torch.float32),
+                              (2, 64, 1 << 26, 1e-10, torch.float64), (10, 50, 1 << 26, 1e-6, torch.float32)]:
         additive = d > 2
         rng = np.random.default_rng(0)
         D = d * (2 * m + 1) if additive else (2 * m + 1) ** d
