@@ -44,7 +44,9 @@ CONFIGS = {
                desc="C5 low-bias additive d=10 m=50 n=1e9 (10 1-D moment/rhs passes + 45 pairwise 2-D cross moments), X SoA"),
 }
 NOMINAL_HBM_GBS = 8000.0
-ATOMS_RANDOM_PEAK = 2.604e12  # measured random-address int32 ATOMS lane-ops/s, chip-wide (profiles/r01_microbench_spread.log)
+# measured int32 shared-memory ATOMS.ADD lane-ops/s, chip-wide (profiles/r01_microbench_spread.log):
+ATOMS_RANDOM_PEAK = 2.604e12     # random addresses (3.5-way bank conflicts: what a random scatter can reach)
+ATOMS_CFREE_PEAK = 9.065e12      # conflict-free (one wavefront per instruction: the hardware ceiling)
 
 
 def parse():
@@ -63,6 +65,11 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-n", type=float, default=float(1 << 30))
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for N > 1 (gloo: exercise the distributed branch on one GPU / CPU transport)")
+    ap.add_argument("--no-paper-precision", action="store_true",
+                    help="skip the fp64-mode (eps = 1e-10, the paper's complex-128 arithmetic) record of the d = 1 configs")
+    ap.add_argument("--pp-steps", type=int, default=3)
     return ap.parse_args()
 
 
@@ -217,16 +224,21 @@ def ncu_traffic(config: str):
 
 
 def es_width(eps):
-    """Taps per dimension of the fp32 d = 2 spreading window (csrc/spread2d.cu es_width, sigma = 2)."""
+    """Taps per dimension of the d = 2 spreading window (csrc/spread2d.cu es_width, sigma = 2):
+    fp32 fixed-point path 5..8, fp64 mode (eps < 1e-7) 9..16."""
     import math
 
-    return min(8, max(5, int(math.ceil(math.log10(1.0 / eps))) + 1))
+    if eps >= 1e-7:
+        return min(8, max(5, int(math.ceil(math.log10(1.0 / eps))) + 1))
+    return min(16, max(9, int(math.ceil(math.log10(1.0 / eps))) + 2))
 
 
 def cross_width(eps, m):
     """Taps per dimension of the cross-moment window: sigma = 4 with one tap fewer when one pair
-    grid fits a CTA (csrc/spread2d.cu make_planx), else the sigma = 2 width."""
+    grid fits a CTA (csrc/spread2d.cu make_planx, fp32 path only), else the sigma = 2 width."""
     w = es_width(eps)
+    if eps < 1e-7:
+        return w
     w4 = max(5, w - 1)
     nf4 = 4 * (2 * m + 1)
     nf4 = next(v for v in range(nf4, 8 * nf4 + 64) if v % 8 == 0 and _smooth(v))
@@ -266,10 +278,14 @@ def main():
 
     if not os.path.exists(fk.LIB_PATH):
         build.build()
+    local = local % max(1, torch.cuda.device_count())  # gloo runs may place several ranks on one GPU
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     d, m, n = cfg["d"], cfg["m"], cfg["n"]
     L, eps = 1.0, args.eps
     lo = n * rank // world
@@ -289,6 +305,7 @@ def main():
         buffers = _moment_buffers(d, m, dev)
         theta = torch.empty((2 * m + 1) ** d, dtype=torch.complex128, device=dev)
     pik = pi_kwargs(cfg)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)  # FK_DSTATUS_* bits of every fit (read after timing)
 
     # small fits are launch-latency bound: one CUDA graph per fit (type-1 pass + solve), one GPU only
     use_graph = args.graph == "on" or (args.graph == "auto" and world == 1 and not additive and n <= 10_000_000)
@@ -302,9 +319,10 @@ def main():
         if graph is not None:
             graph.replay()
         elif additive:
-            fit_additive_distributed(X, Y, n, L, m, cfg["lam"], eps, buffers=buffers, theta_out=theta)
+            fit_additive_distributed(X, Y, n, L, m, cfg["lam"], eps, buffers=buffers, theta_out=theta, status=status)
         else:
-            fit_distributed(X, Y, n, L, m, cfg["lam"], cfg["kind"], cfg["s"], eps, buffers=buffers, theta_out=theta, **pik)
+            fit_distributed(X, Y, n, L, m, cfg["lam"], cfg["kind"], cfg["s"], eps, buffers=buffers, theta_out=theta, status=status,
+                            **pik)
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -340,6 +358,9 @@ def main():
         fk.profile_enable(False)
         sp1, nl1, _ = fk.profile_read()
         spread_ms, spread_launches = sp1 * args.steps, nl1 * args.steps
+    if graph is not None:
+        graph.check()
+    fit_ok = int(status.item()) == 0  # no skipped coordinate, factorisation SPD, no watchdog
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -364,21 +385,33 @@ def main():
     else:
         # d >= 2 / additive: bound by random-address shared-memory atomics (2 w^2 per sample for d = 2,
         # npairs w^2 + 2 d x 4 per sample for the additive model); peak = the measured random ATOMS rate
+        # fp64 mode: 64-bit fixed point as int32 pairs, up to 2 ATOMS per tap (pair_add: low word, and
+        # the high word when the tap's high part or the carry is non-zero -- counted as 2, an upper bound)
         w = es_width(eps)
+        per_tap = 2 if eps < 1e-7 else 1
+        d1 = 8 if eps >= 1e-7 else 2 * 8 * 2  # per-feature 1-D pass: 2 channels x 4 taps (fp32); 2 x 8 septic taps x 2 words
         if additive:
             wc = cross_width(eps, m)
-            atoms = n_loc * (d * (d - 1) // 2 * wc * wc + d * 8)
+            atoms = n_loc * (d * (d - 1) // 2 * wc * wc * per_tap + d * d1)
         else:
-            atoms = n_loc * 2 * w * w
+            atoms = n_loc * 2 * w * w * per_tap
         achieved = atoms / (spread_per_step_ms * 1e-3) / 1e9
         tr = ncu_traffic(args.config)
-        roof = {"bound": "alu", "achieved": achieved, "peak": ATOMS_RANDOM_PEAK / 1e9, "unit": "Gatomic/s",
-                "frac": achieved * 1e9 / ATOMS_RANDOM_PEAK, "traffic": None if tr is None else tr["dram_bytes_per_sample"] * n_loc,
+        roof = {"bound": "alu", "achieved": achieved, "peak": ATOMS_CFREE_PEAK / 1e9, "unit": "Gatomic/s",
+                "frac": achieved * 1e9 / ATOMS_CFREE_PEAK, "traffic": None if tr is None else tr["dram_bytes_per_sample"] * n_loc,
+                "frac_of_random_atoms": achieved * 1e9 / ATOMS_RANDOM_PEAK,
                 "kernel": "spreading kernels (shared-memory int32 atomics)",
-                "peak_source": "measured random-address ATOMS.ADD rate, profiles/r01_microbench_spread.log",
+                "peak_source": "measured conflict-free int32 ATOMS.ADD rate (9.07e12/s); frac_of_random_atoms: vs the measured "
+                               "random-address rate (2.60e12/s), profiles/r01_microbench_spread.log",
+                "atomics_counted": f"{'2 w^2' if not additive else 'npairs w^2 + d x (1-D pass)'} per sample, w = {w}"
+                                   + (f", cross w = {cross_width(eps, m)}" if additive else "")
+                                   + (", x2 int32 words per tap (fp64 mode, upper bound)" if eps < 1e-7 else ""),
                 "hbm_gbs": bytes_step / (spread_per_step_ms * 1e-3) / 1e9, "spread_ms_per_step": spread_per_step_ms,
                 "spread_share_of_step": spread_per_step_ms / ms_step, "atomics_per_step": atoms}
 
+    pp = None
+    if d == 1 and eps >= 1e-7 and not args.no_paper_precision and graph is None:
+        pp = paper_precision(args, cfg, X, Y, n, n_loc, world, dev, buffers, theta, pik, peaks)
     e2e = None
     if not args.no_e2e and rank == 0:
         e2e = run_e2e_additive(args, cfg, dev, eps) if additive else run_e2e(args, cfg, dev, eps)
@@ -402,6 +435,8 @@ def main():
                                  f"inputs {bytes_step / 1e6:.1f} MB/GPU: L2-resident across steps (launch-bound config)"),
                        "cuda_graph": graph is not None},
             "roofline": roof,
+            "fit_status_ok": fit_ok,
+            "paper_precision": pp,
             "hbm_gbs_fit": n_loc * (d + 1) * 4 / (ms_step * 1e-3) / 1e9,
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -413,6 +448,79 @@ def main():
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def paper_precision(args, cfg, X, Y, n, n_loc, world, dev, buffers, theta, pik, peaks):
+    """The same fit at the paper's arithmetic (sec. 3.1: complex-128): the fp64 mode,
+    eps = 1e-10 (septic B-spline window, 64-bit fixed-point sums), on the same resident fp32 X, Y.
+    Timed like the main line (CUDA events between barriers, max over ranks), with its own clocks,
+    the spreading kernels' roofline and the moment checks available at this size."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2509_02649_b200 import fk
+    from paper_2509_02649_b200.fit import _moment_buffers, fit_distributed
+
+    eps = 1e-10
+    bufs = _moment_buffers(1, cfg["m"], dev)
+    st = torch.zeros(1, dtype=torch.int32, device=dev)
+
+    def step():
+        fit_distributed(X, Y, n, 1.0, cfg["m"], cfg["lam"], cfg["kind"], cfg["s"], eps, buffers=bufs, theta_out=theta, status=st, **pik)
+
+    step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    fk.profile_read()
+    fk.profile_enable(True)
+    clocks = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
+    clocks.start()
+    time.sleep(0.3)
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.pp_steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1) / args.pp_steps
+    clk = clocks.stop()
+    fk.profile_enable(False)
+    sp_ms, sp_launches, kernels = fk.profile_read()
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    # one pass per channel (X read twice): algorithmic 8 B per sample over the two passes of a fit
+    sp_step = sp_ms / args.pp_steps
+    achieved = n_loc * 8 / (sp_step * 1e-3) / 1e9
+    peak = peaks.get("hbm_gbs", 6650.0)
+    _, mu64, r64 = bufs
+    _, mu32, r32 = buffers  # the main line's last fit (fp32 mode) of the same data
+    mu64h, mu32h, r64h, r32h = (v.reshape(-1).cpu().numpy() for v in (mu64, mu32, r64, r32))
+    import numpy as np
+
+    K = 2 * cfg["m"]
+    herm = float(np.max(np.abs(mu64h[::-1] - np.conj(mu64h))) / abs(mu64h[K]))
+    return {
+        "value": n / (ms * 1e-3), "unit": "samples/s", "ms_per_step": ms, "steps": args.pp_steps, "dtype": "f64",
+        "config": {"workload": cfg["desc"], "eps": eps, "n": n, "storage": "fp32 X, Y (as the main line)",
+                   "window": "septic B-spline (8 taps, sigma ~ 11), 64-bit fixed point, one pass per channel"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "kernel": "k_spread1d_bs7 (2 launches per fit: moments, rhs)",
+                     "spread_ms_per_step": sp_step, "spread_share_of_step": sp_step / ms,
+                     "note": "algorithmic 8 B/sample per fit; the kernel is bound by its shared-memory pair atomics (DESIGN.md §5)"},
+        "clocks": clk, "gpu_launches": kernels,
+        "moment_checks": {"mu0_exact": bool(mu64h[K].real == n and mu64h[K].imag == 0.0), "hermitian_rel": herm,
+                          "rel_l2_vs_fp32_mode_mu": float(np.linalg.norm(mu64h - mu32h) / np.linalg.norm(mu64h)),
+                          "rel_l2_vs_fp32_mode_r": float(np.linalg.norm(r64h - r32h) / np.linalg.norm(r64h)),
+                          "oracle_parity": "tests/test_gpu_d1.py::test_type1_fp64_matches_oracle, test_fit_c2_shape_end_to_end[*-fp64] "
+                                           "(<= 1e-10 l2 and 1e-9 n per element vs the fp64 direct sums)"},
+        "fit_status_ok": int(st.item()) == 0,
+    }
 
 
 def run_e2e_additive(args, cfg, dev, eps):
@@ -471,7 +579,7 @@ def run_e2e(args, cfg, dev, eps):
 
     from datagen.device import gen_dataset
     from paper_2509_02649_b200 import fk
-    from paper_2509_02649_b200.fit import HostStreamer, _moment_buffers
+    from paper_2509_02649_b200.fit import _moment_buffers
 
     d, m = cfg["d"], cfg["m"]
     n = int(min(args.e2e_n, cfg["n"]))
@@ -486,14 +594,13 @@ def run_e2e(args, cfg, dev, eps):
         Xh[lo:lo + c].copy_(tmpx[:c])
         Yh[lo:lo + c].copy_(tmpy[:c])
     del tmpx, tmpy
-    st = HostStreamer(chunk, d, torch.float32, dev)
     _, mu, r = _moment_buffers(d, m, dev)
     D = (2 * m + 1) ** d
     theta_h = torch.empty(D, dtype=torch.complex128, pin_memory=True)
     pik = pi_kwargs(cfg)
 
-    def step():
-        st.moments(Xh, Yh, 1.0, m, eps, mu, r)
+    def step():  # the library's native host-streaming entry point (chunked H2D overlapped with the spread)
+        fk.fk_rhs_type1_host(Xh, Yh, 1.0, m, eps, r_out=r, mu_out=mu, chunk=chunk, check=False, device=dev)
         th, _ = fk.fk_solve(mu.reshape(-1), r.reshape(-1), n, d, m, 1.0, cfg["lam"], cfg["kind"], cfg["s"], report=False, **pik)
         theta_h.copy_(th, non_blocking=True)
 
@@ -510,7 +617,9 @@ def run_e2e(args, cfg, dev, eps):
     ms = e0.elapsed_time(e1) / steps
     return {"value": n / (ms * 1e-3), "unit": "samples/s", "h2d_bytes_per_step": n * (d + 1) * 4, "d2h_bytes_per_step": D * 16,
             "n": n, "ms_per_step": ms,
-            "path": "fit.HostStreamer + fk_solve: pinned host X,Y -> chunked H2D (X and Y on two copy streams) overlapped with fk_rhs_type1; theta D2H; bound by the PCIe link (~55 GB/s)"}
+            "path": "fk_rhs_type1_host (C ABI: pinned host X, Y -> chunked H2D on the library's copy stream overlapped with the "
+                    "spreading of the previous chunk) + fk_solve; theta D2H; bound by the PCIe link (~55 GB/s); n = 2^30 bounded sample "
+                    "(the rate is PCIe-bound and independent of n)"}
 
 
 if __name__ == "__main__":

@@ -35,8 +35,9 @@
  *   - Accuracy: eps is the requested relative l2 accuracy of each output vector against the
  *     exact sums (reading R7); valid range [1e-14, 1e-1].  eps >= 1e-7 selects the fp32
  *     spreading path (cubic B-spline window, fixed-point shared-memory accumulation); smaller eps
- *     selects the fp64 mode (d = 1: septic B-spline window, 64-bit fixed-point accumulation;
- *     d = 2 / cross moments: exponential-of-semicircle window, fp64 accumulation).
+ *     selects the fp64 mode (d = 1: septic B-spline window; d = 2 / cross moments:
+ *     exponential-of-semicircle window at sigma = 2; both accumulate in 64-bit fixed point held
+ *     as int32 pairs in shared memory, drained into fp64 carry grids).
  */
 #ifndef FK_H
 #define FK_H
@@ -62,6 +63,15 @@ typedef enum fk_status {
 } fk_status;
 
 typedef enum fk_dtype { FK_F32 = 0, FK_F64 = 1 } fk_dtype;
+
+/* Bits a kernel ORs into the caller's device status word (d_status arguments, fk_problem.d_status).
+ * FK_E_RANGE (2) doubles as the bit of a skipped out-of-range / NaN coordinate; the solve adds: */
+enum {
+  FK_DSTATUS_RANGE = FK_E_RANGE, /* a coordinate outside [-L, L] or NaN was skipped */
+  FK_DSTATUS_NOT_SPD = 0x10,     /* fk_solve: the Cholesky factorisation met a non-positive pivot */
+  FK_DSTATUS_WATCHDOG = 0x20     /* fk_solve: a dataflow wait of the factorisation / back
+                                    substitution hit its 5 s watchdog (theta is not valid) */
+};
 
 /* n points in d dimensions: coordinate l of sample j is at element ptr[j*stride_n + l*stride_d]
  * (element strides, not bytes).  Row-major n x d: stride_n = d, stride_d = 1; SoA columns:
@@ -121,6 +131,9 @@ typedef struct fk_problem {
   const double* colloc_moments; /* device: PIK_COLLOC only, (4m+1)^d moments of the n_colloc collocation
                                    points (fk_moments_type1 on them); D is given by alpha / a_alpha */
   double n_colloc;              /* PIK_COLLOC: number of collocation points n_r */
+  int* d_status;                /* optional device int (may be NULL): fk_solve ORs FK_DSTATUS_NOT_SPD /
+                                   FK_DSTATUS_WATCHDOG into it from the device, so a failed
+                                   factorisation is reported even on the asynchronous rep == NULL path */
 } fk_problem;
 
 typedef struct fk_solve_report {
@@ -130,6 +143,10 @@ typedef struct fk_solve_report {
   int32_t n_unknowns;  /* D */
   int32_t iters;       /* conjugate-gradient iterations (0: dense Cholesky) */
   int32_t reserved;
+  double rcond_est;    /* estimate of 1 / cond_2(A) of the solved real-symmetric system (dense path:
+                          8 power steps on A = L L^T and 8 inverse-iteration steps with the factor;
+                          the ratio of the two Rayleigh quotients); 0 on the CG path (not estimated).
+                          With it an fp32-mode theta error ~ cond(A) x moment error can be read. */
 } fk_solve_report;
 
 /* theta = A^{-1} r / n in fp64 (P:513 for the additive block system).  For real Y theta
@@ -142,7 +159,8 @@ typedef struct fk_solve_report {
  * and is skipped while the stream is being captured into a CUDA graph.  theta_out: D complex128,
  * D = (2m+1)^d (d(2m+1) for ADDITIVE).  rep may be NULL (dense path: no synchronisation,
  * CUDA-graph capturable); otherwise the call synchronises `stream` and fills *rep.  Returns FK_E_SOLVE if A is not numerically positive
- * definite (only detected when rep != NULL). */
+ * definite when rep != NULL; on every path a non-positive pivot or a watchdog expiry is also ORed
+ * into *P->d_status (FK_DSTATUS_NOT_SPD / FK_DSTATUS_WATCHDOG) by the device, when d_status != NULL. */
 fk_status fk_solve(const fk_problem* P, double* theta_out, fk_solve_report* rep, void* ws, size_t ws_bytes,
                    fk_stream_t stream);
 
@@ -175,6 +193,18 @@ fk_status fk_solve_path(const fk_problem* P, const double* lambdas, int nlam, do
 fk_status fk_path_validate(const fk_problem* Pv, const double* theta, int nlam, double sum_y2, double* risk_out, void* ws,
                            size_t ws_bytes, fk_stream_t stream);
 
+/* The same one-pass rhs (+ moments) from HOST memory (the end-to-end path of a fit whose data live
+ * on the host): X.ptr and Y point to host arrays (page-locked for overlap; pageable works but the
+ * copies then serialise), X contiguous (stride_n = d, stride_d = 1), d in {1, 2}.  The samples are
+ * streamed in chunks of `chunk` samples (0 = 2^24) through two device staging buffers taken from
+ * `ws`: chunk i+1 is copied host->device on the library's copy stream while `stream` spreads chunk
+ * i (FK_ACCUMULATE across chunks), so the PCIe transfer and the spreading overlap.  Outputs, flags,
+ * d_status and ordering as fk_rhs_type1 (all work is ordered after prior work on `stream`; the
+ * host arrays must stay valid until `stream` has passed the call).  ws: fk_workspace_bytes(
+ * FK_ENTRY_RHS_HOST, d, m, eps, dtype, chunk, 0). */
+fk_status fk_rhs_type1_host(fk_points X, const void* Y, double L, int m, double eps, double* r_out, double* mu_out, int flags,
+                            int64_t chunk, void* ws, size_t ws_bytes, int* d_status, fk_stream_t stream);
+
 typedef enum fk_entry {
   FK_ENTRY_MOMENTS = 0,
   FK_ENTRY_RHS = 1,
@@ -182,7 +212,8 @@ typedef enum fk_entry {
   FK_ENTRY_SOLVE = 3,
   FK_ENTRY_PREDICT = 4,
   FK_ENTRY_SOLVE_PATH = 5, /* n = number of lambdas */
-  FK_ENTRY_PATH_VALIDATE = 6 /* n = number of lambdas */
+  FK_ENTRY_PATH_VALIDATE = 6, /* n = number of lambdas */
+  FK_ENTRY_RHS_HOST = 7        /* n = chunk (samples per staged chunk; 0 = 2^24) */
 } fk_entry;
 
 /* Workspace bytes the call `entry` needs for (d, m, eps, dtype, n, kind) on the current device

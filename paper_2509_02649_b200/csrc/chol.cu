@@ -36,11 +36,17 @@ constexpr int CT = 128;   // threads per CTA
 
 // Flags are polled with relaxed loads: ld.acquire would invalidate the whole L1 (CCTL.IVALL) on every
 // poll; the tile data is read with ld.global.cg (L2, coherent), so no L1 invalidation is needed.
+// Ordering (PTX memory model): the producer publishes with st.release; the consumer, once its
+// relaxed poll has observed the flag, executes ONE fence.acq_rel.gpu (acquire_fence) before the
+// CTA barrier that releases the tile reads, which makes the pattern release -> observe -> acquire
+// fence a synchronisation, so the tile loads cannot be satisfied by stale data.
 __device__ __forceinline__ int ld_relaxed(const int* p) {
   int v;
   asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+
+__device__ __forceinline__ void acquire_fence() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
 __device__ __forceinline__ void st_release(int* p, int v) { asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory"); }
 
@@ -66,8 +72,9 @@ __device__ __forceinline__ void stage(double (*T)[LDS], const double* __restrict
 }
 
 // Watchdog for every spin-wait: a dependency that is not published within 5 s (it never happens
-// in a correct schedule -- the longest legitimate wait is a few ms) ends the wait, so a scheduling
-// bug yields a wrong factor (caught by the backward error) instead of a hung GPU.
+// in a correct schedule -- the longest legitimate wait is a few ms) ends the wait instead of
+// hanging the GPU, and records -1 in *info (unless a pivot failure was recorded first), which
+// fk_solve turns into FK_DSTATUS_WATCHDOG / FK_E_SOLVE: the factor is then reported invalid.
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -76,16 +83,28 @@ __device__ __forceinline__ unsigned long long gtime() {
 constexpr unsigned long long kSpinLimitNs = 5000000000ULL;
 
 // wait until both flags are set (thread 0 polls fa, thread 32 polls fb; fb may be null)
-__device__ __forceinline__ void wait_flags(const int* fa, const int* fb) {
+__device__ __forceinline__ void watchdog_expired(int* info) { atomicCAS(info, 0, -1); }
+
+__device__ __forceinline__ void wait_flags(const int* fa, const int* fb, int* info) {
   if (threadIdx.x == 0) {
     const unsigned long long t0 = gtime();
-    while (ld_relaxed(fa) == 0 && gtime() - t0 < kSpinLimitNs) {
+    while (ld_relaxed(fa) == 0) {
+      if (gtime() - t0 >= kSpinLimitNs) {
+        watchdog_expired(info);
+        break;
+      }
     }
+    acquire_fence();
   }
   if (threadIdx.x == 32 && fb) {
     const unsigned long long t0 = gtime();
-    while (ld_relaxed(fb) == 0 && gtime() - t0 < kSpinLimitNs) {
+    while (ld_relaxed(fb) == 0) {
+      if (gtime() - t0 >= kSpinLimitNs) {
+        watchdog_expired(info);
+        break;
+      }
     }
+    acquire_fence();
   }
   __syncthreads();
 }
@@ -103,7 +122,8 @@ __device__ __forceinline__ double ld_cg_volatile(const double* p) {
 }
 
 // Ta[p][r] = L_jj(r, p), dv[c] = 1 / L_jj(c, c) from the side buffer, waiting until published
-__device__ __forceinline__ void stage_diag(double (*T)[LDS], double* dv, const double* __restrict__ Ld) {
+// (the polled words ARE the data, each an 8-byte value written once, so no fence is needed here)
+__device__ __forceinline__ void stage_diag(double (*T)[LDS], double* dv, const double* __restrict__ Ld, int* info) {
   constexpr int PER = TS * TS / CT;
   double v[PER];
 #pragma unroll
@@ -122,7 +142,11 @@ __device__ __forceinline__ void stage_diag(double (*T)[LDS], double* dv, const d
       d = ld_cg_volatile(Ld + TS * TS + threadIdx.x);
       ok = false;
     }
-    if (ok || gtime() - t0 > kSpinLimitNs) break;
+    if (ok) break;
+    if (gtime() - t0 > kSpinLimitNs) {
+      watchdog_expired(info);
+      break;
+    }
   }
 #pragma unroll
   for (int q = 0; q < PER; ++q) {
@@ -151,16 +175,18 @@ __device__ __forceinline__ int tile_id(int i, int j, int nt) { return j * nt - j
 // one parallel scan of both flag columns finds the first k not yet published (smem min), so the
 // ready prefix is consumed without a flag round trip per update; at a not-ready k the CTA waits on
 // that k alone and scans again afterwards.  Returns the first k that is NOT known ready (> k0).
-__device__ __forceinline__ int ready_prefix(const int* __restrict__ flags, int nt, int ia, int ib, int k0, int kend, int* s_min) {
+__device__ __forceinline__ int ready_prefix(const int* __restrict__ flags, int nt, int ia, int ib, int k0, int kend, int* s_min,
+                                            int* info) {
   if (threadIdx.x == 0) *s_min = kend;
   __syncthreads();
   for (int k = k0 + threadIdx.x; k < kend; k += blockDim.x)
     if (!ld_relaxed(flags + tile_id(ia, k, nt)) || !ld_relaxed(flags + tile_id(ib, k, nt))) atomicMin(s_min, k);
+  acquire_fence();  // every thread that observed a flag orders the later tile loads after it
   __syncthreads();
   int first = *s_min;
   __syncthreads();
   if (first == k0) {  // nothing ready yet: wait for k0 itself
-    wait_flags(flags + tile_id(ia, k0, nt), flags + tile_id(ib, k0, nt));
+    wait_flags(flags + tile_id(ia, k0, nt), flags + tile_id(ib, k0, nt), info);
     first = k0 + 1;
   }
   return first;
@@ -339,7 +365,7 @@ __global__ void __launch_bounds__(CT) k_chol_tiles(double* __restrict__ M, int64
       }
       int rdy = c * UB;
       for (int k = c * UB; k < (c + 1) * UB; ++k) {
-        if (k >= rdy) rdy = ready_prefix(flags, nt, j, j - 1, k, (c + 1) * UB, &s_min);
+        if (k >= rdy) rdy = ready_prefix(flags, nt, j, j - 1, k, (c + 1) * UB, &s_min, info);
         stage(Ta, M, ld, N, j, k);
         stage(Tb, M, ld, N, j - 1, k);
         __syncthreads();
@@ -361,7 +387,7 @@ __global__ void __launch_bounds__(CT) k_chol_tiles(double* __restrict__ M, int64
       acc_load(a, M, ld, N, i, j, qr, qc, g, tq);
       int rdy = 0;
       for (int k = 0; k < j; ++k) {
-        if (k >= rdy) rdy = ready_prefix(flags, nt, i, j, k, j, &s_min);
+        if (k >= rdy) rdy = ready_prefix(flags, nt, i, j, k, j, &s_min, info);
         stage(Ta, M, ld, N, i, k);
         stage(Tb, M, ld, N, j, k);
         __syncthreads();
@@ -370,7 +396,7 @@ __global__ void __launch_bounds__(CT) k_chol_tiles(double* __restrict__ M, int64
       }
       if (trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
       acc_gather(a, Ct, qr, qc, g, tq);
-      stage_diag(Ta, dv, Ld + (int64_t)j * LDW);  // Ta[p][r] = L_jj(r, p)
+      stage_diag(Ta, dv, Ld + (int64_t)j * LDW, info);  // Ta[p][r] = L_jj(r, p)
       __syncthreads();
       if (trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1b));
       if (w == 0) final_trsm(Ct, Ta, dv, lane);
@@ -386,7 +412,7 @@ __global__ void __launch_bounds__(CT) k_chol_tiles(double* __restrict__ M, int64
         acc_load(sb, M, ld, N, j, j - 1, qr, qc, g, tq);
         const int nc = USE_U ? max(0, (j - 2) / UB) : 0;  // chunks summed by the U tasks (they end before k = j - 2)
         for (int c = 0; c < nc; ++c) {
-          wait_flags(uflags + j * maxc + c, nullptr);
+          wait_flags(uflags + j * maxc + c, nullptr, info);
           const double* base = part + ((int64_t)j * maxc + c) * 2 * TS * TS;
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
@@ -396,7 +422,7 @@ __global__ void __launch_bounds__(CT) k_chol_tiles(double* __restrict__ M, int64
         }
         int rdy = nc * UB;
         for (int k = nc * UB; k < j - 1; ++k) {
-          if (k >= rdy) rdy = ready_prefix(flags, nt, j, j - 1, k, j - 1, &s_min);
+          if (k >= rdy) rdy = ready_prefix(flags, nt, j, j - 1, k, j - 1, &s_min, info);
           stage(Ta, M, ld, N, j, k);
           stage(Tb, M, ld, N, j - 1, k);
           __syncthreads();
@@ -407,7 +433,7 @@ __global__ void __launch_bounds__(CT) k_chol_tiles(double* __restrict__ M, int64
         if (trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
         // L_{j, j-1} = A_{j, j-1} L_{j-1, j-1}^{-T}
         acc_gather(sb, Ct, qr, qc, g, tq);
-        stage_diag(Ta, dv, Ld + (int64_t)(j - 1) * LDW);
+        stage_diag(Ta, dv, Ld + (int64_t)(j - 1) * LDW, info);
         __syncthreads();
         if (trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1b));
         if (w == 0) final_trsm(Ct, Ta, dv, lane);

@@ -1,6 +1,9 @@
 // fk_api.cu -- the extern "C" entry points of libfk (include/fk.h): argument validation on the
 // host, then dispatch to the stream-ordered implementations.
+#include <algorithm>
 #include <cmath>
+#include <map>
+#include <mutex>
 
 #include "fk_internal.cuh"
 
@@ -51,9 +54,114 @@ fk_status type1_entry(const fk_points& X, const void* Y, double L, int m, double
   return type1_run(p, X, Y, L, out, ws, ws_bytes, d_status, s);
 }
 
+// ---- host streaming (fk_rhs_type1_host) ----------------------------------------------------
+constexpr int64_t kHostChunk = 1 << 24;
+
+int64_t host_chunk(int64_t c) { return c > 0 ? c : kHostChunk; }
+
+size_t rhs_host_ws_bytes(int d, int m, double eps, int dtype, int64_t chunk) {
+  chunk = host_chunk(chunk);
+  const size_t esz = dtype == FK_F64 ? 8 : 4;
+  size_t t1 = 0;
+  if (d == 2) {
+    t1 = type1_2d_ws_bytes(m, eps, true, true, dtype);
+  } else {
+    Plan1 p;
+    if (make_plan1(d, m, eps, true, true, &p) != FK_OK) return 0;
+    t1 = type1_ws_bytes(p, true, true);
+  }
+  if (t1 == 0) return 0;
+  Bump b(nullptr, 0);
+  for (int k = 0; k < 2; ++k) {
+    b.take((size_t)chunk * d * esz);  // X staging
+    b.take((size_t)chunk * esz);      // Y staging
+  }
+  b.take(t1);
+  return b.used + 256;
+}
+
+// one copy stream per device, created on first use; the enqueue loop holds the mutex so two
+// concurrent callers' copies cannot interleave their event sequences
+struct HostCopy {
+  cudaStream_t cs = nullptr;
+};
+std::mutex g_host_mu;
+std::map<int, HostCopy> g_host;
+
+fk_status rhs_host(const fk_points& X, const void* Y, double L, int m, double eps, double* r_out, double* mu_out, int flags,
+                   int64_t chunk, void* ws, size_t ws_bytes, int* d_status, cudaStream_t s) {
+  const char* who = "fk_rhs_type1_host";
+  set_error("");
+  FK_TRY(check_common(L, m, eps, who));
+  FK_TRY(check_points(X, 1, 2, who));
+  if (!r_out) return fail(FK_E_ARG, std::string(who) + ": r_out is null");
+  if (X.n > 0 && (!Y || !X.ptr)) return fail(FK_E_ARG, std::string(who) + ": null X or Y");
+  if (X.n > 1 && (X.stride_n != X.d || (X.d > 1 && X.stride_d != 1)))
+    return fail(FK_E_ARG, std::string(who) + ": host X must be contiguous (stride_n = d, stride_d = 1)");
+  chunk = host_chunk(chunk);
+  const size_t esz = X.dtype == FK_F64 ? 8 : 4;
+  const int d = X.d;
+  const size_t need = rhs_host_ws_bytes(d, m, eps, X.dtype, chunk);
+  if (need == 0) return fail(FK_E_UNSUPPORTED, std::string(who) + ": no plan for this shape");
+  if (ws_bytes < need) return fail(FK_E_WORKSPACE, std::string(who) + ": workspace too small: need " + std::to_string(need) + " bytes");
+  Bump b(ws, ws_bytes);
+  char* xs[2];
+  char* ys[2];
+  for (int k = 0; k < 2; ++k) {
+    xs[k] = (char*)b.take((size_t)chunk * d * esz);
+    ys[k] = (char*)b.take((size_t)chunk * esz);
+  }
+  void* ws1 = b.take(0);
+  const size_t ws1_bytes = ws_bytes - (size_t)((char*)ws1 - (char*)ws);
+  if (X.n == 0) {
+    fk_points Z = X;
+    Z.n = 0;
+    Z.ptr = xs[0];
+    return type1_entry(Z, ys[0], L, m, eps, r_out, mu_out, flags, ws1, ws1_bytes, d_status, s, who);
+  }
+  int dev = 0;
+  FK_CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_host_mu);
+  HostCopy& hc = g_host[dev];
+  if (!hc.cs) FK_CUDA_TRY(cudaStreamCreateWithFlags(&hc.cs, cudaStreamNonBlocking));
+  cudaEvent_t copied[2], consumed[2];
+  for (int k = 0; k < 2; ++k) {
+    FK_CUDA_TRY(cudaEventCreateWithFlags(&copied[k], cudaEventDisableTiming));
+    FK_CUDA_TRY(cudaEventCreateWithFlags(&consumed[k], cudaEventDisableTiming));
+    FK_CUDA_TRY(cudaEventRecord(consumed[k], s));  // staging k is free once prior work on s is done
+  }
+  const int64_t nch = (X.n + chunk - 1) / chunk;
+  fk_status st = FK_OK;
+  for (int64_t i = 0; i < nch && st == FK_OK; ++i) {
+    const int k = (int)(i & 1);
+    const int64_t lo = i * chunk, c = std::min(chunk, X.n - lo);
+    FK_CUDA_TRY(cudaStreamWaitEvent(hc.cs, consumed[k], 0));
+    FK_CUDA_TRY(cudaMemcpyAsync(xs[k], (const char*)X.ptr + (size_t)lo * d * esz, (size_t)c * d * esz, cudaMemcpyHostToDevice, hc.cs));
+    FK_CUDA_TRY(cudaMemcpyAsync(ys[k], (const char*)Y + (size_t)lo * esz, (size_t)c * esz, cudaMemcpyHostToDevice, hc.cs));
+    FK_CUDA_TRY(cudaEventRecord(copied[k], hc.cs));
+    FK_CUDA_TRY(cudaStreamWaitEvent(s, copied[k], 0));
+    fk_points Xc = X;
+    Xc.ptr = xs[k];
+    Xc.n = c;
+    const int fl = (i == 0) ? flags : (flags | FK_ACCUMULATE);
+    st = type1_entry(Xc, ys[k], L, m, eps, r_out, mu_out, fl, ws1, ws1_bytes, d_status, s, who);
+    FK_CUDA_TRY(cudaEventRecord(consumed[k], s));
+  }
+  for (int k = 0; k < 2; ++k) {  // released once the recorded work completes
+    cudaEventDestroy(copied[k]);
+    cudaEventDestroy(consumed[k]);
+  }
+  return st;
+}
+
 }  // namespace
 
 extern "C" {
+
+fk_status fk_rhs_type1_host(fk_points X, const void* Y, double L, int m, double eps, double* r_out, double* mu_out, int flags,
+                            int64_t chunk, void* ws, size_t ws_bytes, int* d_status, fk_stream_t stream) {
+  return rhs_host(X, Y, L, m, eps, r_out, mu_out, flags, chunk, ws, ws_bytes, d_status, (cudaStream_t)stream);
+}
 
 const char* fk_last_error(void) { return last_error_cstr(); }
 
@@ -180,6 +288,9 @@ size_t fk_workspace_bytes(int entry, int d, int m, double eps, int dtype, int64_
       return path_validate_ws_bytes(d, m, kind, (int)std::min<int64_t>(n, 1 << 20));
     case FK_ENTRY_SOLVE_PATH:
       return solve_path_ws_bytes(d, m, kind, (int)std::min<int64_t>(n, 1 << 20));
+    case FK_ENTRY_RHS_HOST:
+      if (d > 2) return 0;
+      return rhs_host_ws_bytes(d, m, eps, dtype, n);
     default:
       set_error("fk_workspace_bytes: unknown entry");
       return 0;

@@ -96,6 +96,15 @@ int fft_friendly(int n);  // smallest 2^a 3^b 5^c >= n, even, multiple of 8
 // built once per (device, w, beta).
 inline int es_horner_degree(int w) { return w + 2; }
 fk_status es_horner_table(const EsParams& es, const double** d_coef);
+// Constant-memory copies of the tables, one slot per width w (the ES shape is beta = 2.30 w on every
+// path, so slot w never changes): a kernel of width W reads slot W.  horner_slot uploads slot w of
+// `symbol` (a __constant__ double[kHornerSlots][kHornerSlot] of the calling translation unit) once
+// per device -- no per-call copy, so concurrent calls on different streams cannot overwrite a
+// table another kernel is reading.  FK_E_UNSUPPORTED if beta is not 2.30 w (then the caller uses
+// its exp-based taps).
+constexpr int kHornerSlots = 17;
+constexpr int kHornerSlot = 16 * 19;
+fk_status horner_slot(const void* symbol, int w, double beta);
 
 // ES window Fourier transform table phihat[k] = psi-hat(k / nf), k = 0..K (computed on device).
 fk_status es_phihat_table(const EsParams& es, int nf, int K, double* d_tab, cudaStream_t s);

@@ -3,6 +3,7 @@
 #include <atomic>
 #include <cmath>
 #include <map>
+#include <set>
 #include <mutex>
 #include <tuple>
 #include <vector>
@@ -233,6 +234,27 @@ fk_status es_phihat_table(const EsParams& es, int nf, int K, double* d_tab, cuda
 // ------------------------------------------------------------------------------------------
 static std::mutex g_horner_mu;
 static std::map<std::tuple<int, int, long long>, double*> g_horner;
+
+static std::mutex g_slot_mu;
+static std::set<std::tuple<int, const void*, int>> g_slots;
+
+fk_status horner_slot(const void* symbol, int w, double beta) {
+  if (w < 1 || w >= kHornerSlots || w * (w + 3) > kHornerSlot || beta != 2.30 * w) return FK_E_UNSUPPORTED;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(dev, symbol, w);
+  {
+    std::lock_guard<std::mutex> lk(g_slot_mu);
+    if (g_slots.count(key)) return FK_OK;
+  }
+  const double* coef = nullptr;
+  FK_TRY(es_horner_table(EsParams{w, beta}, &coef));
+  // synchronous, once per (device, table, w): the first call of a shape (never inside a graph capture)
+  FK_CUDA_TRY(cudaMemcpyToSymbol(symbol, coef, (size_t)w * (w + 3) * 8, (size_t)w * kHornerSlot * 8, cudaMemcpyDeviceToDevice));
+  std::lock_guard<std::mutex> lk(g_slot_mu);
+  g_slots.insert(key);
+  return FK_OK;
+}
 
 fk_status es_horner_table(const EsParams& es, const double** d_coef) {
   int dev = 0;

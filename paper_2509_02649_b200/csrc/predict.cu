@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(512) k_gather_bs7(const XT* __restrict__ Xq, i
 
 // fp64 gather, d = 1 or additive, grid in shared memory: compile-time width, taps as polynomials
 // from a constant-memory table (es_horner_table) instead of exp + sqrt per tap
-__constant__ double c_pred_coef[16 * 19];
+__constant__ double c_pred_coef[kHornerSlots][kHornerSlot];  // slot W (horner_slot)
 
 template <typename XT, int W>
 __global__ void __launch_bounds__(512) k_gather_es_h(const XT* __restrict__ Xq, int64_t n, int nfeat, int64_t sn, int64_t sd,
@@ -356,9 +356,9 @@ __global__ void __launch_bounds__(512) k_gather_es_h(const XT* __restrict__ Xq, 
       const double* c = sgh + (int64_t)f * G + l0;
 #pragma unroll
       for (int i = 0; i < W; ++i) {
-        double psi = c_pred_coef[i * NP + NP - 1];
+        double psi = c_pred_coef[W][i * NP + NP - 1];
 #pragma unroll
-        for (int q = NP - 2; q >= 0; --q) psi = fma(psi, sv, c_pred_coef[i * NP + q]);
+        for (int q = NP - 2; q >= 0; --q) psi = fma(psi, sv, c_pred_coef[W][i * NP + q]);
         acc = fma(psi, c[i], acc);
       }
     }
@@ -640,9 +640,7 @@ static fk_status gather(const PredPlan& p, const fk_points& Xq, double L, const 
     k<<<sms * per_sm, 512, p.smem, s>>>((const XT*)Xq.ptr, Xq.n, p.nfeat, Xq.stride_n, Xq.stride_d, w.grid, p.nf, p.g.off, p.g.G, a,
                                         (XT*)out, d_status);
   } else {
-    const double* coef = nullptr;
-    if (p.in_smem && p.es.w >= 9 && es_horner_table(p.es, &coef) == FK_OK &&
-        cudaMemcpyToSymbolAsync(c_pred_coef, coef, (size_t)p.es.w * (p.es.w + 3) * 8, 0, cudaMemcpyDeviceToDevice, s) == cudaSuccess) {
+    if (p.in_smem && p.es.w >= 9 && p.es.w <= 14 && horner_slot(c_pred_coef, p.es.w, p.es.beta) == FK_OK) {
       const int per_sm = std::max(1, std::min(4, (int)(200000 / (p.smem + 1024))));
       auto go = [&](auto wtag) {
         constexpr int WW = decltype(wtag)::value;

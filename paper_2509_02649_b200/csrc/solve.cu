@@ -454,8 +454,16 @@ __global__ void k_rhs_real(SysArgs g, const double2* __restrict__ r, double* __r
   M[g.D + u * N] = s;
 }
 
-__global__ void k_theta_from_real(SysArgs g, const double* __restrict__ zs, int64_t zstride, double2* __restrict__ theta) {
+// also turns the factorisation's info word into the caller's device status bits (thread 0):
+// info > 0 = first non-positive pivot + 1, info < 0 = a dataflow wait hit its watchdog
+__global__ void k_theta_from_real(SysArgs g, const double* __restrict__ zs, int64_t zstride, double2* __restrict__ theta,
+                                  const int* __restrict__ info, int* __restrict__ d_status) {
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u == 0 && info && d_status) {
+    const int v = *info;
+    if (v > 0) atomicOr(d_status, (int)FK_DSTATUS_NOT_SPD);
+    if (v < 0) atomicOr(d_status, (int)FK_DSTATUS_WATCHDOG);
+  }
   if (u >= g.D) return;
   auto z = [&](int i) { return zs[(int64_t)i * zstride]; };
   const int v = g.kind == FK_ADDITIVE ? u % (2 * g.m + 1) : u;
@@ -488,7 +496,7 @@ __device__ __forceinline__ double ld_volatile(const double* p) {
 }
 
 __global__ void __launch_bounds__(64) k_trsv_lt(const double* __restrict__ M, int64_t ld, int D, const double* __restrict__ y,
-                                                 int64_t ystride, double* zbuf, int* ticket) {
+                                                 int64_t ystride, double* zbuf, int* ticket, int* info) {
   __shared__ double W[32][33];
   __shared__ double Ls[32][33];
   __shared__ double red[2][32][17];
@@ -541,10 +549,13 @@ __global__ void __launch_bounds__(64) k_trsv_lt(const double* __restrict__ M, in
     if (row < D) {
       unsigned long long t0, t1;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-      do {  // watchdog: a block never published within 5 s ends the wait (wrong z, no hung GPU)
+      // the polled word is the value itself (written once), so no fence is needed; watchdog: a
+      // block never published within 5 s ends the wait and marks the solve invalid (info = -1)
+      do {
         zc = ld_volatile(zbuf + row);
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
       } while (__double_as_longlong(zc) == (long long)kZSentinel && t1 - t0 < 5000000000ULL);
+      if (__double_as_longlong(zc) == (long long)kZSentinel) atomicCAS(info, 0, -1);
     }
     double Lc[16];
 #pragma unroll
@@ -599,6 +610,8 @@ size_t solve_ws_bytes(int d, int m, int kind) {
   b.take((size_t)lwork * 8);
   b.take((size_t)D * 8);
   b.take(64);
+  b.take((size_t)D * 8);  // rcond_estimate vectors
+  b.take((size_t)D * 8);
   if (kind == FK_PIK_BOX || kind == FK_PIK_COLLOC) {
     b.take((size_t)D * 16);
     b.take((size_t)d * (4 * m + 1) * 16);
@@ -1335,6 +1348,7 @@ static fk_status pcg_run(SysArgs g, const double2* r, double* x, int* iters, voi
   void* fwork = b.take(std::max<size_t>(std::max(fz.work, fd.work), 256));
   cusolverDnHandle_t h;
   FK_TRY(handle_for_device(&h));
+  if (cusolverDnSetStream(h, s) != CUSOLVER_STATUS_SUCCESS) return fail(FK_E_CUDA, "cusolverDnSetStream failed");
   int lw_potrf = 0;
   if (Dl > kTilesMaxN &&
       cusolverDnDpotrf_bufferSize(h, CUBLAS_FILL_MODE_LOWER, Dl, Ainv, (int)lda, &lw_potrf) != CUSOLVER_STATUS_SUCCESS)
@@ -1404,6 +1418,47 @@ static fk_status pcg_run(SysArgs g, const double2* r, double* x, int* iters, voi
   return FK_OK;
 }
 
+// 1 / cond_2(A) estimate from the Cholesky factor (report only): 8 power steps on A = L L^T
+// (two cublasDtrmv per step) give lambda_max from below, 8 inverse-iteration steps (two
+// cublasDtrsv) give 1/lambda_min from below; rcond_est = lambda_min_est / lambda_max_est.
+static fk_status rcond_estimate(cublasHandle_t bh, const double* L, int ld, int D, double* v, double* w, cudaStream_t s,
+                                double* out) {
+  if (cublasSetStream(bh, s) != CUBLAS_STATUS_SUCCESS) return fail(FK_E_CUDA, "cublasSetStream failed");
+  std::vector<double> h0(D);
+  for (int i = 0; i < D; ++i) h0[i] = 1.0 + 0.37 * std::sin(1.7 * i + 0.3);  // no special structure
+  double est[2] = {0.0, 0.0};
+  for (int pass = 0; pass < 2; ++pass) {
+    FK_CUDA_TRY(cudaMemcpyAsync(v, h0.data(), (size_t)D * 8, cudaMemcpyHostToDevice, s));
+    double nv = 0.0;
+    if (cublasDnrm2(bh, D, v, 1, &nv) != CUBLAS_STATUS_SUCCESS || !(nv > 0)) return fail(FK_E_CUDA, "cublasDnrm2 failed");
+    double inv = 1.0 / nv;
+    cublasDscal(bh, D, &inv, v, 1);
+    double q = 0.0;
+    for (int it = 0; it < 8; ++it) {
+      FK_CUDA_TRY(cudaMemcpyAsync(w, v, (size_t)D * 8, cudaMemcpyDeviceToDevice, s));
+      cublasStatus_t st1, st2;
+      if (pass == 0) {  // w = L (L^T v)
+        st1 = cublasDtrmv(bh, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, D, L, ld, w, 1);
+        st2 = cublasDtrmv(bh, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, D, L, ld, w, 1);
+      } else {  // w = L^{-T} (L^{-1} v)
+        st1 = cublasDtrsv(bh, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, D, L, ld, w, 1);
+        st2 = cublasDtrsv(bh, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, D, L, ld, w, 1);
+      }
+      if (st1 != CUBLAS_STATUS_SUCCESS || st2 != CUBLAS_STATUS_SUCCESS) return fail(FK_E_CUDA, "cublas trmv/trsv failed");
+      if (cublasDdot(bh, D, v, 1, w, 1, &q) != CUBLAS_STATUS_SUCCESS) return fail(FK_E_CUDA, "cublasDdot failed");
+      double nw = 0.0;
+      if (cublasDnrm2(bh, D, w, 1, &nw) != CUBLAS_STATUS_SUCCESS) return fail(FK_E_CUDA, "cublasDnrm2 failed");
+      if (!(nw > 0) || !(nw < 1e300)) break;
+      inv = 1.0 / nw;
+      cublasDscal(bh, D, &inv, w, 1);
+      std::swap(v, w);
+    }
+    est[pass] = q;  // Rayleigh quotient: lambda_max (pass 0), 1 / lambda_min (pass 1)
+  }
+  *out = (est[0] > 0 && est[1] > 0) ? 1.0 / (est[0] * est[1]) : 0.0;
+  return FK_OK;
+}
+
 fk_status solve_run(const fk_problem* P, double* theta, fk_solve_report* rep, void* ws, size_t ws_bytes, cudaStream_t s) {
   SysArgs g;
   FK_TRY(fill_sysargs(P, &g));
@@ -1417,6 +1472,8 @@ fk_status solve_run(const fk_problem* P, double* theta, fk_solve_report* rep, vo
   double* zbuf = (double*)b.take((size_t)D * 8);
   int* info = (int*)b.take(64);
   double* res = (double*)(info + 4);
+  double* rv1 = (double*)b.take((size_t)D * 8);  // condition estimate (report only)
+  double* rv2 = (double*)b.take((size_t)D * 8);
   double2* dsym = nullptr;
   double2* boxt = nullptr;
   if (P->kind == FK_PIK_BOX || P->kind == FK_PIK_COLLOC) {
@@ -1452,7 +1509,7 @@ fk_status solve_run(const fk_problem* P, double* theta, fk_solve_report* rep, vo
     if (st == FK_OK) {
       done = true;
       FK_CUDA_TRY(cudaMemsetAsync(info, 0, 4, s));
-      k_theta_from_real<<<(D + 255) / 256, 256, 0, s>>>(g, zbuf, 1, (double2*)theta);
+      k_theta_from_real<<<(D + 255) / 256, 256, 0, s>>>(g, zbuf, 1, (double2*)theta, nullptr, nullptr);
       FK_CUDA_TRY(cudaGetLastError());
       count_launch();
     } else if (st != FK_E_UNSUPPORTED && st != FK_E_SOLVE) {
@@ -1483,10 +1540,11 @@ fk_status solve_run(const fk_problem* P, double* theta, fk_solve_report* rep, vo
       return fail(FK_E_CUDA, "cublasDtrsv failed");
   }
   if (own_trsv) {
-    k_trsv_lt<<<(D + 31) / 32, 64, 0, s>>>(M, N, D, M + D, N, zbuf, ticket);
+    k_trsv_lt<<<(D + 31) / 32, 64, 0, s>>>(M, N, D, M + D, N, zbuf, ticket, info);
     count_launch();
   }
-  k_theta_from_real<<<(D + 255) / 256, 256, 0, s>>>(g, own_trsv ? zbuf : M + D, own_trsv ? 1 : N, (double2*)theta);
+  k_theta_from_real<<<(D + 255) / 256, 256, 0, s>>>(g, own_trsv ? zbuf : M + D, own_trsv ? 1 : N, (double2*)theta, info,
+                                                    P->d_status);
   FK_CUDA_TRY(cudaGetLastError());
   count_launch();
   }
@@ -1509,7 +1567,15 @@ fk_status solve_run(const fk_problem* P, double* theta, fk_solve_report* rep, vo
     rep->n_unknowns = D;
     rep->iters = iters;
     rep->backward_err = hres[1] > 0 ? std::sqrt(hres[0] / hres[1]) : 0.0;
+    rep->rcond_est = 0.0;
+    if (hinfo < 0) return fail(FK_E_SOLVE, "fk_solve: a dataflow wait of the factorisation hit its watchdog");
     if (hinfo != 0) return fail(FK_E_SOLVE, "fk_solve: Cholesky failed, info = " + std::to_string(hinfo));
+    if (!done) {  // dense path: the factor L (D x D leading block of M, ld N) is still in place
+      std::lock_guard<std::mutex> lk(g_sol_mu);
+      cublasHandle_t bh;
+      FK_TRY(blas_for_device(&bh));
+      FK_TRY(rcond_estimate(bh, M, N, D, rv1, rv2, s, &rep->rcond_est));
+    }
   }
   return FK_OK;
 }

@@ -13,8 +13,11 @@
 //     threads can add at most once more (<= 2/3 x 2^21 each) before it drains, 2^29 + 1024 x 1.4e6
 //     < 2^31 (tests/test_gpu_d1.py: 10^4 identical samples in one CTA).  The rhs channel uses a per-CTA power-of-two
 //     scale from the CTA's first 4096 |Y|; |Y| outliers (and NaN) take an exact fp64 slow path.
-//   fp64 path: exponential-of-semicircle window (sigma = 2, w ~ log10(1/eps) + 2) accumulated in
-//     fp64 (shared memory when it fits, else global).
+//   fp64 mode (eps < 1e-7): septic B-spline window (8 taps, sigma ~ 11 at 1e-10), one channel per
+//     pass, 64-bit fixed point held as int32 pairs in shared memory (pair_add_n) -- k_spread1d_bs7.
+//     When a grid does not fit a CTA (large m, eps < 1e-13): the exponential-of-semicircle window
+//     (sigma = 2, w ~ log10(1/eps) + 2) in the same fixed point (k_spread1d_esx), else fp64
+//     global atomics (k_spread1d_es).
 //
 // X and Y are streamed once from HBM with 128-bit evict-first loads, software-pipelined one
 // iteration ahead; CTAs are persistent (1-2 per SM) over contiguous sample ranges.
@@ -199,7 +202,9 @@ __global__ void __launch_bounds__(1024, 1) k_spread1d_bs3(const XT* __restrict__
 }
 
 // ------------------------------------------------------------------------------------------
-// fp64 path: exponential-of-semicircle window, fp64 accumulation
+// fallback path (grids beyond a CTA's shared memory): exponential-of-semicircle window, fp64
+// accumulation in global memory (k_spread1d_es) or, in fp64 mode with the grids in shared memory,
+// 64-bit fixed point (k_spread1d_esx below)
 // ------------------------------------------------------------------------------------------
 struct EsArgs {
   int64_t n, stride, per;
@@ -265,20 +270,20 @@ __global__ void __launch_bounds__(1024, 1) k_spread1d_es(const XT* __restrict__ 
 }
 
 // fp64-accuracy mode (eps < 1e-7), shared-memory grids: ES taps as polynomials from a
-// constant-memory table (es_horner_table; uploaded per launch) instead of exp + sqrt per tap, and
+// constant-memory table (es_horner_table; slot W, uploaded once) instead of exp + sqrt per tap, and
 // 64-bit fixed-point accumulation (below).  Measured at C2 shape, n = 1e9, eps = 1e-10: 79 ms with
 // exp taps + fp64 CAS atomics, 77 ms now -- the instruction mix moved (ncu: the 360 coefficient
 // loads per sample became the MIO limiter) but the rate did not; the gain is that the result is
 // now order-independent (bitwise deterministic) like the fp32 path.
-__constant__ double c_es_coef[16 * 19];  // W x (W + 3) Horner table of the launch (es_horner_table)
+__constant__ double c_es_coef[kHornerSlots][kHornerSlot];  // slot W: the W x (W + 3) Horner table (horner_slot)
 
 // tap i of a point at ul from the constant-memory table
 template <int W>
 __device__ __forceinline__ double es_tap_const(double sv, int i) {
   constexpr int NP = W + 3;
-  double acc = c_es_coef[i * NP + NP - 1];
+  double acc = c_es_coef[W][i * NP + NP - 1];
 #pragma unroll
-  for (int q = NP - 2; q >= 0; --q) acc = fma(acc, sv, c_es_coef[i * NP + q]);
+  for (int q = NP - 2; q >= 0; --q) acc = fma(acc, sv, c_es_coef[W][i * NP + q]);
   return acc;
 }
 
@@ -624,9 +629,7 @@ static void launch_bs3(const Plan1& p, const XT* X, const XT* Y, const Bs3Args& 
 
 template <typename XT, bool MU, bool R>
 static void launch_es(const Plan1& p, const XT* X, const XT* Y, const EsArgs& a, cudaStream_t s) {
-  const double* coef = nullptr;
-  if (p.smem && p.es.w >= 9 && (!MU || a.carryA) && (!R || a.carryB) && es_horner_table(p.es, &coef) == FK_OK &&
-      cudaMemcpyToSymbolAsync(c_es_coef, coef, (size_t)p.es.w * (p.es.w + 3) * 8, 0, cudaMemcpyDeviceToDevice, s) == cudaSuccess) {
+  if (p.smem && p.es.w >= 9 && (!MU || a.carryA) && (!R || a.carryB) && horner_slot(c_es_coef, p.es.w, p.es.beta) == FK_OK) {
     const size_t smem = p.smem_bytes;  // 2 x int32 per cell = the fp64 grid's bytes
     auto go = [&](auto wtag) {
       constexpr int WW = decltype(wtag)::value;

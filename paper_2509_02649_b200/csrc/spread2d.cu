@@ -8,8 +8,10 @@
 // the samples whose first tap row lies in its row range and keeps those rows plus a (w-1)-row
 // halo in shared memory; CTA (chunk, t) streams its chunk of samples and spreads the ones it
 // owns.  Accumulation: int32 fixed point (weights x 2^21, rhs with a per-CTA power-of-two scale,
-// native ATOMS.ADD, drain-at-2^29 into fp64 carry grids) on the fp32 path; fp64 smem atomics on
-// the fp64 path.  Partials are reduced per fine-grid cell in a fixed CTA order, FFT'd (cuFFT 2-D
+// native ATOMS.ADD, drain-at-2^29 into fp64 carry grids) on the fp32 path; on the fp64 path
+// 64-bit fixed point held as int32 pairs (pair_add: ATOMS.ADD on the low word, the carry read off
+// its return value, the high word when non-zero; high words drained at 2^29 into fp64 carry
+// grids), weights from a Chebyshev-fitted Horner table.  Partials are reduced per fine-grid cell in a fixed CTA order, FFT'd (cuFFT 2-D
 // D2Z, batched over pairs) and deconvolved by psi-hat(q0) psi-hat(q1).
 #include <cmath>
 #include <cstdlib>
@@ -112,7 +114,7 @@ __device__ __forceinline__ void es_taps_f64(double f, int d0, double beta, doubl
 // (es_horner_table: W polynomials of degree W + 2 in s in [-1, 1], the same table the 1-D fp64
 // kernel uses) instead of 2W fp64 exp + sqrt; each coefficient serves both dimensions.  The
 // first tap d0 = first_tap_d(f, W) puts u = f - d0 in [W/2 - 1, W/2], the table's interval.
-__constant__ double c_es2_coef[16 * 19];
+__constant__ double c_es2_coef[kHornerSlots][kHornerSlot];  // slot W (horner_slot)
 
 template <int W>
 __device__ __forceinline__ void es_taps2_horner(double fy, int dy, double fx, int dx, double* py, double* px) {
@@ -121,10 +123,10 @@ __device__ __forceinline__ void es_taps2_horner(double fy, int dy, double fx, in
   const double sx = 2.0 * (fx - dx - 0.5 * W + 1.0) - 1.0;
 #pragma unroll
   for (int i = 0; i < W; ++i) {
-    double ay = c_es2_coef[i * NP + NP - 1], ax = ay;
+    double ay = c_es2_coef[W][i * NP + NP - 1], ax = ay;
 #pragma unroll
     for (int q = NP - 2; q >= 0; --q) {
-      const double c = c_es2_coef[i * NP + q];
+      const double c = c_es2_coef[W][i * NP + q];
       ay = fma(ay, sy, c);
       ax = fma(ax, sx, c);
     }
@@ -133,13 +135,9 @@ __device__ __forceinline__ void es_taps2_horner(double fy, int dy, double fx, in
   }
 }
 
-static fk_status upload_es2_table(int w, double beta, cudaStream_t s) {
-  const double* coef = nullptr;
-  const fk_status st = es_horner_table(EsParams{w, beta}, &coef);
-  if (st != FK_OK) return st;
-  if (cudaMemcpyToSymbolAsync(c_es2_coef, coef, (size_t)w * (w + 3) * 8, 0, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
-    return FK_E_CUDA;
-  return FK_OK;
+static fk_status upload_es2_table(int w, double beta, cudaStream_t) {
+  const fk_status st = horner_slot(c_es2_coef, w, beta);
+  return st == FK_OK ? FK_OK : fail(st, "fp64 ES Horner table unavailable for w = " + std::to_string(w));
 }
 
 __device__ __noinline__ void drain_row(int* row, int w, double* carry_row, double inv_scale) {
@@ -784,7 +782,7 @@ static void es_geo(int nf, int w, int* off, int* K, int* G) {
   *G = nf / 2 + w + 4;
 }
 
-// fp64 = fp64 accumulation (and fp64 window): eps < 1e-7 or fp64 input coordinates
+// fp64 = 64-bit fixed-point accumulation (and fp64 window taps): eps < 1e-7 or fp64 input coordinates
 static fk_status make_plan2(int m, double eps, bool mu, bool r, int dtype, Plan2* p) {
   Plan2 q{};
   q.m = m;

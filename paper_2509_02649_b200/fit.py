@@ -32,6 +32,18 @@ class FitResult:
     r: torch.Tensor            # complex128 rhs, (2m+1,)*d
     n_total: int
     report: Optional[dict] = None
+    status: Optional[torch.Tensor] = None  # device int32: FK_DSTATUS_* bits of the type-1 passes and the solve
+
+    def check(self) -> "FitResult":
+        """Raise if a coordinate was out of range / NaN (skipped) or the factorisation failed
+        (not SPD, watchdog).  Synchronises (reads the device status word)."""
+        if self.status is not None:
+            v = int(self.status.item())
+            if v & (fk.FK_DSTATUS_NOT_SPD | fk.FK_DSTATUS_WATCHDOG):
+                fk.solve_status(self.status)
+            if v & fk.FK_E_RANGE:
+                raise fk.FkError(fk.FK_E_RANGE, "a coordinate outside [-L, L] (or NaN) was skipped")
+        return self
 
 
 def _moment_buffers(d: int, m: int, device):
@@ -44,9 +56,10 @@ def fit(X: torch.Tensor, Y: torch.Tensor, L: float, m: int, lam: float, kind: st
         eps: float = 1e-6, report: bool = False, **pi) -> FitResult:
     d = 1 if X.dim() == 1 else X.shape[1]
     _, mu, r = _moment_buffers(d, m, X.device)
-    fk.fk_rhs_type1(X, Y, L, m, eps, r_out=r, mu_out=mu, check=False)
-    theta, rep = fk.fk_solve(mu.reshape(-1), r.reshape(-1), X.shape[0], d, m, L, lam, kind, s, report=report, **pi)
-    return FitResult(theta, mu, r, X.shape[0], rep)
+    st = torch.zeros(1, dtype=torch.int32, device=X.device)
+    fk.fk_rhs_type1(X, Y, L, m, eps, r_out=r, mu_out=mu, d_status=st)
+    theta, rep = fk.fk_solve(mu.reshape(-1), r.reshape(-1), X.shape[0], d, m, L, lam, kind, s, report=report, d_status=st, **pi)
+    return FitResult(theta, mu, r, X.shape[0], rep, st)
 
 
 def _world(group=None) -> int:
@@ -74,23 +87,27 @@ def broadcast_theta(theta: torch.Tensor, group=None, src: int = 0) -> None:
 
 def fit_distributed(X_shard: torch.Tensor, Y_shard: torch.Tensor, n_total: int, L: float, m: int, lam: float,
                     kind: str = "sobolev", s: float = 1.0, eps: float = 1e-6, group=None, buffers=None, theta_out=None,
-                    report: bool = False, **pi) -> FitResult:
+                    report: bool = False, status: Optional[torch.Tensor] = None, **pi) -> FitResult:
     """Data-parallel fit: call on every rank with that rank's shard (one process per GPU).
-    pi: mu_pde, alpha, a_alpha, box for kind = "pik_box"."""
+    pi: mu_pde, alpha, a_alpha, box for kind = "pik_box".  status: device int32 the kernels OR
+    their FK_DSTATUS_* bits into (this rank's range flag; the solve's bits on rank 0); read it with
+    FitResult.check() outside any timed region."""
     import torch.distributed as dist
 
     d = 1 if X_shard.dim() == 1 else X_shard.shape[1]
     buf, mu, r = buffers if buffers is not None else _moment_buffers(d, m, X_shard.device)
-    fk.fk_rhs_type1(X_shard, Y_shard, L, m, eps, r_out=r, mu_out=mu, check=False)
+    st = status if status is not None else torch.zeros(1, dtype=torch.int32, device=X_shard.device)
+    fk.fk_rhs_type1(X_shard, Y_shard, L, m, eps, r_out=r, mu_out=mu, d_status=st)
     reduce_moments(buf, group)
     D = (2 * m + 1) ** d
     if theta_out is None:
         theta_out = torch.empty(D, dtype=torch.complex128, device=X_shard.device)
     rep = None
     if _world(group) == 1 or dist.get_rank(group) == 0:
-        _, rep = fk.fk_solve(mu.reshape(-1), r.reshape(-1), n_total, d, m, L, lam, kind, s, theta_out=theta_out, report=report, **pi)
+        _, rep = fk.fk_solve(mu.reshape(-1), r.reshape(-1), n_total, d, m, L, lam, kind, s, theta_out=theta_out, report=report,
+                             d_status=st, **pi)
     broadcast_theta(theta_out, group)
-    return FitResult(theta_out, mu, r, n_total, rep)
+    return FitResult(theta_out, mu, r, n_total, rep, st)
 
 
 def additive_buffers(d: int, m: int, device):
@@ -102,7 +119,8 @@ def additive_buffers(d: int, m: int, device):
 
 
 def fit_additive_distributed(X_shard: torch.Tensor, Y_shard: torch.Tensor, n_total: int, L: float, m: int, lam: float,
-                             eps: float = 1e-6, group=None, buffers=None, theta_out=None, report: bool = False) -> FitResult:
+                             eps: float = 1e-6, group=None, buffers=None, theta_out=None, report: bool = False,
+                             status: Optional[torch.Tensor] = None) -> FitResult:
     """Low-bias additive model: per-feature 1-D moments / rhs (one fk_rhs_type1 pass
     per feature column), all pairwise cross moments (fk_additive_cross_moments), one all-reduce
     of everything, block solve on rank 0, broadcast.  X_shard: (n, d), any strides (SoA is
@@ -111,17 +129,18 @@ def fit_additive_distributed(X_shard: torch.Tensor, Y_shard: torch.Tensor, n_tot
 
     d = X_shard.shape[1]
     buf, mus, rs, G = buffers if buffers is not None else additive_buffers(d, m, X_shard.device)
+    st = status if status is not None else torch.zeros(1, dtype=torch.int32, device=X_shard.device)
     for l in range(d):
-        fk.fk_rhs_type1(X_shard[:, l], Y_shard, L, m, eps, r_out=rs[l], mu_out=mus[l], check=False)
-    fk.fk_additive_cross_moments(X_shard, L, m, eps, G_out=G, check=False)
+        fk.fk_rhs_type1(X_shard[:, l], Y_shard, L, m, eps, r_out=rs[l], mu_out=mus[l], d_status=st)
+    fk.fk_additive_cross_moments(X_shard, L, m, eps, G_out=G, d_status=st)
     reduce_moments(buf, group)
     if theta_out is None:
         theta_out = torch.empty(d * (2 * m + 1), dtype=torch.complex128, device=X_shard.device)
     rep = None
     if _world(group) == 1 or dist.get_rank(group) == 0:
-        _, rep = fk.fk_solve(mus, rs, n_total, d, m, L, lam, "additive", cross=G, theta_out=theta_out, report=report)
+        _, rep = fk.fk_solve(mus, rs, n_total, d, m, L, lam, "additive", cross=G, theta_out=theta_out, report=report, d_status=st)
     broadcast_theta(theta_out, group)
-    return FitResult(theta_out, mus, rs, n_total, rep)
+    return FitResult(theta_out, mus, rs, n_total, rep, st)
 
 
 @dataclass
@@ -238,7 +257,12 @@ class HostStreamer:
         self.yb = [torch.empty(chunk, dtype=dtype, device=device) for _ in range(2)]
         self.copy_streams = [torch.cuda.Stream(device), torch.cuda.Stream(device)]
         self.copied = [[torch.cuda.Event() for _ in range(2)] for _ in range(2)]
+        # buffer b may be refilled only after the compute stream has consumed it: the events start
+        # recorded (on the stream that allocated the buffers) so the first copies of EVERY call --
+        # also a reused streamer's next call -- wait for the previous call's kernels
         self.consumed = [torch.cuda.Event() for _ in range(2)]
+        for e in self.consumed:
+            e.record(torch.cuda.current_stream(device))
 
     def moments(self, Xh: torch.Tensor, Yh: torch.Tensor, L: float, m: int, eps: float, mu, r):
         n = Xh.shape[0]
@@ -250,8 +274,7 @@ class HostStreamer:
             for c, (dst, src) in enumerate(((self.xb[b], Xh), (self.yb[b], Yh))):
                 cs = self.copy_streams[c]
                 with torch.cuda.stream(cs):
-                    if i >= 2:
-                        cs.wait_event(self.consumed[b])
+                    cs.wait_event(self.consumed[b])
                     dst[: hi - lo].copy_(src[lo:hi], non_blocking=True)
                     self.copied[c][b].record(cs)
                 comp.wait_event(self.copied[c][b])
@@ -274,7 +297,9 @@ class HostStreamerAdditive:
         self.yb = [torch.empty(chunk, dtype=torch.float32, device=device) for _ in range(2)]
         self.copy_streams = [torch.cuda.Stream(device), torch.cuda.Stream(device)]
         self.copied = [[torch.cuda.Event() for _ in range(2)] for _ in range(2)]
-        self.consumed = [torch.cuda.Event() for _ in range(2)]
+        self.consumed = [torch.cuda.Event() for _ in range(2)]  # see HostStreamer
+        for e in self.consumed:
+            e.record(torch.cuda.current_stream(device))
 
     def moments(self, Xh_soa: torch.Tensor, Yh: torch.Tensor, L: float, m: int, eps: float, mus, rs, G):
         d, n = Xh_soa.shape
@@ -287,8 +312,7 @@ class HostStreamerAdditive:
             for c in range(2):
                 cs = self.copy_streams[c]
                 with torch.cuda.stream(cs):
-                    if i >= 2:
-                        cs.wait_event(self.consumed[b])
+                    cs.wait_event(self.consumed[b])
                     if c == 0:
                         for l in range(d):  # contiguous 1-D copies (a 2-D strided slice is not a plain DMA)
                             self.xb[b][l, :k].copy_(Xh_soa[l, lo:hi], non_blocking=True)
@@ -327,10 +351,12 @@ class FitGraph:
         n = X.shape[0] if n_total is None else n_total
         self.buf, self.mu, self.r = _moment_buffers(d, m, X.device)
         self.theta = torch.empty((2 * m + 1) ** d, dtype=torch.complex128, device=X.device)
+        self.status = torch.zeros(1, dtype=torch.int32, device=X.device)  # FK_DSTATUS_* bits of every replay
 
         def run():
-            fk.fk_rhs_type1(X, Y, L, m, eps, r_out=self.r, mu_out=self.mu, check=False)
-            fk.fk_solve(self.mu.reshape(-1), self.r.reshape(-1), n, d, m, L, lam, kind, s, theta_out=self.theta, report=False, **pi)
+            fk.fk_rhs_type1(X, Y, L, m, eps, r_out=self.r, mu_out=self.mu, d_status=self.status)
+            fk.fk_solve(self.mu.reshape(-1), self.r.reshape(-1), n, d, m, L, lam, kind, s, theta_out=self.theta, report=False,
+                        d_status=self.status, **pi)
 
         side = torch.cuda.Stream(device=X.device)
         side.wait_stream(torch.cuda.current_stream(X.device))
@@ -341,16 +367,21 @@ class FitGraph:
         torch.cuda.synchronize(X.device)
         fk.profile_read()
         self.graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self.graph):
+        with torch.cuda.graph(self.graph, stream=side):  # same stream as the warm-up: its cached workspace
             run()
         self.launches = fk.profile_read()[2]
-        # the captured kernels hold raw pointers into the cached workspace: keep that buffer alive
-        # even if a later call with a larger workspace replaces the cache entry
-        self._ws = fk._workspace(0, X.device)
+        # the captured kernels hold raw pointers into the workspace cached for `side`: keep that
+        # buffer alive even if a later call with a larger workspace replaces the cache entry
+        self._ws = fk._workspace(0, X.device, side)
+        self._side = side
 
     def replay(self) -> torch.Tensor:
         self.graph.replay()
         return self.theta
+
+    def check(self) -> None:
+        """Raise if any replay so far skipped a coordinate or failed to factor (synchronises)."""
+        FitResult(self.theta, self.mu, self.r, 0, None, self.status).check()
 
 
 def predict(theta: torch.Tensor, d: int, m: int, L: float, Xq: torch.Tensor, eps: float = 1e-6, additive: bool = False):

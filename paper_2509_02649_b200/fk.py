@@ -20,10 +20,11 @@ LIB_PATH = os.path.join(_HERE, "libfk.so")
 FK_OK, FK_E_ARG, FK_E_RANGE, FK_E_EPS, FK_E_CUDA, FK_E_WORKSPACE, FK_E_SOLVE, FK_E_UNSUPPORTED = range(8)
 FK_F32, FK_F64 = 0, 1
 FK_ACCUMULATE = 1
+FK_DSTATUS_RANGE, FK_DSTATUS_NOT_SPD, FK_DSTATUS_WATCHDOG = 2, 0x10, 0x20
 FK_SOBOLEV, FK_LOWBIAS, FK_PIK_BOX, FK_ADDITIVE, FK_PIK_COLLOC = 0, 1, 2, 3, 4
 KINDS = {"sobolev": FK_SOBOLEV, "lowbias": FK_LOWBIAS, "pik_box": FK_PIK_BOX, "additive": FK_ADDITIVE, "pik_colloc": FK_PIK_COLLOC}
 (FK_ENTRY_MOMENTS, FK_ENTRY_RHS, FK_ENTRY_CROSS, FK_ENTRY_SOLVE, FK_ENTRY_PREDICT, FK_ENTRY_SOLVE_PATH,
- FK_ENTRY_PATH_VALIDATE) = range(7)
+ FK_ENTRY_PATH_VALIDATE, FK_ENTRY_RHS_HOST) = range(8)
 _STATUS = {1: "FK_E_ARG", 2: "FK_E_RANGE", 3: "FK_E_EPS", 4: "FK_E_CUDA", 5: "FK_E_WORKSPACE", 6: "FK_E_SOLVE", 7: "FK_E_UNSUPPORTED"}
 
 
@@ -43,12 +44,13 @@ class fk_problem(ctypes.Structure):
                 ("n_total", ctypes.c_double), ("L", ctypes.c_double), ("s", ctypes.c_double), ("lam", ctypes.c_double),
                 ("mu_pde", ctypes.c_double), ("alpha", ctypes.POINTER(ctypes.c_int32)), ("a_alpha", ctypes.POINTER(ctypes.c_double)),
                 ("box", ctypes.POINTER(ctypes.c_double)), ("mu_moments", ctypes.c_void_p), ("rhs", ctypes.c_void_p),
-                ("cross", ctypes.c_void_p), ("colloc_moments", ctypes.c_void_p), ("n_colloc", ctypes.c_double)]
+                ("cross", ctypes.c_void_p), ("colloc_moments", ctypes.c_void_p), ("n_colloc", ctypes.c_double),
+                ("d_status", ctypes.c_void_p)]
 
 
 class fk_solve_report(ctypes.Structure):
     _fields_ = [("backward_err", ctypes.c_double), ("ms", ctypes.c_double), ("info", ctypes.c_int32), ("n_unknowns", ctypes.c_int32),
-                ("iters", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("iters", ctypes.c_int32), ("reserved", ctypes.c_int32), ("rcond_est", ctypes.c_double)]
 
 
 _lib = None
@@ -64,6 +66,7 @@ def lib():
         vp, dp, ip, sz = ctypes.c_void_p, ctypes.c_double, ctypes.c_int, ctypes.c_size_t
         L.fk_moments_type1.argtypes = [fk_points, dp, ip, dp, vp, ip, vp, sz, vp, vp]
         L.fk_rhs_type1.argtypes = [fk_points, vp, dp, ip, dp, vp, vp, ip, vp, sz, vp, vp]
+        L.fk_rhs_type1_host.argtypes = [fk_points, vp, dp, ip, dp, vp, vp, ip, ctypes.c_int64, vp, sz, vp, vp]
         L.fk_additive_cross_moments.argtypes = [fk_points, dp, ip, dp, vp, ip, vp, sz, vp, vp]
         L.fk_solve.argtypes = [ctypes.POINTER(fk_problem), vp, ctypes.POINTER(fk_solve_report), vp, sz, vp]
         L.fk_solve_path.argtypes = [ctypes.POINTER(fk_problem), vp, ip, vp, vp, vp, sz, vp]
@@ -73,7 +76,7 @@ def lib():
         L.fk_workspace_bytes.restype = ctypes.c_size_t
         L.fk_last_error.restype = ctypes.c_char_p
         L.fk_version.restype = ctypes.c_char_p
-        for f in ("fk_moments_type1", "fk_rhs_type1", "fk_additive_cross_moments", "fk_solve", "fk_solve_path", "fk_path_validate",
+        for f in ("fk_moments_type1", "fk_rhs_type1", "fk_rhs_type1_host", "fk_additive_cross_moments", "fk_solve", "fk_solve_path", "fk_path_validate",
                   "fk_predict_type2"):
             getattr(L, f).restype = ctypes.c_int
         _lib = L
@@ -88,6 +91,33 @@ def _check(status: int):
 def _stream(stream: Optional[torch.cuda.Stream]) -> ctypes.c_void_p:
     s = stream if stream is not None else torch.cuda.current_stream()
     return ctypes.c_void_p(s.cuda_stream)
+
+
+class _On:
+    """Stream plumbing of one call on `stream` (default: torch's current stream).  Outputs, the
+    status word and the workspace are allocated / zeroed on the current stream, so a different
+    `stream` first waits for the current one; afterwards the tensors the library wrote are marked
+    as used on `stream` (record_stream) so the caching allocator does not recycle them early."""
+
+    def __init__(self, stream, device):
+        self.cur = torch.cuda.current_stream(device)
+        self.s = stream if stream is not None else self.cur
+        self.other = self.s != self.cur
+        if self.other:
+            self.s.wait_stream(self.cur)
+
+    @property
+    def handle(self):
+        return ctypes.c_void_p(self.s.cuda_stream)
+
+    def done(self, *tensors):
+        if self.other:
+            for t in tensors:
+                if t is not None:
+                    t.record_stream(self.s)
+
+    def sync(self):
+        self.s.synchronize()
 
 
 def _points(X: torch.Tensor) -> fk_points:
@@ -108,10 +138,18 @@ def _points(X: torch.Tensor) -> fk_points:
 _ws_cache = {}
 
 
-def _workspace(nbytes: int, device) -> torch.Tensor:
-    key = (device.index if device.index is not None else torch.cuda.current_device())
+def _workspace(nbytes: int, device, stream=None) -> torch.Tensor:
+    """Scratch for a call, cached per (device, stream): calls on different streams may run
+    concurrently and must not share scratch; calls on one stream are ordered, so they can.  A grown
+    buffer replaces the old one, which is freed only after the work queued on that stream so far
+    (record_stream when the stream is not the allocating one)."""
+    dev = device.index if device.index is not None else torch.cuda.current_device()
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    key = (dev, s.cuda_stream)
     buf = _ws_cache.get(key)
     if buf is None or buf.numel() < nbytes:
+        if buf is not None and s != torch.cuda.current_stream(dev):
+            buf.record_stream(s)
         buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
         _ws_cache[key] = buf
     return buf
@@ -142,11 +180,14 @@ def fk_moments_type1(X: torch.Tensor, L: float, m: int, eps: float = 1e-6, mu_ou
     if mu_out is None:
         mu_out = torch.zeros((4 * m + 1,) * P.d, dtype=torch.complex128, device=X.device)
     nb = fk_workspace_bytes(FK_ENTRY_MOMENTS, P.d, m, eps, P.dtype, P.n)
-    ws = _workspace(nb, X.device)
     ds = _dstatus(d_status, X.device)
+    on = _On(stream, X.device)
+    ws = _workspace(nb, X.device, on.s)
     _check(lib().fk_moments_type1(P, L, m, eps, mu_out.data_ptr(), FK_ACCUMULATE if accumulate else 0, ws.data_ptr(), ws.numel(),
-                                  ds.data_ptr(), _stream(stream)))
+                                  ds.data_ptr(), on.handle))
+    on.done(mu_out, ds, X)
     if check and d_status is None:
+        on.sync()
         raise_on_status(ds)
     return mu_out
 
@@ -164,11 +205,47 @@ def fk_rhs_type1(X: torch.Tensor, Y: torch.Tensor, L: float, m: int, eps: float 
         mu_out = torch.zeros((4 * m + 1,) * P.d, dtype=torch.complex128, device=X.device)
     entry = FK_ENTRY_RHS
     nb = fk_workspace_bytes(entry, P.d, m, eps, P.dtype, P.n)
-    ws = _workspace(nb, X.device)
     ds = _dstatus(d_status, X.device)
+    on = _On(stream, X.device)
+    ws = _workspace(nb, X.device, on.s)
     _check(lib().fk_rhs_type1(P, Y.data_ptr(), L, m, eps, r_out.data_ptr(), mu_out.data_ptr() if mu_out is not None else None,
-                              FK_ACCUMULATE if accumulate else 0, ws.data_ptr(), ws.numel(), ds.data_ptr(), _stream(stream)))
+                              FK_ACCUMULATE if accumulate else 0, ws.data_ptr(), ws.numel(), ds.data_ptr(), on.handle))
+    on.done(r_out, mu_out, ds, X, Y)
     if check and d_status is None:
+        on.sync()
+        raise_on_status(ds)
+    return r_out, mu_out
+
+
+def fk_rhs_type1_host(Xh: torch.Tensor, Yh: torch.Tensor, L: float, m: int, eps: float = 1e-6, r_out: Optional[torch.Tensor] = None,
+                      mu_out: Optional[torch.Tensor] = None, with_moments: bool = True, accumulate: bool = False, chunk: int = 0,
+                      d_status: Optional[torch.Tensor] = None, stream=None, check: bool = True, device=None):
+    """fk_rhs_type1 from HOST tensors (pinned for overlap): the library streams chunks to the device
+    through two staging buffers on its own copy stream, overlapped with the spreading."""
+    if Xh.is_cuda or Yh.is_cuda:
+        raise ValueError("fk_rhs_type1_host takes host tensors")
+    if Xh.dtype not in (torch.float32, torch.float64) or Yh.dtype != Xh.dtype:
+        raise ValueError("X, Y must share a float dtype")
+    Xh, Yh = Xh.contiguous(), Yh.contiguous()
+    d = 1 if Xh.dim() == 1 else Xh.shape[1]
+    n = Xh.shape[0]
+    if Yh.dim() != 1 or Yh.shape[0] != n:
+        raise ValueError("Y must be a vector of X's length")
+    dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    P = fk_points(Xh.data_ptr(), FK_F32 if Xh.dtype == torch.float32 else FK_F64, d, n, d, 1)
+    if r_out is None:
+        r_out = torch.zeros((2 * m + 1,) * d, dtype=torch.complex128, device=dev)
+    if with_moments and mu_out is None:
+        mu_out = torch.zeros((4 * m + 1,) * d, dtype=torch.complex128, device=dev)
+    nb = fk_workspace_bytes(FK_ENTRY_RHS_HOST, d, m, eps, P.dtype, chunk)
+    ds = _dstatus(d_status, dev)
+    on = _On(stream, dev)
+    ws = _workspace(nb, dev, on.s)
+    _check(lib().fk_rhs_type1_host(P, Yh.data_ptr(), L, m, eps, r_out.data_ptr(), mu_out.data_ptr() if mu_out is not None else None,
+                                   FK_ACCUMULATE if accumulate else 0, int(chunk), ws.data_ptr(), ws.numel(), ds.data_ptr(), on.handle))
+    on.done(r_out, mu_out, ds)
+    if check and d_status is None:
+        on.sync()
         raise_on_status(ds)
     return r_out, mu_out
 
@@ -182,11 +259,14 @@ def fk_additive_cross_moments(X: torch.Tensor, L: float, m: int, eps: float = 1e
     if G_out is None:
         G_out = torch.zeros((npairs, 2 * m + 1, 2 * m + 1), dtype=torch.complex128, device=X.device)
     nb = fk_workspace_bytes(FK_ENTRY_CROSS, P.d, m, eps, P.dtype, P.n)
-    ws = _workspace(nb, X.device)
     ds = _dstatus(d_status, X.device)
+    on = _On(stream, X.device)
+    ws = _workspace(nb, X.device, on.s)
     _check(lib().fk_additive_cross_moments(P, L, m, eps, G_out.data_ptr(), FK_ACCUMULATE if accumulate else 0, ws.data_ptr(),
-                                           ws.numel(), ds.data_ptr(), _stream(stream)))
+                                           ws.numel(), ds.data_ptr(), on.handle))
+    on.done(G_out, ds, X)
     if check and d_status is None:
+        on.sync()
         raise_on_status(ds)
     return G_out
 
@@ -194,23 +274,40 @@ def fk_additive_cross_moments(X: torch.Tensor, L: float, m: int, eps: float = 1e
 def fk_solve(mu: torch.Tensor, r: torch.Tensor, n_total: float, d: int, m: int, L: float, lam: float, kind: str = "sobolev",
              s: float = 1.0, mu_pde: float = 0.0, alpha: Optional[Sequence] = None, a_alpha: Optional[Sequence[float]] = None,
              box: Optional[Sequence] = None, cross: Optional[torch.Tensor] = None, theta_out: Optional[torch.Tensor] = None,
-             report: bool = True, stream=None, colloc_moments: Optional[torch.Tensor] = None, n_colloc: float = 0.0):
-    """theta = A^{-1} r/n (dense fp64 Cholesky).  Returns (theta complex128, report dict or None)."""
+             report: bool = True, stream=None, colloc_moments: Optional[torch.Tensor] = None, n_colloc: float = 0.0,
+             d_status: Optional[torch.Tensor] = None):
+    """theta = A^{-1} r/n (dense fp64 Cholesky, or CG for large Sobolev systems).  Returns (theta
+    complex128, report dict or None).  d_status (device int32, optional): FK_DSTATUS_NOT_SPD /
+    FK_DSTATUS_WATCHDOG are ORed into it by the device, also when report=False (no sync)."""
     k = KINDS[kind] if isinstance(kind, str) else int(kind)
     D = d * (2 * m + 1) if k == FK_ADDITIVE else (2 * m + 1) ** d
     if theta_out is None:
         theta_out = torch.empty(D, dtype=torch.complex128, device=mu.device)
     prob, keep = _problem(mu, r, n_total, d, m, L, lam, k, s, mu_pde, alpha, a_alpha, box, cross, colloc_moments, n_colloc)
+    if d_status is not None:
+        prob.d_status = d_status.data_ptr()
     nb = fk_workspace_bytes(FK_ENTRY_SOLVE, d, m, 1e-6, FK_F64, 0, k)
-    ws = _workspace(nb, mu.device)
+    on = _On(stream, mu.device)
+    ws = _workspace(nb, mu.device, on.s)
     rep = fk_solve_report()
     _check(lib().fk_solve(ctypes.byref(prob), theta_out.data_ptr(), ctypes.byref(rep) if report else None, ws.data_ptr(), ws.numel(),
-                          _stream(stream)))
+                          on.handle))
+    on.done(theta_out, d_status, *[t for t in keep if isinstance(t, torch.Tensor)])
     del keep
     out = None
     if report:
-        out = {"backward_err": rep.backward_err, "ms": rep.ms, "info": rep.info, "n_unknowns": rep.n_unknowns, "iters": rep.iters}
+        out = {"backward_err": rep.backward_err, "ms": rep.ms, "info": rep.info, "n_unknowns": rep.n_unknowns, "iters": rep.iters,
+               "rcond_est": rep.rcond_est}
     return theta_out, out
+
+
+def solve_status(d_status: torch.Tensor) -> None:
+    """Raise if the device status word of fk_solve calls reports a failed factorisation (syncs)."""
+    v = int(d_status.item())
+    if v & FK_DSTATUS_WATCHDOG:
+        raise FkError(FK_E_SOLVE, "a dataflow wait of the factorisation hit its watchdog: theta is not valid")
+    if v & FK_DSTATUS_NOT_SPD:
+        raise FkError(FK_E_SOLVE, "the system is not numerically positive definite")
 
 
 def fk_solve_path(mu: torch.Tensor, r: torch.Tensor, n_total: float, d: int, m: int, L: float, lambdas: Sequence[float],
@@ -227,10 +324,12 @@ def fk_solve_path(mu: torch.Tensor, r: torch.Tensor, n_total: float, d: int, m: 
         theta_out = torch.empty(len(lambdas), D, dtype=torch.complex128, device=mu.device)
     prob, keep = _problem(mu, r, n_total, d, m, L, 0.0, k, s, mu_pde, alpha, a_alpha, box, cross, colloc_moments, n_colloc)
     nb = fk_workspace_bytes(FK_ENTRY_SOLVE_PATH, d, m, 1e-6, FK_F64, len(lambdas), k)
-    ws = _workspace(nb, mu.device)
+    on = _On(stream, mu.device)
+    ws = _workspace(nb, mu.device, on.s)
     info = ctypes.c_int(0)
     _check(lib().fk_solve_path(ctypes.byref(prob), lams, len(lambdas), theta_out.data_ptr(), ctypes.byref(info) if check else None,
-                               ws.data_ptr(), ws.numel(), _stream(stream)))
+                               ws.data_ptr(), ws.numel(), on.handle))
+    on.done(theta_out, *[t for t in keep if isinstance(t, torch.Tensor)])
     del keep
     return theta_out
 
@@ -250,9 +349,11 @@ def fk_path_validate(theta: torch.Tensor, mu_v: torch.Tensor, r_v: torch.Tensor,
         risk_out = torch.empty(nlam, dtype=torch.float64, device=theta.device)
     prob, keep = _problem(mu_v, r_v, n_v, d, m, L, 0.0, k, 1.0, 0.0, None, None, None, cross_v, None, 0.0)
     nb = fk_workspace_bytes(FK_ENTRY_PATH_VALIDATE, d, m, 1e-6, FK_F64, nlam, k)
-    ws = _workspace(nb, theta.device)
+    on = _On(stream, theta.device)
+    ws = _workspace(nb, theta.device, on.s)
     _check(lib().fk_path_validate(ctypes.byref(prob), theta.data_ptr(), nlam, float(sum_y2), risk_out.data_ptr(), ws.data_ptr(),
-                                  ws.numel(), _stream(stream)))
+                                  ws.numel(), on.handle))
+    on.done(risk_out, theta, *[t for t in keep if isinstance(t, torch.Tensor)])
     del keep
     return risk_out
 
@@ -298,12 +399,15 @@ def fk_predict_type2(theta: torch.Tensor, d: int, m: int, L: float, Xq: torch.Te
     if out is None:
         out = torch.empty(P.n, dtype=Xq.dtype, device=Xq.device)
     nb = fk_workspace_bytes(FK_ENTRY_PREDICT, d, m, eps, P.dtype, P.n, 1 if additive else 0)
-    ws = _workspace(nb, Xq.device)
     ds = _dstatus(d_status, Xq.device)
     theta = theta.contiguous()
+    on = _On(stream, Xq.device)
+    ws = _workspace(nb, Xq.device, on.s)
     _check(lib().fk_predict_type2(theta.data_ptr(), d, m, L, 1 if additive else 0, P, eps, out.data_ptr(), ws.data_ptr(), ws.numel(),
-                                  ds.data_ptr(), _stream(stream)))
+                                  ds.data_ptr(), on.handle))
+    on.done(out, ds, theta, Xq)
     if check and d_status is None:
+        on.sync()
         raise_on_status(ds)
     return out
 
