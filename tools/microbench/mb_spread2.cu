@@ -1,0 +1,372 @@
+// Round-2 study of the d = 1 spreading formulation (verdict r01 #2): which organisation of the
+// 8 random-address shared-memory atomics per sample (4 cubic B-spline taps x {moments, rhs}) and
+// of its arithmetic gets past the shared-memory (bank-conflict) and issue ceilings of k_spread1d_bs3.
+// Not product code: a standalone executable run on a B200 via gpurun; every variant writes its CTA
+// partial grids and the host checks that the integer sums match (sum of all mu cells = n S exactly,
+// sum of all rhs cells = sum_j round(Y_j SY) exactly), so no variant can skip work.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -o mb_spread2 mb_spread2.cu
+//
+// Variants (all: 148 persistent 1024-thread CTAs, float4 evict-first loads, fixed point int32
+// with drain-on-return at 2^29 into fp64 carries, as the product kernel):
+//   base   two grids (mu: nf 65536 -> 32772 cells, rhs: nf 32768 -> 16388 cells); one sample per
+//          lane, 8 ATOMS per sample at independent random banks (the r01 product organisation)
+//   lean   base with a trimmed instruction stream (same atomics)
+//   quad   tap-major lanes (verdict (a)): lane 4g + t does tap t of 8 samples per instruction; one
+//          channel per instruction, 4 consecutive banks per sample
+//   pair   rhs at the moment grid's resolution, cells interleaved [mu_c, r_c]: lanes 2i (moments)
+//          and 2i+1 (rhs) of a pair take the same sample, so each instruction hits 16 aligned bank
+//          pairs (16 balls in 16 bins, E max 3.08, instead of 32 in 32, E max 3.53); sigma = 14
+//          so both grids fit (2 x 28004 cells = 224 KB)
+//   mathX  the variant's arithmetic without shared-memory accumulation (its issue ceiling)
+#include <cstdio>
+#include <cstdint>
+#include <vector>
+#include <cuda_runtime.h>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s at %d\n", cudaGetErrorString(e), __LINE__); return 1; } } while (0)
+#define MAGIC 12582912.0f
+#define MAGIC_BITS 0x4B400000
+
+__device__ __forceinline__ uint32_t hash32(uint32_t x) {
+  x ^= x >> 16; x *= 0x7feb352dU; x ^= x >> 15; x *= 0x846ca68bU; x ^= x >> 16; return x;
+}
+
+__global__ void gen(float* X, float* Y, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t h = hash32((uint32_t)i * 2654435761u + 17u);
+    float x = (float)(h >> 8) * (2.0f / 16777216.0f) - 1.0f;
+    X[i] = x; Y[i] = __sinf(3.f * x) + ((float)(hash32(h) >> 8) * (1.0f / 16777216.0f) - 0.5f);
+  }
+}
+
+constexpr float SA = 2097152.f;   // mu weights x 2^21 (partition of unity closed exactly)
+constexpr float SY = 262144.f;    // rhs: Y x 2^18 (|Y| < 2: |Y SY| < 2^19)
+constexpr int GA = 32772, GB = 16388;  // base grids (sigma 16)
+constexpr int GP = 28004;              // pair grid cells (sigma 14, nf 56000)
+
+__device__ __noinline__ void drain4(int* c, int stride, double* carry) {
+  for (int k = 0; k < 4; ++k) {
+    const int v = atomicExch(c + k * stride, 0);
+    if (v) atomicAdd(carry, (double)v);
+  }
+}
+
+// cubic B-spline fixed-point taps for fraction f, scale K (= S/6), closure total S
+__device__ __forceinline__ void bs3(float f, float K, int S, int& i0, int& i1, int& i2, int& i3) {
+  const float g = 1.0f - f;
+  const float f2 = f * f, f3 = f2 * f, g3 = g * g * g;
+  i0 = __float_as_int(fmaf(g3, K, MAGIC)) - MAGIC_BITS;
+  i3 = __float_as_int(fmaf(f3, K, MAGIC)) - MAGIC_BITS;
+  i1 = __float_as_int(fmaf(f3, 3.f * K, fmaf(f2, -6.f * K, fmaf(4.f, K, MAGIC)))) - MAGIC_BITS;
+  i2 = S - i0 - i1 - i3;
+}
+
+template <int MODE>  // 0: atomics, 1: math only
+__global__ void __launch_bounds__(1024, 1) k_base(const float4* __restrict__ X, const float4* __restrict__ Y, int64_t n4,
+                                                  double* carry, int* part, int* sink) {
+  extern __shared__ int sm[];
+  int* A = sm;
+  int* B = sm + GA;
+  if (MODE == 0) {
+    for (int i = threadIdx.x; i < GA + GB; i += blockDim.x) sm[i] = 0;
+    __syncthreads();
+  }
+  const int64_t per = (n4 + gridDim.x - 1) / gridDim.x;
+  const int64_t beg = per * blockIdx.x, end = min(n4, beg + per);
+  int acc = 0;
+  for (int64_t i = beg + threadIdx.x; i < end; i += blockDim.x) {
+    const float4 xv = __ldcs(X + i), yv = __ldcs(Y + i);
+    const float xs[4] = {xv.x, xv.y, xv.z, xv.w}, ys[4] = {yv.x, yv.y, yv.z, yv.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float p = xs[q] * 16384.f;
+      const float fl = floorf(p);
+      const float f = p - fl;
+      const int ca = __float_as_int(fl + MAGIC) - MAGIC_BITS + 16384;
+      const float pb = p * 0.5f;
+      const float flb = floorf(pb);
+      const float fb = pb - flb;
+      const int cb = __float_as_int(flb + MAGIC) - MAGIC_BITS + 8192;
+      int i0, i1, i2, i3, j0, j1, j2, j3;
+      bs3(f, SA / 6.f, (int)SA, i0, i1, i2, i3);
+      const int jS = __float_as_int(fmaf(ys[q], SY, MAGIC)) - MAGIC_BITS;
+      bs3(fb, ys[q] * (SY / 6.f), jS, j0, j1, j2, j3);
+      if (MODE == 0) {
+        const int o0 = atomicAdd(A + ca, i0), o1 = atomicAdd(A + ca + 1, i1), o2 = atomicAdd(A + ca + 2, i2), o3 = atomicAdd(A + ca + 3, i3);
+        const unsigned p0 = atomicAdd(B + cb, j0), p1 = atomicAdd(B + cb + 1, j1), p2 = atomicAdd(B + cb + 2, j2), p3 = atomicAdd(B + cb + 3, j3);
+        if ((o0 | o1 | o2 | o3) & 0x60000000) drain4(A + ca, 1, carry);
+        const unsigned T = 1u << 29;
+        if (((p0 + T) | (p1 + T) | (p2 + T) | (p3 + T)) & 0xC0000000u) drain4(B + cb, 1, carry);
+      } else {
+        acc += (i0 ^ i1 ^ i2 ^ i3 ^ ca) + (j0 ^ j1 ^ j2 ^ j3 ^ cb);
+      }
+    }
+  }
+  if (MODE == 0) {
+    __syncthreads();
+    int* dst = part + (int64_t)blockIdx.x * (GA + GB);
+    for (int i = threadIdx.x; i < GA + GB; i += blockDim.x) dst[i] = sm[i];
+  } else if (acc == 0x12345) {
+    sink[0] = acc;
+  }
+}
+
+// lean: floor/fraction once (the rhs position from the moment cell: cb = ca >> 1 and fb = (f + (ca & 1)) / 2,
+// exact), weights with fewer instructions, shared-memory addresses as 32-bit offsets
+template <int MODE>
+__global__ void __launch_bounds__(1024, 1) k_lean(const float4* __restrict__ X, const float4* __restrict__ Y, int64_t n4,
+                                                  double* carry, int* part, int* sink) {
+  extern __shared__ int sm[];
+  int* A = sm;
+  int* B = sm + GA;
+  if (MODE == 0) {
+    for (int i = threadIdx.x; i < GA + GB; i += blockDim.x) sm[i] = 0;
+    __syncthreads();
+  }
+  const int64_t per = (n4 + gridDim.x - 1) / gridDim.x;
+  const int64_t beg = per * blockIdx.x, end = min(n4, beg + per);
+  int acc = 0;
+  for (int64_t i = beg + threadIdx.x; i < end; i += blockDim.x) {
+    const float4 xv = __ldcs(X + i), yv = __ldcs(Y + i);
+    const float xs[4] = {xv.x, xv.y, xv.z, xv.w}, ys[4] = {yv.x, yv.y, yv.z, yv.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      // p = x 16384 + 16384 in [0, 32768]: ca = floor(p) is the first tap; the rhs grid (half the
+      // cells) has cb = floor(p / 2) = ca >> 1 and fb = (f + (ca & 1)) / 2, both exact
+      const float p = fmaf(xs[q], 16384.f, 16384.f);
+      const float fl = floorf(p);
+      const float f = p - fl;
+      const int ca = __float_as_int(fl + 8388608.f) - 0x4B000000;
+      const int cb = ca >> 1;
+      const float fb = fmaf(f, 0.5f, (ca & 1) ? 0.5f : 0.0f);
+      int i0, i1, i2, i3, j0, j1, j2, j3;
+      bs3(f, SA / 6.f, (int)SA, i0, i1, i2, i3);
+      const int jS = __float_as_int(fmaf(ys[q], SY, MAGIC)) - MAGIC_BITS;
+      bs3(fb, ys[q] * (SY / 6.f), jS, j0, j1, j2, j3);
+      if (MODE == 0) {
+        const int o0 = atomicAdd(A + ca, i0), o1 = atomicAdd(A + ca + 1, i1), o2 = atomicAdd(A + ca + 2, i2), o3 = atomicAdd(A + ca + 3, i3);
+        const int p0 = atomicAdd(B + cb, j0), p1 = atomicAdd(B + cb + 1, j1), p2 = atomicAdd(B + cb + 2, j2), p3 = atomicAdd(B + cb + 3, j3);
+        // |cell| >= 2^29 on either grid: v + 2^29 outside [0, 2^30) (one test for both grids)
+        const unsigned T = 1u << 29;
+        const unsigned t = ((unsigned)o0 + T) | ((unsigned)o1 + T) | ((unsigned)o2 + T) | ((unsigned)o3 + T) | ((unsigned)p0 + T) |
+                           ((unsigned)p1 + T) | ((unsigned)p2 + T) | ((unsigned)p3 + T);
+        if (t & 0xC0000000u) {
+          drain4(A + ca, 1, carry);
+          drain4(B + cb, 1, carry);
+        }
+      } else {
+        acc += (i0 ^ i1 ^ i2 ^ i3 ^ ca) + (j0 ^ j1 ^ j2 ^ j3 ^ cb);
+      }
+    }
+  }
+  if (MODE == 0) {
+    __syncthreads();
+    int* dst = part + (int64_t)blockIdx.x * (GA + GB);
+    for (int i = threadIdx.x; i < GA + GB; i += blockDim.x) dst[i] = sm[i];
+  } else if (acc == 0x12345) {
+    sink[0] = acc;
+  }
+}
+
+// quad: tap-major lanes.  Lane 4g + t, 8 groups; the 4 lanes of a group load the same float4s
+// (4 samples) and lane t adds tap t of each sample to both grids.  Closure: every lane evaluates all
+// four fixed-point taps (needed for exact partition of unity) and keeps its own.
+template <int MODE>
+__global__ void __launch_bounds__(1024, 1) k_quad(const float4* __restrict__ X, const float4* __restrict__ Y, int64_t n4,
+                                                  double* carry, int* part, int* sink) {
+  extern __shared__ int sm[];
+  int* A = sm;
+  int* B = sm + GA;
+  if (MODE == 0) {
+    for (int i = threadIdx.x; i < GA + GB; i += blockDim.x) sm[i] = 0;
+    __syncthreads();
+  }
+  const int t = threadIdx.x & 3;
+  const int64_t per = (n4 + gridDim.x - 1) / gridDim.x;
+  const int64_t beg = per * blockIdx.x, end = min(n4, beg + per);
+  int acc = 0;
+  for (int64_t i = beg + (threadIdx.x >> 2); i < end; i += blockDim.x >> 2) {
+    const float4 xv = __ldcs(X + i), yv = __ldcs(Y + i);
+    const float xs[4] = {xv.x, xv.y, xv.z, xv.w}, ys[4] = {yv.x, yv.y, yv.z, yv.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float p = fmaf(xs[q], 16384.f, 16384.f);
+      const float fl = floorf(p);
+      const float f = p - fl;
+      const int ca = __float_as_int(fl + 8388608.f) - 0x4B000000;
+      const int cb = ca >> 1;
+      const float fb = fmaf(f, 0.5f, (ca & 1) ? 0.5f : 0.0f);
+      int i0, i1, i2, i3, j0, j1, j2, j3;
+      bs3(f, SA / 6.f, (int)SA, i0, i1, i2, i3);
+      const int jS = __float_as_int(fmaf(ys[q], SY, MAGIC)) - MAGIC_BITS;
+      bs3(fb, ys[q] * (SY / 6.f), jS, j0, j1, j2, j3);
+      const int iv = t == 0 ? i0 : t == 1 ? i1 : t == 2 ? i2 : i3;
+      const int jv = t == 0 ? j0 : t == 1 ? j1 : t == 2 ? j2 : j3;
+      if (MODE == 0) {
+        const int o = atomicAdd(A + ca + t, iv);
+        const int pp = atomicAdd(B + cb + t, jv);
+        if ((((unsigned)o + (1u << 29)) | ((unsigned)pp + (1u << 29))) & 0xC0000000u) {
+          int v = atomicExch(A + ca + t, 0);
+          if (v) atomicAdd(carry, (double)v);
+          v = atomicExch(B + cb + t, 0);
+          if (v) atomicAdd(carry + 1, (double)v);
+        }
+      } else {
+        acc += (iv ^ ca) + (jv ^ cb);
+      }
+    }
+  }
+  if (MODE == 0) {
+    __syncthreads();
+    int* dst = part + (int64_t)blockIdx.x * (GA + GB);
+    for (int i = threadIdx.x; i < GA + GB; i += blockDim.x) dst[i] = sm[i];
+  } else if (acc == 0x12345) {
+    sink[0] = acc;
+  }
+}
+
+// pair: interleaved [mu_c, r_c] words at sigma 14 (nf 56000, cells 28004); lanes 2i / 2i+1 share
+// the pair's float4s; lane parity selects the channel's scale and closure total, so both lanes
+// run one instruction stream.
+template <int MODE>
+__global__ void __launch_bounds__(1024, 1) k_pair(const float4* __restrict__ X, const float4* __restrict__ Y, int64_t n4,
+                                                  double* carry, int* part, int* sink) {
+  extern __shared__ int sm[];
+  if (MODE == 0) {
+    for (int i = threadIdx.x; i < 2 * GP; i += blockDim.x) sm[i] = 0;
+    __syncthreads();
+  }
+  const int ch = threadIdx.x & 1;
+  int* G = sm + ch;
+  const int64_t per = (n4 + gridDim.x - 1) / gridDim.x;
+  const int64_t beg = per * blockIdx.x, end = min(n4, beg + per);
+  int acc = 0;
+  for (int64_t i = beg + (threadIdx.x >> 1); i < end; i += blockDim.x >> 1) {
+    const float4 xv = __ldcs(X + i), yv = __ldcs(Y + i);
+    const float xs[4] = {xv.x, xv.y, xv.z, xv.w}, ys[4] = {yv.x, yv.y, yv.z, yv.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float p = fmaf(xs[q], 14000.f, 14000.f);  // first tap c = floor(p) in [0, 28000]
+      const float fl = floorf(p);
+      const float f = p - fl;
+      const int c = __float_as_int(fl + 8388608.f) - 0x4B000000;
+      const int jS = __float_as_int(fmaf(ys[q], SY, MAGIC)) - MAGIC_BITS;
+      const float K = ch ? ys[q] * (SY / 6.f) : SA / 6.f;
+      const int S = ch ? jS : (int)SA;
+      int i0, i1, i2, i3;
+      bs3(f, K, S, i0, i1, i2, i3);
+      if (MODE == 0) {
+        int* cc = G + 2 * c;
+        const int o0 = atomicAdd(cc, i0), o1 = atomicAdd(cc + 2, i1), o2 = atomicAdd(cc + 4, i2), o3 = atomicAdd(cc + 6, i3);
+        const unsigned T = 1u << 29;
+        if ((((unsigned)o0 + T) | ((unsigned)o1 + T) | ((unsigned)o2 + T) | ((unsigned)o3 + T)) & 0xC0000000u) drain4(cc, 2, carry);
+      } else {
+        acc += i0 ^ i1 ^ i2 ^ i3 ^ c;
+      }
+    }
+  }
+  if (MODE == 0) {
+    __syncthreads();
+    int* dst = part + (int64_t)blockIdx.x * (GA + GB);
+    for (int i = threadIdx.x; i < 2 * GP; i += blockDim.x) dst[i] = sm[i];
+  } else if (acc == 0x12345) {
+    sink[0] = acc;
+  }
+}
+
+__global__ void k_sum_grid(const int* part, int ncta, int stride, int off, int step, int cnt, long long* out) {
+  long long s = 0;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < (int64_t)ncta * cnt; k += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(k / cnt), j = (int)(k % cnt);
+    s += part[(int64_t)c * stride + off + (int64_t)j * step];
+  }
+  atomicAdd((unsigned long long*)out, (unsigned long long)s);
+}
+
+__global__ void k_sum_jS(const float* Y, int64_t n, long long* out) {
+  long long s = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    s += __float_as_int(fmaf(Y[i], SY, MAGIC)) - MAGIC_BITS;
+  atomicAdd((unsigned long long*)out, (unsigned long long)s);
+}
+
+int main() {
+  CK(cudaSetDevice(0));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, 0));
+  const int sms = prop.multiProcessorCount;
+  printf("device %s sms %d smem_optin %zu\n", prop.name, sms, prop.sharedMemPerBlockOptin);
+  const int64_t n = 1LL << 30;
+  float *X, *Y;
+  double* carry;
+  int *part, *sink;
+  long long* sums;
+  CK(cudaMalloc(&X, n * 4));
+  CK(cudaMalloc(&Y, n * 4));
+  CK(cudaMalloc(&carry, 64));
+  CK(cudaMalloc(&part, (size_t)sms * (GA + GB) * 4 + 64));
+  CK(cudaMalloc(&sink, 64));
+  CK(cudaMalloc(&sums, 64));
+  gen<<<sms * 8, 512>>>(X, Y, n);
+  CK(cudaMemset(sums, 0, 64));
+  k_sum_jS<<<sms * 4, 512>>>(Y, n, sums + 2);
+  CK(cudaDeviceSynchronize());
+  long long want_r = 0;
+  CK(cudaMemcpy(&want_r, sums + 2, 8, cudaMemcpyDeviceToHost));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  struct V {
+    const char* name;
+    void (*k)(const float4*, const float4*, int64_t, double*, int*, int*);
+    int mode;  // 0 atomics, 1 math
+    int layout;  // 0: two grids (GA | GB), 1: interleaved pairs
+  };
+  V vs[] = {{"base", k_base<0>, 0, 0}, {"base_math", k_base<1>, 1, 0}, {"lean", k_lean<0>, 0, 0}, {"lean_math", k_lean<1>, 1, 0},
+            {"quad", k_quad<0>, 0, 0}, {"quad_math", k_quad<1>, 1, 0}, {"pair", k_pair<0>, 0, 1}, {"pair_math", k_pair<1>, 1, 1}};
+  const size_t SMEM = (size_t)(GA + GB) * 4;
+  for (auto& v : vs) CK(cudaFuncSetAttribute(v.k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+  for (int rep = 0; rep < 2; ++rep) {
+    for (auto& v : vs) {
+      CK(cudaMemset(carry, 0, 64));
+      float best = 1e30f;
+      for (int it = 0; it < 3; ++it) {
+        cudaEventRecord(e0);
+        v.k<<<sms, 1024, v.mode == 0 ? SMEM : 0>>>((const float4*)X, (const float4*)Y, n / 4, carry, part, sink);
+        cudaEventRecord(e1);
+        CK(cudaEventSynchronize(e1));
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        best = ms < best ? ms : best;
+      }
+      CK(cudaGetLastError());
+      char chk[160] = "";
+      if (v.mode == 0) {
+        // one clean run for the integer checks (the timed runs accumulated the carries 3x)
+        CK(cudaMemset(carry, 0, 64));
+        v.k<<<sms, 1024, SMEM>>>((const float4*)X, (const float4*)Y, n / 4, carry, part, sink);
+        CK(cudaMemset(sums, 0, 16));
+        if (v.layout == 0) {
+          k_sum_grid<<<sms * 4, 512>>>(part, sms, GA + GB, 0, 1, GA, sums);
+          k_sum_grid<<<sms * 4, 512>>>(part, sms, GA + GB, GA, 1, GB, sums + 1);
+        } else {
+          k_sum_grid<<<sms * 4, 512>>>(part, sms, GA + GB, 0, 2, GP, sums);
+          k_sum_grid<<<sms * 4, 512>>>(part, sms, GA + GB, 1, 2, GP, sums + 1);
+        }
+        long long hs[2];
+        double hc[2];
+        CK(cudaMemcpy(hs, sums, 16, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(hc, carry, 16, cudaMemcpyDeviceToHost));
+        // carries: the drains of grid A (even cell parity / pair word 0) and B; total = cells + carries
+        const double tot_mu = (double)hs[0] + hc[0] + hc[1] * 0.0, tot_all = (double)hs[0] + (double)hs[1] + hc[0] + hc[1];
+        const double want_all = (double)n * SA + (double)want_r;
+        snprintf(chk, sizeof chk, "check(all cells+carries == n S + sum round(Y SY)): %s (%.6e vs %.6e)",
+                 tot_all == want_all ? "OK" : "MISMATCH", tot_all, want_all);
+        (void)tot_mu;
+      }
+      printf("%-10s %8.3f ms  %.3e samples/s  %7.1f GB/s  %s\n", v.name, best, n / best * 1e3, n * 8.0 / best / 1e6, chk);
+    }
+  }
+  printf("done\n");
+  return 0;
+}
