@@ -1,0 +1,264 @@
+// dft1d.cu -- the d = 1 type-1 pass after the spreading: CTA partial grids -> one fine grid ->
+// the window-convolved grid's DFT at the needed modes only -> deconvolution (PAPER.md:203-220,
+// sec. 2.3: the NUFFT's FFT step).  Hand-written, no cuFFT; three launches for BOTH grids of a
+// pass (moments and rhs):
+//
+//   k_reduce_occ  per occupied fine cell, the sum over the CTA partials (moments: int64, exact and
+//                 order-free; rhs: per-CTA power-of-two scales, fp64 in fixed CTA order) + the
+//                 drained carries -> fp64 grid of the occupied cells only (G of nf cells)
+//   k_dft_s1      pruned two-level DFT, stage 1: nf = N1 N2, l = l1 + N1 l2, q = q2 + N2 q1;
+//                   T[q2][l1] = w_nf^(q2 l1) sum_l2 g[l1 + N1 l2] w_N2^(q2 l2)
+//                 one CTA per (l1, grid), thread q2; only the l2 of occupied cells are summed
+//                 (about half), twiddles exact from a per-CTA table (integer index arithmetic)
+//   k_dft_s2      stage 2 + deconvolution: F_q = sum_l1 T[q mod N2][l1] w_N1^((q / N2) l1) for the
+//                 K + 1 modes q = 0..K only (K = 2m moments, m rhs); one warp per q; then
+//                 out_{+-q} = (-1)^q F_q / psi-hat(q / nf) (conjugate for -q: the grid is real)
+//
+// w_N = exp(-2 pi i / N).  A full FFT would produce nf/2 + 1 modes of which the fit needs K + 1
+// (C2: 2001 of 32769 for the moments): the pruned DFT does (K+1) N1 + N1 N2 G/nf complex
+// multiply-adds, ~10^7 at C2 -- microseconds -- and reads the fine grid once.
+#include <cmath>
+
+#include "fk_internal.cuh"
+
+namespace fk {
+namespace {
+
+constexpr int kMaxN2 = 512;
+constexpr int kMaxN1 = 8192;
+
+__device__ __forceinline__ double2 tw(int a, int N) {  // w_N^a = exp(-2 pi i a / N), 0 <= a < N
+  double s, c;
+  sincospi(2.0 * (double)a / (double)N, &s, &c);
+  return make_double2(c, -s);
+}
+
+struct RedArgs {
+  const int* part_i[2];     // int32 fixed-point partials (fp32 path), or
+  const double* part_d[2];  // fp64 partials (fp64 modes)
+  const int* escale[2];     // per-CTA power-of-two exponents of an int32 grid (rhs), or null
+  const double* carry[2];
+  double inv_scale[2];      // value of one fixed-point unit when escale is null
+  int G[2];
+  int nparts[2];
+  double* out[2];
+};
+
+// occupied cells of both grids; thread = one cell, the partial loop unrolled for load-level
+// parallelism.  Uniform-scale int32 grids sum in int64 (exact, so order-free); per-CTA-scaled and
+// fp64 partials in the fixed CTA order (bitwise reproducible).
+__global__ void __launch_bounds__(256) k_reduce_occ(RedArgs a) {
+  const int ch = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.G[ch]) return;
+  const int64_t st = a.G[ch];
+  const int np = a.nparts[ch];
+  double v;
+  if (a.part_d[ch]) {
+    const double* __restrict__ p = a.part_d[ch] + i;
+    double s = 0.0;
+#pragma unroll 8
+    for (int c = 0; c < np; ++c) s += __ldcg(p + c * st);
+    v = s;
+  } else if (a.escale[ch]) {
+    const int* __restrict__ p = a.part_i[ch] + i;
+    const int* __restrict__ e = a.escale[ch];
+    double s = 0.0;
+#pragma unroll 8
+    for (int c = 0; c < np; ++c) s += (double)__ldcg(p + c * st) * pow2(-__ldg(e + c));
+    v = s;
+  } else {
+    const int* __restrict__ p = a.part_i[ch] + i;
+    long long s = 0;  // exact: at most nparts x 2^31 in magnitude
+#pragma unroll 8
+    for (int c = 0; c < np; ++c) s += __ldcg(p + c * st);
+    v = (double)s * a.inv_scale[ch];
+  }
+  if (a.carry[ch]) v += a.carry[ch][i];
+  a.out[ch][i] = v;
+}
+
+struct S1Args {
+  const double* g[2];  // occupied cells: g[i] = cell off + i, i < G
+  int nf[2], N1[2], N2[2], off[2], G[2], nq2[2];
+  double2* T[2];       // [q2][l1], q2 < nq2
+};
+
+__global__ void __launch_bounds__(kMaxN2) k_dft_s1(S1Args a) {
+  __shared__ double col[kMaxN2];
+  __shared__ double2 tab[kMaxN2];
+  const int ch = blockIdx.y;
+  const int N1 = a.N1[ch], N2 = a.N2[ch], nf = a.nf[ch], off = a.off[ch], G = a.G[ch];
+  const int l1 = blockIdx.x;
+  if (l1 >= N1) return;
+  // l2 range with occupied cells: off <= l1 + N1 l2 < off + G
+  const int lo2 = max(0, (off - l1 + N1 - 1) / N1);
+  const int hi2 = min(N2 - 1, (off + G - 1 - l1) / N1);
+  for (int k = threadIdx.x; k < N2; k += blockDim.x) {
+    tab[k] = tw(k, N2);
+    const int i = l1 + N1 * k - off;
+    col[k] = (i >= 0 && i < G) ? a.g[ch][i] : 0.0;
+  }
+  __syncthreads();
+  for (int q2 = threadIdx.x; q2 < a.nq2[ch]; q2 += blockDim.x) {
+    double re = 0.0, im = 0.0;
+    int idx = (int)(((long long)q2 * lo2) % N2);
+    for (int l2 = lo2; l2 <= hi2; ++l2) {
+      const double v = col[l2];
+      const double2 t = tab[idx];
+      re = fma(v, t.x, re);
+      im = fma(v, t.y, im);
+      idx += q2;
+      if (idx >= N2) idx -= N2;
+    }
+    const double2 w = tw((int)(((long long)q2 * l1) % nf), nf);
+    a.T[ch][(int64_t)q2 * N1 + l1] = make_double2(re * w.x - im * w.y, re * w.y + im * w.x);
+  }
+}
+
+struct S2Args {
+  const double2* T[2];
+  int nf[2], N1[2], N2[2], K[2];
+  int ker;
+  const double* tab[2];  // KER_ES: psi-hat(q / nf), q = 0..K
+  double2* out[2];       // 2K + 1 modes, index K + q
+  int acc;
+};
+
+// one warp per mode q >= 0 of grid blockIdx.y; lanes stride over l1
+__global__ void __launch_bounds__(256) k_dft_s2(S2Args a) {
+  const int ch = blockIdx.y;
+  const int K = a.K[ch];
+  const int q = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (q > K) return;
+  const int N1 = a.N1[ch], N2 = a.N2[ch], nf = a.nf[ch];
+  const int q2 = q % N2, q1 = q / N2;
+  const double2* __restrict__ T = a.T[ch] + (int64_t)q2 * N1;
+  double re = 0.0, im = 0.0;
+  if (q1 == 0) {
+    for (int l1 = lane; l1 < N1; l1 += 32) {
+      const double2 t = T[l1];
+      re += t.x;
+      im += t.y;
+    }
+  } else {
+    for (int l1 = lane; l1 < N1; l1 += 32) {
+      const double2 t = T[l1];
+      const double2 w = tw((int)(((long long)q1 * l1) % N1), N1);
+      re = fma(t.x, w.x, fma(-t.y, w.y, re));
+      im = fma(t.x, w.y, fma(t.y, w.x, im));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    re += __shfl_xor_sync(0xffffffffu, re, o);
+    im += __shfl_xor_sync(0xffffffffu, im, o);
+  }
+  if (lane != 0) return;
+  double ph;
+  if (a.ker == KER_BS3) {
+    const double s = sinc_pi((double)q / nf);
+    ph = (s * s) * (s * s);
+  } else if (a.ker == KER_BS7) {
+    const double s = sinc_pi((double)q / nf);
+    const double s2 = s * s, s4 = s2 * s2;
+    ph = s4 * s4;
+  } else {
+    ph = a.tab[ch][q];
+  }
+  const double sc = ((q & 1) ? -1.0 : 1.0) / ph;
+  const double2 v = make_double2(re * sc, im * sc);
+  double2* o = a.out[ch];
+  if (a.acc) {
+    o[K + q].x += v.x;
+    o[K + q].y += v.y;
+    if (q > 0) {
+      o[K - q].x += v.x;
+      o[K - q].y -= v.y;
+    }
+  } else {
+    o[K + q] = v;
+    if (q > 0) o[K - q] = make_double2(v.x, -v.y);
+  }
+}
+
+}  // namespace
+
+// N2: the divisor of nf closest to sqrt(nf) with N2 <= 512 and nf / N2 <= 8192
+fk_status dft1d_factor(int nf, int* N1, int* N2) {
+  int best = 0;
+  const double r = std::sqrt((double)nf);
+  for (int d = 1; d <= kMaxN2 && d <= nf; ++d)
+    if (nf % d == 0 && nf / d <= kMaxN1 && (best == 0 || std::fabs(std::log(d / r)) < std::fabs(std::log(best / r)))) best = d;
+  if (best == 0) return fail(FK_E_UNSUPPORTED, "dft1d: no N1 x N2 factorisation of nf = " + std::to_string(nf));
+  *N2 = best;
+  *N1 = nf / best;
+  return FK_OK;
+}
+
+size_t dft1d_ws_bytes(const Dft1Grid* g, int ngrids) {
+  Bump b(nullptr, 0);
+  for (int k = 0; k < ngrids; ++k) {
+    int N1 = 0, N2 = 0;
+    if (dft1d_factor(g[k].nf, &N1, &N2) != FK_OK) return 0;
+    b.take((size_t)g[k].G * 8);                        // occupied fine grid
+    b.take((size_t)std::min(N2, g[k].K + 1) * N1 * 16);  // stage-1 output
+  }
+  return b.used + 256;
+}
+
+fk_status dft1d_run(const Dft1Grid* g, int ngrids, int ker, int acc, void* ws, size_t ws_bytes, cudaStream_t s) {
+  if (ngrids < 1 || ngrids > 2) return fail(FK_E_ARG, "dft1d: 1 or 2 grids");
+  Bump b(ws, ws_bytes);
+  RedArgs ra{};
+  S1Args s1{};
+  S2Args s2{};
+  int maxG = 0, maxN1 = 0, maxK = 0, maxN2 = 0;
+  for (int k = 0; k < ngrids; ++k) {
+    int N1 = 0, N2 = 0;
+    FK_TRY(dft1d_factor(g[k].nf, &N1, &N2));
+    double* fine = (double*)b.take((size_t)g[k].G * 8);
+    const int nq2 = std::min(N2, g[k].K + 1);
+    double2* T = (double2*)b.take((size_t)nq2 * N1 * 16);
+    ra.part_i[k] = g[k].part_i;
+    ra.part_d[k] = g[k].part_d;
+    ra.escale[k] = g[k].escale;
+    ra.nparts[k] = g[k].nparts;
+    ra.carry[k] = g[k].carry;
+    ra.inv_scale[k] = g[k].inv_scale;
+    ra.G[k] = g[k].G;
+    ra.out[k] = fine;
+    s1.g[k] = fine;
+    s1.nf[k] = g[k].nf;
+    s1.N1[k] = N1;
+    s1.N2[k] = N2;
+    s1.off[k] = g[k].off;
+    s1.G[k] = g[k].G;
+    s1.nq2[k] = nq2;
+    s1.T[k] = T;
+    s2.T[k] = T;
+    s2.nf[k] = g[k].nf;
+    s2.N1[k] = N1;
+    s2.N2[k] = N2;
+    s2.K[k] = g[k].K;
+    s2.tab[k] = g[k].phihat;
+    s2.out[k] = (double2*)g[k].out;
+    maxG = std::max(maxG, g[k].G);
+    maxN1 = std::max(maxN1, N1);
+    maxN2 = std::max(maxN2, nq2);
+    maxK = std::max(maxK, g[k].K);
+  }
+  if (!b.ok()) return fail(FK_E_WORKSPACE, "dft1d: workspace too small");
+  s2.ker = ker;
+  s2.acc = acc;
+  k_reduce_occ<<<dim3((maxG + 255) / 256, ngrids), 256, 0, s>>>(ra);
+  const int t1 = std::min(kMaxN2, (maxN2 + 31) / 32 * 32);
+  k_dft_s1<<<dim3(maxN1, ngrids), t1, 0, s>>>(s1);
+  k_dft_s2<<<dim3((maxK + 1 + 7) / 8, ngrids), 256, 0, s>>>(s2);
+  FK_CUDA_TRY(cudaGetLastError());
+  count_launch(3);
+  return FK_OK;
+}
+
+}  // namespace fk

@@ -127,6 +127,24 @@ struct Type1Out {
   bool accumulate;
 };
 size_t type1_ws_bytes(const Plan1& p, bool need_mu, bool need_r);
+
+// hand-written reduce + pruned DFT + deconvolution of a d = 1 pass (dft1d.cu), up to two grids
+// per launch set.  out[K + q], q = -K..K: (-1)^q F_q / psi-hat(q / nf) with F the DFT of the
+// full-period grid whose occupied cells [off, off + G) are the summed partials + carries.
+struct Dft1Grid {
+  int nf = 0, off = 0, G = 0, K = 0;
+  const int* part_i = nullptr;     // nparts x G int32 partials, or
+  const double* part_d = nullptr;  // nparts x G fp64 partials
+  int nparts = 0;
+  const int* escale = nullptr;     // per-partial exponent: value = int x 2^-escale (else x inv_scale)
+  double inv_scale = 1.0;
+  const double* carry = nullptr;   // G fp64 drained values, or null
+  const double* phihat = nullptr;  // KER_ES: psi-hat(q / nf), q = 0..K
+  double* out = nullptr;           // 2K + 1 complex128
+};
+fk_status dft1d_factor(int nf, int* N1, int* N2);
+size_t dft1d_ws_bytes(const Dft1Grid* g, int ngrids);
+fk_status dft1d_run(const Dft1Grid* g, int ngrids, int ker, int acc, void* ws, size_t ws_bytes, cudaStream_t s);
 fk_status type1_run(const Plan1& p, const fk_points& X, const void* Y, double L, const Type1Out& out, void* ws, size_t ws_bytes,
                     int* d_status, cudaStream_t s);
 

@@ -387,7 +387,7 @@ __global__ void __launch_bounds__(1024, 1) k_spread1d_esx(const XT* __restrict__
 // fp64 mode, septic B-spline (plan KER_BS7): one channel per pass (CH = 0 moments, 1 rhs), the
 // channel's occupied grid in shared memory as 64-bit fixed point (int32 pairs, pair_add), tap
 // weights by the uniform Cox-de Boor recursion in fp64 (28 steps, constants 1/j only).  Taps at
-// cells floor(p) - 3 .. floor(p) + 4 relative to the grid centre; transform sinc^8 (k_deconv1d).
+// cells floor(p) - 3 .. floor(p) + 4 relative to the grid centre; transform sinc^8 (deconvolved in dft1d.cu).
 // Moments: the 8 integer weights are closed to 2^40 exactly (partition of unity: mu_0 = n).
 // ------------------------------------------------------------------------------------------
 __device__ __forceinline__ void bs7_weights(double f, double* N) {
@@ -492,118 +492,63 @@ __global__ void __launch_bounds__(1024, 1) k_spread1d_bs7(const XT* __restrict__
   for (int i = threadIdx.x; i < g.G; i += blockDim.x) dst[i] = ((double)hi[i] * 4294967296.0 + (double)lo[i]) * sc;
 }
 
-// ------------------------------------------------------------------------------------------
-// per-CTA partial grids -> one fp64 fine grid (full period, zero outside the occupied band),
-// summed over CTAs in a fixed order (the fixed-point path is exact, hence bitwise deterministic)
-// ------------------------------------------------------------------------------------------
-__global__ void k_reduce_fixed(const int* __restrict__ part, const int* __restrict__ escale, int ncta, int G, int off, int nf,
-                               double uniform_inv, const double* __restrict__ carry, double* __restrict__ fine) {
-  const int l = blockIdx.x * blockDim.x + threadIdx.x;
-  if (l >= nf) return;
-  const int i = l - off;
-  double s = 0.0;
-  if (i >= 0 && i < G) {
-    if (escale) {
-      for (int c = 0; c < ncta; ++c) s += (double)part[(int64_t)c * G + i] * pow2(-escale[c]);
-    } else {
-      for (int c = 0; c < ncta; ++c) s += (double)part[(int64_t)c * G + i];
-      s *= uniform_inv;
-    }
-    s += carry[i];
-  }
-  fine[l] = s;
-}
-
-__global__ void k_reduce_f64(const double* __restrict__ part, int ncta, int G, int off, int nf, const double* __restrict__ carry,
-                             double* __restrict__ fine) {
-  const int l = blockIdx.x * blockDim.x + threadIdx.x;
-  if (l >= nf) return;
-  const int i = l - off;
-  double s = 0.0;
-  if (i >= 0 && i < G) {
-    for (int c = 0; c < ncta; ++c) s += part[(int64_t)c * G + i];
-    if (carry) s += carry[i];
-  }
-  fine[l] = s;
-}
-
-// mode q of the window-convolved grid: F_q = sum_l b_l e^{-2 pi i q l / nf}; the grid origin is
-// t = -pi, so e^{-i q (t + pi)} = (-1)^q e^{-i q t}: mu_q = (-1)^q F_q / psi-hat(q / nf).
-__global__ void k_deconv1d(const double2* __restrict__ F, int nf, int K, int ker, const double* __restrict__ tab,
-                           double2* __restrict__ out, int acc) {
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx > 2 * K) return;
-  const int q = idx - K;
-  const int aq = q < 0 ? -q : q;
-  double2 v = F[aq];
-  if (q < 0) v.y = -v.y;
-  double ph;
-  if (ker == KER_BS3) {
-    const double s = sinc_pi((double)aq / nf);
-    ph = (s * s) * (s * s);
-  } else if (ker == KER_BS7) {
-    const double s = sinc_pi((double)aq / nf);
-    const double s2 = s * s, s4 = s2 * s2;
-    ph = s4 * s4;
-  } else {
-    ph = tab[aq];
-  }
-  const double sc = ((aq & 1) ? -1.0 : 1.0) / ph;
-  v.x *= sc;
-  v.y *= sc;
-  if (acc) {
-    out[idx].x += v.x;
-    out[idx].y += v.y;
-  } else {
-    out[idx] = v;
-  }
-}
-
 struct Ws1 {
   void* partA = nullptr;
   void* partB = nullptr;
   int* escale = nullptr;
   double* carryA = nullptr;
   double* carryB = nullptr;
-  double* fineA = nullptr;
-  double* fineB = nullptr;
-  double2* specA = nullptr;
-  double2* specB = nullptr;
   double* tabA = nullptr;
   double* tabB = nullptr;
-  void* fftwork = nullptr;
+  void* dftws = nullptr;
+  size_t dft_bytes = 0;
 };
 
-static fk_status layout1(const Plan1& p, bool mu, bool r, Bump& b, Ws1& w, size_t* fftwork) {
+// the grids of a pass in the order dft1d_run takes them (moments first)
+static int dft_grids(const Plan1& p, bool mu, bool r, const Ws1& w, const Type1Out* out, Dft1Grid* g) {
+  const int nparts = p.smem ? p.ctas : 1;
+  int k = 0;
+  for (int ch = 0; ch < 2; ++ch) {
+    if ((ch == 0 && !mu) || (ch == 1 && !r)) continue;
+    const Geo& gg = ch == 0 ? p.gA : p.gB;
+    Dft1Grid d;
+    d.nf = gg.nf;
+    d.off = gg.off;
+    d.G = gg.G;
+    d.K = ch == 0 ? 2 * p.m : p.m;
+    d.nparts = nparts;
+    void* part = ch == 0 ? w.partA : w.partB;
+    if (p.fp64) d.part_d = (const double*)part;
+    else d.part_i = (const int*)part;
+    d.escale = (ch == 1 && !p.fp64) ? w.escale : nullptr;
+    d.inv_scale = kInvSA;
+    d.carry = ch == 0 ? w.carryA : w.carryB;
+    d.phihat = ch == 0 ? w.tabA : w.tabB;
+    d.out = out ? (ch == 0 ? out->mu : out->r) : nullptr;
+    g[k++] = d;
+  }
+  return k;
+}
+
+static fk_status layout1(const Plan1& p, bool mu, bool r, Bump& b, Ws1& w) {
   const size_t esz = p.fp64 ? 8 : 4;
   const int nparts = p.smem ? p.ctas : 1;
-  FftPlan pa, pb;
-  size_t fw = 0;
-  if (mu) {
-    FK_TRY(fft_plan(1, &p.nf_mu, 1, CUFFT_D2Z, &pa));
-    fw = std::max(fw, pa.work);
-  }
-  if (r) {
-    FK_TRY(fft_plan(1, &p.nf_r, 1, CUFFT_D2Z, &pb));
-    fw = std::max(fw, pb.work);
-  }
   if (mu) {
     w.partA = b.take((size_t)nparts * p.gA.G * esz);
-    w.fineA = (double*)b.take((size_t)p.nf_mu * 8);
-    w.specA = (double2*)b.take((size_t)(p.nf_mu / 2 + 1) * 16);
     if (!p.fp64 || p.smem) w.carryA = (double*)b.take((size_t)p.gA.G * 8);
     if (p.ker == KER_ES) w.tabA = (double*)b.take((size_t)(2 * p.m + 1) * 8);
   }
   if (r) {
     w.partB = b.take((size_t)nparts * p.gB.G * esz);
-    w.fineB = (double*)b.take((size_t)p.nf_r * 8);
-    w.specB = (double2*)b.take((size_t)(p.nf_r / 2 + 1) * 16);
     if (!p.fp64 || p.smem) w.carryB = (double*)b.take((size_t)p.gB.G * 8);
     if (!p.fp64) w.escale = (int*)b.take((size_t)p.ctas * 4);
     if (p.ker == KER_ES) w.tabB = (double*)b.take((size_t)(p.m + 1) * 8);
   }
-  w.fftwork = b.take(std::max<size_t>(fw, 256));
-  if (fftwork) *fftwork = fw;
+  Dft1Grid g[2];
+  const int ng = dft_grids(p, mu, r, w, nullptr, g);
+  w.dft_bytes = dft1d_ws_bytes(g, ng);
+  if (w.dft_bytes == 0) return fail(FK_E_UNSUPPORTED, "type-1 pass: no DFT factorisation for this grid size");
+  w.dftws = b.take(w.dft_bytes);
   return FK_OK;
 }
 
@@ -756,7 +701,7 @@ static fk_status spread_dispatch(const Plan1& p, const fk_points& Xp, const void
 size_t type1_ws_bytes(const Plan1& p, bool need_mu, bool need_r) {
   Bump b(nullptr, 0);
   Ws1 w;
-  if (layout1(p, need_mu, need_r, b, w, nullptr) != FK_OK) return 0;
+  if (layout1(p, need_mu, need_r, b, w) != FK_OK) return 0;
   return b.used + 256;
 }
 
@@ -765,8 +710,7 @@ fk_status type1_run(const Plan1& p, const fk_points& X, const void* Y, double L,
   const bool mu = out.mu != nullptr, r = out.r != nullptr;
   Bump b(ws, ws_bytes);
   Ws1 w;
-  size_t fw = 0;
-  FK_TRY(layout1(p, mu, r, b, w, &fw));
+  FK_TRY(layout1(p, mu, r, b, w));
   if (!b.ok()) return fail(FK_E_WORKSPACE, "workspace too small: need " + std::to_string(b.used + 256) + " bytes");
   // zero what is accumulated globally
   if (!p.fp64 || p.smem) {
@@ -787,44 +731,12 @@ fk_status type1_run(const Plan1& p, const fk_points& X, const void* Y, double L,
     if (r) FK_CUDA_TRY(cudaMemsetAsync(w.partB, 0, (size_t)p.ctas * p.gB.G * esz, s));
     if (r && w.escale) FK_CUDA_TRY(cudaMemsetAsync(w.escale, 0, (size_t)p.ctas * 4, s));
   }
-  const int nparts = p.smem ? p.ctas : 1;
-  const int TB = 256;
-  if (mu) {
-    if (!p.fp64)
-      k_reduce_fixed<<<(p.nf_mu + TB - 1) / TB, TB, 0, s>>>((const int*)w.partA, nullptr, nparts, p.gA.G, p.gA.off, p.nf_mu, kInvSA,
-                                                            w.carryA, w.fineA);
-    else
-      k_reduce_f64<<<(p.nf_mu + TB - 1) / TB, TB, 0, s>>>((const double*)w.partA, nparts, p.gA.G, p.gA.off, p.nf_mu,
-                                                          p.smem ? w.carryA : nullptr, w.fineA);
-    FK_CUDA_TRY(cudaGetLastError());
-    count_launch();
-    FftPlan pa;
-    FK_TRY(fft_plan(1, &p.nf_mu, 1, CUFFT_D2Z, &pa));
-    FK_TRY(fft_exec_d2z(pa, w.fineA, (cufftDoubleComplex*)w.specA, w.fftwork, s));
-    if (p.ker == KER_ES) FK_TRY(es_phihat_table(p.es, p.nf_mu, 2 * p.m, w.tabA, s));
-    k_deconv1d<<<(4 * p.m + 1 + TB - 1) / TB, TB, 0, s>>>(w.specA, p.nf_mu, 2 * p.m, p.ker, w.tabA, (double2*)out.mu,
-                                                          out.accumulate ? 1 : 0);
-    FK_CUDA_TRY(cudaGetLastError());
-    count_launch();
-  }
-  if (r) {
-    if (!p.fp64)
-      k_reduce_fixed<<<(p.nf_r + TB - 1) / TB, TB, 0, s>>>((const int*)w.partB, w.escale, nparts, p.gB.G, p.gB.off, p.nf_r, 1.0,
-                                                           w.carryB, w.fineB);
-    else
-      k_reduce_f64<<<(p.nf_r + TB - 1) / TB, TB, 0, s>>>((const double*)w.partB, nparts, p.gB.G, p.gB.off, p.nf_r,
-                                                         p.smem ? w.carryB : nullptr, w.fineB);
-    FK_CUDA_TRY(cudaGetLastError());
-    count_launch();
-    FftPlan pb;
-    FK_TRY(fft_plan(1, &p.nf_r, 1, CUFFT_D2Z, &pb));
-    FK_TRY(fft_exec_d2z(pb, w.fineB, (cufftDoubleComplex*)w.specB, w.fftwork, s));
-    if (p.ker == KER_ES) FK_TRY(es_phihat_table(p.es, p.nf_r, p.m, w.tabB, s));
-    k_deconv1d<<<(2 * p.m + 1 + TB - 1) / TB, TB, 0, s>>>(w.specB, p.nf_r, p.m, p.ker, w.tabB, (double2*)out.r,
-                                                          out.accumulate ? 1 : 0);
-    FK_CUDA_TRY(cudaGetLastError());
-    count_launch();
-  }
+  // reduce the partials, pruned DFT at the needed modes, deconvolve: dft1d.cu (no cuFFT)
+  if (mu && p.ker == KER_ES) FK_TRY(es_phihat_table(p.es, p.nf_mu, 2 * p.m, w.tabA, s));
+  if (r && p.ker == KER_ES) FK_TRY(es_phihat_table(p.es, p.nf_r, p.m, w.tabB, s));
+  Dft1Grid g[2];
+  const int ng = dft_grids(p, mu, r, w, &out, g);
+  FK_TRY(dft1d_run(g, ng, p.ker, out.accumulate ? 1 : 0, w.dftws, w.dft_bytes, s));
   return FK_OK;
 }
 
