@@ -381,7 +381,14 @@ def main():
                 "kernel": "k_spread1d_bs3 (one pass over X, Y)",
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s",
                 "frac_of_nominal_8tbs": achieved / NOMINAL_HBM_GBS, "spread_ms_avg": avg, "bytes_per_launch": n_loc * 8,
-                "spread_share_of_step": spread_per_step_ms / ms_step}
+                "spread_share_of_step": spread_per_step_ms / ms_step,
+                # the resource that binds this kernel: 8 int32 shared-memory atomics per sample (4 cubic
+                # B-spline taps x 2 channels) against the measured random-address ATOMS.ADD rate --
+                # ~9.5 lane-ops/clk/SM for ANY non-consecutive address pattern, bank-conflict-free ones
+                # included (profiles/r02_microbench_atoms_patterns.log)
+                "atomics": {"bound": "alu", "achieved": 8 * n_loc / (avg * 1e-3) / 1e9, "peak": ATOMS_RANDOM_PEAK / 1e9,
+                            "unit": "Gatomic/s", "frac": 8 * n_loc / (avg * 1e-3) / ATOMS_RANDOM_PEAK,
+                            "peak_source": "measured random-address int32 ATOMS.ADD, profiles/r01_microbench_spread.log"}}
     else:
         # d >= 2 / additive: bound by random-address shared-memory atomics (2 w^2 per sample for d = 2,
         # npairs w^2 + 2 d x 4 per sample for the additive model); peak = the measured random ATOMS rate

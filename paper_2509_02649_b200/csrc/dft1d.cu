@@ -44,38 +44,94 @@ struct RedArgs {
   double* out[2];
 };
 
-// occupied cells of both grids; thread = one cell, the partial loop unrolled for load-level
-// parallelism.  Uniform-scale int32 grids sum in int64 (exact, so order-free); per-CTA-scaled and
-// fp64 partials in the fixed CTA order (bitwise reproducible).
+// occupied cells of both grids.  A 256-thread block takes 32 consecutive cells; its 8 warps split the
+// partials (warp k sums partials k, k + 8, ...), so 8x more loads are in flight than with one thread
+// per cell, then warp 0 combines the 8 sums in fixed order.  Uniform-scale int32 grids sum in int64
+// (exact, so order-free); per-CTA-scaled and fp64 partials in a fixed order (bitwise reproducible).
+constexpr int kRedSplit = 8;  // warps per block, each a share of the partials
+
+// V cells per thread (V = 4: int4 loads, needs G % 4 == 0 -- the fp32 path's grids -- so every
+// partial row starts 16-byte aligned); block = 32 V consecutive cells x kRedSplit warps
+template <int V>
 __global__ void __launch_bounds__(256) k_reduce_occ(RedArgs a) {
+  __shared__ double sd[kRedSplit][32 * V];
+  __shared__ long long sl[kRedSplit][32 * V];
   const int ch = blockIdx.y;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= a.G[ch]) return;
-  const int64_t st = a.G[ch];
+  const int lane = threadIdx.x & 31, k = threadIdx.x >> 5;
+  const int G = a.G[ch];
+  const int i0 = blockIdx.x * 32 * V + lane * V;
+  if (blockIdx.x * 32 * V >= G) return;
+  const int64_t st = G;
   const int np = a.nparts[ch];
-  double v;
-  if (a.part_d[ch]) {
-    const double* __restrict__ p = a.part_d[ch] + i;
+  const bool ok = i0 < G;
+  const bool fixed = !a.part_d[ch] && !a.escale[ch];
+  if (a.part_d[ch]) {  // fp64 partials (V == 1 only)
+    const double* __restrict__ p = a.part_d[ch] + i0;
     double s = 0.0;
-#pragma unroll 8
-    for (int c = 0; c < np; ++c) s += __ldcg(p + c * st);
-    v = s;
-  } else if (a.escale[ch]) {
-    const int* __restrict__ p = a.part_i[ch] + i;
-    const int* __restrict__ e = a.escale[ch];
-    double s = 0.0;
-#pragma unroll 8
-    for (int c = 0; c < np; ++c) s += (double)__ldcg(p + c * st) * pow2(-__ldg(e + c));
-    v = s;
+    if (ok)
+#pragma unroll 4
+      for (int c = k; c < np; c += kRedSplit) s += __ldcg(p + c * st);
+    sd[k][lane] = s;
   } else {
-    const int* __restrict__ p = a.part_i[ch] + i;
-    long long s = 0;  // exact: at most nparts x 2^31 in magnitude
-#pragma unroll 8
-    for (int c = 0; c < np; ++c) s += __ldcg(p + c * st);
-    v = (double)s * a.inv_scale[ch];
+    const int* __restrict__ p = a.part_i[ch] + i0;
+    const int* __restrict__ e = a.escale[ch];
+    long long si[V];
+    double sf[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      si[v] = 0;
+      sf[v] = 0.0;
+    }
+    if (ok) {
+#pragma unroll 4
+      for (int c = k; c < np; c += kRedSplit) {
+        int x[V];
+        if (V == 4) {
+          const int4 q = __ldcg(reinterpret_cast<const int4*>(p + c * st));
+          x[0] = q.x;
+          x[V > 1 ? 1 : 0] = q.y;
+          x[V > 2 ? 2 : 0] = q.z;
+          x[V > 3 ? 3 : 0] = q.w;
+        } else {
+          x[0] = __ldcg(p + c * st);
+        }
+        if (e) {
+          const double sc = pow2(-__ldg(e + c));
+#pragma unroll
+          for (int v = 0; v < V; ++v) sf[v] += (double)x[v] * sc;
+        } else {
+#pragma unroll
+          for (int v = 0; v < V; ++v) si[v] += x[v];  // exact: at most nparts x 2^31 in magnitude
+        }
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      sd[k][lane * V + v] = sf[v];
+      sl[k][lane * V + v] = si[v];
+    }
   }
-  if (a.carry[ch]) v += a.carry[ch][i];
-  a.out[ch][i] = v;
+  __syncthreads();
+  if (k != 0 || !ok) return;
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const int i = i0 + v;
+    if (i >= G) break;
+    double val;
+    if (fixed) {
+      long long t = 0;
+#pragma unroll
+      for (int q = 0; q < kRedSplit; ++q) t += sl[q][lane * V + v];
+      val = (double)t * a.inv_scale[ch];
+    } else {
+      double t = 0.0;
+#pragma unroll
+      for (int q = 0; q < kRedSplit; ++q) t += sd[q][lane * V + v];
+      val = t;
+    }
+    if (a.carry[ch]) val += a.carry[ch][i];
+    a.out[ch][i] = val;
+  }
 }
 
 struct S1Args {
@@ -101,18 +157,34 @@ __global__ void __launch_bounds__(kMaxN2) k_dft_s1(S1Args a) {
   }
   __syncthreads();
   for (int q2 = threadIdx.x; q2 < a.nq2[ch]; q2 += blockDim.x) {
-    double re = 0.0, im = 0.0;
-    int idx = (int)(((long long)q2 * lo2) % N2);
-    for (int l2 = lo2; l2 <= hi2; ++l2) {
-      const double v = col[l2];
-      const double2 t = tab[idx];
-      re = fma(v, t.x, re);
-      im = fma(v, t.y, im);
-      idx += q2;
-      if (idx >= N2) idx -= N2;
+    // four independent accumulation chains (l2 = lo2 + 4 j + u); chain u's twiddle starts exact from
+    // the table and advances by the complex rotation w_N2^(4 q2) (a table lookup per term would hit
+    // shared-memory bank conflicts at the index stride q2; ~N2/8 rotations per chain: ~1e-14)
+    double re[4] = {0.0, 0.0, 0.0, 0.0}, im[4] = {0.0, 0.0, 0.0, 0.0};
+    double2 t[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) t[u] = tab[(q2 * (lo2 + u)) % N2];
+    const double2 r4 = tab[(4 * q2) % N2];
+    int l2 = lo2;
+    for (; l2 + 3 <= hi2; l2 += 4) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double v = col[l2 + u];
+        re[u] = fma(v, t[u].x, re[u]);
+        im[u] = fma(v, t[u].y, im[u]);
+        const double tx = t[u].x * r4.x - t[u].y * r4.y;
+        t[u].y = fma(t[u].x, r4.y, t[u].y * r4.x);
+        t[u].x = tx;
+      }
     }
-    const double2 w = tw((int)(((long long)q2 * l1) % nf), nf);
-    a.T[ch][(int64_t)q2 * N1 + l1] = make_double2(re * w.x - im * w.y, re * w.y + im * w.x);
+    for (int u = 0; l2 <= hi2; ++l2, ++u) {
+      const double v = col[l2];
+      re[u] = fma(v, t[u].x, re[u]);
+      im[u] = fma(v, t[u].y, im[u]);
+    }
+    const double r0 = (re[0] + re[1]) + (re[2] + re[3]), i0 = (im[0] + im[1]) + (im[2] + im[3]);
+    const double2 w = tw((q2 * l1) % nf, nf);
+    a.T[ch][(int64_t)q2 * N1 + l1] = make_double2(r0 * w.x - i0 * w.y, r0 * w.y + i0 * w.x);
   }
 }
 
@@ -125,14 +197,22 @@ struct S2Args {
   int acc;
 };
 
-// one warp per mode q >= 0 of grid blockIdx.y; lanes stride over l1
+// one warp per mode q >= 0 of grid blockIdx.y; lanes stride over l1; w_N1 table in shared memory
+constexpr int kS2Tab = 2048;
+
 __global__ void __launch_bounds__(256) k_dft_s2(S2Args a) {
+  __shared__ double2 tab[kS2Tab];
   const int ch = blockIdx.y;
   const int K = a.K[ch];
+  const int N1 = a.N1[ch], N2 = a.N2[ch], nf = a.nf[ch];
+  if (blockIdx.x * 8 > K) return;
+  const bool use_tab = N1 <= kS2Tab;
+  if (use_tab)
+    for (int k = threadIdx.x; k < N1; k += blockDim.x) tab[k] = tw(k, N1);
+  __syncthreads();
   const int q = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (q > K) return;
-  const int N1 = a.N1[ch], N2 = a.N2[ch], nf = a.nf[ch];
   const int q2 = q % N2, q1 = q / N2;
   const double2* __restrict__ T = a.T[ch] + (int64_t)q2 * N1;
   double re = 0.0, im = 0.0;
@@ -143,11 +223,15 @@ __global__ void __launch_bounds__(256) k_dft_s2(S2Args a) {
       im += t.y;
     }
   } else {
+    int idx = (q1 * lane) % N1;
+    const int step = (q1 * 32) % N1;
     for (int l1 = lane; l1 < N1; l1 += 32) {
       const double2 t = T[l1];
-      const double2 w = tw((int)(((long long)q1 * l1) % N1), N1);
+      const double2 w = use_tab ? tab[idx] : tw(idx, N1);
       re = fma(t.x, w.x, fma(-t.y, w.y, re));
       im = fma(t.x, w.y, fma(t.y, w.x, im));
+      idx += step;
+      if (idx >= N1) idx -= N1;
     }
   }
 #pragma unroll
@@ -252,7 +336,10 @@ fk_status dft1d_run(const Dft1Grid* g, int ngrids, int ker, int acc, void* ws, s
   if (!b.ok()) return fail(FK_E_WORKSPACE, "dft1d: workspace too small");
   s2.ker = ker;
   s2.acc = acc;
-  k_reduce_occ<<<dim3((maxG + 255) / 256, ngrids), 256, 0, s>>>(ra);
+  bool vec4 = true;  // int32 partials with G % 4 == 0 in every grid
+  for (int k = 0; k < ngrids; ++k) vec4 = vec4 && g[k].part_i && g[k].G % 4 == 0;
+  if (vec4) k_reduce_occ<4><<<dim3((maxG + 127) / 128, ngrids), 256, 0, s>>>(ra);
+  else k_reduce_occ<1><<<dim3((maxG + 31) / 32, ngrids), 256, 0, s>>>(ra);
   const int t1 = std::min(kMaxN2, (maxN2 + 31) / 32 * 32);
   k_dft_s1<<<dim3(maxN1, ngrids), t1, 0, s>>>(s1);
   k_dft_s2<<<dim3((maxK + 1 + 7) / 8, ngrids), 256, 0, s>>>(s2);

@@ -87,6 +87,7 @@ struct Plan1 {
   int threads = 1024;
   int ctas = 0;
   size_t smem_bytes = 0;
+  double eps = 1e-6;      // the requested accuracy (fp64-mode fixed-point scale)
 };
 
 fk_status make_plan1(int d, int m, double eps, bool need_mu, bool need_r, Plan1* p);

@@ -99,6 +99,7 @@ fk_status make_plan1(int d, int m, double eps, bool need_mu, bool need_r, Plan1*
   Plan1 q;
   q.d = d;
   q.m = m;
+  q.eps = eps;
   const int sms = device_sm_count();
   if (sms <= 0) return fail(FK_E_CUDA, "no CUDA device");
   const int smem_cap = max_smem_optin();

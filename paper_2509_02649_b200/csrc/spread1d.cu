@@ -390,25 +390,84 @@ __global__ void __launch_bounds__(1024, 1) k_spread1d_esx(const XT* __restrict__
 // cells floor(p) - 3 .. floor(p) + 4 relative to the grid centre; transform sinc^8 (deconvolved in dft1d.cu).
 // Moments: the 8 integer weights are closed to 2^40 exactly (partition of unity: mu_0 = n).
 // ------------------------------------------------------------------------------------------
+// The 8 weights are degree-7 polynomials in f (the pieces of the cardinal B-spline M_8, exact
+// rational coefficients, from the uniform Cox-de Boor recursion): taps 0..3 are P_0..P_3 at f and,
+// by symmetry, taps 7..4 are P_0..P_3 at 1 - f (exact in fp64).  Horner from constant memory:
+// 56 DFMA per sample instead of the recursion's ~140 fp64 operations.
+__constant__ double c_bs7[4][8] = {
+    {1.0 / 5040, -1.0 / 720, 1.0 / 240, -1.0 / 144, 1.0 / 144, -1.0 / 240, 1.0 / 720, -1.0 / 5040},
+    {1.0 / 42, -7.0 / 90, 1.0 / 10, -1.0 / 18, 0.0, 1.0 / 60, -1.0 / 120, 1.0 / 720},
+    {397.0 / 1680, -49.0 / 144, 1.0 / 16, 19.0 / 144, -1.0 / 16, -1.0 / 48, 1.0 / 48, -1.0 / 240},
+    {151.0 / 315, 0.0, -1.0 / 3, 0.0, 1.0 / 9, 0.0, -1.0 / 36, 1.0 / 144}};
+
 __device__ __forceinline__ void bs7_weights(double f, double* N) {
-  N[0] = 1.0;
+  const double g = 1.0 - f;
 #pragma unroll
-  for (int j = 1; j <= 7; ++j) {
-    const double invj = 1.0 / j;  // folded at compile time
-    double saved = 0.0;
+  for (int i = 0; i < 4; ++i) {
+    double a = c_bs7[i][7], b = c_bs7[i][7];
 #pragma unroll
-    for (int r = 0; r < j; ++r) {
-      const double temp = N[r] * invj;
-      N[r] = fma((double)(r + 1) - f, temp, saved);  // right[r+1] = r + 1 - f
-      saved = ((double)(j - r - 1) + f) * temp;      // left[j-r]  = f + j - r - 1
+    for (int k = 6; k >= 0; --k) {
+      a = fma(a, f, c_bs7[i][k]);
+      b = fma(b, g, c_bs7[i][k]);
     }
-    N[j] = saved;
+    N[i] = a;
+    N[7 - i] = b;
   }
+}
+
+// round(v) for |v| < 2^51 as a two's-complement int64 by the 1.5 x 2^52 shift: one DFMA (folded
+// with the scaling) and a 64-bit subtract instead of F2I.S64.F64
+__device__ __forceinline__ long long round_fma(double w, double scale) {
+  return __double_as_longlong(fma(w, scale, 6755399441055744.0)) - 0x4338000000000000LL;
+}
+
+// 8 consecutive 64-bit fixed-point taps (int32 pairs) of one sample, branch-free: the 8 low-word
+// atomics, the carries read off their return values with add.cc/addc (2 instructions per tap),
+// then the 8 high-word atomics UNCONDITIONALLY (adding 0 where the high part and carry are 0) and
+// one test of all 8 new high words for the rare drain (|hi| >= 2^29 -> fp64 carry grid).  ncu of
+// the per-tap-branch version (pair_add_n): the BSSY/BRA/BSYNC around each conditional high-word
+// atomic were ~20 % of the fp64 kernel's issued instructions (ptxas turns a predicated atom into a
+// branch), while an always-issued high-word atomic costs only atomic-unit time (5 of 8 taps need
+// it anyway).
+__device__ __forceinline__ void pair_add8(unsigned* __restrict__ lo, int* __restrict__ hi, int c0, const unsigned* l, const int* h,
+                                          double* carry, double hi_unit) {
+  unsigned o[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) o[i] = atomicAdd(lo + c0 + i, l[i]);
+  unsigned any = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    int hc;
+    asm("{\n\t.reg .u32 t;\n\tadd.cc.u32 t, %1, %2;\n\taddc.s32 %0, %3, 0;\n\t}" : "=r"(hc) : "r"(o[i]), "r"(l[i]), "r"(h[i]));
+    const int old = atomicAdd(hi + c0 + i, hc);
+    any |= (unsigned)(old + hc + (1 << 29));  // >= 2^30 iff the new high word is >= 2^29 in magnitude
+  }
+  if (any >= (1u << 30)) {
+#pragma unroll 1
+    for (int i = 0; i < 8; ++i) {
+      const int t = atomicExch(hi + c0 + i, 0);  // drain (the OR test is conservative: any of the 8)
+      if (t) atomicAdd(carry + c0 + i, (double)t * hi_unit);
+    }
+  }
+}
+
+// round(w S) as the two int32 words of a two's-complement int64 (|w S| < 2^51) via the 1.5 x 2^52
+// shift: the low word is the double's low word, the high word its high word minus 0x43380000
+__device__ __forceinline__ void split_fma(double w, double scale, unsigned& l, int& h) {
+  const double d = fma(w, scale, 6755399441055744.0);
+  l = (unsigned)__double2loint(d);
+  h = __double2hiint(d) - 0x43380000;
 }
 
 struct Bs7Args {
   int64_t n, stride, per;
   double a;  // nf / (4L) of the channel's grid (moment grid: nf_mu; rhs grid: nf_r)
+  // fixed-point scale of a weight: moments 2^34 for eps >= 1e-10 (then a tap's value fits the low
+  // word unless it exceeds 1/4: ~5 high-word atomics per sample instead of ~7 at 2^40; rounding
+  // 2^-35 relative per tap, worst case 8 x 2^-35 = 2.3e-10 of mu_0 per mode); the rhs always 2^40
+  // (its l2 norm can be ~sqrt(n) times smaller than sum |Y|: 2^34 gave 2.6e-10 l2 at n = 2e4 and
+  // 2^37 1.6e-10 at n = 10, eps = 1e-11); 2^40 for both below eps = 1e-10
+  double S;
   int nq, G;
   double* part;
   double* carry;
@@ -452,10 +511,24 @@ __global__ void __launch_bounds__(1024, 1) k_spread1d_bs7(const XT* __restrict__
   }
   __syncthreads();
   const double sy = CH == 1 ? ldexp(1.0, E) : 0.0;
-  const double unit = CH == 0 ? 4294967296.0 / kSX : ldexp(4294967296.0, -(E + 20));
+  // rhs: |Y 2^E| < 2^21 on the fast path, so Y 2^E x S 2^-21 keeps a tap below S
+  const double Rm = g.S * (1.0 / 2097152.0);
+  const double unit = CH == 0 ? 4294967296.0 / g.S : 4294967296.0 / (ldexp(1.0, E) * Rm);
+  const long long S64 = (long long)g.S;  // the closure total as two words
+  const unsigned S_lo = (unsigned)S64;
+  const int S_hi = (int)(S64 >> 32);
   bool bad = false;
-  for (int64_t j = beg + threadIdx.x; j < end; j += blockDim.x) {
-    const double p = (double)X[j * g.stride] * g.a;
+  // software pipeline: the next sample's X (and Y) are loaded one iteration ahead
+  int64_t j = beg + threadIdx.x;
+  XT xn = j < end ? X[j * g.stride] : (XT)0;
+  XT yn = (CH == 1 && j < end) ? Y[j] : (XT)0;
+  for (; j < end; j += blockDim.x) {
+    const XT xc = xn, yc = yn;
+    if (j + blockDim.x < end) {
+      xn = X[(j + blockDim.x) * g.stride];
+      if (CH == 1) yn = Y[j + blockDim.x];
+    }
+    const double p = (double)xc * g.a;
     const double fl = floor(p);
     const double f = p - fl;
     const int t0 = (p == p && fabs(p) < 1e9) ? (int)fl + g.nq : -1;
@@ -466,19 +539,28 @@ __global__ void __launch_bounds__(1024, 1) k_spread1d_bs7(const XT* __restrict__
     double wv[8];
     bs7_weights(f, wv);
     if (CH == 0) {
-      long long q[8], sum = 0;
+      unsigned l[8];
+      int h[8];
+      unsigned sl = 0;
+      int sh = 0;
 #pragma unroll
       for (int i = 0; i < 7; ++i) {
-        q[i] = __double2ll_rn(wv[i] * kSX);
-        sum += q[i];
+        split_fma(wv[i], g.S, l[i], h[i]);
+        asm("add.cc.u32 %0, %0, %2;\n\taddc.s32 %1, %1, %3;" : "+r"(sl), "+r"(sh) : "r"(l[i]), "r"(h[i]));
       }
-      q[7] = (long long)kSX - sum;  // partition of unity closed in integers
-      pair_add_n<8>(lo, hi, t0, [&](int i) { return q[i]; }, g.carry, unit);
+      // partition of unity closed in integers: tap 7 = S - sum of taps 0..6 (64-bit, as two words)
+      asm("sub.cc.u32 %0, %2, %3;\n\tsubc.s32 %1, %4, %5;" : "=r"(l[7]), "=r"(h[7]) : "r"(S_lo), "r"(sl), "r"(S_hi), "r"(sh));
+      pair_add8(lo, hi, t0, l, h, g.carry, unit);
     } else {
-      const double y = (double)Y[j];
+      const double y = (double)yc;
       const double ys = y * sy;
       if (fabs(ys) < 2097152.0) {
-        pair_add_n<8>(lo, hi, t0, [&](int i) { return __double2ll_rn(wv[i] * ys * 1048576.0); }, g.carry, unit);
+        const double ysr = ys * Rm;
+        unsigned l[8];
+        int h[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) split_fma(wv[i], ysr, l[i], h[i]);
+        pair_add8(lo, hi, t0, l, h, g.carry, unit);
       } else {  // |Y| outlier or NaN: exact fp64 into the carry grid
 #pragma unroll 1
         for (int i = 0; i < 8; ++i) atomicAdd(g.carry + t0 + i, y * wv[i]);
@@ -488,7 +570,7 @@ __global__ void __launch_bounds__(1024, 1) k_spread1d_bs7(const XT* __restrict__
   if (bad && g.d_status) atomicOr(g.d_status, (int)FK_E_RANGE);
   __syncthreads();
   double* dst = g.part + (int64_t)blockIdx.x * g.G;
-  const double sc = CH == 0 ? 1.0 / kSX : ldexp(1.0, -(E + 20));
+  const double sc = CH == 0 ? 1.0 / g.S : 1.0 / (ldexp(1.0, E) * Rm);
   for (int i = threadIdx.x; i < g.G; i += blockDim.x) dst[i] = ((double)hi[i] * 4294967296.0 + (double)lo[i]) * sc;
 }
 
@@ -631,6 +713,7 @@ static fk_status spread_dispatch(const Plan1& p, const fk_points& Xp, const void
       a.part = (double*)(ch == 0 ? w.partA : w.partB);
       a.carry = ch == 0 ? w.carryA : w.carryB;
       a.d_status = d_status;
+      a.S = (p.eps >= 1e-10 && ch == 0) ? 17179869184.0 : 1099511627776.0;  // 2^34 / 2^40 (Bs7Args)
       const size_t smem = (size_t)gg.G * 8;
       auto k = ch == 0 ? k_spread1d_bs7<XT, 0> : k_spread1d_bs7<XT, 1>;
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
