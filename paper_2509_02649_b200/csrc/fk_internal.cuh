@@ -146,6 +146,12 @@ struct Dft1Grid {
 fk_status dft1d_factor(int nf, int* N1, int* N2);
 size_t dft1d_ws_bytes(const Dft1Grid* g, int ngrids);
 fk_status dft1d_run(const Dft1Grid* g, int ngrids, int ker, int acc, void* ws, size_t ws_bytes, cudaStream_t s);
+
+// hand-written DFT of batch d = 2 fine grids (dft2d.cu): the (2K+1)^2 modes of full-period nf x nf
+// grids non-zero on [off, off + G)^2, deconvolved by phihat (psi-hat(q / nf), q = 0..K) per dimension
+size_t dft2d_ws_bytes(int nf, int G, int K, int batch);
+fk_status dft2d_run(const double* fine, int nf, int off, int G, int K, int batch, const double* phihat, double* out, int acc, void* ws,
+                    size_t ws_bytes, cudaStream_t s);
 fk_status type1_run(const Plan1& p, const fk_points& X, const void* Y, double L, const Type1Out& out, void* ws, size_t ws_bytes,
                     int* d_status, cudaStream_t s);
 

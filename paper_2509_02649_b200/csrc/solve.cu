@@ -16,6 +16,7 @@
 #include <cusolverDn.h>
 
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <map>
 #include <vector>
@@ -1091,10 +1092,52 @@ __global__ void k_pcg_mul(double* __restrict__ G, const double* __restrict__ muh
   if (t < n && sc[4] == 0.0) G[t] *= muhat[t];
 }
 
+// ---- physics-informed penalty in the CG product (readings R3, R12) -----------------
+// mu_pde D^* S D with S Toeplitz: the box's Fourier matrix S[k1][k2] = prod_l boxt_l(k2_l - k1_l)
+// (PIK_BOX) or the collocation moments' T(mu_r)/n_r (PIK_COLLOC).  As a convolution S v =
+// s' * v with s'(j) = prod_l boxt_l(-j_l) (box) / mu_r(j) / n_r (colloc), a Hermitian sequence,
+// so it takes the same half-spectrum -> real grid -> pointwise product -> back route as T(mu).
+__device__ __forceinline__ int mode_lin(const SysArgs& g, int k0, int k1) {  // index of mode (k0, k1) / (k1)
+  const int side = 2 * g.m + 1;
+  return g.d == 2 ? (k0 + g.m) * side + (k1 + g.m) : k1 + g.m;
+}
+
+__global__ void k_pcg_pi_half(SysArgs g, PcgGrid q, double2* __restrict__ H) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)(q.d == 2 ? q.L0 : 1) * q.H1) return;
+  int k0, k1;
+  half_to_k(q, t, k0, k1);
+  const int M2 = 2 * g.m, qs = 4 * g.m + 1;
+  double2 v = make_double2(0.0, 0.0);
+  if (k1 <= M2 && k0 >= -M2 && k0 <= M2) {
+    if (g.kind == FK_PIK_COLLOC) {
+      v = q.d == 2 ? g.mur[(int64_t)(k0 + M2) * qs + (k1 + M2)] : g.mur[k1 + M2];
+      v.x *= g.inv_nr;
+      v.y *= g.inv_nr;
+    } else if (q.d == 2) {
+      v = cmul(g.boxt[0 * qs + (-k0 + M2)], g.boxt[1 * qs + (-k1 + M2)]);
+    } else {
+      v = g.boxt[-k1 + M2];
+    }
+  }
+  H[t] = v;
+}
+
+// Hd = d_k H_k for |k| <= m (the PDE symbol of the iterate), zero elsewhere
+__global__ void k_pcg_dmul(SysArgs g, PcgGrid q, const double2* __restrict__ H, double2* __restrict__ Hd, const double* __restrict__ sc) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)(q.d == 2 ? q.L0 : 1) * q.H1 || sc[4] != 0.0) return;
+  int k0, k1;
+  half_to_k(q, t, k0, k1);
+  double2 v = make_double2(0.0, 0.0);
+  if (k1 <= g.m && k0 >= -g.m && k0 <= g.m) v = cmul(g.dsym[mode_lin(g, k0, k1)], H[t]);
+  Hd[t] = v;
+}
+
 // q = P^* (T theta / n + lambda R theta), theta = P p; alpha = rz / p.q
 __global__ void __launch_bounds__(256) k_pcg_gather(SysArgs g, PcgGrid q, const double2* __restrict__ C, const double* __restrict__ p,
                                                     double* __restrict__ out, double* __restrict__ sc, double* __restrict__ part,
-                                                    unsigned* __restrict__ ticket) {
+                                                    unsigned* __restrict__ ticket, const double2* __restrict__ Cd) {
   if (sc[4] != 0.0) return;
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
   double pq = 0.0;
@@ -1108,11 +1151,18 @@ __global__ void __launch_bounds__(256) k_pcg_gather(SysArgs g, PcgGrid q, const 
       k1 = lin % side - m;
     }
     double2 c;
+    const int64_t at = k1 >= 0 ? (int64_t)(q.d == 2 ? (k0 >= 0 ? k0 : k0 + q.L0) : 0) * q.H1 + k1
+                               : (int64_t)(-k0 >= 0 ? -k0 : -k0 + q.L0) * q.H1 + (-k1);
     if (k1 >= 0) {
-      c = C[(int64_t)(q.d == 2 ? (k0 >= 0 ? k0 : k0 + q.L0) : 0) * q.H1 + k1];
+      c = C[at];
     } else {  // k1 < 0 (d = 2 only): c_k = conj c_{-k}
-      const int n0 = -k0;
-      c = cconj(C[(int64_t)(n0 >= 0 ? n0 : n0 + q.L0) * q.H1 + (-k1)]);
+      c = cconj(C[at]);
+    }
+    if (Cd) {  // + mu_pde conj(d_k) (S D theta)_k (the PI penalty; Cd is Hermitian like C)
+      const double2 e = k1 >= 0 ? Cd[at] : cconj(Cd[at]);
+      const double2 pi = cmul(cconj(g.dsym[mode_lin(g, k0, k1)]), e);
+      c.x += pi.x;
+      c.y += pi.y;
     }
     const double nk2 = (double)k0 * k0 + (double)k1 * k1;
     const double lr = g.lambda * (1.0 + pow(nk2, g.s));
@@ -1266,9 +1316,17 @@ static fk_status lauum(cublasHandle_t bh, const double* X, int64_t ldx, double* 
   return lauum(bh, X + n1 + n1 * ldx, ldx, A + n1 + n1 * lda, lda, n2);
 }
 
+static bool pcg_pi(const SysArgs& g) { return (g.kind == FK_PIK_BOX || g.kind == FK_PIK_COLLOC) && g.mu_pde != 0.0; }
+
 static bool pcg_eligible(const SysArgs& g) {
-  if (g.kind != FK_SOBOLEV || g.d > 2 || g.mu_pde != 0.0) return false;
+  // Sobolev, and the physics-informed estimators (their penalty mu_pde D^* S D joins the product as
+  // a second Toeplitz convolution)
+  if (g.d > 2) return false;
+  if (!(g.kind == FK_SOBOLEV || ((g.kind == FK_PIK_BOX || g.kind == FK_PIK_COLLOC) && g.dsym))) return false;
+  if (g.kind == FK_SOBOLEV && g.mu_pde != 0.0) return false;
   const char* e = getenv("FK_SOLVER");
+  if (pcg_pi(g)) return e && e[0] == 'p';  // PI systems: CG on request (its preconditioner treats the
+                                            // non-diagonal penalty of the high modes by Jacobi only)
   if (e && e[0] == 'd') return false;
   if (e && e[0] == 'p') return true;
   return g.D + 1 > kTilesMaxN;
@@ -1295,7 +1353,7 @@ static void pcg_low_set(const SysArgs& g, double tau, std::vector<int>& low, std
 // predicted ms of fk_solve for g (the cheaper of the two paths; same model as pcg_run's choice)
 static double solve_cost_ms(const SysArgs& g) {
   const double t_dense = 56.0 * std::pow((g.D + 1) / 16642.0, 3.0) + 0.5;
-  if (g.kind != FK_SOBOLEV || g.d > 2 || g.mu_pde != 0.0 || g.D + 1 <= kTilesMaxN) return t_dense;
+  if (g.kind != FK_SOBOLEV || g.d > 2 || g.mu_pde != 0.0 || g.D + 1 <= kTilesMaxN) return t_dense;  // (PI: dense unless forced)
   std::vector<int> low, lowpos;
   pcg_low_set(g, pcg_tau(), low, lowpos);
   return std::min(t_dense, 3.0 * std::pow(low.size() / 2221.0, 1.8) + 2.8);
@@ -1342,6 +1400,10 @@ static fk_status pcg_run(SysArgs g, const double2* r, double* x, int* iters, voi
   double2* H = (double2*)b.take((size_t)nhalf * 16);
   double* G = (double*)b.take((size_t)nreal * 8);
   double* muhat = (double*)b.take((size_t)nreal * 8);
+  const bool pi = pcg_pi(g);
+  double2* Hd = pi ? (double2*)b.take((size_t)nhalf * 16) : nullptr;  // PI penalty: D theta, then S D theta
+  double* Gd = pi ? (double*)b.take((size_t)nreal * 8) : nullptr;
+  double* shat = pi ? (double*)b.take((size_t)nreal * 8) : nullptr;   // mu_pde x real-grid values of s'
   double* sc = (double*)b.take(64);
   double* part = (double*)b.take((size_t)(gP + 64) * 8);
   unsigned* tickets = (unsigned*)b.take(64);
@@ -1354,7 +1416,10 @@ static fk_status pcg_run(SysArgs g, const double2* r, double* x, int* iters, voi
       cusolverDnDpotrf_bufferSize(h, CUBLAS_FILL_MODE_LOWER, Dl, Ainv, (int)lda, &lw_potrf) != CUSOLVER_STATUS_SUCCESS)
     return fail(FK_E_CUDA, "cusolverDnDpotrf_bufferSize failed");
   double* swork = (double*)b.take((size_t)std::max(lw_potrf, 1) * 8);
-  if (!b.ok()) return FK_E_UNSUPPORTED;  // the block does not fit the dense path's matrix slot: dense path
+  if (!b.ok()) {  // the block does not fit the dense path's matrix slot: dense path
+    if (getenv("FK_PCG_DEBUG")) fprintf(stderr, "fk pcg: block Dl %d of %d does not fit the workspace\n", Dl, D);
+    return FK_E_UNSUPPORTED;
+  }
   if (Dl > 0) FK_CUDA_TRY(cudaMemcpyAsync(d_low, low.data(), (size_t)Dl * 4, cudaMemcpyHostToDevice, s));
   FK_CUDA_TRY(cudaMemcpyAsync(d_lowpos, lowpos.data(), (size_t)D * 4, cudaMemcpyHostToDevice, s));
   FK_CUDA_TRY(cudaMemsetAsync(tickets, 0, 64, s));
@@ -1387,6 +1452,12 @@ static fk_status pcg_run(SysArgs g, const double2* r, double* x, int* iters, voi
   k_pcg_mu_half<<<(unsigned)((nhalf + TB - 1) / TB), TB, 0, s>>>(g, q, H);
   FK_TRY(fft_exec_z2d(fz, (cufftDoubleComplex*)H, muhat, fwork, s));
   k_pcg_scale<<<(unsigned)((nreal + TB - 1) / TB), TB, 0, s>>>(muhat, nreal, g.inv_n / (double)nreal);
+  if (pi) {
+    k_pcg_pi_half<<<(unsigned)((nhalf + TB - 1) / TB), TB, 0, s>>>(g, q, Hd);
+    FK_TRY(fft_exec_z2d(fz, (cufftDoubleComplex*)Hd, shat, fwork, s));
+    k_pcg_scale<<<(unsigned)((nreal + TB - 1) / TB), TB, 0, s>>>(shat, nreal, g.mu_pde / (double)nreal);
+    count_launch(2);
+  }
   k_pcg_init<<<gD, TB, 0, s>>>(D, bz, d_low, Dl, x, rv, rl, sc, part, tickets);
   k_pcg_precond<<<gP, TB, 0, s>>>(D, rv, dinv, d_lowpos, d_low, Dl, Ainv, lda, rl, zv, sc, 1, nlow_ctas, part, tickets + 1);
   FK_CUDA_TRY(cudaGetLastError());
@@ -1400,16 +1471,26 @@ static fk_status pcg_run(SysArgs g, const double2* r, double* x, int* iters, voi
       double* p_old = pv[it & 1];
       double* p_new = pv[(it + 1) & 1];
       k_pcg_scatter<<<(unsigned)((nhalf + TB - 1) / TB), TB, 0, s>>>(g, q, zv, p_old, p_new, H, sc);
+      // PI penalty: D theta from the scattered iterate, before the C2R transform below consumes H
+      if (pi) k_pcg_dmul<<<(unsigned)((nhalf + TB - 1) / TB), TB, 0, s>>>(g, q, H, Hd, sc);
       FK_TRY(fft_exec_z2d(fz, (cufftDoubleComplex*)H, G, fwork, s));
       k_pcg_mul<<<(unsigned)((nreal + TB - 1) / TB), TB, 0, s>>>(G, muhat, nreal, sc);
       FK_TRY(fft_exec_d2z(fd, G, (cufftDoubleComplex*)H, fwork, s));
-      k_pcg_gather<<<gD, TB, 0, s>>>(g, q, H, p_new, qv, sc, part, tickets + 2);
+      if (pi) {  // the PI penalty's convolution: values of D theta -> x s' -> back
+        FK_TRY(fft_exec_z2d(fz, (cufftDoubleComplex*)Hd, Gd, fwork, s));
+        k_pcg_mul<<<(unsigned)((nreal + TB - 1) / TB), TB, 0, s>>>(Gd, shat, nreal, sc);
+        FK_TRY(fft_exec_d2z(fd, Gd, (cufftDoubleComplex*)Hd, fwork, s));
+        count_launch(2);
+      }
+      k_pcg_gather<<<gD, TB, 0, s>>>(g, q, H, p_new, qv, sc, part, tickets + 2, Hd);
       k_pcg_update<<<gD, TB, 0, s>>>(D, p_new, qv, d_lowpos, x, rv, rl, sc, tol * tol, part, tickets + 3);
       k_pcg_precond<<<gP, TB, 0, s>>>(D, rv, dinv, d_lowpos, d_low, Dl, Ainv, lda, rl, zv, sc, 0, nlow_ctas, part, tickets + 1);
       count_launch(5);
     }
     FK_CUDA_TRY(cudaMemcpyAsync(hsc, sc, 56, cudaMemcpyDeviceToHost, s));
     FK_CUDA_TRY(cudaStreamSynchronize(s));
+    if (getenv("FK_PCG_DEBUG"))
+      fprintf(stderr, "fk pcg: it %d |r|^2/|b|^2 %.3e (Dl %d of %d, pi %d)\n", (int)hsc[6], hsc[1] / hsc[2], Dl, D, (int)pi);
     if (hsc[4] != 0.0 || !(hsc[1] == hsc[1])) break;  // converged, or NaN (a failed block factor)
   }
   FK_CUDA_TRY(cudaGetLastError());

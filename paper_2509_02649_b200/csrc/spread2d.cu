@@ -873,6 +873,7 @@ struct Ws2 {
   double* tabA = nullptr;
   double* tabB = nullptr;
   void* work = nullptr;
+  size_t work_bytes = 0;
   int* gsync = nullptr;
 };
 
@@ -880,28 +881,23 @@ static fk_status layout2(const Plan2& p, bool mu, bool r, Bump& b, Ws2& w) {
   const size_t esz = p.fp64 ? 8 : 4;
   const int ctas = p.chunks * p.T;
   size_t fw = 0;
-  FftPlan pa, pb;
-  int dA[2] = {p.nfA, p.nfA}, dB[2] = {p.nfB, p.nfB};
   if (mu) {
-    FK_TRY(fft_plan(2, dA, 1, CUFFT_D2Z, &pa));
-    fw = std::max(fw, pa.work);
+    fw = std::max(fw, dft2d_ws_bytes(p.nfA, p.gA.G, 2 * p.m, 1));
     w.partA = b.take((size_t)ctas * p.gA.rows * p.gA.G * esz);
     w.fineA = (double*)b.take((size_t)p.nfA * p.nfA * 8);
-    w.specA = (double2*)b.take((size_t)p.nfA * (p.nfA / 2 + 1) * 16);
     w.tabA = (double*)b.take((size_t)(2 * p.m + 1) * 8);
     w.carryA = (double*)b.take((size_t)p.gA.G * p.gA.G * 8);  // fixed point: drained cells (both paths)
   }
   if (r) {
-    FK_TRY(fft_plan(2, dB, 1, CUFFT_D2Z, &pb));
-    fw = std::max(fw, pb.work);
+    fw = std::max(fw, dft2d_ws_bytes(p.nfB, p.gB.G, p.m, 1));
     w.partB = b.take((size_t)ctas * p.gB.rows * p.gB.G * esz);
     w.fineB = (double*)b.take((size_t)p.nfB * p.nfB * 8);
-    w.specB = (double2*)b.take((size_t)p.nfB * (p.nfB / 2 + 1) * 16);
     w.tabB = (double*)b.take((size_t)(p.m + 1) * 8);
     w.carryB = (double*)b.take((size_t)p.gB.G * p.gB.G * 8);
     if (!p.fp64) w.escale = (int*)b.take((size_t)ctas * 4);
   }
-  w.work = b.take(std::max<size_t>(fw, 256));
+  w.work = b.take(std::max<size_t>(fw, 256));  // the hand-written DFT's scratch (dft2d.cu)
+  w.work_bytes = std::max<size_t>(fw, 256);
   w.gsync = (int*)b.take((size_t)p.chunks * 4 + 16);
   return FK_OK;
 }
@@ -1014,16 +1010,10 @@ fk_status type1_2d_run(int m, double eps, const fk_points& X, const void* Y, dou
                                                              kInvS2, carry, fine, 1, 0,
                                                              (int64_t)g.rows * g.G);
     FK_CUDA_TRY(cudaGetLastError());
-    FftPlan fp;
-    int dims[2] = {nf, nf};
-    FK_TRY(fft_plan(2, dims, 1, CUFFT_D2Z, &fp));
-    FK_TRY(fft_exec_d2z(fp, fine, (cufftDoubleComplex*)spec, w.work, s));
+    count_launch();
+    (void)spec;
     FK_TRY(es_phihat_table(es, nf, K, tab, s));
-    const int64_t nout = (int64_t)(2 * K + 1) * (2 * K + 1);
-    k_deconv2d<<<(unsigned)((nout + TB - 1) / TB), TB, 0, s>>>(spec, nf, K, tab, (double2*)out, acc ? 1 : 0, 1, 0);
-    FK_CUDA_TRY(cudaGetLastError());
-    count_launch(2);
-    return FK_OK;
+    return dft2d_run(fine, nf, off, g.G, K, 1, tab, out, acc ? 1 : 0, w.work, w.work_bytes, s);
   };
   if (mu) FK_TRY(finish(w.partA, nullptr, p.gA, p.offA, p.nfA, w.carryA, w.fineA, w.specA, w.tabA, 2 * m, mu_out));
   if (r) FK_TRY(finish(w.partB, w.escale, p.gB, p.offB, p.nfB, w.carryB, w.fineB, w.specB, w.tabB, m, r_out));
@@ -1094,17 +1084,14 @@ static fk_status make_planx(int d, int m, double eps, int dtype, PlanX* p) {
 
 static fk_status layoutx(const PlanX& p, Bump& b, void** part, double** carry, double** fine, double2** spec, double** tab, void** work,
                          ArgsX** args) {
-  FftPlan fp;
-  int dims[2] = {p.nf, p.nf};
-  FK_TRY(fft_plan(2, dims, p.npairs, CUFFT_D2Z, &fp));
   const size_t esz = p.fp64 ? 8 : 4;
   *part = b.take((size_t)std::max(p.chunks * p.npairs, p.nctas + p.npairs) * p.G * p.G * esz);
   *carry = (double*)b.take((size_t)p.npairs * p.G * p.G * 8);
   *fine = (double*)b.take((size_t)p.npairs * p.nf * p.nf * 8);
-  *spec = (double2*)b.take((size_t)p.npairs * p.nf * (p.nf / 2 + 1) * 16);
+  *spec = nullptr;
   *tab = (double*)b.take((size_t)(p.m + 1) * 8);
   *args = (ArgsX*)b.take(sizeof(ArgsX));
-  *work = b.take(std::max<size_t>(fp.work, 256));
+  *work = b.take(dft2d_ws_bytes(p.nf, p.G, p.m, p.npairs));  // the hand-written DFT's scratch (dft2d.cu)
   return FK_OK;
 }
 
@@ -1285,17 +1272,11 @@ fk_status cross_run(const fk_points& X, double L, int m, double eps, double* G, 
                                                              kInvS2, carry, fine, p.npairs, (int64_t)p.G * p.G,
                                                              (int64_t)p.npairs * p.G * p.G);
   FK_CUDA_TRY(cudaGetLastError());
-  FftPlan fp;
-  int dims[2] = {p.nf, p.nf};
-  FK_TRY(fft_plan(2, dims, p.npairs, CUFFT_D2Z, &fp));
-  FK_TRY(fft_exec_d2z(fp, fine, (cufftDoubleComplex*)spec, work, s));
+  count_launch();
+  (void)spec;
   EsParams es{p.w, p.beta};
   FK_TRY(es_phihat_table(es, p.nf, m, tab, s));
-  const int64_t nout = (int64_t)p.npairs * (2 * m + 1) * (2 * m + 1);
-  k_deconv2d<<<(unsigned)((nout + TB - 1) / TB), TB, 0, s>>>(spec, p.nf, m, tab, (double2*)G, accumulate ? 1 : 0, p.npairs, 0);
-  FK_CUDA_TRY(cudaGetLastError());
-  count_launch(2);
-  return FK_OK;
+  return dft2d_run(fine, p.nf, p.off, p.G, m, p.npairs, tab, G, accumulate ? 1 : 0, work, dft2d_ws_bytes(p.nf, p.G, m, p.npairs), s);
 }
 
 }  // namespace fk
