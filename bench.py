@@ -70,6 +70,8 @@ def parse():
     ap.add_argument("--no-paper-precision", action="store_true",
                     help="skip the fp64-mode (eps = 1e-10, the paper's complex-128 arithmetic) record of the d = 1 configs")
     ap.add_argument("--pp-steps", type=int, default=3)
+    ap.add_argument("--no-other-configs", action="store_true",
+                    help="skip the compact records of C1, C3, C4, C5 appended to the default (C2, one GPU) line")
     return ap.parse_args()
 
 
@@ -419,6 +421,11 @@ def main():
     pp = None
     if d == 1 and eps >= 1e-7 and not args.no_paper_precision and graph is None:
         pp = paper_precision(args, cfg, X, Y, n, n_loc, world, dev, buffers, theta, pik, peaks)
+    others = None
+    if args.config == "c2" and args.n is None and world == 1 and not args.no_other_configs:
+        del X, Y, buffers
+        torch.cuda.empty_cache()
+        others = other_configs(args, dev)
     e2e = None
     if not args.no_e2e and rank == 0:
         e2e = run_e2e_additive(args, cfg, dev, eps) if additive else run_e2e(args, cfg, dev, eps)
@@ -444,6 +451,7 @@ def main():
             "roofline": roof,
             "fit_status_ok": fit_ok,
             "paper_precision": pp,
+            "other_configs": others,
             "hbm_gbs_fit": n_loc * (d + 1) * 4 / (ms_step * 1e-3) / 1e9,
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -528,6 +536,82 @@ def paper_precision(args, cfg, X, Y, n, n_loc, world, dev, buffers, theta, pik, 
                                            "(<= 1e-10 l2 and 1e-9 n per element vs the fp64 direct sums)"},
         "fit_status_ok": int(st.item()) == 0,
     }
+
+
+def other_configs(args, dev):
+    """Compact records of the other BASELINE configurations (C1, C3, C4, C5) at their full n, so the
+    driver's default run sees every configuration: the same fit step (type-1 passes + solve; C1 as
+    one CUDA graph), CUDA events over the timed steps, the spreading kernels' share and their
+    atomic-unit roofline (d >= 2), the fit status word."""
+    import torch
+
+    from datagen.device import gen_dataset
+    from paper_2509_02649_b200 import fk
+    from paper_2509_02649_b200.fit import FitGraph, _moment_buffers, additive_buffers, fit_additive_distributed, fit_distributed
+
+    out = {}
+    for name in ("c1", "c3", "c4", "c5"):
+        cfg = dict(CONFIGS[name])
+        d, m, n, eps = cfg["d"], cfg["m"], cfg["n"], 1e-6
+        additive = cfg["kind"] == "additive"
+        pik = pi_kwargs(cfg)
+        st = torch.zeros(1, dtype=torch.int32, device=dev)
+        Y = torch.empty(n, dtype=torch.float32, device=dev)
+        if additive:
+            Xs = torch.empty((d, n), dtype=torch.float32, device=dev)
+            gen_dataset(Xs, Y, n, d, xkind=cfg["xkind"], ykind=cfg["ykind"], seed=0, stride_n=1, stride_d=n)
+            X = Xs.t()
+            bufs = additive_buffers(d, m, dev)
+            theta = torch.empty(d * (2 * m + 1), dtype=torch.complex128, device=dev)
+        else:
+            X = torch.empty((n,) if d == 1 else (n, d), dtype=torch.float32, device=dev)
+            gen_dataset(X, Y, n, d, xkind=cfg["xkind"], ykind=cfg["ykind"], seed=0)
+            bufs = _moment_buffers(d, m, dev)
+            theta = torch.empty((2 * m + 1) ** d, dtype=torch.complex128, device=dev)
+        graph = FitGraph(X, Y, 1.0, m, cfg["lam"], cfg["kind"], cfg["s"], eps, **pik) if name == "c1" else None
+
+        def step():
+            if graph is not None:
+                graph.replay()
+            elif additive:
+                fit_additive_distributed(X, Y, n, 1.0, m, cfg["lam"], eps, buffers=bufs, theta_out=theta, status=st)
+            else:
+                fit_distributed(X, Y, n, 1.0, m, cfg["lam"], cfg["kind"], cfg["s"], eps, buffers=bufs, theta_out=theta, status=st, **pik)
+
+        steps = 20 if name == "c1" else (3 if name == "c5" else 5)
+        for _ in range(3):
+            step()
+        torch.cuda.synchronize()
+        fk.profile_read()
+        fk.profile_enable(True)
+        s = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for _ in range(steps):
+            step()
+        e1.record(s)
+        torch.cuda.synchronize()
+        fk.profile_enable(False)
+        sp_ms, _, _ = fk.profile_read()
+        ms = e0.elapsed_time(e1) / steps
+        if graph is not None:
+            graph.check()
+        rec = {"workload": cfg["desc"], "value": n / (ms * 1e-3), "unit": "samples/s", "ms_per_step": ms, "steps": steps,
+               "fit_status_ok": int(st.item()) == 0, "cuda_graph": graph is not None}
+        if d >= 2:
+            w = es_width(eps)
+            atoms = n * (d * (d - 1) // 2 * cross_width(eps, m) ** 2 + d * 8) if additive else n * 2 * w * w
+            sp = sp_ms / steps
+            rec["roofline"] = {"bound": "alu", "unit": "Gatomic/s", "achieved": atoms / (sp * 1e-3) / 1e9,
+                               "peak": ATOMS_CFREE_PEAK / 1e9, "frac": atoms / (sp * 1e-3) / ATOMS_CFREE_PEAK,
+                               "frac_of_random_atoms": atoms / (sp * 1e-3) / ATOMS_RANDOM_PEAK,
+                               "spread_share_of_step": sp / ms}
+        out[name] = rec
+        del X, Y, bufs, theta, graph
+        if additive:
+            del Xs
+        torch.cuda.empty_cache()
+    return out
 
 
 def run_e2e_additive(args, cfg, dev, eps):

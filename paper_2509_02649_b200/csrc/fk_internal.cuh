@@ -243,6 +243,41 @@ __device__ __forceinline__ void pair_add_n(unsigned* __restrict__ lo, int* __res
   }
 }
 
+// N consecutive cells c0.. of one row, values round(wy x[b]) (|wy x[b]| < 2^51), branch-free: the
+// 1.5 x 2^52 shift gives both int32 words of each value, then the N low-word atomics, the carries by
+// add.cc/addc, the N high-word atomics unconditionally (ptxas turns any conditional atomic into
+// BSSY/BRA/BSYNC -- 3 issue slots per tap -- and in the 2-D fp64 kernels nearly every tap carries
+// anyway: sum_ab w_a w_b ~ (W/2)^2 low-word wraps per sample), and one drain test per row.
+template <int N>
+__device__ __forceinline__ void pair_add_row(unsigned* __restrict__ lo, int* __restrict__ hi, int c0, double wy, const double* x,
+                                             double* carry, double hi_unit) {
+  unsigned l[N], o[N];
+  int h[N];
+#pragma unroll
+  for (int b = 0; b < N; ++b) {
+    const double d = fma(wy, x[b], 6755399441055744.0);
+    l[b] = (unsigned)__double2loint(d);
+    h[b] = __double2hiint(d) - 0x43380000;
+  }
+#pragma unroll
+  for (int b = 0; b < N; ++b) o[b] = atomicAdd(lo + c0 + b, l[b]);
+  unsigned any = 0;
+#pragma unroll
+  for (int b = 0; b < N; ++b) {
+    int hc;
+    asm("{\n\t.reg .u32 t;\n\tadd.cc.u32 t, %1, %2;\n\taddc.s32 %0, %3, 0;\n\t}" : "=r"(hc) : "r"(o[b]), "r"(l[b]), "r"(h[b]));
+    const int old = atomicAdd(hi + c0 + b, hc);
+    any |= (unsigned)(old + hc + (1 << 29));
+  }
+  if (any >= (1u << 30)) {
+#pragma unroll 1
+    for (int b = 0; b < N; ++b) {
+      const int t = atomicExch(hi + c0 + b, 0);
+      if (t) atomicAdd(carry + c0 + b, (double)t * hi_unit);
+    }
+  }
+}
+
 // exact 2^e for |e| < 1000 without the libm ldexp call
 __device__ inline double pow2(int e) { return __longlong_as_double((long long)(1023 + e) << 52); }
 

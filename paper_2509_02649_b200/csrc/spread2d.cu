@@ -467,13 +467,8 @@ __global__ void __launch_bounds__(1024, 1) k_spread2d_f64(const XT* __restrict__
     }
     if (MU && lrA >= rA0 && lrA < rA0 + g.gA.R) {
       es_taps2_horner<W>(f0, d00, f1, d01, py, px);
-#pragma unroll
-      for (int a = 0; a < W; ++a) {
-        const double wy = py[a] * kSX;
-        const int rowc = (lrA - rA0 + a) * g.gA.G + lcA;
-#pragma unroll
-        for (int b = 0; b < W; ++b) pair_add(Alo, Ahi, rowc + b, __double2ll_rn(wy * px[b]), carA, unitA);
-      }
+#pragma unroll 1
+      for (int a = 0; a < W; ++a) pair_add_row<W>(Alo, Ahi, (lrA - rA0 + a) * g.gA.G + lcA, py[a] * kSX, px, carA, unitA);
     }
     if (R) {
       const double h0 = 0.5 * p0, h1 = 0.5 * p1;
@@ -487,13 +482,8 @@ __global__ void __launch_bounds__(1024, 1) k_spread2d_f64(const XT* __restrict__
         const double y = (double)Y[j];
         const double ys = y * sy;
         if (fabs(ys) < 2097152.0) {
-#pragma unroll
-          for (int a = 0; a < W; ++a) {
-            const double wy = py[a] * ys * 1048576.0;
-            const int rowc = (lrB - rB0 + a) * g.gB.G + lcB;
-#pragma unroll
-            for (int b = 0; b < W; ++b) pair_add(Blo, Bhi, rowc + b, __double2ll_rn(wy * px[b]), carB, unitB);
-          }
+#pragma unroll 1
+          for (int a = 0; a < W; ++a) pair_add_row<W>(Blo, Bhi, (lrB - rB0 + a) * g.gB.G + lcB, py[a] * ys * 1048576.0, px, carB, unitB);
         } else {  // |Y| outlier or NaN: exact fp64 into the carry grid
           for (int a = 0; a < W; ++a)
             for (int b = 0; b < W; ++b) atomicAdd(carB + (lrB - rB0 + a) * g.gB.G + lcB + b, y * py[a] * px[b]);
@@ -663,13 +653,8 @@ __global__ void __launch_bounds__(1024, 1) k_cross2d_f64(const XT* __restrict__ 
       unsigned* lo = smxp + 2 * q * cells;
       int* hi = (int*)(lo + cells);
       double* carry = g.carry + (int64_t)(p0 + q) * cells;
-#pragma unroll
-      for (int a = 0; a < W; ++a) {
-        const double wy = py[a] * kSX;
-        const int rowc = (lr + a) * g.G + lc;
-#pragma unroll
-        for (int b = 0; b < W; ++b) pair_add(lo, hi, rowc + b, __double2ll_rn(wy * px[b]), carry, unit);
-      }
+#pragma unroll 1
+      for (int a = 0; a < W; ++a) pair_add_row<W>(lo, hi, (lr + a) * g.G + lc, py[a] * kSX, px, carry, unit);
     }
   }
   if (bad && g.d_status) atomicOr(g.d_status, (int)FK_E_RANGE);
