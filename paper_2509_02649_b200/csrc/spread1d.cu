@@ -561,8 +561,9 @@ __global__ void __launch_bounds__(1024, 1) k_spread1d_bs7(const XT* __restrict__
 #pragma unroll
         for (int i = 0; i < 8; ++i) split_fma(wv[i], ysr, l[i], h[i]);
         pair_add8(lo, hi, t0, l, h, g.carry, unit);
-      } else {  // |Y| outlier or NaN: exact fp64 into the carry grid
-#pragma unroll 1
+      } else {  // |Y| outlier or NaN: exact fp64 into the carry grid (unrolled: a runtime index
+                // would put wv in local memory, stored on every sample -- ncu showed the STLs)
+#pragma unroll
         for (int i = 0; i < 8; ++i) atomicAdd(g.carry + t0 + i, y * wv[i]);
       }
     }
