@@ -235,6 +235,15 @@ def es_width(eps):
     return min(16, max(9, int(math.ceil(math.log10(1.0 / eps))) + 2))
 
 
+def spread2d_width(eps):
+    """Taps per dimension of the d = 2 type-1 pass (csrc/spread2d.cu make_plan2): sigma = 2, or
+    sigma = 4 with one tap fewer on the fp32 path when FK_SPREAD2D_SIGMA=4 (measurement)."""
+    w = es_width(eps)
+    if eps >= 1e-7 and os.environ.get("FK_SPREAD2D_SIGMA", "2") == "4":
+        return max(5, w - 1)
+    return w
+
+
 def cross_width(eps, m):
     """Taps per dimension of the cross-moment window: sigma = 4 with one tap fewer when one pair
     grid fits a CTA (csrc/spread2d.cu make_planx, fp32 path only), else the sigma = 2 width."""
@@ -396,7 +405,7 @@ def main():
         # npairs w^2 + 2 d x 4 per sample for the additive model); peak = the measured random ATOMS rate
         # fp64 mode: 64-bit fixed point as int32 pairs, up to 2 ATOMS per tap (pair_add: low word, and
         # the high word when the tap's high part or the carry is non-zero -- counted as 2, an upper bound)
-        w = es_width(eps)
+        w = spread2d_width(eps)
         per_tap = 2 if eps < 1e-7 else 1
         d1 = 8 if eps >= 1e-7 else 2 * 8 * 2  # per-feature 1-D pass: 2 channels x 4 taps (fp32); 2 x 8 septic taps x 2 words
         if additive:
@@ -599,7 +608,7 @@ def other_configs(args, dev):
         rec = {"workload": cfg["desc"], "value": n / (ms * 1e-3), "unit": "samples/s", "ms_per_step": ms, "steps": steps,
                "fit_status_ok": int(st.item()) == 0, "cuda_graph": graph is not None}
         if d >= 2:
-            w = es_width(eps)
+            w = spread2d_width(eps)
             atoms = n * (d * (d - 1) // 2 * cross_width(eps, m) ** 2 + d * 8) if additive else n * 2 * w * w
             sp = sp_ms / steps
             rec["roofline"] = {"bound": "alu", "unit": "Gatomic/s", "achieved": atoms / (sp * 1e-3) / 1e9,

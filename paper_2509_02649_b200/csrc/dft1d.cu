@@ -267,6 +267,78 @@ __global__ void __launch_bounds__(256) k_dft_s2(S2Args a) {
   }
 }
 
+// ---- type-2 direction (predict): the occupied cells of the real fine grid from its half spectrum
+// out[l] = H_0 + 2 Re sum_{k=1..m} H_k w^(-k l) (cuFFT Z2D semantics, H_0 real), l in [off, off+G),
+// with the same factorisation (k = k2 + N2 k1, l = l1 + N1 l2; w^(-1) = exp(+2 pi i / nf)):
+//   U[k2][l1] = w_nf^(-k2 l1) sum_k1 H'_(k2 + N2 k1) w_N1^(-k1 l1)      (H'_0 = H_0 / 2)
+//   out[l1 + N1 l2] = 2 Re sum_k2 U[k2][l1] w_N2^(-k2 l2)
+struct I1Args {
+  const double2* H;  // nfeat half spectra, row stride hstride
+  int64_t hstride;
+  int nf, N1, N2, m, off, G, K2;  // K2 = min(N2, m + 1) k2 values carry a coefficient
+  double2* U;        // [feat][k2][l1]
+  double* out;       // [feat][nf] (only [off, off + G) written)
+  int64_t ostride;
+};
+
+__global__ void __launch_bounds__(256) k_idft_s1(I1Args a) {
+  const int f = blockIdx.y;
+  const int l1 = blockIdx.x;
+  const double2* __restrict__ H = a.H + f * a.hstride;
+  for (int k2 = threadIdx.x; k2 < a.K2; k2 += blockDim.x) {
+    double re = 0.0, im = 0.0;
+    for (int k1 = 0, k = k2; k <= a.m; ++k1, k += a.N2) {
+      double2 h = H[k];
+      if (k == 0) h.x *= 0.5;
+      const double2 t = tw((k1 * l1) % a.N1, a.N1);  // w^(+) -> conjugate below
+      re += h.x * t.x + h.y * t.y;                   // h * conj(t)
+      im += h.y * t.x - h.x * t.y;
+    }
+    const double2 w = tw((int)(((long long)k2 * l1) % a.nf), a.nf);
+    a.U[((int64_t)f * a.K2 + k2) * a.N1 + l1] = make_double2(re * w.x + im * w.y, im * w.x - re * w.y);  // x conj(w)
+  }
+}
+
+__global__ void __launch_bounds__(256) k_idft_s2(I1Args a) {
+  __shared__ double2 tab[kMaxN2];
+  __shared__ double2 ucol[kMaxN2];
+  const int f = blockIdx.y;
+  const int l1 = blockIdx.x;
+  const int N1 = a.N1, N2 = a.N2;
+  for (int k = threadIdx.x; k < N2; k += blockDim.x) {
+    const double2 t = tw(k, N2);
+    tab[k] = make_double2(t.x, -t.y);  // w_N2^(-k)
+    ucol[k] = k < a.K2 ? a.U[((int64_t)f * a.K2 + k) * N1 + l1] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  const int lo2 = max(0, (a.off - l1 + N1 - 1) / N1);
+  const int hi2 = min(N2 - 1, (a.off + a.G - 1 - l1) / N1);
+  for (int l2 = lo2 + threadIdx.x; l2 <= hi2; l2 += blockDim.x) {
+    // four chains over k2 = 4 j + u, twiddles w_N2^(-k2 l2) advanced by rotation (exact start)
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    double2 t[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) t[u] = tab[(u * l2) % N2];
+    const double2 r4 = tab[(4 * l2) % N2];
+    int k2 = 0;
+    for (; k2 + 3 < a.K2; k2 += 4) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double2 c = ucol[k2 + u];
+        acc[u] += c.x * t[u].x - c.y * t[u].y;  // Re(c t)
+        const double tx = t[u].x * r4.x - t[u].y * r4.y;
+        t[u].y = fma(t[u].x, r4.y, t[u].y * r4.x);
+        t[u].x = tx;
+      }
+    }
+    for (int u = 0; k2 < a.K2; ++k2, ++u) {
+      const double2 c = ucol[k2];
+      acc[u] += c.x * t[u].x - c.y * t[u].y;
+    }
+    a.out[f * a.ostride + l1 + (int64_t)N1 * l2] = 2.0 * ((acc[0] + acc[1]) + (acc[2] + acc[3]));
+  }
+}
+
 }  // namespace
 
 // N2: the divisor of nf closest to sqrt(nf) with N2 <= 512 and nf / N2 <= 8192
@@ -345,6 +417,41 @@ fk_status dft1d_run(const Dft1Grid* g, int ngrids, int ker, int acc, void* ws, s
   k_dft_s2<<<dim3((maxK + 1 + 7) / 8, ngrids), 256, 0, s>>>(s2);
   FK_CUDA_TRY(cudaGetLastError());
   count_launch(3);
+  return FK_OK;
+}
+
+}  // namespace fk
+
+namespace fk {
+
+size_t idft1d_ws_bytes(int nf, int m, int nfeat) {
+  int N1 = 0, N2 = 0;
+  if (dft1d_factor(nf, &N1, &N2) != FK_OK) return 0;
+  return (size_t)nfeat * std::min(N2, m + 1) * N1 * 16 + 256;
+}
+
+fk_status idft1d_run(const double2* H, int64_t hstride, int nfeat, int nf, int m, int off, int G, double* out, int64_t ostride, void* ws,
+                     size_t ws_bytes, cudaStream_t s) {
+  int N1 = 0, N2 = 0;
+  FK_TRY(dft1d_factor(nf, &N1, &N2));
+  if (ws_bytes < idft1d_ws_bytes(nf, m, nfeat)) return fail(FK_E_WORKSPACE, "idft1d: workspace too small");
+  I1Args a{};
+  a.H = H;
+  a.hstride = hstride;
+  a.nf = nf;
+  a.N1 = N1;
+  a.N2 = N2;
+  a.m = m;
+  a.off = off;
+  a.G = G;
+  a.K2 = std::min(N2, m + 1);
+  a.U = (double2*)ws;
+  a.out = out;
+  a.ostride = ostride;
+  k_idft_s1<<<dim3(N1, nfeat), 256, 0, s>>>(a);
+  k_idft_s2<<<dim3(N1, nfeat), 256, 0, s>>>(a);
+  FK_CUDA_TRY(cudaGetLastError());
+  count_launch(2);
   return FK_OK;
 }
 

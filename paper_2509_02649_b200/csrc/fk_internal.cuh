@@ -146,6 +146,11 @@ struct Dft1Grid {
 fk_status dft1d_factor(int nf, int* N1, int* N2);
 size_t dft1d_ws_bytes(const Dft1Grid* g, int ngrids);
 fk_status dft1d_run(const Dft1Grid* g, int ngrids, int ker, int acc, void* ws, size_t ws_bytes, cudaStream_t s);
+// the type-2 direction (predict, dft1d.cu): cells [off, off + G) of nfeat real grids from their half
+// spectra H (coefficients k = 0..m; Z2D semantics), no cuFFT
+size_t idft1d_ws_bytes(int nf, int m, int nfeat);
+fk_status idft1d_run(const double2* H, int64_t hstride, int nfeat, int nf, int m, int off, int G, double* out, int64_t ostride, void* ws,
+                     size_t ws_bytes, cudaStream_t s);
 
 // hand-written DFT of batch d = 2 fine grids (dft2d.cu): the (2K+1)^2 modes of full-period nf x nf
 // grids non-zero on [off, off + G)^2, deconvolved by phihat (psi-hat(q / nf), q = 0..K) per dimension

@@ -502,6 +502,7 @@ struct PredWs {
   double* grid;
   double* tab;
   void* work;
+  size_t work_bytes;
 };
 
 static bool is2d(const PredPlan& p) { return !p.additive && p.d == 2; }
@@ -513,13 +514,15 @@ static fk_status pred_layout(const PredPlan& p, Bump& b, PredWs& w) {
     FK_TRY(fft_plan(2, dims, 1, CUFFT_Z2D, &fp));
     w.H = (double2*)b.take((size_t)p.nf * (p.nf / 2 + 1) * 16);
     w.grid = (double*)b.take((size_t)p.nf * p.nf * 8);
-  } else {
-    FK_TRY(fft_plan(1, &p.nf, p.nfeat, CUFFT_Z2D, &fp));
+  } else {  // d = 1 / additive: the hand-written inverse DFT (dft1d.cu) fills the occupied cells
+    fp.work = idft1d_ws_bytes(p.nf, p.m, p.nfeat);
+    if (fp.work == 0) return fail(FK_E_UNSUPPORTED, "fk_predict_type2: no DFT factorisation of the fine grid");
     w.H = (double2*)b.take((size_t)p.nfeat * (p.nf / 2 + 1) * 16);
     w.grid = (double*)b.take((size_t)p.nfeat * p.nf * 8);
   }
   w.tab = (double*)b.take((size_t)(p.m + 1) * 8);
   w.work = b.take(std::max<size_t>(fp.work, 256));
+  w.work_bytes = std::max<size_t>(fp.work, 256);
   return FK_OK;
 }
 
@@ -711,9 +714,7 @@ fk_status predict_run(const double* theta, int d, int m, double L, int additive,
   k_pred_prep<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>((const double2*)theta, p.nfeat, m, p.nf, p.ker, w.tab, w.H);
   FK_CUDA_TRY(cudaGetLastError());
   count_launch();
-  FftPlan fp;
-  FK_TRY(fft_plan(1, &p.nf, p.nfeat, CUFFT_Z2D, &fp));
-  FK_TRY(fft_exec_z2d(fp, (cufftDoubleComplex*)w.H, w.grid, w.work, s));
+  FK_TRY(idft1d_run(w.H, p.nf / 2 + 1, p.nfeat, p.nf, m, p.g.off, p.g.G, w.grid, p.nf, w.work, w.work_bytes, s));
   if (Xq.n == 0) return FK_OK;
   if (Xq.dtype == FK_F32) return gather<float>(p, Xq, L, w, out, d_status, s);
   return gather<double>(p, Xq, L, w, out, d_status, s);

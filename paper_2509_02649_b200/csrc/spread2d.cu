@@ -814,8 +814,18 @@ static fk_status make_plan2(int m, double eps, bool mu, bool r, int dtype, Plan2
   q.fp64 = eps < 1e-7 || dtype == FK_F64;
   q.w = es_width(eps, q.fp64);
   q.beta = 2.30 * q.w;
+  // sigma = 2.  sigma = 4 (as the cross moments) saves a tap per dimension (w = 6 at eps = 1e-6:
+  // 2 x 36 instead of 2 x 49 atomics per sample) but quadruples the grid, so more row tiles each
+  // re-scan the chunk: measured C3 82.3 vs 54.8 ms, C4 5.91 vs 5.95 ms per fit -- not the default.
+  // FK_SPREAD2D_SIGMA=4 selects it (fp32 path; measurement).
+  int sigma = 2;
+  if (const char* e = getenv("FK_SPREAD2D_SIGMA")) sigma = (atoi(e) == 4 && !q.fp64) ? 4 : 2;
+  if (sigma == 4) {
+    q.w = std::max(5, q.w - 1);
+    q.beta = 0.97 * 3.14159265358979 * (1.0 - 1.0 / (2.0 * sigma)) * q.w;
+  }
   // tiles (nf/2 + w + 4 cells from nf/4 - w/2 - 2) must not wrap: nfB = nfA/2 >= 2w + 8
-  q.nfA = fft_friendly(std::max(2 * (4 * m + 1), 4 * q.w + 16));
+  q.nfA = fft_friendly(std::max(sigma * (4 * m + 1), 4 * q.w + 16));
   q.nfB = q.nfA / 2;
   int GA, GB;
   es_geo(q.nfA, q.w, &q.offA, &q.KA, &GA);
