@@ -4,7 +4,7 @@ on their own), each against its roofline and beside the CPU oracle:
 
   A12 predict (type-2 gather)     queries/s and GB/s of Xq in + f out (8 B/query fp32) vs HBM peak
   A10/A11 solve                   GFLOP/s of the real Cholesky (D^3/3) vs the fp64 FMA peak
-  A7/A8 FFT + deconvolution       post-spread time of fk_rhs_type1 (reduce + cuFFT + deconv)
+  A7/A8 DFT + deconvolution       post-spread time of fk_rhs_type1 (reduce + hand-written DFT + deconv)
   NEXT-1 lambda path              fk_solve_path over 300 lambdas vs 300 fk_solve calls
 
     python bench_rows.py [--rows predict,solve,post,path]     -> one JSON line per measurement

@@ -722,36 +722,6 @@ __global__ void k_reduce_slots(const int* __restrict__ part, const ArgsX* __rest
   fine[t] = s;
 }
 
-// out[q0][q1] = (-1)^(q0+q1) F[q0 mod nf][q1 mod nf] / (psi-hat(q0) psi-hat(q1)), |q| <= K,
-// F the D2Z output [nf][nf/2+1] (Hermitian: F[a][-b] = conj F[-a][b]).
-__global__ void k_deconv2d(const double2* __restrict__ F, int nf, int K, const double* __restrict__ tab, double2* __restrict__ out,
-                           int acc, int batch, int flip1) {
-  const int side = 2 * K + 1;
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= (int64_t)side * side * batch) return;
-  const int bi = (int)(t / ((int64_t)side * side));
-  const int rem = (int)(t % ((int64_t)side * side));
-  const int q0 = rem / side - K, q1 = rem % side - K;
-  const int half = nf / 2 + 1;
-  const double2* Fb = F + (int64_t)bi * nf * half;
-  double2 v;
-  if (q1 >= 0) {
-    v = Fb[(int64_t)((q0 % nf + nf) % nf) * half + q1];
-  } else {
-    v = Fb[(int64_t)(((-q0) % nf + nf) % nf) * half + (-q1)];
-    v.y = -v.y;
-  }
-  const double sc = (((q0 + q1) & 1) ? -1.0 : 1.0) / (tab[q0 < 0 ? -q0 : q0] * tab[q1 < 0 ? -q1 : q1]);
-  v.x *= sc;
-  v.y *= sc;
-  (void)flip1;
-  if (acc) {
-    out[t].x += v.x;
-    out[t].y += v.y;
-  } else {
-    out[t] = v;
-  }
-}
 
 }  // namespace
 
@@ -863,8 +833,6 @@ struct Ws2 {
   double* carryB = nullptr;
   double* fineA = nullptr;
   double* fineB = nullptr;
-  double2* specA = nullptr;
-  double2* specB = nullptr;
   double* tabA = nullptr;
   double* tabB = nullptr;
   void* work = nullptr;
@@ -998,7 +966,7 @@ fk_status type1_2d_run(int m, double eps, const fk_points& X, const void* Y, dou
   const bool fixed = !p.fp64;
   EsParams es{p.w, p.beta};
   const int TB = 256;
-  auto finish = [&](void* part, int* esc, const Tile& g, int off, int nf, double* carry, double* fine, double2* spec, double* tab,
+  auto finish = [&](void* part, int* esc, const Tile& g, int off, int nf, double* carry, double* fine, double* tab,
                     int K, double* out) -> fk_status {
     const int64_t tot = (int64_t)nf * nf;
     k_reduce2d<<<(unsigned)((tot + TB - 1) / TB), TB, 0, s>>>(part, fixed ? 1 : 0, esc, p.chunks, p.T, g.R, g.rows, g.G, off, nf,
@@ -1006,12 +974,11 @@ fk_status type1_2d_run(int m, double eps, const fk_points& X, const void* Y, dou
                                                              (int64_t)g.rows * g.G);
     FK_CUDA_TRY(cudaGetLastError());
     count_launch();
-    (void)spec;
     FK_TRY(es_phihat_table(es, nf, K, tab, s));
     return dft2d_run(fine, nf, off, g.G, K, 1, tab, out, acc ? 1 : 0, w.work, w.work_bytes, s);
   };
-  if (mu) FK_TRY(finish(w.partA, nullptr, p.gA, p.offA, p.nfA, w.carryA, w.fineA, w.specA, w.tabA, 2 * m, mu_out));
-  if (r) FK_TRY(finish(w.partB, w.escale, p.gB, p.offB, p.nfB, w.carryB, w.fineB, w.specB, w.tabB, m, r_out));
+  if (mu) FK_TRY(finish(w.partA, nullptr, p.gA, p.offA, p.nfA, w.carryA, w.fineA, w.tabA, 2 * m, mu_out));
+  if (r) FK_TRY(finish(w.partB, w.escale, p.gB, p.offB, p.nfB, w.carryB, w.fineB, w.tabB, m, r_out));
   return FK_OK;
 }
 
