@@ -72,7 +72,8 @@ int main(int argc, char** argv) {
     cudaMemcpy(t.data(), trace, t.size() * 8, cudaMemcpyDeviceToHost);
     FILE* f = fopen(tr, "w");
     unsigned long long base = ~0ULL;
-    for (int k = 0; k < ntiles; ++k) base = std::min(base, t[6 * k]);
+    for (int k = 0; k < ntiles; ++k)
+      if (t[6 * k]) base = std::min(base, t[6 * k]);  // slots past the last ticket stay 0
     for (int k = 0; k < ntiles; ++k)
       fprintf(f, "%d %llu %llu %llu %llu %llu %llu\n", k, t[6 * k] - base, t[6 * k + 1] - base, t[6 * k + 2] - base,
               t[6 * k + 3] - base, t[6 * k + 4] - base, t[6 * k + 5]);
