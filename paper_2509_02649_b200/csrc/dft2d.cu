@@ -12,6 +12,13 @@
 // One tiled kernel does both stages: C[b][i][j] = sum_k D[b][i][k] w^(((j + jbase) (off + k)) mod nf)
 // with 32 x 32 output tiles, 2 x 2 per thread, 32-wide k chunks staged in shared memory (D and the
 // twiddles from a per-call w^t table).  C3: ~8e7 fp64 multiply-adds; C5: ~7e8 over the 45 pairs.
+//
+// The type-2 direction (idft2d_run, the d = 2 predict grid, round 2: replaces cuFFT Z2D) is the same
+// two products with conjugate twiddles, evaluated only on the occupied block:
+//   P[k1][r]  = sum_{k0=-m..m} c_k1 Hf[k0][k1] w^(-k0 (off + r)),         k1 = 0..m
+//   g[r][c]   = Re sum_{k1=0..m} P[k1][r] w^(-k1 (off + c))
+// (Hf Hermitian, c_0 = 1, c_k1 = 2 folded into the input), i.e. exactly the real inverse transform
+// of the half spectrum on the cells the gather reads.
 #include <cmath>
 
 #include "fk_internal.cuh"
@@ -21,12 +28,12 @@ namespace {
 
 constexpr int TT = 32;  // output tile (i and j) and k chunk
 
-__global__ void k_twtab(int nf, double2* tab) {
+__global__ void k_twtab(int nf, double2* tab, double sign) {  // tab[t] = exp(sign 2 pi i t / nf)
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nf) return;
   double s, c;
   sincospi(2.0 * (double)t / (double)nf, &s, &c);
-  tab[t] = make_double2(c, -s);
+  tab[t] = make_double2(c, sign * s);
 }
 
 struct TwArgs {
@@ -36,11 +43,11 @@ struct TwArgs {
   int jbase;                  // frequency of column j: q = j + jbase
   int off, nf;                // fine-grid index of k: off + k
   const double2* tab;         // w^t, t = 0..nf-1
-  double2* C;
+  void* C;                    // double2, or double (the real part) when REALOUT
   int64_t c_b, c_i, c_j;      // element strides of C
 };
 
-template <bool CPLX>
+template <bool CPLX, bool REALOUT = false>
 __global__ void __launch_bounds__(256) k_twdft(TwArgs a) {
   __shared__ double2 Ds[TT][TT + 1];  // [i][k]
   __shared__ double2 Ws[TT][TT + 1];  // [k][j]
@@ -107,7 +114,11 @@ __global__ void __launch_bounds__(256) k_twdft(TwArgs a) {
 #pragma unroll
     for (int v = 0; v < 2; ++v) {
       const int gi = i0 + ty + 16 * u, gj = j0 + tx + 16 * v;
-      if (gi < a.M && gj < a.N) a.C[b * a.c_b + gi * a.c_i + gj * a.c_j] = acc[u][v];
+      if (gi < a.M && gj < a.N) {
+        const int64_t o = b * a.c_b + gi * a.c_i + gj * a.c_j;
+        if (REALOUT) reinterpret_cast<double*>(a.C)[o] = acc[u][v].x;
+        else reinterpret_cast<double2*>(a.C)[o] = acc[u][v];
+      }
     }
 }
 
@@ -161,7 +172,7 @@ fk_status dft2d_run(const double* fine, int nf, int off, int G, int K, int batch
   double2* H = (double2*)bp.take((size_t)batch * G * (2 * K + 1) * 16);
   double2* FT = (double2*)bp.take((size_t)batch * (2 * K + 1) * (K + 1) * 16);
   if (!bp.ok()) return fail(FK_E_WORKSPACE, "dft2d: workspace too small");
-  k_twtab<<<(nf + 255) / 256, 256, 0, s>>>(nf, tab);
+  k_twtab<<<(nf + 255) / 256, 256, 0, s>>>(nf, tab, -1.0);
   const int side = 2 * K + 1;
   // stage A: H[b][r][j] = sum_c fine[b][off + r][off + c] w^((j - K)(off + c))
   TwArgs A{};
@@ -203,6 +214,64 @@ fk_status dft2d_run(const double* fine, int nf, int off, int G, int K, int batch
   k_deconv2d_t<<<(unsigned)((nout + 255) / 256), 256, 0, s>>>(FT, K, phihat, (double2*)out, acc, batch);
   FK_CUDA_TRY(cudaGetLastError());
   count_launch(4);
+  return FK_OK;
+}
+
+size_t idft2d_ws_bytes(int nf, int G, int m) {
+  Bump b(nullptr, 0);
+  b.take((size_t)nf * 16);             // conjugate twiddle table
+  b.take((size_t)(m + 1) * G * 16);    // P
+  return b.used + 256;
+}
+
+// Hc: (2m+1) x (m+1) complex, Hc[(k0 + m)(m+1) + k1] = c_k1 Hf[k0][k1] (deconvolved, Hermitian part);
+// grid: row-major with leading dimension ldg, cells [off, off + G)^2 written (the rest untouched)
+fk_status idft2d_run(const double2* Hc, int m, int nf, int off, int G, double* grid, int64_t ldg, void* ws, size_t ws_bytes, cudaStream_t s) {
+  if (off < 0 || off + G > nf) return fail(FK_E_ARG, "idft2d: occupied block outside the grid");
+  if (nf >= 46341) return fail(FK_E_UNSUPPORTED, "idft2d: fine grid too large (nf >= 46341)");
+  Bump bp(ws, ws_bytes);
+  double2* tab = (double2*)bp.take((size_t)nf * 16);
+  double2* P = (double2*)bp.take((size_t)(m + 1) * G * 16);
+  if (!bp.ok()) return fail(FK_E_WORKSPACE, "idft2d: workspace too small");
+  k_twtab<<<(nf + 255) / 256, 256, 0, s>>>(nf, tab, 1.0);
+  // stage A: P[k1][r] = sum_k Hc[k][k1] w^(-(off + r)(k - m))   (i = k1, j = r, contraction k = k0 + m)
+  TwArgs A{};
+  A.D = Hc;
+  A.d_b = 0;
+  A.d_i = 1;
+  A.d_k = m + 1;
+  A.M = m + 1;
+  A.N = G;
+  A.Kd = 2 * m + 1;
+  A.jbase = off;
+  A.off = -m;
+  A.nf = nf;
+  A.tab = tab;
+  A.C = P;
+  A.c_b = 0;
+  A.c_i = G;
+  A.c_j = 1;
+  k_twdft<true><<<dim3((G + TT - 1) / TT, (m + 1 + TT - 1) / TT, 1), 256, 0, s>>>(A);
+  // stage B: g[off + r][off + c] = Re sum_k1 P[k1][r] w^(-(off + c) k1)   (i = r, j = c, contraction k1)
+  TwArgs B{};
+  B.D = P;
+  B.d_b = 0;
+  B.d_i = 1;
+  B.d_k = G;
+  B.M = G;
+  B.N = G;
+  B.Kd = m + 1;
+  B.jbase = off;
+  B.off = 0;
+  B.nf = nf;
+  B.tab = tab;
+  B.C = grid + (int64_t)off * ldg + off;
+  B.c_b = 0;
+  B.c_i = ldg;
+  B.c_j = 1;
+  k_twdft<true, true><<<dim3((G + TT - 1) / TT, (G + TT - 1) / TT, 1), 256, 0, s>>>(B);
+  FK_CUDA_TRY(cudaGetLastError());
+  count_launch(3);
   return FK_OK;
 }
 

@@ -157,6 +157,10 @@ fk_status idft1d_run(const double2* H, int64_t hstride, int nfeat, int nf, int m
 size_t dft2d_ws_bytes(int nf, int G, int K, int batch);
 fk_status dft2d_run(const double* fine, int nf, int off, int G, int K, int batch, const double* phihat, double* out, int acc, void* ws,
                     size_t ws_bytes, cudaStream_t s);
+// the type-2 direction for the d = 2 predict grid (dft2d.cu): Hc (2m+1) x (m+1) half spectrum
+// (k1 >= 0, the k1 > 0 entries doubled) -> the real grid on the occupied block [off, off + G)^2
+size_t idft2d_ws_bytes(int nf, int G, int m);
+fk_status idft2d_run(const double2* Hc, int m, int nf, int off, int G, double* grid, int64_t ldg, void* ws, size_t ws_bytes, cudaStream_t s);
 fk_status type1_run(const Plan1& p, const fk_points& X, const void* Y, double L, const Type1Out& out, void* ws, size_t ws_bytes,
                     int* d_status, cudaStream_t s);
 

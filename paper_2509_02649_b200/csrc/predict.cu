@@ -2,9 +2,11 @@
 //   f(x) = Re sum_{|k|<=m} theta_k exp(+i k t(x))
 // Since only the real part is returned, theta is replaced by its Hermitian part
 // h_k = (theta_k + conj theta_{-k}) / 2, so the fine grid
-//   g_l = sum_k h_k (-1)^k / psi-hat(k/nf) exp(+2 pi i k l / nf)       (one cuFFT Z2D)
-// is real, and f(x) = sum_l g_l psi(u(x) - l) is a w-tap gather from the occupied half of the
-// grid, held in shared memory (fp32 path: cubic B-spline, 4 taps; fp64 path: ES window).
+//   g_l = sum_k h_k (-1)^k / psi-hat(k/nf) exp(+2 pi i k l / nf)
+// is real (hand-written inverse DFT evaluated only on the occupied cells: dft1d.cu for d = 1 /
+// additive, dft2d.cu for d = 2; no cuFFT), and f(x) = sum_l g_l psi(u(x) - l) is a w-tap gather
+// from the occupied half of the grid, held in shared memory (fp32 path: cubic B-spline, 4 taps,
+// d = 2: ES window; fp64 path: septic B-spline or ES window).
 // The gather streams Xq once and writes f once: 8 B per query in fp32 (HBM-bound).
 #include <cmath>
 #include <type_traits>
@@ -405,23 +407,17 @@ __global__ void __launch_bounds__(512) k_gather_es(const XT* __restrict__ Xq, in
   if (bad && d_status) atomicOr(d_status, (int)FK_E_RANGE);
 }
 
-// ---- d = 2: H[k0 mod nf][k1], 0 <= k1 <= nf/2, from the Hermitian part of theta ----
-__global__ void k_pred_prep2d(const double2* __restrict__ theta, int m, int nf, const double* __restrict__ tab,
-                              double2* __restrict__ H) {
-  const int half = nf / 2 + 1;
+// ---- d = 2: Hc[(k0 + m)(m + 1) + k1] = c_k1 (-1)^(k0+k1) (theta_k + conj theta_-k) / 2 / (psi-hat psi-hat),
+// |k0| <= m, 0 <= k1 <= m, c_0 = 1, c_k1>0 = 2: the half spectrum idft2d_run turns into the grid ----
+__global__ void k_pred_prep2d(const double2* __restrict__ theta, int m, const double* __restrict__ tab, double2* __restrict__ H) {
+  const int side = 2 * m + 1;
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= (int64_t)nf * half) return;
-  const int row = (int)(t / half), k1 = (int)(t % half);
-  const int k0 = row <= nf / 2 ? row : row - nf;
-  double2 h = make_double2(0.0, 0.0);
-  if (k1 <= m && k0 >= -m && k0 <= m) {
-    const int side = 2 * m + 1;
-    const double2 a = theta[(int64_t)(k0 + m) * side + (k1 + m)];
-    const double2 b = theta[(int64_t)(-k0 + m) * side + (-k1 + m)];
-    const double sc = 0.5 * (((k0 + k1) & 1) ? -1.0 : 1.0) / (tab[k0 < 0 ? -k0 : k0] * tab[k1]);
-    h = make_double2((a.x + b.x) * sc, (a.y - b.y) * sc);
-  }
-  H[t] = h;
+  if (t >= (int64_t)side * (m + 1)) return;
+  const int k0 = (int)(t / (m + 1)) - m, k1 = (int)(t % (m + 1));
+  const double2 a = theta[(int64_t)(k0 + m) * side + (k1 + m)];
+  const double2 b = theta[(int64_t)(-k0 + m) * side + (-k1 + m)];
+  const double sc = (k1 > 0 ? 1.0 : 0.5) * (((k0 + k1) & 1) ? -1.0 : 1.0) / (tab[k0 < 0 ? -k0 : k0] * tab[k1]);
+  H[t] = make_double2((a.x + b.x) * sc, (a.y - b.y) * sc);
 }
 
 template <typename GT>
@@ -509,10 +505,9 @@ static bool is2d(const PredPlan& p) { return !p.additive && p.d == 2; }
 
 static fk_status pred_layout(const PredPlan& p, Bump& b, PredWs& w) {
   FftPlan fp;
-  if (is2d(p)) {
-    int dims[2] = {p.nf, p.nf};
-    FK_TRY(fft_plan(2, dims, 1, CUFFT_Z2D, &fp));
-    w.H = (double2*)b.take((size_t)p.nf * (p.nf / 2 + 1) * 16);
+  if (is2d(p)) {  // d = 2: the hand-written 2-D inverse DFT (dft2d.cu) fills the occupied block
+    fp.work = idft2d_ws_bytes(p.nf, p.g.G, p.m);
+    w.H = (double2*)b.take((size_t)(2 * p.m + 1) * (p.m + 1) * 16);
     w.grid = (double*)b.take((size_t)p.nf * p.nf * 8);
   } else {  // d = 1 / additive: the hand-written inverse DFT (dft1d.cu) fills the occupied cells
     fp.work = idft1d_ws_bytes(p.nf, p.m, p.nfeat);
@@ -698,14 +693,11 @@ fk_status predict_run(const double* theta, int d, int m, double L, int additive,
   if (!b.ok()) return fail(FK_E_WORKSPACE, "fk_predict_type2: workspace too small");
   if (p.ker == KER_ES) FK_TRY(es_phihat_table(p.es, p.nf, p.m, w.tab, s));
   if (is2d(p)) {
-    const int64_t tot2 = (int64_t)p.nf * (p.nf / 2 + 1);
-    k_pred_prep2d<<<(unsigned)((tot2 + 255) / 256), 256, 0, s>>>((const double2*)theta, m, p.nf, w.tab, w.H);
+    const int64_t tot2 = (int64_t)(2 * m + 1) * (m + 1);
+    k_pred_prep2d<<<(unsigned)((tot2 + 255) / 256), 256, 0, s>>>((const double2*)theta, m, w.tab, w.H);
     FK_CUDA_TRY(cudaGetLastError());
     count_launch();
-    FftPlan fp2;
-    int dims[2] = {p.nf, p.nf};
-    FK_TRY(fft_plan(2, dims, 1, CUFFT_Z2D, &fp2));
-    FK_TRY(fft_exec_z2d(fp2, (cufftDoubleComplex*)w.H, w.grid, w.work, s));
+    FK_TRY(idft2d_run(w.H, m, p.nf, p.g.off, p.g.G, w.grid, p.nf, w.work, w.work_bytes, s));
     if (Xq.n == 0) return FK_OK;
     if (Xq.dtype == FK_F32) return gather2d<float>(p, Xq, L, w, out, d_status, s);
     return gather2d<double>(p, Xq, L, w, out, d_status, s);
