@@ -6,8 +6,12 @@ on their own), each against its roofline and beside the CPU oracle:
   A10/A11 solve                   GFLOP/s of the real Cholesky (D^3/3) vs the fp64 FMA peak
   A7/A8 DFT + deconvolution       post-spread time of fk_rhs_type1 (reduce + hand-written DFT + deconv)
   NEXT-1 lambda path              fk_solve_path over 300 lambdas vs 300 fk_solve calls
+  NEXT-1 large path (path_large)  16 lambdas at D = 4225 / 9409 / 16641: path vs one fk_solve per lambda
+  NEXT-3 CG vs dense (cg)         fk_solve with FK_SOLVER=pcg / dense on C3-size Sobolev systems
+  library reference (libref)      cuBLAS DGEMM and cuSOLVER potrf rates (context for the solve rows)
 
     python bench_rows.py [--rows predict,solve,post,path]     -> one JSON line per measurement
+    (cg, path_large and libref run only when named)
 """
 from __future__ import annotations
 
@@ -201,6 +205,108 @@ def row_path(out):
         del Xd, Yd
 
 
+def _device_data(n, d, m, xkind=0, seed=0):
+    import torch
+
+    from datagen.device import gen_dataset
+    from paper_2509_02649_b200 import fk
+
+    X = torch.empty(n, d, device="cuda") if d == 2 else torch.empty(n, device="cuda")
+    Y = torch.empty(n, device="cuda")
+    gen_dataset(X, Y, n, d, xkind=xkind, ykind=2 if d == 2 else 0, seed=seed)
+    r, mu = fk.fk_rhs_type1(X, Y, 1.0, m, 1e-6)
+    del X, Y
+    return r, mu
+
+
+def row_cg(out):
+    """CG (FK_SOLVER=pcg) against dense Cholesky (FK_SOLVER=dense) on C3-size Sobolev systems: time,
+    iterations, backward error, agreement of theta -- the data behind fk_solve's cost model."""
+    from paper_2509_02649_b200 import fk
+
+    def run(how, mu, r, n, d, m, lam, s, reps=3):
+        os.environ["FK_SOLVER"] = how
+        try:
+            best = 1e9
+            for _ in range(reps):
+                th, rep = fk.fk_solve(mu, r, n, d, m, 1.0, lam, "sobolev", s)
+                best = min(best, rep["ms"])
+        finally:
+            del os.environ["FK_SOLVER"]
+        return best, th, rep
+
+    n = 20_000_000
+    for d, m, s, lam, xk in [(2, 64, 2.0, 1e-6, 0), (2, 64, 2.0, 1e-6, 1), (2, 40, 2.0, 1e-6, 0), (1, 3000, 1.0, 2.15e-7, 0),
+                             (2, 90, 2.0, 1e-7, 0), (2, 64, 2.0, 1e-8, 0), (2, 64, 2.0, 1e-4, 0)]:
+        r, mu = _device_data(n, d, m, xkind=xk)
+        ms_d, th_d, rep_d = run("dense", mu, r, n, d, m, lam, s)
+        ms_p, th_p, rep_p = run("pcg", mu, r, n, d, m, lam, s)
+        diff = ((th_p - th_d).abs().norm() / th_d.abs().norm()).item()
+        out.append({"row": "NEXT-3 CG vs dense solve", "d": d, "m": m, "s": s, "lambda": lam, "xkind": xk, "D": rep_d["n_unknowns"],
+                    "dense_ms": ms_d, "dense_backward_err": rep_d["backward_err"], "cg_ms": ms_p, "cg_iters": rep_p["iters"],
+                    "cg_backward_err": rep_p["backward_err"], "rel_diff": diff})
+
+
+def row_path_large(out):
+    """fk_solve_path for 16 lambdas at D = 4225 / 9409 / 16641 against one fk_solve per lambda (the
+    library picks the eigendecomposition or per-lambda solves by cost)."""
+    import numpy as np
+    import torch
+
+    from paper_2509_02649_b200 import fk
+
+    n, d = 4_000_000, 2
+    lams = list(np.logspace(-9, -3, 16))
+    for m in (32, 48, 64):
+        r, mu = _device_data(n, d, m)
+        fk.fk_solve_path(mu, r, n, d, m, 1.0, lams[:2], "sobolev", 2.0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        fk.fk_solve_path(mu, r, n, d, m, 1.0, lams, "sobolev", 2.0)
+        torch.cuda.synchronize()
+        path_ms = 1e3 * (time.perf_counter() - t0)
+        per = []
+        for lam in lams:
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            fk.fk_solve(mu, r, n, d, m, 1.0, lam, "sobolev", 2.0)
+            torch.cuda.synchronize()
+            per.append(1e3 * (time.perf_counter() - t0))
+        out.append({"row": "NEXT-1 lambda path, large D", "d": d, "m": m, "D": (2 * m + 1) ** 2, "n_lambda": len(lams),
+                    "path_ms": path_ms, "solve_per_lambda_ms": per, "solve_all_ms": sum(per)})
+
+
+def row_libref(out):
+    """Library reference rates on this GPU (context for the solve rows): cuBLAS DGEMM and the cuSOLVER
+    Cholesky behind torch.linalg.cholesky at the C3 system size."""
+    import torch
+
+    def t(f, r=5):
+        f()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        best = 1e9
+        for _ in range(r):
+            e0.record()
+            f()
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        return best
+
+    for N in (4096, 8192, 16384):
+        a = torch.randn(N, N, dtype=torch.float64, device="cuda")
+        b = torch.randn_like(a)
+        ms = t(lambda: a @ b)
+        out.append({"row": "library reference: cuBLAS DGEMM", "N": N, "ms": ms, "tflops": 2 * N ** 3 / ms / 1e9})
+        del a, b
+    N = 16641
+    A = torch.randn(N, N, dtype=torch.float64, device="cuda")
+    A = A @ A.T / N + torch.eye(N, dtype=torch.float64, device="cuda")
+    ms = t(lambda: torch.linalg.cholesky(A), 3)
+    out.append({"row": "library reference: cuSOLVER potrf (torch.linalg.cholesky)", "N": N, "ms": ms, "tflops": N ** 3 / 3 / ms / 1e9})
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--rows", default="predict,solve,post,path")
@@ -212,8 +318,10 @@ def main():
     build.build()
     torch.cuda.set_device(0)
     out = []
+    rows = {"predict": row_predict, "solve": row_solve, "post": row_post, "path": row_path, "cg": row_cg,
+            "path_large": row_path_large, "libref": row_libref}
     for r in a.rows.split(","):
-        {"predict": row_predict, "solve": row_solve, "post": row_post, "path": row_path}[r](out)
+        rows[r](out)
     for o in out:
         print(json.dumps(o), flush=True)
 
