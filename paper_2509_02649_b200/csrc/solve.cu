@@ -482,9 +482,14 @@ __global__ void k_theta_from_real(SysArgs g, const double* __restrict__ zs, int6
 
 
 // ---- back substitution L^T z = y on many SMs (replaces the single-SM cublasDtrsv) ------------
-// Block I (32 rows of z) is owned by one 64-thread CTA.  It inverts its diagonal block W = L_II^{-1}
+// Block I (32 rows of z) is owned by one 128-thread CTA.  It inverts its diagonal block W = L_II^{-1}
 // and prefetches its off-diagonal blocks while z is not yet known, then accumulates
-// sum_{J>I} L_JI^T z_J as the blocks z_J appear (J descending) and finishes with z_I = W^T (y_I - acc).
+// sum_{J>I} L_JI^T z_J as the blocks z_J appear (J descending; thread (lane, warp h) holds row lane
+// of block J times columns 8h..8h+7 of block I) and finishes with z_I = W^T (y_I - acc) plus one
+// refinement step with L_II.  Only the last block's term is on the chain: the sum over J > I+1 is
+// reduced (shuffles) and L_{I+1,I} staged while z_{I+1} is awaited, and every 32 x 32 product of
+// the tail is split over the four warps (8 terms each) instead of 32-term serial dot products
+// (round 2: ~1.6 -> ~1 us per block on the chain).
 // z_J is published element by element: zbuf is pre-filled with a sentinel NaN pattern (k_rhs_real)
 // that no computed value has, so a reader spins on the value itself (one L2 round trip per block
 // on the critical path, no separate flag).  Blocks are taken in ticket order (an atomic counter,
@@ -496,98 +501,121 @@ __device__ __forceinline__ double ld_volatile(const double* p) {
   return v;
 }
 
-__global__ void __launch_bounds__(64) k_trsv_lt(const double* __restrict__ M, int64_t ld, int D, const double* __restrict__ y,
-                                                 int64_t ystride, double* zbuf, int* ticket, int* info) {
-  __shared__ double W[32][33];
-  __shared__ double Ls[32][33];
-  __shared__ double red[2][32][17];
-  __shared__ double rv[32];
-  __shared__ double zv[32];
+// value of z at row `row`, waiting for its publication (watchdog: 5 s, then info = -1)
+__device__ __forceinline__ double wait_z(const double* zbuf, int row, int* info) {
+  unsigned long long t0, t1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  double zc;
+  do {
+    zc = ld_volatile(zbuf + row);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+  } while (__double_as_longlong(zc) == (long long)kZSentinel && t1 - t0 < 5000000000ULL);
+  if (__double_as_longlong(zc) == (long long)kZSentinel) atomicCAS(info, 0, -1);
+  return zc;
+}
+
+// out[c] = base[c] + sgn * sum_k A[k][c] v[k] over k in [c, 32) (A lower triangular in [k][c]) or all
+// k (FULL): thread (c = lane, part h) sums k in [8h, 8h + 8), the four parts are added by warp 0.
+// Starts after a barrier that published v and ends with one that publishes out.
+template <bool FULL>
+__device__ __forceinline__ void mv32(const double (*A)[33], const double* v, const double* base, double sgn, double* out,
+                                     double (*part)[33]) {
+  const int c = threadIdx.x & 31, h = threadIdx.x >> 5;
+  double t = 0.0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int k = 8 * h + q;
+    if (FULL || k >= c) t = fma(A[k][c], v[k], t);
+  }
+  part[h][c] = t;
+  __syncthreads();
+  if (h == 0) out[c] = base[c] + sgn * ((part[0][c] + part[1][c]) + (part[2][c] + part[3][c]));
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(128) k_trsv_lt(const double* __restrict__ M, int64_t ld, int D, const double* __restrict__ y,
+                                                  int64_t ystride, double* zbuf, int* ticket, int* info) {
+  __shared__ double W[32][33];   // W[k][c] = (L_II^{-1})(k, c)
+  __shared__ double Ls[32][33];  // Ls[k][c] = L_II(k, c)
+  __shared__ double Ln[32][33];  // Ln[r][c] = L_{I+1, I}(r, c)
+  __shared__ double part[4][33];
+  __shared__ double pacc[32], rv[32], zv[32], res[32], zn[32], zero[32];
   __shared__ int tk;
   const int nb = (D + 31) / 32;
   if (threadIdx.x == 0) tk = atomicAdd(ticket, 1);
   __syncthreads();
   const int I = nb - 1 - tk;
-  const int lane = threadIdx.x & 31, h = threadIdx.x >> 5;  // warp h holds columns 16h .. 16h+15 of block I
+  const int lane = threadIdx.x & 31, h = threadIdx.x >> 5;
   const int r0 = I * 32;
-  // stage L_II (identity on padded rows) in shared memory, then W = L_II^{-1}: lane j solves L w = e_j
-  for (int c = h; c < 32; c += 2) {
-    const int gr = r0 + lane, gc = r0 + c;
-    const double l = (gr < D && gc < D) ? M[gr + (int64_t)gc * ld] : (lane == c ? 1.0 : 0.0);
-    W[lane][c] = l;
-    Ls[lane][c] = l;
+  auto Lval = [&](int gr, int gc) { return (gr < D && gc < D) ? M[gr + (int64_t)gc * ld] : (gr == gc ? 1.0 : 0.0); };
+  // stage L_II (identity on padded rows) and L_{I+1,I}, then W = L_II^{-1}: lane j of warp 0 solves L w = e_j
+  for (int c = h; c < 32; c += 4) {
+    Ls[lane][c] = Lval(r0 + lane, r0 + c);
+    Ln[lane][c] = (I + 1 < nb) ? Lval(r0 + 32 + lane, r0 + c) : 0.0;
   }
+  if (threadIdx.x < 32) zero[threadIdx.x] = 0.0;
   __syncthreads();
-  double w[32];  // column `lane` of W, built top-down in registers
   if (h == 0) {
+    // column `lane` of W by right-looking forward substitution (the chain per row is one multiply and
+    // one FMA; the reciprocals of the diagonal are formed in parallel first)
+    const double rinv = 1.0 / Ls[lane][lane];
+    double w[32];
 #pragma unroll
-    for (int r = 0; r < 32; ++r) {
-      double a = (r == lane) ? 1.0 : 0.0;
+    for (int r = 0; r < 32; ++r) w[r] = (r == lane) ? 1.0 : 0.0;
 #pragma unroll
-      for (int c = 0; c < r; ++c) a -= W[r][c] * w[c];
-      w[r] = (r >= lane) ? a / W[r][r] : 0.0;
+    for (int c = 0; c < 32; ++c) {
+      w[c] *= __shfl_sync(~0u, rinv, c);
+#pragma unroll
+      for (int r = c + 1; r < 32; ++r) w[r] = fma(-Ls[r][c], w[c], w[r]);
     }
-  }
-  __syncthreads();
-  if (h == 0) {
 #pragma unroll
     for (int r = 0; r < 32; ++r) W[r][lane] = w[r];
   }
-  double acc[16];
+  // sum_{J > I+1} L_JI^T z_J: thread (lane = row of block J, h) x columns 8h .. 8h+7 of block I
+  double acc[8];
 #pragma unroll
-  for (int q = 0; q < 16; ++q) acc[q] = 0.0;
-  const int cbase = r0 + 16 * h;
-  double Lb[16];
+  for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+  const int cbase = r0 + 8 * h;
+  double Lb[8];
   auto load_block = [&](int J) {
     const int row = J * 32 + lane;
 #pragma unroll
-    for (int q = 0; q < 16; ++q) Lb[q] = (row < D && cbase + q < D) ? M[row + (int64_t)(cbase + q) * ld] : 0.0;
+    for (int q = 0; q < 8; ++q) Lb[q] = (row < D && cbase + q < D) ? M[row + (int64_t)(cbase + q) * ld] : 0.0;
   };
-  if (I + 1 < nb) load_block(nb - 1);
-  for (int J = nb - 1; J > I; --J) {
+  if (I + 2 < nb) load_block(nb - 1);
+  for (int J = nb - 1; J > I + 1; --J) {
     const int row = J * 32 + lane;
-    double zc = 0.0;
-    if (row < D) {
-      unsigned long long t0, t1;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-      // the polled word is the value itself (written once), so no fence is needed; watchdog: a
-      // block never published within 5 s ends the wait and marks the solve invalid (info = -1)
-      do {
-        zc = ld_volatile(zbuf + row);
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-      } while (__double_as_longlong(zc) == (long long)kZSentinel && t1 - t0 < 5000000000ULL);
-      if (__double_as_longlong(zc) == (long long)kZSentinel) atomicCAS(info, 0, -1);
-    }
-    double Lc[16];
+    const double zc = (row < D) ? wait_z(zbuf, row, info) : 0.0;
+    double Lc[8];
 #pragma unroll
-    for (int q = 0; q < 16; ++q) Lc[q] = Lb[q];
-    if (J - 1 > I) load_block(J - 1);  // prefetch the next block while this one is consumed
+    for (int q = 0; q < 8; ++q) Lc[q] = Lb[q];
+    if (J - 1 > I + 1) load_block(J - 1);  // prefetch the next block while this one is consumed
 #pragma unroll
-    for (int q = 0; q < 16; ++q) acc[q] = fma(Lc[q], zc, acc[q]);
+    for (int q = 0; q < 8; ++q) acc[q] = fma(Lc[q], zc, acc[q]);
   }
-  // reduce over lanes: red[h][lane][q] -> column 16h + q
+  // reduce over the 32 rows (lanes) while z_{I+1} is not yet known
 #pragma unroll
-  for (int q = 0; q < 16; ++q) red[h][lane][q] = acc[q];
+  for (int q = 0; q < 8; ++q) {
+    double t = acc[q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(~0u, t, o);
+    if (lane == q) pacc[8 * h + q] = t;
+  }
   __syncthreads();
   if (h == 0) {
-    const int col = lane, hh = col >> 4, q = col & 15;
-    double t = 0.0;
-    for (int l = 0; l < 32; ++l) t += red[hh][l][q];
-    const int gr = r0 + col;
-    rv[col] = (gr < D) ? y[(int64_t)gr * ystride] - t : 0.0;
-    __syncwarp();
-    double z = 0.0;
-    for (int c = 0; c < 32; ++c) z = fma(W[c][col], rv[c], z);
-    // one step of refinement with L_II itself keeps the block solve backward stable
-    zv[col] = z;
-    __syncwarp();
-    double res = rv[col];
-    for (int r = col; r < 32; ++r) res = fma(-Ls[r][col], zv[r], res);
-    __syncwarp();
-    rv[col] = res;
-    __syncwarp();
-    for (int c = 0; c < 32; ++c) z = fma(W[c][col], rv[c], z);
-    if (gr < D) asm volatile("st.volatile.global.f64 [%0], %1;" ::"l"(zbuf + gr), "d"(z) : "memory");
+    const int gr = r0 + lane;
+    pacc[lane] = (gr < D) ? y[(int64_t)gr * ystride] - pacc[lane] : 0.0;  // y_I - sum_{J > I+1}
+    const int row = r0 + 32 + lane;
+    zn[lane] = (I + 1 < nb && row < D) ? wait_z(zbuf, row, info) : 0.0;  // the chain: z_{I+1}
+  }
+  __syncthreads();
+  mv32<true>(Ln, zn, pacc, -1.0, rv, part);     // rv = y_I - sum_{J > I} L_JI^T z_J
+  mv32<false>(W, rv, zero, 1.0, zv, part);      // z = W^T rv
+  mv32<false>(Ls, zv, rv, -1.0, res, part);     // res = rv - L_II^T z   (one refinement step)
+  mv32<false>(W, res, zv, 1.0, rv, part);       // z += W^T res
+  if (h == 0) {
+    const int gr = r0 + lane;
+    if (gr < D) asm volatile("st.volatile.global.f64 [%0], %1;" ::"l"(zbuf + gr), "d"(rv[lane]) : "memory");
   }
 }
 
@@ -1621,7 +1649,7 @@ fk_status solve_run(const fk_problem* P, double* theta, fk_solve_report* rep, vo
       return fail(FK_E_CUDA, "cublasDtrsv failed");
   }
   if (own_trsv) {
-    k_trsv_lt<<<(D + 31) / 32, 64, 0, s>>>(M, N, D, M + D, N, zbuf, ticket, info);
+    k_trsv_lt<<<(D + 31) / 32, 128, 0, s>>>(M, N, D, M + D, N, zbuf, ticket, info);
     count_launch();
   }
   k_theta_from_real<<<(D + 255) / 256, 256, 0, s>>>(g, own_trsv ? zbuf : M + D, own_trsv ? 1 : N, (double2*)theta, info,
