@@ -527,7 +527,19 @@ static fk_status task_table(int nt, int4** d_tasks, int* ntasks) {
 
 // Factor the N x N SPD matrix M (column-major, leading dimension ld, lower triangle read and
 // overwritten with L).  ws: chol_ws_bytes(N) bytes; info: device int, set to 0 here.
-fk_status chol_tiles(double* M, int64_t ld, int N, int* info, void* ws, cudaStream_t s, unsigned long long* trace) {
+// workspace layout: flags (+ ticket) | side buffer Ld | uflags | partial sums
+CholReset chol_reset_args(int N, void* ws, int* info) {
+  const int nt = (N + TS - 1) / TS;
+  CholReset c;
+  c.ld = (unsigned long long*)((char*)ws + flags_bytes(nt));
+  c.n_ld = (int64_t)nt * LDW;
+  c.zero = (int*)ws;  // flags, ticket: flags_bytes(nt); uflags follow the side buffer
+  c.n_zero = (int64_t)flags_bytes(nt) / (int64_t)sizeof(int);
+  c.info = info;
+  return c;
+}
+
+fk_status chol_tiles(double* M, int64_t ld, int N, int* info, void* ws, cudaStream_t s, unsigned long long* trace, bool preset) {
   const int nt = (N + TS - 1) / TS;
   const int ntiles = nt * (nt + 1) / 2;
   int4* tasks = nullptr;
@@ -538,10 +550,12 @@ fk_status chol_tiles(double* M, int64_t ld, int N, int* info, void* ws, cudaStre
   double* Ld = (double*)((char*)ws + flags_bytes(nt));
   int* uflags = (int*)((char*)Ld + (size_t)nt * LDW * sizeof(double));
   double* part = (double*)((char*)uflags + uflags_bytes(nt));
-  FK_CUDA_TRY(cudaMemsetAsync(Ld, 0xff, (size_t)nt * LDW * sizeof(double), s));
-  FK_CUDA_TRY(cudaMemsetAsync(flags, 0, (size_t)(ntiles + 8) * sizeof(int), s));
+  if (!preset) {
+    FK_CUDA_TRY(cudaMemsetAsync(Ld, 0xff, (size_t)nt * LDW * sizeof(double), s));
+    FK_CUDA_TRY(cudaMemsetAsync(flags, 0, (size_t)(ntiles + 8) * sizeof(int), s));
+    FK_CUDA_TRY(cudaMemsetAsync(info, 0, sizeof(int), s));
+  }
   if (nt >= kUMinTiles) FK_CUDA_TRY(cudaMemsetAsync(uflags, 0, uflags_bytes(nt), s));
-  FK_CUDA_TRY(cudaMemsetAsync(info, 0, sizeof(int), s));
   const bool use_u = nt >= kUMinTiles;
   auto kern = use_u ? k_chol_tiles<true> : k_chol_tiles<false>;
   static int per_sm = 0;

@@ -169,7 +169,24 @@ fk_status type1_run(const Plan1& p, const fk_points& X, const void* Y, double L,
 // ------------------------------------------------------------------------------------------
 size_t solve_ws_bytes(int d, int m, int kind);
 size_t chol_ws_bytes(int N);
-fk_status chol_tiles(double* M, int64_t ld, int N, int* info, void* ws, cudaStream_t s, unsigned long long* trace = nullptr);
+// the state chol_tiles resets before its kernel (side buffer to the sentinel, flags / ticket / info
+// to zero): a caller that already launches a kernel before it can do the reset there (chol_reset)
+// and pass preset = true, saving the memset nodes on the solve's latency chain
+struct CholReset {
+  unsigned long long* ld;  // side buffer, filled with all-ones
+  int64_t n_ld;            // 8-byte words
+  int* zero;               // flags + ticket (+ uflags when used), zeroed
+  int64_t n_zero;
+  int* info;               // zeroed
+};
+CholReset chol_reset_args(int N, void* ws, int* info);
+__device__ __forceinline__ void chol_reset(const CholReset& c, int64_t t, int64_t stride) {
+  for (int64_t i = t; i < c.n_ld; i += stride) c.ld[i] = ~0ULL;
+  for (int64_t i = t; i < c.n_zero; i += stride) c.zero[i] = 0;
+  if (t == 0) *c.info = 0;
+}
+fk_status chol_tiles(double* M, int64_t ld, int N, int* info, void* ws, cudaStream_t s, unsigned long long* trace = nullptr,
+                     bool preset = false);
 size_t solve_path_ws_bytes(int d, int m, int kind, int nlam);
 fk_status solve_path_run(const fk_problem* P, const double* lambdas, int nlam, double* theta, int* info, void* ws, size_t ws_bytes,
                          cudaStream_t s);

@@ -439,8 +439,10 @@ void launch_assemble(const SysArgs& g, double* M, cudaStream_t s) {
 }
 
 __global__ void k_rhs_real(SysArgs g, const double2* __restrict__ r, double* __restrict__ M, double* __restrict__ zbuf,
-                           int* __restrict__ ticket) {  // last row of M (+ reset of k_trsv_lt's sentinels / ticket)
+                           int* __restrict__ ticket, CholReset cr) {  // last row of M (+ reset of k_trsv_lt's sentinels / ticket,
+                                                                     // and of chol_tiles' state when cr.info is set)
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (cr.info) chol_reset(cr, u, (int64_t)gridDim.x * blockDim.x);
   const int64_t N = g.D + 1;
   if (u == g.D) M[g.D + g.D * N] = 1e200;  // any value above c^T (P*AP)^{-1} c keeps it SPD
   if (u == 0 && ticket) *ticket = 0;
@@ -849,7 +851,7 @@ fk_status solve_path_run(const fk_problem* P, const double* lambdas, int nlam, d
     count_launch();
   }
   launch_assemble(g, M, s);
-  k_rhs_real<<<(N + 255) / 256, 256, 0, s>>>(g, (const double2*)P->rhs, M, nullptr, nullptr);
+  k_rhs_real<<<(N + 255) / 256, 256, 0, s>>>(g, (const double2*)P->rhs, M, nullptr, nullptr, CholReset{});
   k_path_diag<<<(D + 255) / 256, 256, 0, s>>>(g, dg);
   k_path_scale<<<sms * 8, 256, 0, s>>>(M, N, D, dg);
   k_path_rhs<<<(D + 255) / 256, 256, 0, s>>>(M, N, D, dg, Z);  // scaled c into Z[:,0] (scratch)
@@ -953,7 +955,7 @@ fk_status path_validate_run(const fk_problem* Pv, const double* theta, int nlam,
   if (!b.ok()) return fail(FK_E_WORKSPACE, "fk_path_validate: workspace too small");
   const int sms = device_sm_count();
   launch_assemble(g, M, s);
-  k_rhs_real<<<(N + 255) / 256, 256, 0, s>>>(g, (const double2*)Pv->rhs, M, nullptr, nullptr);
+  k_rhs_real<<<(N + 255) / 256, 256, 0, s>>>(g, (const double2*)Pv->rhs, M, nullptr, nullptr, CholReset{});
   k_z_from_theta<<<sms * 4, 256, 0, s>>>(g, (const double2*)theta, nlam, Z);
   FK_CUDA_TRY(cudaGetLastError());
   count_launch(3);
@@ -1627,7 +1629,9 @@ fk_status solve_run(const fk_problem* P, double* theta, fk_solve_report* rep, vo
   }
   if (!done) {
   launch_assemble(g, M, s);
-  k_rhs_real<<<(N + 255) / 256, 256, 0, s>>>(g, (const double2*)P->rhs, M, zbuf, ticket);
+  const bool tiles = use_tiles(N);
+  k_rhs_real<<<tiles ? std::max((N + 255) / 256, 64) : (N + 255) / 256, 256, 0, s>>>(
+      g, (const double2*)P->rhs, M, zbuf, ticket, tiles ? chol_reset_args(N, chol_ws, info) : CholReset{});
   FK_CUDA_TRY(cudaGetLastError());
   count_launch(2);
   {
@@ -1635,8 +1639,8 @@ fk_status solve_run(const fk_problem* P, double* theta, fk_solve_report* rep, vo
     cusolverDnHandle_t h;
     FK_TRY(handle_for_device(&h));
     if (cusolverDnSetStream(h, s) != CUSOLVER_STATUS_SUCCESS) return fail(FK_E_CUDA, "cusolverDnSetStream failed");
-    if (use_tiles(N)) {
-      FK_TRY(chol_tiles(M, N, N, info, chol_ws, s));
+    if (tiles) {
+      FK_TRY(chol_tiles(M, N, N, info, chol_ws, s, nullptr, /*preset=*/true));
     } else if (cusolverDnDpotrf(h, CUBLAS_FILL_MODE_LOWER, N, M, N, work, lwork, info) != CUSOLVER_STATUS_SUCCESS) {
       return fail(FK_E_CUDA, "cusolverDnDpotrf failed");
     }
