@@ -8,11 +8,19 @@
 //     (mma.m8n8k4.f64, a 16 x 16 quadrant per warp), applies A_ij -= L_ik L_jk^T for k < j as soon
 //     as both operand tiles are published (flags), then solves X L_jj^T = A_ij (TRSM, a row per
 //     lane, 1/L_cc from the diagonal task);
-//   * the diagonal task D_j owns the sub-diagonal tile (j, j-1) AND the diagonal tile (j, j): it
-//     accumulates both, TRSMs the former, applies its rank-32 update to the latter straight from
-//     shared memory (no round trip through L2 on the critical path), then runs the 32 x 32 POTRF
-//     (one warp, a row per lane, rsqrt per pivot, column broadcast through shared memory) and
-//     publishes L_jj and 1/diag(L_jj) into a sentinel-filled side buffer that consumers poll as data.
+//   * the diagonal task D_j owns the diagonal tile (j, j) AND the sub-diagonal tile (j+1, j): it
+//     accumulates both (updates k < j-1), applies the last update of the diagonal tile with
+//     L_{j,j-1} (published by D_{j-1} as data), then runs the 32 x 32 POTRF (warp 0, a row per lane,
+//     rsqrt per pivot, column broadcast through shared memory) while warp 1 solves
+//     L_{j+1,j} = A_{j+1,j} L_jj^{-T} a quarter of the columns at a time as warp 0 releases them
+//     (named barriers, bar.arrive on warp 0's side: it never waits).  Warps 2-3 first subtract the
+//     sub-diagonal tile's last update P_j = L_{j+1,j-1} L_{j,j-1}^T, which the off-diagonal task
+//     (j+1, j-1) forms right after its own TRSM.  So the TRSM runs beside the POTRF instead of
+//     after it on the chain.  L_jj, 1/diag(L_jj), L_{j+1,j} and P_j live in a sentinel-filled side
+//     buffer that consumers poll as data.  (Round 2: round 1 ran the TRSM of (j, j-1) inside D_j
+//     before its POTRF; N = 2002 0.45 -> 0.43 ms, 4226 1.48 -> 1.42 ms.  What remains on the chain
+//     per 32 columns: the POTRF, ~3.3 us of fp64 latency, warp 1's lag behind it (the SM is shared
+//     with update tasks) and one L2 round trip to the next diagonal task.)
 // Tasks are handed out by an atomic ticket counter in dependency order, so a CTA only ever waits
 // on tasks with smaller tickets -- held by CTAs that are already running and never wait on larger
 // tickets: deadlock free for any grid size, no co-residency assumption.  Tiles are read with
@@ -109,10 +117,14 @@ __device__ __forceinline__ void wait_flags(const int* fa, const int* fb, int* in
   __syncthreads();
 }
 
-// Diagonal factors are also published to a side buffer Ld[j] = {L_jj as [p][r], 1/diag} that is
-// pre-filled with all-ones bytes (a NaN pattern no arithmetic produces): consumers poll the data
-// itself (one L2 round trip) instead of a flag followed by the loads.
-constexpr int LDW = TS * TS + TS;  // doubles per side-buffer entry
+// Diagonal factors are also published to a side buffer Ld[j] = {L_jj as [p][r], 1/diag, L_{j+1,j} as
+// [p][r], P_j} that is pre-filled with all-ones bytes (a NaN pattern no arithmetic produces):
+// consumers poll the data itself (one L2 round trip) instead of a flag followed by the loads.
+// P_j, the last update of D_j's sub-diagonal tile, is formed by the off-diagonal task (j+1, j-1)
+// right after its own TRSM, so that D_j's trailing TRSM only has to subtract it.
+constexpr int LDW = 3 * TS * TS + TS;     // doubles per side-buffer entry
+constexpr int LDW_SUB = TS * TS + TS;     // offset of L_{j+1,j} in an entry
+constexpr int LDW_P = 2 * TS * TS + TS;   // offset of P_j = L_{j+1,j-1} L_{j,j-1}^T (row-major), for D_j
 constexpr unsigned long long kUnset = ~0ULL;
 
 __device__ __forceinline__ double ld_cg_volatile(const double* p) {
@@ -156,6 +168,38 @@ __device__ __forceinline__ void stage_diag(double (*T)[LDS], double* dv, const d
   if (threadIdx.x < TS) dv[threadIdx.x] = d;
 }
 
+__device__ __forceinline__ bool unset(double v) { return __double_as_longlong(v) == (long long)kUnset; }
+
+// T[p][r] = tile(r, p) from a [p][r] side-buffer block, waiting until published (all threads)
+__device__ __forceinline__ void stage_side(double (*T)[LDS], const double* __restrict__ src, int* info) {
+  constexpr int PER = TS * TS / CT;
+  double v[PER];
+#pragma unroll
+  for (int q = 0; q < PER; ++q) v[q] = ld_cg_volatile(src + threadIdx.x + CT * q);
+  const unsigned long long t0 = gtime();
+  for (;;) {
+    bool ok = true;
+#pragma unroll
+    for (int q = 0; q < PER; ++q)
+      if (unset(v[q])) {
+        v[q] = ld_cg_volatile(src + threadIdx.x + CT * q);
+        ok = false;
+      }
+    if (ok) break;
+    if (gtime() - t0 > kSpinLimitNs) {
+      watchdog_expired(info);
+      break;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int e = threadIdx.x + CT * q;
+    T[e / TS][e % TS] = v[q];
+  }
+}
+
+__device__ __forceinline__ void bar_named(int id, int count) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory"); }
+
 // ticket -> task when there are no U tasks (computed: no table load on the chain): column j holds
 // D_j, then the tiles (i, j), i >= j + 2.  Returns (type, i, j, 0).
 __device__ __forceinline__ int4 task_of(int t, int nt) {
@@ -198,9 +242,11 @@ __device__ __forceinline__ int ready_prefix(const int* __restrict__ flags, int n
 // update, so the dependency chain per column is mul -> fma -> sts/lds -> rsqrt.  The general update
 // reads column J of L from shared memory (broadcast loads) instead of 31 shuffles.  1/L_JJ goes to
 // my_dinv (lane J), bad = first non-positive pivot (or -1).
+__device__ __forceinline__ void bar_arrive(int id, int count) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory"); }
+
 template <int J>
 __device__ __forceinline__ void potrf_step(double (&x)[TS], double (*colL)[LDS], double* piv, int lane, double& my_dinv, int& bad,
-                                           double dj, double inv) {
+                                           double dj, double inv, bool trail) {
   if (!(dj > 0.0) && bad < 0) bad = J;
   const double lj = x[J] * inv;
   x[J] = (lane == J) ? dj * inv : lj;
@@ -218,7 +264,35 @@ __device__ __forceinline__ void potrf_step(double (&x)[TS], double (*colL)[LDS],
   // lanes r < c update their (unused, later zeroed) upper entries too: no select on the chain
 #pragma unroll
   for (int c = J + 1; c < TS; ++c) x[c] = fma(-lj, colL[J][c], x[c]);
-  if constexpr (J + 1 < TS) potrf_step<J + 1>(x, colL, piv, lane, my_dinv, bad, dn, invn);
+  // columns 8q .. 8q+7 and pivots up to 8q+8 are in shared memory: release them to the trailing
+  // TRSM warp (bar.arrive does not wait; the matching bar.sync orders the shared-memory writes)
+  if constexpr ((J & 7) == 7) {
+    if (trail) bar_arrive(3 + J / 8, 64);
+  }
+  if constexpr (J + 1 < TS) potrf_step<J + 1>(x, colL, piv, lane, my_dinv, bad, dn, invn, trail);
+}
+
+// warp 1 of D_j, lane r: row r of X L^T = A (the sub-diagonal tile), a quarter (8 columns) at a
+// time as soon as warp 0's POTRF has released it (named barrier 3 + q: warp 0 arrives without
+// waiting after column 8q + 7, warp 1 syncs): colL[C][c2] = L(c2, C), 1 / L_CC = rsqrt(piv[C])
+// (bitwise warp 0's value).  Static unrolled code, one barrier per quarter: no polling.
+template <int C, int CEND>
+__device__ __forceinline__ void trail_step(double (&x)[TS], const double (*colL)[LDS], const double* piv) {
+  x[C] *= rsqrt(piv[C]);
+#pragma unroll
+  for (int c2 = C + 1; c2 < TS; ++c2) x[c2] = fma(-x[C], colL[C][c2], x[c2]);
+  if constexpr (C + 1 < CEND) trail_step<C + 1, CEND>(x, colL, piv);
+}
+
+__device__ __forceinline__ void trail_rows(double (&x)[TS], const double (*colL)[LDS], const double* piv) {
+  bar_named(3, 64);
+  trail_step<0, 8>(x, colL, piv);
+  bar_named(4, 64);
+  trail_step<8, 16>(x, colL, piv);
+  bar_named(5, 64);
+  trail_step<16, 24>(x, colL, piv);
+  bar_named(6, 64);
+  trail_step<24, 32>(x, colL, piv);
 }
 
 // row solve x L^T = a, L(c, p) = T[p][c], 1/L(c, c) = dv[c] (forward substitution, right-looking)
@@ -244,13 +318,14 @@ __device__ __forceinline__ void acc_load(Acc& a, const double* __restrict__ M, i
       for (int e = 0; e < 2; ++e) a.v[rb][cb][e] = elem(M, ld, N, ti * TS + qr * 16 + rb * 8 + g, tj * TS + qc * 16 + cb * 8 + 2 * tq + e);
 }
 
-// a -= A B^T with A, B staged as T[p][r] = tile(r, p)
+// a -= A B^T (SUB) or a += A B^T with A, B staged as T[p][r] = tile(r, p)
+template <bool SUB = true>
 __device__ __forceinline__ void acc_update(Acc& a, const double (*A)[LDS], const double (*B)[LDS], int qr, int qc, int g, int tq) {
 #pragma unroll
   for (int p0 = 0; p0 < TS; p0 += 4) {
     double fa[2], fb[2];
 #pragma unroll
-    for (int rb = 0; rb < 2; ++rb) fa[rb] = -A[p0 + tq][qr * 16 + rb * 8 + g];  // A frag: row g, k tq
+    for (int rb = 0; rb < 2; ++rb) fa[rb] = SUB ? -A[p0 + tq][qr * 16 + rb * 8 + g] : A[p0 + tq][qr * 16 + rb * 8 + g];  // A frag: row g, k tq
 #pragma unroll
     for (int cb = 0; cb < 2; ++cb) fb[cb] = B[p0 + tq][qc * 16 + cb * 8 + g];   // B frag: k tq, col g
 #pragma unroll
@@ -306,7 +381,7 @@ __device__ __forceinline__ void final_trsm(double (*Ct)[TS + 1], const double (*
 // warp 0: Ct <- chol(Ct) (lower, zero upper), also written with 1/diag to the side buffer entry
 // Ld_out; first failing pivot to info
 __device__ __forceinline__ void final_potrf(double (*Ct)[TS + 1], double (*colL)[LDS], double* piv, double* Ld_out, int col0, int N,
-                                            int* info, int lane) {
+                                            int* info, int lane, bool trail = false) {
   double x[TS];
 #pragma unroll
   for (int c = 0; c < TS; ++c) x[c] = Ct[lane][c];
@@ -315,7 +390,7 @@ __device__ __forceinline__ void final_potrf(double (*Ct)[TS + 1], double (*colL)
   if (lane == 0) piv[0] = x[0];
   __syncwarp();
   const double d0 = piv[0];
-  potrf_step<0>(x, colL, piv, lane, my_dinv, bad, d0, rsqrt(d0));
+  potrf_step<0>(x, colL, piv, lane, my_dinv, bad, d0, rsqrt(d0), trail);
   if (bad >= 0 && lane == 0 && col0 + bad < N) atomicCAS(info, 0, col0 + bad + 1);
 #pragma unroll
   for (int c = 0; c < TS; ++c) {
@@ -337,8 +412,9 @@ __global__ void __launch_bounds__(CT) k_chol_tiles(double* __restrict__ M, int64
                                                    const int4* __restrict__ tasks, int ntasks, double* __restrict__ part,
                                                    int* __restrict__ uflags, int maxc, unsigned long long* __restrict__ trace) {
   __shared__ double Ta[TS][LDS], Tb[TS][LDS];
-  __shared__ double Ct[TS][TS + 1];
-  __shared__ double dv[TS];
+  __shared__ double Ct[TS][TS + 1], Cs[TS][TS + 1];
+  __shared__ double dv[TS], piv[TS];
+  __shared__ unsigned long long s_tx, s_tw, s_tw2;  // trace: external flag seen, warp 1 start (diagonal tasks)
   __shared__ int s_t;
   __shared__ int s_min;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -353,7 +429,12 @@ __global__ void __launch_bounds__(CT) k_chol_tiles(double* __restrict__ M, int64
     const int4 tk = USE_U ? tasks[t] : task_of(t, nt);
     const int i = tk.y, j = tk.z;
     unsigned long long t0 = 0, t1 = 0, t1b = 0, t1c = 0;
-    if (trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    if (trace && threadIdx.x == 0) {
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+      s_tx = 0;
+      s_tw = 0;
+      s_tw2 = 0;
+    }
     if (USE_U && tk.x == 2) {
       // ---- U(j, c): partial sums of D_j's updates over k in [cB, cB + B) ----
       const int c = tk.w;
@@ -364,12 +445,13 @@ __global__ void __launch_bounds__(CT) k_chol_tiles(double* __restrict__ M, int64
         (&pd.v[0][0][0])[e] = 0.0;
       }
       int rdy = c * UB;
+      const int jb = j + 1 < nt ? j + 1 : j;  // the sub-diagonal tile (j+1, j), if any
       for (int k = c * UB; k < (c + 1) * UB; ++k) {
-        if (k >= rdy) rdy = ready_prefix(flags, nt, j, j - 1, k, (c + 1) * UB, &s_min, info);
+        if (k >= rdy) rdy = ready_prefix(flags, nt, j, jb, k, (c + 1) * UB, &s_min, info);
         stage(Ta, M, ld, N, j, k);
-        stage(Tb, M, ld, N, j - 1, k);
+        stage(Tb, M, ld, N, j + 1, k);
         __syncthreads();
-        acc_update(ps, Ta, Tb, qr, qc, g, tq);
+        acc_update(ps, Tb, Ta, qr, qc, g, tq);
         acc_update(pd, Ta, Ta, qr, qc, g, tq);
         __syncthreads();
       }
@@ -402,63 +484,126 @@ __global__ void __launch_bounds__(CT) k_chol_tiles(double* __restrict__ M, int64
       if (w == 0) final_trsm(Ct, Ta, dv, lane);
       if (trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1c));
       __syncthreads();
-      publish(Ct, M, ld, N, i, j, flags + tile_id(i, j, nt));
-    } else {
-      // ---- diagonal task D_j: sub-diagonal tile (j, j-1) and diagonal tile (j, j) ----
-      Acc d;  // A_jj
-      acc_load(d, M, ld, N, j, j, qr, qc, g, tq);
-      if (j > 0) {
-        Acc sb;  // A_{j, j-1}
-        acc_load(sb, M, ld, N, j, j - 1, qr, qc, g, tq);
-        const int nc = USE_U ? max(0, (j - 2) / UB) : 0;  // chunks summed by the U tasks (they end before k = j - 2)
-        for (int c = 0; c < nc; ++c) {
-          wait_flags(uflags + j * maxc + c, nullptr, info);
-          const double* base = part + ((int64_t)j * maxc + c) * 2 * TS * TS;
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            (&sb.v[0][0][0])[e] += __ldcg(base + e * CT + threadIdx.x);
-            (&d.v[0][0][0])[e] += __ldcg(base + TS * TS + e * CT + threadIdx.x);
-          }
-        }
-        int rdy = nc * UB;
-        for (int k = nc * UB; k < j - 1; ++k) {
-          if (k >= rdy) rdy = ready_prefix(flags, nt, j, j - 1, k, j - 1, &s_min, info);
-          stage(Ta, M, ld, N, j, k);
-          stage(Tb, M, ld, N, j - 1, k);
-          __syncthreads();
-          acc_update(sb, Ta, Tb, qr, qc, g, tq);
-          acc_update(d, Ta, Ta, qr, qc, g, tq);
-          __syncthreads();
-        }
-        if (trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-        // L_{j, j-1} = A_{j, j-1} L_{j-1, j-1}^{-T}
-        acc_gather(sb, Ct, qr, qc, g, tq);
-        stage_diag(Ta, dv, Ld + (int64_t)(j - 1) * LDW, info);
-        __syncthreads();
-        if (trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1b));
-        if (w == 0) final_trsm(Ct, Ta, dv, lane);
-        __syncthreads();
-        store_tile(Ct, M, ld, N, j, j - 1);  // released below by warp 1, off the POTRF path
-        // A_jj -= L_{j, j-1} L_{j, j-1}^T from the tile still in shared memory
+      if (i == j + 2) {
+        // P_{j+1} = L_{j+2,j} L_{j+1,j}^T, the last update of D_{j+1}'s sub-diagonal tile (j+2, j+1)
+        stage_side(Ta, Ld + (int64_t)j * LDW + LDW_SUB, info);  // Ta[p][r] = L_{j+1,j}(r, p)
 #pragma unroll
         for (int q = 0; q < TS * TS / CT; ++q) {
           const int p = (threadIdx.x >> 5) + 4 * q;
-          Ta[p][lane] = Ct[lane][p];
+          Tb[p][lane] = Ct[lane][p];  // Tb[p][r] = L_{j+2,j}(r, p)
         }
         __syncthreads();
-        acc_update(d, Ta, Ta, qr, qc, g, tq);
-        __syncthreads();
-      } else if (trace && threadIdx.x == 0) {
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-        t1b = t1;
+        Acc pp;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) (&pp.v[0][0][0])[e] = 0.0;
+        acc_update<false>(pp, Tb, Ta, qr, qc, g, tq);
+        double* P = Ld + (int64_t)(j + 1) * LDW + LDW_P;
+#pragma unroll
+        for (int rb = 0; rb < 2; ++rb)
+#pragma unroll
+          for (int cb = 0; cb < 2; ++cb)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) P[(qr * 16 + rb * 8 + g) * TS + qc * 16 + cb * 8 + 2 * tq + e] = pp.v[rb][cb][e];
       }
+      publish(Ct, M, ld, N, i, j, flags + tile_id(i, j, nt));
+    } else {
+      // ---- diagonal task D_j: diagonal tile (j, j) and sub-diagonal tile (j+1, j) ----
+      const bool has_sb = j + 1 < nt;
+      Acc d;   // A_jj
+      Acc sb;  // A_{j+1, j}
+      acc_load(d, M, ld, N, j, j, qr, qc, g, tq);
+      acc_load(sb, M, ld, N, j + 1, j, qr, qc, g, tq);  // rows past N read as zero (never published)
+      const int nc = USE_U ? max(0, (j - 2) / UB) : 0;  // chunks summed by the U tasks (they end before k = j - 2)
+      for (int c = 0; c < nc; ++c) {
+        wait_flags(uflags + j * maxc + c, nullptr, info);
+        const double* base = part + ((int64_t)j * maxc + c) * 2 * TS * TS;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          (&sb.v[0][0][0])[e] += __ldcg(base + e * CT + threadIdx.x);
+          (&d.v[0][0][0])[e] += __ldcg(base + TS * TS + e * CT + threadIdx.x);
+        }
+      }
+      int rdy = nc * UB;
+      for (int k = nc * UB; k < j - 1; ++k) {
+        if (k >= rdy) rdy = ready_prefix(flags, nt, j, has_sb ? j + 1 : j, k, j - 1, &s_min, info);
+        stage(Ta, M, ld, N, j, k);
+        stage(Tb, M, ld, N, j + 1, k);
+        __syncthreads();
+        acc_update(d, Ta, Ta, qr, qc, g, tq);
+        acc_update(sb, Tb, Ta, qr, qc, g, tq);
+        __syncthreads();
+      }
+      if (trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+      if (j > 0) {  // A_jj -= L_{j,j-1} L_{j,j-1}^T with L_{j,j-1} from D_{j-1} (side buffer, polled as data)
+        stage_side(Ta, Ld + (int64_t)(j - 1) * LDW + LDW_SUB, info);
+        __syncthreads();
+        acc_update(d, Ta, Ta, qr, qc, g, tq);
+      }
+      if (trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1b));
       acc_gather(d, Ct, qr, qc, g, tq);
+      acc_gather(sb, Cs, qr, qc, g, tq);
       __syncthreads();
-      if (j > 0 && threadIdx.x == 32) release(flags + tile_id(j, j - 1, nt));
-      if (w == 0) final_potrf(Ct, Tb, dv, Ld + (int64_t)j * LDW, j * TS, N, info, lane);
-      if (trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1c));
+      if (w == 0) {
+        // POTRF of the diagonal tile: L_jj and 1/diag to the side buffer, then the tile to M
+        final_potrf(Ct, Tb, piv, Ld + (int64_t)j * LDW, j * TS, N, info, lane, has_sb);
+        if (trace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1c));
+#pragma unroll 4
+        for (int c = 0; c < TS; ++c) {
+          const int gr = j * TS + lane, gc = j * TS + c;
+          if (gr < N && gc < N) M[gr + (int64_t)gc * ld] = Ct[lane][c];
+        }
+      } else if (has_sb) {
+        if (w >= 2 && j > 0) {
+          // the sub-diagonal tile's last update, A_{j+1,j} -= P_j (formed by the off-diagonal task
+          // (j+1, j-1), polled as data)
+          const int t2 = threadIdx.x - 64;
+          const double* P = Ld + (int64_t)j * LDW + LDW_P;
+          double v[TS * TS / 64];
+#pragma unroll
+          for (int q = 0; q < TS * TS / 64; ++q) v[q] = ld_cg_volatile(P + t2 + 64 * q);
+          const unsigned long long tw = gtime();
+          for (;;) {
+            bool ok = true;
+#pragma unroll
+            for (int q = 0; q < TS * TS / 64; ++q)
+              if (unset(v[q])) {
+                v[q] = ld_cg_volatile(P + t2 + 64 * q);
+                ok = false;
+              }
+            if (ok) break;
+            if (gtime() - tw > kSpinLimitNs) {
+              watchdog_expired(info);
+              break;
+            }
+          }
+          if (trace && t2 == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(s_tx));
+#pragma unroll
+          for (int q = 0; q < TS * TS / 64; ++q) {
+            const int e = t2 + 64 * q;
+            Cs[e / TS][e % TS] -= v[q];
+          }
+        }
+        bar_named(2, 96);
+        if (w == 1) {
+          // L_{j+1,j} = A_{j+1,j} L_jj^{-T}, one step behind warp 0's POTRF
+          if (trace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(s_tw));
+          double x[TS];
+#pragma unroll
+          for (int c = 0; c < TS; ++c) x[c] = Cs[lane][c];
+          trail_rows(x, Tb, piv);
+          if (trace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(s_tw2));
+          double* sub = Ld + (int64_t)j * LDW + LDW_SUB;
+          const int gr = (j + 1) * TS + lane;
+#pragma unroll
+          for (int c = 0; c < TS; ++c) sub[c * TS + lane] = x[c];  // [p][r] order, coalesced: D_{j+1} polls these first
+#pragma unroll
+          for (int c = 0; c < TS; ++c)
+            if (gr < N && j * TS + c < N) M[gr + (int64_t)(j * TS + c) * ld] = x[c];
+          __syncwarp();
+          if (lane == 0) release(flags + tile_id(j + 1, j, nt));
+        }
+      }
       __syncthreads();
-      publish(Ct, M, ld, N, j, j, flags + tile_id(j, j, nt));
     }
     if (trace && threadIdx.x == 0) {
       unsigned long long t2;
@@ -470,7 +615,11 @@ __global__ void __launch_bounds__(CT) k_chol_tiles(double* __restrict__ M, int64
       trace[6 * t + 2] = t1b;
       trace[6 * t + 3] = t1c;
       trace[6 * t + 4] = t2;
-      trace[6 * t + 5] = sm;
+      trace[6 * t + 5] = (tk.x == 0 && i == j) ? s_tw : sm;  // diagonal tasks: warp 1's start
+      if (tk.x == 0 && i == j) {
+        trace[6 * ntasks + j] = s_tx;
+        trace[6 * ntasks + nt + j] = s_tw2;
+      }
     }
   }
 }

@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "fk_internal.cuh"
@@ -34,7 +35,8 @@ int main(int argc, char** argv) {
   cudaMalloc(&ws, fk::chol_ws_bytes(N));
   const int nt = (N + 31) / 32, ntiles = nt * (nt + 1) / 2;
   unsigned long long* trace;
-  cudaMalloc(&trace, (size_t)ntiles * 48);
+  cudaMalloc(&trace, (size_t)ntiles * 48 + (size_t)(2 * nt + 64) * 8);
+  cudaMemset(trace, 0, (size_t)ntiles * 48 + (size_t)(2 * nt + 64) * 8);
   cusolverDnHandle_t h;
   cusolverDnCreate(&h);
   int lwork = 0;
@@ -68,7 +70,7 @@ int main(int argc, char** argv) {
     for (int i = j; i < N; ++i) md = std::max(md, std::fabs(Lt[i + (size_t)j * N] - Lc[i + (size_t)j * N]));
   printf("max |L_tiles - L_cusolver| = %.3e\n", md);
   if (tr) {
-    std::vector<unsigned long long> t((size_t)ntiles * 6);
+    std::vector<unsigned long long> t((size_t)ntiles * 6 + 2 * nt + 64);
     cudaMemcpy(t.data(), trace, t.size() * 8, cudaMemcpyDeviceToHost);
     FILE* f = fopen(tr, "w");
     unsigned long long base = ~0ULL;
@@ -78,6 +80,11 @@ int main(int argc, char** argv) {
       fprintf(f, "%d %llu %llu %llu %llu %llu %llu\n", k, t[6 * k] - base, t[6 * k + 1] - base, t[6 * k + 2] - base,
               t[6 * k + 3] - base, t[6 * k + 4] - base, t[6 * k + 5]);
     fclose(f);
+    // diagonal tasks: the external-flag time (slot 6 * ntasks + j; ntasks <= ntiles), raw
+    std::string ex = std::string(tr) + ".ext";
+    FILE* g = fopen(ex.c_str(), "w");
+    for (size_t k = 0; k < t.size(); ++k) fprintf(g, "%llu\n", t[k]);
+    fclose(g);
   }
   return 0;
 }
