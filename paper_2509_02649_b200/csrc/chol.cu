@@ -688,6 +688,8 @@ CholReset chol_reset_args(int N, void* ws, int* info) {
   return c;
 }
 
+// trace (measurement only, tools/microbench/mb_chol_tiles.cu): 6 words per ticket, then 2 per tile
+// column (diagonal tasks: the time P_j was seen, the time warp 1's TRSM ended), or null.
 fk_status chol_tiles(double* M, int64_t ld, int N, int* info, void* ws, cudaStream_t s, unsigned long long* trace, bool preset) {
   const int nt = (N + TS - 1) / TS;
   const int ntiles = nt * (nt + 1) / 2;

@@ -35,8 +35,11 @@ int main(int argc, char** argv) {
   cudaMalloc(&ws, fk::chol_ws_bytes(N));
   const int nt = (N + 31) / 32, ntiles = nt * (nt + 1) / 2;
   unsigned long long* trace;
-  cudaMalloc(&trace, (size_t)ntiles * 48 + (size_t)(2 * nt + 64) * 8);
-  cudaMemset(trace, 0, (size_t)ntiles * 48 + (size_t)(2 * nt + 64) * 8);
+  // trace layout (chol.cu): 6 words per ticket (U tasks included: < ntiles + nt * (nt / 16 + 1) tickets),
+  // then 2 * nt words for the diagonal tasks
+  const size_t tr_words = (size_t)6 * (ntiles + (size_t)nt * (nt / 16 + 1)) + 2 * nt + 64;
+  cudaMalloc(&trace, tr_words * 8);
+  cudaMemset(trace, 0, tr_words * 8);
   cusolverDnHandle_t h;
   cusolverDnCreate(&h);
   int lwork = 0;
@@ -70,7 +73,7 @@ int main(int argc, char** argv) {
     for (int i = j; i < N; ++i) md = std::max(md, std::fabs(Lt[i + (size_t)j * N] - Lc[i + (size_t)j * N]));
   printf("max |L_tiles - L_cusolver| = %.3e\n", md);
   if (tr) {
-    std::vector<unsigned long long> t((size_t)ntiles * 6 + 2 * nt + 64);
+    std::vector<unsigned long long> t(tr_words);
     cudaMemcpy(t.data(), trace, t.size() * 8, cudaMemcpyDeviceToHost);
     FILE* f = fopen(tr, "w");
     unsigned long long base = ~0ULL;
