@@ -431,7 +431,9 @@ def main():
     if d == 1 and eps >= 1e-7 and not args.no_paper_precision and graph is None:
         pp = paper_precision(args, cfg, X, Y, n, n_loc, world, dev, buffers, theta, pik, peaks)
     others = None
+    rows = None
     if args.config == "c2" and args.n is None and world == 1 and not args.no_other_configs:
+        rows = c2_rows(args, cfg, buffers, theta, n, peaks, dev)
         del X, Y, buffers
         torch.cuda.empty_cache()
         others = other_configs(args, dev)
@@ -461,6 +463,7 @@ def main():
             "fit_status_ok": fit_ok,
             "paper_precision": pp,
             "other_configs": others,
+            "rows": rows,
             "hbm_gbs_fit": n_loc * (d + 1) * 4 / (ms_step * 1e-3) / 1e9,
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -545,6 +548,47 @@ def paper_precision(args, cfg, X, Y, n, n_loc, world, dev, buffers, theta, pik, 
                                            "(<= 1e-10 l2 and 1e-9 n per element vs the fp64 direct sums)"},
         "fit_status_ok": int(st.item()) == 0,
     }
+
+
+def c2_rows(args, cfg, buffers, theta, n, peaks, dev):
+    """The two other timed rows of the C2 path, on the fit's own moments and theta, so the driver's
+    default run sees them (bench_rows.py has the full set): the solve (A10/A11: assembly, tile
+    Cholesky, back substitution; CUDA events inside fk_solve, median of 7) and the type-2 prediction
+    (A12) of 2^30 resident fp32 queries, against the HBM roofline of its 8 B per query."""
+    import torch
+
+    from paper_2509_02649_b200 import fk
+
+    d, m, L = cfg["d"], cfg["m"], 1.0
+    _, mu, r = buffers
+    ms = []
+    for _ in range(9):
+        _, rep_ = fk.fk_solve(mu.reshape(-1), r.reshape(-1), n, d, m, L, cfg["lam"], cfg["kind"], cfg["s"], report=True)
+        ms.append(rep_["ms"])
+    ms = sorted(ms[2:])
+    solve = {"row": "A10/A11 assemble + solve", "D": rep_["n_unknowns"], "ms": ms[len(ms) // 2], "backward_err": rep_["backward_err"],
+             "rcond_est": rep_["rcond_est"], "method": "tile dataflow Cholesky + multi-SM back substitution (fp64)"}
+    nq = 1 << 30
+    Xq = torch.rand(nq, device=dev, dtype=torch.float32) * 2.0 - 1.0
+    out = torch.empty(nq, device=dev, dtype=torch.float32)
+    for _ in range(3):
+        fk.fk_predict_type2(theta, d, m, L, Xq, args.eps, out=out)
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 10
+    torch.cuda.synchronize()
+    e0.record(s)
+    for _ in range(reps):
+        fk.fk_predict_type2(theta, d, m, L, Xq, args.eps, out=out)
+    e1.record(s)
+    torch.cuda.synchronize()
+    pms = e0.elapsed_time(e1) / reps
+    gbs = nq * 8 / (pms * 1e-3) / 1e9
+    peak = peaks.get("hbm_gbs", 6650.0)
+    pred = {"row": "A12 predict (type-2)", "queries": nq, "ms": pms, "queries_per_s": nq / (pms * 1e-3),
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak, "bytes_per_query": 8}}
+    del Xq, out
+    return {"solve": solve, "predict": pred}
 
 
 def other_configs(args, dev):
