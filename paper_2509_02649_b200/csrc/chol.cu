@@ -16,9 +16,10 @@
 //     (named barriers, bar.arrive on warp 0's side: it never waits).  Warps 2-3 first subtract the
 //     sub-diagonal tile's last update P_j = L_{j+1,j-1} L_{j,j-1}^T, which the off-diagonal task
 //     (j+1, j-1) forms right after its own TRSM.  So the TRSM runs beside the POTRF instead of
-//     after it on the chain.  L_jj, 1/diag(L_jj), L_{j+1,j} and P_j live in a sentinel-filled side
-//     buffer that consumers poll as data.  (Round 2: round 1 ran the TRSM of (j, j-1) inside D_j
-//     before its POTRF; N = 2002 0.45 -> 0.43 ms, 4226 1.48 -> 1.42 ms.  What remains on the chain
+//     after it on the chain (warp 0 also publishes 1/L_CC per column, so warp 1 has no rsqrt on its
+//     own chain).  L_jj, 1/diag(L_jj), L_{j+1,j} and P_j live in a sentinel-filled side buffer that
+//     consumers poll as data.  (Round 2: round 1 ran the TRSM of (j, j-1) inside D_j before its
+//     POTRF; N = 2002 0.45 -> 0.405 ms, 2600 0.70 -> 0.60, 4226 1.48 -> 1.40 ms.  What remains on the chain
 //     per 32 columns: the POTRF, ~3.3 us of fp64 latency, warp 1's lag behind it (the SM is shared
 //     with update tasks) and one L2 round trip to the next diagonal task.)
 // Tasks are handed out by an atomic ticket counter in dependency order, so a CTA only ever waits
@@ -245,12 +246,15 @@ __device__ __forceinline__ int ready_prefix(const int* __restrict__ flags, int n
 __device__ __forceinline__ void bar_arrive(int id, int count) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory"); }
 
 template <int J>
-__device__ __forceinline__ void potrf_step(double (&x)[TS], double (*colL)[LDS], double* piv, int lane, double& my_dinv, int& bad,
-                                           double dj, double inv, bool trail) {
+__device__ __forceinline__ void potrf_step(double (&x)[TS], double (*colL)[LDS], double* piv, double* dinv, int lane, double& my_dinv,
+                                           int& bad, double dj, double inv, bool trail) {
   if (!(dj > 0.0) && bad < 0) bad = J;
   const double lj = x[J] * inv;
   x[J] = (lane == J) ? dj * inv : lj;
-  if (lane == J) my_dinv = inv;
+  if (lane == J) {
+    my_dinv = inv;
+    dinv[J] = inv;
+  }
   colL[J][lane] = lj;
   if constexpr (J + 1 < TS) {
     if (lane == J + 1) piv[J + 1] = fma(-lj, lj, x[J + 1]);
@@ -269,30 +273,31 @@ __device__ __forceinline__ void potrf_step(double (&x)[TS], double (*colL)[LDS],
   if constexpr ((J & 7) == 7) {
     if (trail) bar_arrive(3 + J / 8, 64);
   }
-  if constexpr (J + 1 < TS) potrf_step<J + 1>(x, colL, piv, lane, my_dinv, bad, dn, invn, trail);
+  if constexpr (J + 1 < TS) potrf_step<J + 1>(x, colL, piv, dinv, lane, my_dinv, bad, dn, invn, trail);
 }
+
 
 // warp 1 of D_j, lane r: row r of X L^T = A (the sub-diagonal tile), a quarter (8 columns) at a
 // time as soon as warp 0's POTRF has released it (named barrier 3 + q: warp 0 arrives without
 // waiting after column 8q + 7, warp 1 syncs): colL[C][c2] = L(c2, C), 1 / L_CC = rsqrt(piv[C])
 // (bitwise warp 0's value).  Static unrolled code, one barrier per quarter: no polling.
 template <int C, int CEND>
-__device__ __forceinline__ void trail_step(double (&x)[TS], const double (*colL)[LDS], const double* piv) {
-  x[C] *= rsqrt(piv[C]);
+__device__ __forceinline__ void trail_step(double (&x)[TS], const double (*colL)[LDS], const double* dinv) {
+  x[C] *= dinv[C];
 #pragma unroll
   for (int c2 = C + 1; c2 < TS; ++c2) x[c2] = fma(-x[C], colL[C][c2], x[c2]);
-  if constexpr (C + 1 < CEND) trail_step<C + 1, CEND>(x, colL, piv);
+  if constexpr (C + 1 < CEND) trail_step<C + 1, CEND>(x, colL, dinv);
 }
 
-__device__ __forceinline__ void trail_rows(double (&x)[TS], const double (*colL)[LDS], const double* piv) {
+__device__ __forceinline__ void trail_rows(double (&x)[TS], const double (*colL)[LDS], const double* dinv) {
   bar_named(3, 64);
-  trail_step<0, 8>(x, colL, piv);
+  trail_step<0, 8>(x, colL, dinv);
   bar_named(4, 64);
-  trail_step<8, 16>(x, colL, piv);
+  trail_step<8, 16>(x, colL, dinv);
   bar_named(5, 64);
-  trail_step<16, 24>(x, colL, piv);
+  trail_step<16, 24>(x, colL, dinv);
   bar_named(6, 64);
-  trail_step<24, 32>(x, colL, piv);
+  trail_step<24, 32>(x, colL, dinv);
 }
 
 // row solve x L^T = a, L(c, p) = T[p][c], 1/L(c, c) = dv[c] (forward substitution, right-looking)
@@ -380,17 +385,19 @@ __device__ __forceinline__ void final_trsm(double (*Ct)[TS + 1], const double (*
 
 // warp 0: Ct <- chol(Ct) (lower, zero upper), also written with 1/diag to the side buffer entry
 // Ld_out; first failing pivot to info
-__device__ __forceinline__ void final_potrf(double (*Ct)[TS + 1], double (*colL)[LDS], double* piv, double* Ld_out, int col0, int N,
-                                            int* info, int lane, bool trail = false) {
+__device__ __forceinline__ void final_potrf(double (*Ct)[TS + 1], double (*colL)[LDS], double* piv, double* dinv, double* Ld_out, int col0,
+                                            int N, int* info, int lane, bool trail = false) {
   double x[TS];
 #pragma unroll
   for (int c = 0; c < TS; ++c) x[c] = Ct[lane][c];
   double my_dinv = 1.0;
   int bad = -1;
+  // (2 x 2 pivot blocks in this one-warp loop -- two independent rsqrt per two columns -- measured
+  // 11.3k vs 6.5k cycles per tile: tools/microbench/mb_potrf.cu, profiles/r02_solve_study.md)
   if (lane == 0) piv[0] = x[0];
   __syncwarp();
   const double d0 = piv[0];
-  potrf_step<0>(x, colL, piv, lane, my_dinv, bad, d0, rsqrt(d0), trail);
+  potrf_step<0>(x, colL, piv, dinv, lane, my_dinv, bad, d0, rsqrt(d0), trail);
   if (bad >= 0 && lane == 0 && col0 + bad < N) atomicCAS(info, 0, col0 + bad + 1);
 #pragma unroll
   for (int c = 0; c < TS; ++c) {
@@ -413,7 +420,7 @@ __global__ void __launch_bounds__(CT) k_chol_tiles(double* __restrict__ M, int64
                                                    int* __restrict__ uflags, int maxc, unsigned long long* __restrict__ trace) {
   __shared__ double Ta[TS][LDS], Tb[TS][LDS];
   __shared__ double Ct[TS][TS + 1], Cs[TS][TS + 1];
-  __shared__ double dv[TS], piv[TS];
+  __shared__ double dv[TS], piv[TS], dinv_s[TS];
   __shared__ unsigned long long s_tx, s_tw, s_tw2;  // trace: external flag seen, warp 1 start (diagonal tasks)
   __shared__ int s_t;
   __shared__ int s_min;
@@ -545,7 +552,7 @@ __global__ void __launch_bounds__(CT) k_chol_tiles(double* __restrict__ M, int64
       __syncthreads();
       if (w == 0) {
         // POTRF of the diagonal tile: L_jj and 1/diag to the side buffer, then the tile to M
-        final_potrf(Ct, Tb, piv, Ld + (int64_t)j * LDW, j * TS, N, info, lane, has_sb);
+        final_potrf(Ct, Tb, piv, dinv_s, Ld + (int64_t)j * LDW, j * TS, N, info, lane, has_sb);
         if (trace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1c));
 #pragma unroll 4
         for (int c = 0; c < TS; ++c) {
@@ -590,7 +597,7 @@ __global__ void __launch_bounds__(CT) k_chol_tiles(double* __restrict__ M, int64
           double x[TS];
 #pragma unroll
           for (int c = 0; c < TS; ++c) x[c] = Cs[lane][c];
-          trail_rows(x, Tb, piv);
+          trail_rows(x, Tb, dinv_s);
           if (trace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(s_tw2));
           double* sub = Ld + (int64_t)j * LDW + LDW_SUB;
           const int gr = (j + 1) * TS + lane;

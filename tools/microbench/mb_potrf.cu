@@ -11,7 +11,7 @@ namespace {
 __global__ void __launch_bounds__(CT) k_potrf_lat(const double* A, double* Lout, double* Wout, long long* cyc, int reps, int mode) {
   __shared__ double Tb[TS][LDS];
   __shared__ double Ct[TS][TS + 1];
-  __shared__ double dv[TS];
+  __shared__ double dv[TS], piv[TS];
   __shared__ int info;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int r = 0; r < reps; ++r) {
@@ -23,7 +23,7 @@ __global__ void __launch_bounds__(CT) k_potrf_lat(const double* A, double* Lout,
     __syncthreads();
     long long t0 = clock64();
     if (w == 0) {
-      if (mode == 0) final_potrf(Ct, Tb, dv, Wout, 0, TS, &info, lane);
+      if (mode == 0) final_potrf(Ct, Tb, piv, dv, Wout, 0, TS, &info, lane);
       else final_trsm(Ct, Tb, dv, lane);
     }
     __syncthreads();

@@ -8,7 +8,7 @@ namespace fk { namespace {
 __global__ void __launch_bounds__(CT) k_conc(const double* A, const double* B, double* Lout, double* Xout, long long* cyc, int reps, int mode) {
   __shared__ double Tb[TS][LDS];
   __shared__ double Ct[TS][TS + 1], Cs[TS][TS + 1];
-  __shared__ double piv[TS];
+  __shared__ double piv[TS], dinv[TS];
   __shared__ int info;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int r = 0; r < reps; ++r) {
@@ -16,11 +16,11 @@ __global__ void __launch_bounds__(CT) k_conc(const double* A, const double* B, d
     if (threadIdx.x == 0) info = 0;
     __syncthreads();
     long long t0 = clock64(), t1 = 0;
-    if (w == 0) { final_potrf(Ct, Tb, piv, Lout + 2 * TS * TS, 0, TS, &info, lane, mode != 0); t1 = clock64(); }
+    if (w == 0) { final_potrf(Ct, Tb, piv, dinv, Lout + 2 * TS * TS, 0, TS, &info, lane, mode != 0); t1 = clock64(); }
     else if (w == 1 && mode) {
       double x[TS];
       for (int c = 0; c < TS; ++c) x[c] = Cs[lane][c];
-      trail_rows(x, Tb, piv);
+      trail_rows(x, Tb, dinv);
       for (int c = 0; c < TS; ++c) Cs[lane][c] = x[c];
       t1 = clock64();
     }
