@@ -90,3 +90,20 @@ def test_tiles_report_not_spd_with_partial_tasks(F):
             F.fk_solve(mu, r, 1000, 1, m, 1.0, 1e-9, "sobolev", 1.0)
     finally:
         del os.environ["FK_CHOL"]
+
+
+@pytest.mark.parametrize("m", [14, 15, 16, 30, 31, 47, 63, 1278, 1279, 1280])
+def test_tiles_size_sweep(F, oracle, m):
+    """Tile-boundary sizes of the dataflow Cholesky (N = 2m + 2: partial last tile, exact multiples
+    of 32, the one-tile-column-per-step structure of the diagonal task with its trailing TRSM warp,
+    and the switch to the partial-accumulation tasks at 80 tile columns, N = 2560) against
+    cuSOLVER potrf on the same d = 1 fit system."""
+    n = 3000
+    X, Y = datagen.dataset(n, d=1, ykind="sin", seed=90 + m)
+    mu, r = oracle.moments(X, 1.0, m), oracle.rhs(X, Y, 1.0, m)
+    args = (dev(mu.reshape(-1)), dev(r.reshape(-1)), n, 1, m, 1.0, 1e-5, "sobolev", 1.0)
+    th_t, rep_t = _solve(F, "tiles", *args)
+    th_c, rep_c = _solve(F, "cusolver", *args)
+    assert rep_t["info"] == 0
+    assert rep_t["backward_err"] <= max(10 * rep_c["backward_err"], 1e-14)
+    assert rel(th_t, th_c) <= 1e-9
