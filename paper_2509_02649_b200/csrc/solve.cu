@@ -19,6 +19,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <map>
+#include <tuple>
 #include <vector>
 #include <mutex>
 
@@ -1346,6 +1347,28 @@ static fk_status lauum(cublasHandle_t bh, const double* X, int64_t ldx, double* 
   return lauum(bh, X + n1 + n1 * ldx, ldx, A + n1 + n1 * lda, lda, n2);
 }
 
+// per-device stream + events for the CG iterations (created once, kept for the process)
+static fk_status pcg_stream(cudaStream_t* cs, cudaEvent_t* ev_in, cudaEvent_t* ev_out) {
+  static std::mutex mu;
+  static std::map<int, std::tuple<cudaStream_t, cudaEvent_t, cudaEvent_t>> per_dev;
+  int dev = 0;
+  FK_CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = per_dev.find(dev);
+  if (it == per_dev.end()) {
+    cudaStream_t st;
+    cudaEvent_t a, b;
+    FK_CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    FK_CUDA_TRY(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+    FK_CUDA_TRY(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+    it = per_dev.emplace(dev, std::make_tuple(st, a, b)).first;
+  }
+  *cs = std::get<0>(it->second);
+  *ev_in = std::get<1>(it->second);
+  *ev_out = std::get<2>(it->second);
+  return FK_OK;
+}
+
 static bool pcg_pi(const SysArgs& g) { return (g.kind == FK_PIK_BOX || g.kind == FK_PIK_COLLOC) && g.mu_pde != 0.0; }
 
 static bool pcg_eligible(const SysArgs& g) {
@@ -1495,34 +1518,76 @@ static fk_status pcg_run(SysArgs g, const double2* r, double* x, int* iters, voi
   const double tol = 1e-13;
   const int kMaxIter = 1000, kCheck = 10;
   double hsc[7] = {0, 0, 0, 0, 0, 0, 0};
-  int it = 0;
-  for (; it < kMaxIter;) {
-    for (int j = 0; j < kCheck; ++j, ++it) {
+  // the iterations run on the library's per-device CG stream (capturable even when the caller passes
+  // the legacy default stream), ordered after / before the caller's stream by events
+  cudaStream_t cs = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  FK_TRY(pcg_stream(&cs, &ev_in, &ev_out));
+  FK_CUDA_TRY(cudaEventRecord(ev_in, s));
+  FK_CUDA_TRY(cudaStreamWaitEvent(cs, ev_in, 0));
+  // one block of kCheck iterations (kCheck even: the p ping-pong parity repeats), launched as ONE
+  // CUDA graph per block after the first: ~9 launches per iteration otherwise left the GPU idle
+  // between its short kernels (round 2: C3 solve 5.7 -> see DESIGN §5).  The kernels skip their
+  // work once converged (sc[4]), so a block may overrun the convergence point harmlessly.
+  auto block = [&](int it0) -> fk_status {
+    for (int j = 0; j < kCheck; ++j) {
+      const int it = it0 + j;
       double* p_old = pv[it & 1];
       double* p_new = pv[(it + 1) & 1];
-      k_pcg_scatter<<<(unsigned)((nhalf + TB - 1) / TB), TB, 0, s>>>(g, q, zv, p_old, p_new, H, sc);
+      k_pcg_scatter<<<(unsigned)((nhalf + TB - 1) / TB), TB, 0, cs>>>(g, q, zv, p_old, p_new, H, sc);
       // PI penalty: D theta from the scattered iterate, before the C2R transform below consumes H
-      if (pi) k_pcg_dmul<<<(unsigned)((nhalf + TB - 1) / TB), TB, 0, s>>>(g, q, H, Hd, sc);
-      FK_TRY(fft_exec_z2d(fz, (cufftDoubleComplex*)H, G, fwork, s));
-      k_pcg_mul<<<(unsigned)((nreal + TB - 1) / TB), TB, 0, s>>>(G, muhat, nreal, sc);
-      FK_TRY(fft_exec_d2z(fd, G, (cufftDoubleComplex*)H, fwork, s));
+      if (pi) k_pcg_dmul<<<(unsigned)((nhalf + TB - 1) / TB), TB, 0, cs>>>(g, q, H, Hd, sc);
+      FK_TRY(fft_exec_z2d(fz, (cufftDoubleComplex*)H, G, fwork, cs));
+      k_pcg_mul<<<(unsigned)((nreal + TB - 1) / TB), TB, 0, cs>>>(G, muhat, nreal, sc);
+      FK_TRY(fft_exec_d2z(fd, G, (cufftDoubleComplex*)H, fwork, cs));
       if (pi) {  // the PI penalty's convolution: values of D theta -> x s' -> back
-        FK_TRY(fft_exec_z2d(fz, (cufftDoubleComplex*)Hd, Gd, fwork, s));
-        k_pcg_mul<<<(unsigned)((nreal + TB - 1) / TB), TB, 0, s>>>(Gd, shat, nreal, sc);
-        FK_TRY(fft_exec_d2z(fd, Gd, (cufftDoubleComplex*)Hd, fwork, s));
-        count_launch(2);
+        FK_TRY(fft_exec_z2d(fz, (cufftDoubleComplex*)Hd, Gd, fwork, cs));
+        k_pcg_mul<<<(unsigned)((nreal + TB - 1) / TB), TB, 0, cs>>>(Gd, shat, nreal, sc);
+        FK_TRY(fft_exec_d2z(fd, Gd, (cufftDoubleComplex*)Hd, fwork, cs));
       }
-      k_pcg_gather<<<gD, TB, 0, s>>>(g, q, H, p_new, qv, sc, part, tickets + 2, Hd);
-      k_pcg_update<<<gD, TB, 0, s>>>(D, p_new, qv, d_lowpos, x, rv, rl, sc, tol * tol, part, tickets + 3);
-      k_pcg_precond<<<gP, TB, 0, s>>>(D, rv, dinv, d_lowpos, d_low, Dl, Ainv, lda, rl, zv, sc, 0, nlow_ctas, part, tickets + 1);
-      count_launch(5);
+      k_pcg_gather<<<gD, TB, 0, cs>>>(g, q, H, p_new, qv, sc, part, tickets + 2, Hd);
+      k_pcg_update<<<gD, TB, 0, cs>>>(D, p_new, qv, d_lowpos, x, rv, rl, sc, tol * tol, part, tickets + 3);
+      k_pcg_precond<<<gP, TB, 0, cs>>>(D, rv, dinv, d_lowpos, d_low, Dl, Ainv, lda, rl, zv, sc, 0, nlow_ctas, part, tickets + 1);
     }
-    FK_CUDA_TRY(cudaMemcpyAsync(hsc, sc, 56, cudaMemcpyDeviceToHost, s));
-    FK_CUDA_TRY(cudaStreamSynchronize(s));
+    return FK_OK;
+  };
+  const int per_block = kCheck * (pi ? 7 : 5);
+  struct GraphGuard {  // the block's graph, destroyed on every exit path
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    ~GraphGuard() {
+      if (exec) cudaGraphExecDestroy(exec);
+      if (graph) cudaGraphDestroy(graph);
+    }
+  } gg;
+  cudaGraph_t& graph = gg.graph;
+  cudaGraphExec_t& gexec = gg.exec;
+  int it = 0;
+  for (; it < kMaxIter; it += kCheck) {
+    if (it == 0) {
+      const fk_status st = block(0);  // the first block eagerly (most solves need several)
+      if (st != FK_OK) return st;
+    } else {
+      if (!gexec) {
+        fk_status st = FK_OK;
+        if (cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return fail(FK_E_CUDA, "pcg: stream capture failed");
+        st = block(it);
+        const cudaError_t ce = cudaStreamEndCapture(cs, &graph);
+        if (st != FK_OK) return st;
+        if (ce != cudaSuccess || cudaGraphInstantiate(&gexec, graph, 0) != cudaSuccess)
+          return fail(FK_E_CUDA, "pcg: graph capture of the CG block failed");
+      }
+      if (cudaGraphLaunch(gexec, cs) != cudaSuccess) return fail(FK_E_CUDA, "pcg: graph launch failed");
+    }
+    count_launch(per_block);
+    FK_CUDA_TRY(cudaMemcpyAsync(hsc, sc, 56, cudaMemcpyDeviceToHost, cs));
+    FK_CUDA_TRY(cudaStreamSynchronize(cs));
     if (getenv("FK_PCG_DEBUG"))
       fprintf(stderr, "fk pcg: it %d |r|^2/|b|^2 %.3e (Dl %d of %d, pi %d)\n", (int)hsc[6], hsc[1] / hsc[2], Dl, D, (int)pi);
     if (hsc[4] != 0.0 || !(hsc[1] == hsc[1])) break;  // converged, or NaN (a failed block factor)
   }
+  FK_CUDA_TRY(cudaEventRecord(ev_out, cs));
+  FK_CUDA_TRY(cudaStreamWaitEvent(s, ev_out, 0));
   FK_CUDA_TRY(cudaGetLastError());
   *iters = (int)hsc[6];
   if (hsc[4] == 0.0) return fail(FK_E_SOLVE, "fk_solve (pcg): no convergence in " + std::to_string(kMaxIter) + " iterations");
