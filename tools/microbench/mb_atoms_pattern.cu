@@ -27,7 +27,11 @@ __global__ void __launch_bounds__(1024, 1) k(int iters, int* out) {
     else if (P == 4) a = ((it * 37 + (threadIdx.x >> 5) * 101) & 1023) * 32 + lane;  // consecutive (conflict-free)
     else if (P == 5) a = (__shfl_sync(~0u, r, lane & ~1) % (W - 1)) + (lane & 1);   // 16 random unaligned adjacent pairs
     else if (P == 6) a = (__shfl_sync(~0u, r, lane & ~1) % (W / 64)) * 64 + (lane & 1) * 32 + (r & 31) ;  // pairs 32 words apart (same bank)
-    else a = ((r % (W / 32)) * 32) + lane;                                    // lane-ℓ-in-bank-ℓ, random rows
+    else if (P == 7) a = ((r % (W / 32)) * 32) + lane;                        // lane-ℓ-in-bank-ℓ, random rows
+    else if (P == 8) a = (__shfl_sync(~0u, r, lane & ~15) % (W / 16)) * 16 + (lane & 15);  // 2 random 16-word runs
+    else if (P == 9) a = (__shfl_sync(~0u, r, lane & ~7) % (W / 8)) * 8 + (lane & 7);      // 4 random 8-word runs
+    else if (P == 10) a = (__shfl_sync(~0u, r, lane & ~7) % (W - 8)) + (lane & 7);         // 4 random unaligned 8-word runs
+    else a = (__shfl_sync(~0u, r, lane & ~1) % (W / 2)) * 2 + (lane & 1) + 0 * P;          // (unused)
     chk |= atomicAdd(sm + a, 1);
   }
   __syncthreads();
@@ -39,11 +43,12 @@ int main() {
   int sms = 0; CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
   int* out; CK(cudaMalloc(&out, 4096 * 4));
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-  const char* names[] = {"rand32", "pairs_aligned", "quads_aligned", "parity_split", "consecutive", "pairs_unaligned", "pairs_same_bank", "lane_bank_rows"};
-  void (*ks[])(int, int*) = {k<0>, k<1>, k<2>, k<3>, k<4>, k<5>, k<6>, k<7>};
+  const char* names[] = {"rand32", "pairs_aligned", "quads_aligned", "parity_split", "consecutive", "pairs_unaligned", "pairs_same_bank",
+                         "lane_bank_rows", "runs16_x2", "runs8_x4", "runs8_x4_unal"};
+  void (*ks[])(int, int*) = {k<0>, k<1>, k<2>, k<3>, k<4>, k<5>, k<6>, k<7>, k<8>, k<9>, k<10>};
   const int iters = 8192;
   for (int rep = 0; rep < 2; ++rep)
-    for (int p = 0; p < 8; ++p) {
+    for (int p = 0; p < 11; ++p) {
       CK(cudaFuncSetAttribute(ks[p], cudaFuncAttributeMaxDynamicSharedMemorySize, W * 4));
       cudaEventRecord(e0);
       ks[p]<<<sms, 1024, W * 4>>>(iters, out);
