@@ -592,7 +592,7 @@ __global__ void __launch_bounds__(CT) k_chol_tiles(double* __restrict__ M, int64
         }
         bar_named(2, 96);
         if (w == 1) {
-          // L_{j+1,j} = A_{j+1,j} L_jj^{-T}, one step behind warp 0's POTRF
+          // L_{j+1,j} = A_{j+1,j} L_jj^{-T}, a quarter of the columns at a time as warp 0 releases them
           if (trace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(s_tw));
           double x[TS];
 #pragma unroll
